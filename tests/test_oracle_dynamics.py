@@ -1,0 +1,229 @@
+"""Pins of the oracle's neuron dynamics, STDP and delivery against closed forms,
+textbook routines and hand-wired spike trains (never against itself)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+F = 20
+Q = 2.0 ** F
+DT = 0.1
+
+
+def q(x):
+    return int(np.rint(np.float32(x) * np.float32(Q)))
+
+
+# ------------------------------------------------------------------ LIF (delta)
+def _delta(n=1, v_reset=10.0, v_th=20.0, tau_ref=0.0, seed=5):
+    o = O.Oracle(seed, DT, 0, F)
+    o.add_population(O.LIF_DELTA, n, tau_m=20.0, v_reset=v_reset, v_th=v_th, tau_ref=tau_ref)
+    o.finalize()
+    return o
+
+
+def test_delta_lif_free_decay_closed_form():
+    """No input: V_n = V_0 (1 - dt/tau)^n (Euler)."""
+    o = _delta(4)
+    V = o.array("V")
+    v0 = V.astype(np.float64).copy()
+    assert np.all((v0 >= 10.0) & (v0 < 20.0))       # initial V in [v_reset, v_th)
+    for n in range(1, 201):
+        o.step(1)
+        exact = v0 * (1.0 - DT / 20.0) ** n
+        assert np.allclose(V, exact, rtol=2e-5, atol=0)
+
+
+def test_delta_lif_constant_input_closed_form_and_first_spike():
+    """Constant input I per step: V_n = V_inf + (V_0 - V_inf) k^n with
+    V_inf = I / (1 - k); the first threshold crossing happens at the step the
+    closed form predicts."""
+    o = _delta(1, v_th=1e9)               # no firing: follow the trajectory
+    V, ine = o.array("V"), o.array("in_e")
+    I = 0.5
+    k = 1.0 - DT / 20.0
+    v0 = float(V[0])
+    vinf = I / (1 - k)
+    for n in range(1, 300):
+        ine[0] = q(I)
+        o.step(1)
+        exact = vinf + (v0 - vinf) * k ** n
+        assert abs(V[0] - exact) <= 3e-5 * abs(exact)
+    o2 = _delta(1, v_th=30.0)
+    V2, ine2 = o2.array("V"), o2.array("in_e")
+    v0 = float(V2[0])
+    n_pred = next(n for n in range(1, 10000) if vinf + (v0 - vinf) * k ** n >= 30.0)
+    for n in range(1, n_pred + 1):
+        ine2[0] = q(I)
+        o2.step(1)
+        fired = int(o2.array("hist")[0] & 1)
+        assert fired == (n == n_pred)
+    assert V2[0] == np.float32(10.0)      # reset value exact
+
+
+def test_refractory_length_exact_and_inputs_discarded():
+    """tau_ref = 2 ms -> 20 steps held at V_reset, delta inputs discarded (R20)."""
+    o = _delta(1, tau_ref=2.0)
+    V, ine, ref = o.array("V"), o.array("in_e"), o.array("ref")
+    ine[0] = q(50.0)
+    o.step(1)
+    assert o.array("hist")[0] & 1
+    assert ref[0] == 20
+    for s in range(20):
+        ine[0] = q(50.0)
+        o.step(1)
+        assert not (o.array("hist")[0] & 1)
+        assert V[0] == np.float32(10.0)
+    ine[0] = q(50.0)
+    o.step(1)                              # 21st step: integrates and fires again
+    assert o.array("hist")[0] & 1
+
+
+# -------------------------------------------------------------------- CUBA LIF
+def test_cuba_exponential_conductance_and_voltage_closed_form():
+    """A pulse g0 into the exc receptor: g_n = g0 d^n; V follows the linear
+    recurrence V_{n+1} = V_n + a (E_l - V_n + g_n), whose closed form is
+    V_n = E_l + (V0-E_l) r^n + a g0 (d^n - r^n)/(d - r), r = 1 - a."""
+    o = O.Oracle(9, DT, 0, F)
+    o.add_population(O.LIF_CUBA, 1, tau_m=20.0, v_rest=-49.0, v_reset=-60.0, v_th=1e9,
+                     tau_ref=5.0, tau_e=5.0, tau_i=10.0)
+    o.finalize()
+    V, ge, ine = o.array("V"), o.array("ge"), o.array("in_e")
+    v0 = float(V[0])
+    g0 = 2.0
+    a = DT / 20.0
+    r = 1 - a
+    d = math.exp(-DT / 5.0)
+    ine[0] = q(g0)
+    for n in range(1, 400):
+        o.step(1)
+        assert abs(ge[0] - g0 * d ** n) <= 2e-5 * g0 * d ** n + 1e-30
+        # V after n updates: uses g_0..g_{n-1}
+        exact = -49.0 + (v0 + 49.0) * r ** n + a * g0 * (d ** n - r ** n) / (d - r)
+        assert abs(V[0] - exact) <= 2e-5 * abs(exact)
+
+
+# --------------------------------------------------------------------- Poisson
+def test_poisson_rate_and_independence():
+    o = O.Oracle(123, DT, 0, F)
+    o.add_population(O.POISSON, 2000, rate_hz=16.0)
+    o.finalize()
+    T = 2000
+    counts = np.zeros(2000)
+    prev = None
+    same = 0
+    for t in range(T):
+        o.step(1)
+        s = (o.array("hist") & 1).astype(bool)
+        counts += s
+        if prev is not None:
+            same += int(np.sum(s & prev))
+        prev = s
+    p = 16.0 * 1e-3 * DT
+    n = 2000 * T
+    assert abs(counts.sum() / n - p) < 5 * math.sqrt(p * (1 - p) / n)
+    # consecutive steps independent: joint rate ~ p^2
+    assert abs(same / (2000 * (T - 1)) - p * p) < 5 * math.sqrt(p * p / (2000 * (T - 1)))
+
+
+# ------------------------------------------------------------------ STDP (R7)
+A_PLUS, A_MINUS, W_MAX, TAU = 0.01, 0.0105, 1.0, 20.0
+
+
+def _pair(delay=0, w0=0.5, seed=1):
+    """Two delta neurons A -> B (p = 1, STDP).  Neither fires unless forced."""
+    o = O.Oracle(seed, DT, delay, F)
+    a = o.add_population(O.LIF_DELTA, 1, tau_m=20.0, v_reset=0.0, v_th=20.0)
+    b = o.add_population(O.LIF_DELTA, 1, tau_m=20.0, v_reset=0.0, v_th=20.0)
+    o.connect(a, b, O.STDP, 0, 1.0, w0, tau_plus=TAU, tau_minus=TAU, a_plus=A_PLUS,
+              a_minus=A_MINUS, w_max=W_MAX)
+    o.finalize()
+    return o
+
+
+def _run(o, fire_at, T):
+    """fire_at: {step: [neuron ids]} forced by a large input."""
+    ine = o.array("in_e")
+    for t in range(T):
+        for i in fire_at.get(t, []):
+            ine[i] = q(100.0)
+        o.step(1)
+
+
+@pytest.mark.parametrize("delay", [0, 3, 15])
+@pytest.mark.parametrize("dlt", [1, 5, 37, 63])
+def test_stdp_pre_then_post_potentiation_closed_form(delay, dlt):
+    """Pre at u (arrival D steps after the source spike), post at u+dlt:
+    dw = A+ exp(-dlt dt / tau+)."""
+    o = _pair(delay)
+    u = 10 + delay
+    _run(o, {10: [0], u + dlt: [1]}, u + dlt + 1)
+    dw = float(o.array("w")[0]) - 0.5
+    assert abs(dw - A_PLUS * math.exp(-dlt * DT / TAU)) <= 1e-5 * A_PLUS + 1e-7
+
+
+@pytest.mark.parametrize("dlt", [1, 7, 40])
+def test_stdp_post_then_pre_depression_closed_form(dlt):
+    o = _pair(0)
+    _run(o, {10: [1], 10 + dlt: [0]}, 10 + dlt + 1)
+    dw = float(o.array("w")[0]) - 0.5
+    assert abs(dw + A_MINUS * math.exp(-dlt * DT / TAU)) <= 1e-5 * A_MINUS + 1e-7
+
+
+def test_stdp_same_step_is_post_then_pre():
+    """Same step: potentiation sees x_pre before the pre increment (0) and the
+    depression sees x_post after the post increment (1): dw = -A- (R7)."""
+    o = _pair(0)
+    _run(o, {10: [0, 1]}, 11)
+    assert abs(float(o.array("w")[0]) - (0.5 - A_MINUS)) < 1e-7
+
+
+def test_stdp_hard_bounds_and_no_spike_no_change():
+    o = _pair(0, w0=W_MAX - 1e-4)
+    _run(o, {10: [0], 11: [1]}, 12)
+    assert o.array("w")[0] == np.float32(W_MAX)
+    o = _pair(0, w0=1e-4)
+    _run(o, {10: [1], 11: [0]}, 12)
+    assert o.array("w")[0] == np.float32(0.0)
+    o = _pair(0)
+    _run(o, {}, 300)
+    assert o.array("w")[0] == np.float32(0.5)
+
+
+# -------------------------------------------------------------------- delivery
+def test_delivery_equals_dense_matvec():
+    """Row-wise delivery (Fig. 3a) = the matrix-vector product of the spike
+    vector s(t-D) with the quantised weight matrix (a textbook routine)."""
+    import workloads as W
+    rc = W.brunel(1200, p=0.05, plastic=False, delay=2, seed=4)
+    o = O.Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits)
+    rc.apply(o)
+    o.finalize()
+    N = o.n
+    rp, idx, w = o.array("row_ptr"), o.array("idx"), o.array("w")
+    Wq = np.zeros((N, N), dtype=np.int64)
+    for i in range(N):
+        for c in range(rp[i], rp[i + 1]):
+            Wq[i, idx[c]] += int(np.rint(np.float64(w[c]) * Q))
+    checked = 0
+    for t in range(60):
+        o.step(1)
+        s = ((o.array("hist") >> np.uint64(rc.delay)) & np.uint64(1)).astype(np.int64)
+        assert np.array_equal(o.array("in_e").astype(np.int64), s @ Wq)
+        checked += int(s.sum())
+    assert checked > 0
+
+
+def test_quantisation_rounds_half_to_even():
+    """q(w) = RNE(w 2^F) (R18): ties go to the even integer."""
+    for frac, expect in [(2.5, 2), (3.5, 4), (-2.5, -2), (1.25, 1)]:
+        o = O.Oracle(1, DT, 0, F)
+        a = o.add_population(O.LIF_DELTA, 1, v_reset=0.0, v_th=20.0)
+        b = o.add_population(O.LIF_DELTA, 1, v_reset=0.0, v_th=1e9)
+        o.connect(a, b, O.STATIC, 0, 1.0, frac / Q)
+        o.finalize()
+        o.array("in_e")[0] = q(100.0)
+        o.step(1)
+        assert o.array("in_e")[1] == expect
