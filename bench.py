@@ -1,0 +1,289 @@
+"""bench.py -- throughput of the clock-driven SNN step (BASELINE.json metric:
+wall-s per bio-second & synaptic events/s; % HBM roofline) on synthetic
+Brunel+ / Brunel / Vogels-Abbott networks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+A "step" is one simulation step (dt = 0.1 ms) of the whole hot path: neuron
+update, lazy+event-driven STDP, sliced shared-atomic delivery.
+Default workload: BASELINE config 3 (Brunel+, 316,228 neurons, ~1e9 synapses,
+40 % plastic) -- the only single-GPU config that exercises every 8(a) row.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "wall-s per bio-second & synaptic events/s at 1/2/4/8 B200; % HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10000)
+    ap.add_argument("--warmup", type=int, default=1000)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--slice-width", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--phase-steps", type=int, default=0, help="steps of the per-phase timing pass (0 = --steps)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_sample_recipe(cfg: int, seed: int):
+    """Bounded oracle sample of the same workload family."""
+    if cfg in (3, 4):
+        return W.brunel(31_623, plastic=True, seed=seed), "Brunel+ scaled to N=31,623 (same composition, p=0.02, ~1e7 synapses, 40% plastic)"
+    if cfg == 2:
+        return W.brunel(31_623, plastic=False, seed=seed), "Brunel scaled to N=31,623 (same composition, p=0.02, ~1e7 synapses)"
+    if cfg == 5:
+        return W.vogels(31_623, seed=seed), "Vogels CUBA scaled to N=31,623 (p=0.02, ~2e7 synapses)"
+    return W.config(1, seed=seed), "Vogels CUBA 4,000 (the full config 1)"
+
+
+def run_oracle(cfg: int, seed: int, steps: int, warmup: int, budget_s: float = 20.0):
+    """Time the oracle as it stands (test infrastructure; only this leg of bench.py runs it)."""
+    from oracle.oracle import Oracle
+    rc, sample = cpu_sample_recipe(cfg, seed)
+    cores = os.cpu_count() or 1
+    o = Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, threads=cores)
+    rc.apply(o)
+    o.finalize()
+    o.step(warmup)
+    e0 = o.events
+    t0 = time.perf_counter()
+    done = 0
+    while done < steps:
+        o.step(1)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    ev = o.events - e0
+    return dict(value=ev / dt, unit="events/s", cores=cores, kind="oracle",
+                sample=f"{sample}; {done} timed steps after {warmup} warm-up steps",
+                wall_s_per_bio_s=(dt / done) / (rc.dt_ms * 1e-3), steps=done, seconds=dt,
+                synapses=int(o.nsyn))
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        r = run_oracle(a.config, a.seed, a.steps, max(a.warmup, 0), budget_s=60.0)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "events/s",
+            "n_gpus": a.gpus, "steps": r["steps"], "warmup": a.warmup,
+            "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"BASELINE config {a.config} (oracle sample: {r['sample']})"},
+            "wall_s_per_bio_s": r["wall_s_per_bio_s"],
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    import torch
+    if world > 1:
+        raise SystemExit("multi-GPU bench: see DESIGN.md section 7 (not in this build yet)")
+    from paper_2107_04092_b200 import Snn, FLAG_PHASE_TIMING
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    rc = W.config(a.config, seed=a.seed, gpus=world)
+    stream = torch.cuda.Stream(dev)
+
+    # ---------------------------------------------------------- device-timed
+    sim = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream)
+    rc.apply(sim)
+    t0 = time.perf_counter()
+    sim.finalize()
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    info = sim.info()
+    with ClockSampler(dev) as clk:
+        sim.step(a.warmup)
+        torch.cuda.synchronize()
+        m0 = sim.metrics()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        sim.step(a.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    m1 = sim.metrics()
+    dm = {k: m1[k] - m0[k] for k in m1}
+    spikes = sim.read_state("SPIKE_COUNT")
+    t_total = (a.warmup + a.steps) * rc.dt_ms * 1e-3
+    rates = {p.name: float(spikes[b:b + p.n].sum()) / p.n / t_total
+             for p, b in zip(rc.pops, np.cumsum([0] + [p.n for p in rc.pops])[:-1])}
+    sec = ms * 1e-3
+    events_per_s = dm["EVENTS"] / sec
+    ms_per_step = ms / a.steps
+    wall_per_bio = (ms_per_step * 1e-3) / (rc.dt_ms * 1e-3)
+
+    # --------------------------------------------------- e2e through the C ABI
+    e2e = None
+    if not a.no_e2e:
+        chunk = 64
+        ring = np.empty(64 * ((info["N"] + 31) // 32), dtype=np.uint32)
+        m0e = sim.metrics()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        done = 0
+        while done < a.steps:
+            n = min(chunk, a.steps - done)
+            sim.step(n)
+            sim.read_state("SPIKE_RING", out=ring)     # D2H of the step rasters into a host buffer
+            done += n
+        t1 = time.perf_counter()
+        m1e = sim.metrics()
+        e2e = {"value": (m1e["EVENTS"] - m0e["EVENTS"]) / (t1 - t0), "unit": "events/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(ring.nbytes / chunk),
+               "wall_s_per_bio_s": (t1 - t0) / (a.steps * rc.dt_ms * 1e-3),
+               "note": "snn_step(64) + snn_read_state(SPIKE_RING) per 64 steps; an SNN step has no host input "
+                       "(Poisson drive is counter-based on device), so h2d = 0"}
+    sim.close()
+    del sim
+    torch.cuda.synchronize()
+
+    # ------------------------------------------- per-phase timing (roofline)
+    psteps = a.phase_steps or a.steps
+    sp = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream,
+             flags=FLAG_PHASE_TIMING)
+    rc.apply(sp)
+    sp.step(a.warmup)
+    sp.phase_times()   # drain warm-up events
+    base = sp.phase_times()
+    mp0 = sp.metrics()
+    sp.step(psteps)
+    ph = sp.phase_times()
+    mp1 = sp.metrics()
+    ph = {k: ph[k] - base[k] for k in ph}
+    d = {k: mp1[k] - mp0[k] for k in mp1}
+    sp.close()
+    nrcpt = 2 if any(pr.receptor == W.INH for pr in rc.projs) else 1
+    # algorithmic HBM bytes per phase
+    bytes_ph = {
+        "STDP": 4 * d["STDP_SYN"] + 8 * d["STDP_WTOUCH"] + 24 * d["STDP_ROWS"],
+        "DELIVERY": 8 * d["EVENTS"] + 8 * d["SPIKES"] * info["nslices"] + 16 * d["SPIKES"]
+                    + 8 * nrcpt * info["R"] * 0,
+        "NEURON": psteps * sum(p.n * (16 if p.kind == W.POISSON else 40) for p in rc.pops) // 1,
+    }
+    hbm, peak_src = peaks()
+    dom = max(("STDP", "DELIVERY", "NEURON", "WORKLIST"), key=lambda k: ph.get(k, 0.0))
+    dom_bytes = bytes_ph.get(dom, 0)
+    dom_ms = ph[dom]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
+    shares = {k: ph[k] / ph["TOTAL"] for k in ("NEURON", "WORKLIST", "STDP", "DELIVERY")} if ph["TOTAL"] else {}
+    sd_bytes = bytes_ph["STDP"] + bytes_ph["DELIVERY"]
+    sd_ms = ph["STDP"] + ph["DELIVERY"]
+
+    out = {
+        "metric": METRIC, "value": events_per_s, "unit": "events/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (int32 fixed-point accumulators)", "data": "synthetic",
+        "config": {"workload": f"BASELINE config {a.config}: {rc.name}", "neurons": info["N"],
+                   "synapses": info["S"], "plastic": rc.plastic, "dt_ms": rc.dt_ms, "delay_steps": rc.delay,
+                   "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
+                   "l2": "inputs larger than L2: %.1f GB of graph, each step touches the rows of that step's spikes"
+                         % (info["S"] * 8 / 1e9)},
+        "wall_s_per_bio_s": wall_per_bio,
+        "setup_s": setup_s,
+        "rates_hz": rates,
+        "per_step": {"events": dm["EVENTS"] / a.steps, "spikes": dm["SPIKES"] / a.steps,
+                     "stdp_rows": dm["STDP_ROWS"] / a.steps, "stdp_syn": dm["STDP_SYN"] / a.steps,
+                     "stdp_wtouch": dm["STDP_WTOUCH"] / a.steps},
+        "gpu_launches": a.steps * (4 if rc.plastic else 3),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                     "phase_ms_per_step": {k: ph[k] / psteps for k in ph}, "phase_share": shares,
+                     "stdp_plus_delivery": {"achieved": sd_bytes / (sd_ms * 1e-3) / 1e9 if sd_ms else 0.0,
+                                            "frac": (sd_bytes / (sd_ms * 1e-3) / 1e9 / hbm) if sd_ms else 0.0,
+                                            "bytes_per_step": sd_bytes / psteps}},
+        "e2e": e2e,
+        "clocks": clk.summary(),
+    }
+    if not a.no_cpu_baseline and rank == 0:
+        r = run_oracle(a.config, a.seed, 2000, 50, budget_s=15.0)
+        out["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        out["cpu_baseline"]["wall_s_per_bio_s"] = r["wall_s_per_bio_s"]
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,234 @@
+/*
+ * snn.h -- C ABI of libsnn.so, a B200-native (sm_100a) implementation of the
+ * clock-driven SNN simulation step accelerated by arXiv 2107.04092 ("Spice").
+ *
+ * The problem statement followed (PAPER.md line numbers "P:n"):
+ *   - a static directed graph, grouped by source and sorted, built once;
+ *   - neurons with a 64-bit firing history, LSB = most recent, synapses
+ *     with state, one network-wide delay in steps;
+ *   - per step: (1) update neurons and note which fire; (2) update
+ *     synapses -- lazy + event-driven plasticity over the history bitfields
+ *     (Fig. 2c, Sec. III-A); (3) deliver spikes through
+ *     an adjacency list partitioned into equal-width neuron slices with
+ *     shared-memory atomics (Fig. 3b, Sec. III-B);
+ *   - "users can still define custom models" is narrowed to the built-in
+ *     population and synapse kinds below.
+ *
+ * Conventions for every entry point:
+ *   - Plain C types only; no C++ type or exception crosses this boundary.
+ *   - Every call returns an snn_status (0 = SNN_OK, < 0 = error).  On error a
+ *     message is available from snn_last_error(sim) until the next call on that
+ *     handle.  CUDA errors map to SNN_E_CUDA, NCCL errors to SNN_E_NCCL.
+ *   - Ownership: the handle owns every DEVICE buffer it allocates (through the
+ *     dev_alloc/dev_free hooks when given, e.g. PyTorch's caching allocator,
+ *     else cudaMalloc) and frees them in snn_destroy.  Parameter structs are
+ *     copied at call time.  HOST buffers passed in (host_dst) stay owned by the
+ *     caller.
+ *   - Lifecycle: CONFIG (add_population / connect allowed) -> FINALIZED by the
+ *     first snn_step (graph construction = setup) -> RUNNING.
+ *     add_population / connect after that return SNN_E_STATE.
+ *   - Threading: a handle is not thread-safe; use one handle per (process, GPU).
+ *   - All device work is enqueued on cfg.stream (a borrowed cudaStream_t;
+ *     NULL = the legacy default stream).
+ *   - world > 1: every rank makes the identical call sequence (collective
+ *     semantics, like NCCL).  Rank r owns the target-neuron range given by
+ *     snn_read_state(SNN_FIELD_PARTITION); see DESIGN.md section 7.
+ */
+#ifndef SNN_H
+#define SNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNN_ABI_VERSION 1u
+
+typedef struct snn_sim snn_sim; /* opaque; owned by the library */
+typedef int32_t snn_status;
+
+enum {
+    SNN_OK = 0,
+    SNN_E_INVALID = -1,     /* bad argument: p outside [0,1], n == 0, D >= H,
+                               slice width not a power of two in [32, 32768],
+                               fixed-point overflow bound violated, ...      */
+    SNN_E_STATE = -2,       /* call not allowed in the handle's lifecycle state */
+    SNN_E_OOM = -3,         /* device allocation failed                        */
+    SNN_E_CUDA = -4,        /* a CUDA runtime error (text in snn_last_error)   */
+    SNN_E_NCCL = -5,        /* an NCCL error                                   */
+    SNN_E_UNSUPPORTED = -6  /* valid but not implemented (e.g. 2 STDP
+                               projections from one source population)        */
+};
+
+/* population kinds (R9): */
+enum {
+    SNN_POP_POISSON = 0,    /* Bernoulli(rate*dt) per step from Philox, no inputs */
+    SNN_POP_LIF_DELTA = 1,  /* Brunel 2000 model A: delta-current LIF, 1 receptor */
+    SNN_POP_LIF_CUBA = 2    /* Vogels-Abbott CUBA: exc/inh exponential currents   */
+};
+/* synapse kinds: */
+enum { SNN_SYN_STATIC = 0, SNN_SYN_STDP = 1 };
+/* receptors: */
+enum { SNN_RCPT_EXC = 0, SNN_RCPT_INH = 1 };
+
+/* config flags */
+enum {
+    SNN_FLAG_NO_GRAPH = 1u << 0,     /* launch kernels directly instead of replaying
+                                        a captured CUDA graph of the step          */
+    SNN_FLAG_PHASE_TIMING = 1u << 1  /* record CUDA events around every phase of
+                                        every step (implies NO_GRAPH); read with
+                                        SNN_FIELD_PHASE_TIMES                       */
+};
+
+typedef struct {
+    uint32_t abi_version;    /* must be SNN_ABI_VERSION                          */
+    uint32_t struct_size;    /* sizeof(snn_config)                                */
+    float dt_ms;             /* step length; 0.1 ms in the paper          */
+    uint32_t delay_steps;    /* network-wide delay D in steps; D < 64     */
+    uint32_t history_bits;   /* H: 64; only 64 is supported        */
+    uint32_t slice_width;    /* C: neurons per slice; power of two
+                                in [32, 32768]; 0 = automatic                      */
+    int32_t accum_frac_bits; /* F: fixed-point fraction bits of the int32 input
+                                accumulators (R18); 0..30, default 20   */
+    uint32_t flags;          /* SNN_FLAG_*                                        */
+    uint64_t seed;           /* Philox key = (seed & 0xffffffff, seed >> 32)      */
+    int32_t device;          /* CUDA device ordinal                               */
+    int32_t rank, world;     /* this process' rank and the number of ranks (GPUs) */
+    void *stream;            /* cudaStream_t, borrowed                            */
+    /* optional device allocator hooks (e.g. torch caching allocator); both NULL
+       -> cudaMalloc / cudaFree.  dev_alloc returns NULL on failure.            */
+    void *(*dev_alloc)(size_t bytes, void *stream, void *ctx);
+    void (*dev_free)(void *ptr, void *stream, void *ctx);
+    void *alloc_ctx;
+    /* world > 1: the 128-byte ncclUniqueId, identical on all ranks (the caller
+       broadcasts it, e.g. with torch.distributed).  Ignored when world == 1.   */
+    const void *nccl_unique_id;
+} snn_config;
+
+typedef struct {
+    uint32_t struct_size;    /* sizeof(snn_pop_params)                            */
+    uint32_t kind;           /* SNN_POP_*                                         */
+    float rate_hz;           /* POISSON: firing rate                              */
+    float tau_m_ms;          /* LIF membrane time constant                        */
+    float v_rest_mv;         /* CUBA leak reversal E_l (unused by LIF_DELTA: 0)   */
+    float v_reset_mv;        /* reset potential; initial V ~ U[v_reset, v_th)      */
+    float v_th_mv;           /* threshold: fire iff V >= v_th (R20)               */
+    float tau_ref_ms;        /* refractory period, rounded to steps               */
+    float tau_e_ms, tau_i_ms;/* CUBA receptor time constants                      */
+} snn_pop_params;
+
+typedef struct {
+    uint32_t struct_size;    /* sizeof(snn_syn_params)                            */
+    uint32_t kind;           /* SNN_SYN_STATIC | SNN_SYN_STDP                     */
+    uint32_t receptor;       /* SNN_RCPT_*; LIF_DELTA targets accept only EXC     */
+    uint32_t allow_autapses; /* 0: no i -> i synapse (R21)                        */
+    double p;                /* connection probability in [0, 1] (Bernoulli per
+                                ordered pair, Philox, R22/R23)                    */
+    float weight;            /* initial weight, FINAL value (caller scales, R10)  */
+    float tau_plus_ms, tau_minus_ms; /* STDP trace time constants (R7)            */
+    float a_plus, a_minus;   /* STDP amplitudes (additive rule, R7)               */
+    float w_max;             /* STDP hard upper bound; lower bound is 0           */
+} snn_syn_params;
+
+/* fields for snn_read_state (element type / count in brackets).  Neuron
+ * fields cover the population pop_id; pop_id = UINT32_MAX means all N neurons.
+ * Synapse fields are in CSR order of this rank's graph. */
+enum {
+    SNN_FIELD_V = 0,            /* [f32 / n]   membrane potential               */
+    SNN_FIELD_REFRACTORY = 1,   /* [i32 / n]   remaining refractory steps       */
+    SNN_FIELD_G_EXC = 2,        /* [f32 / n]   CUBA exc current                 */
+    SNN_FIELD_G_INH = 3,        /* [f32 / n]   CUBA inh current                 */
+    SNN_FIELD_INPUT_EXC = 4,    /* [i32 / n]   pending fixed-point input, exc   */
+    SNN_FIELD_INPUT_INH = 5,    /* [i32 / n]   pending fixed-point input, inh   */
+    SNN_FIELD_HIST = 6,         /* [u64 / n]   64-bit firing history    */
+    SNN_FIELD_SPIKE_COUNT = 7,  /* [u32 / n]   spikes since start               */
+    SNN_FIELD_XPOST = 8,        /* [f32 / n]   post-synaptic trace per neuron   */
+    SNN_FIELD_XPRE_ROW = 9,     /* [f32 / n]   pre-synaptic trace per source row (after flush) */
+    SNN_FIELD_TLU = 10,         /* [i32 / n]   timeOfLastUpdate per row (after flush) */
+    SNN_FIELD_ROW_PTR = 11,     /* [i64 / N+1] CSR row offsets                  */
+    SNN_FIELD_IDX = 12,         /* [u32 / S]   CSR target ids                   */
+    SNN_FIELD_WEIGHTS = 13,     /* [f32 / S]   weights, after the read-out flush (R11) */
+    SNN_FIELD_PIVOTS = 14,      /* [u32 / N*(nslices+1)] row-relative pivots    */
+    SNN_FIELD_STEP = 15,        /* [i64 / 1]   number of steps simulated        */
+    SNN_FIELD_METRICS = 16,     /* [u64 / 8]   see SNN_METRIC_*                 */
+    SNN_FIELD_SPIKE_RING = 17,  /* [u32 / 64*ceil(N/32)] bitmask ring; slot t%64
+                                   holds the spikes of step t                    */
+    SNN_FIELD_PHASE_TIMES = 18, /* [f64 / 8]  ms per phase (SNN_PHASE_*), summed
+                                   over steps run with SNN_FLAG_PHASE_TIMING     */
+    SNN_FIELD_INFO = 19,        /* [i64 / 8]  N, S, nslices, C, R, tgt_lo, tgt_hi,
+                                   pivot bytes                                    */
+    SNN_FIELD_COUNT = 20
+};
+
+/* SNN_FIELD_METRICS layout (device counters, cumulative over steps) */
+enum {
+    SNN_METRIC_EVENTS = 0,       /* delivered (arriving spike, target) pairs (R24) */
+    SNN_METRIC_SPIKES = 1,       /* arriving spikes (rows delivered)               */
+    SNN_METRIC_STDP_ROWS = 2,    /* plastic rows visited (arrivals + flushes)      */
+    SNN_METRIC_STDP_SYN = 3,     /* plastic synapses visited                       */
+    SNN_METRIC_STDP_WTOUCH = 4,  /* plastic synapses whose weight was read+written */
+    SNN_METRIC_FLUSH_ROWS = 5,   /* rows visited by a forced flush (R3)            */
+    SNN_METRIC_SEGMENTS = 6,     /* non-empty (row, slice) segments delivered      */
+    SNN_METRIC_RESERVED = 7
+};
+
+/* SNN_FIELD_PHASE_TIMES layout */
+enum {
+    SNN_PHASE_NEURON = 0, SNN_PHASE_WORKLIST = 1, SNN_PHASE_STDP = 2,
+    SNN_PHASE_DELIVERY = 3, SNN_PHASE_EXCHANGE = 4, SNN_PHASE_TOTAL = 5
+};
+
+/* Creates a simulation handle bound to cfg->device / cfg->stream.
+ * out receives the handle (NULL on failure).  Errors: SNN_E_INVALID (bad cfg),
+ * SNN_E_CUDA, SNN_E_NCCL (world > 1 communicator setup). */
+snn_status snn_create(const snn_config *cfg, snn_sim **out);
+
+/* Appends a population of n neurons; ids are contiguous in call order
+ * (list populations that receive synapses first, so slices span only them).
+ * pop_id receives its index.  Errors: SNN_E_INVALID (n == 0, bad kind or
+ * parameters), SNN_E_STATE (after finalize). */
+snn_status snn_add_population(snn_sim *sim, uint32_t n, const snn_pop_params *params,
+                              uint32_t *pop_id);
+
+/* Declares the projection src_pop -> dst_pop: every ordered pair (i, j) is a
+ * synapse with probability p (Philox Bernoulli, R22), one projection per pair
+ * of populations.  Errors: SNN_E_INVALID (p outside [0,1], POISSON target,
+ * bad receptor, duplicate projection), SNN_E_UNSUPPORTED (second STDP
+ * projection from one source population), SNN_E_STATE. */
+snn_status snn_connect(snn_sim *sim, uint32_t src_pop, uint32_t dst_pop,
+                       const snn_syn_params *params);
+
+/* Enqueues n_steps simulation steps on cfg->stream (asynchronous).  The first
+ * call finalizes: it builds the sliced CSR graph and the initial state on the
+ * device (setup).  n_steps == 0 only finalizes.  Errors: SNN_E_INVALID
+ * (fixed-point overflow bound, empty network), SNN_E_OOM, SNN_E_CUDA,
+ * SNN_E_NCCL. */
+snn_status snn_step(snn_sim *sim, uint32_t n_steps);
+
+/* Copies a state field (SNN_FIELD_*) of population pop_id (UINT32_MAX = all
+ * neurons; ignored for synapse / global fields) into the caller's HOST buffer
+ * host_dst of dst_bytes bytes, synchronising cfg->stream.  If host_dst is
+ * NULL, only *needed (bytes required) is written.  Reading WEIGHTS, XPRE_ROW
+ * or TLU first brings every stale plastic row up to the current step without a
+ * pre spike (read-out flush, R11), which does not change future results.
+ * Errors: SNN_E_INVALID (unknown field / pop, dst_bytes too small),
+ * SNN_E_STATE (before finalize), SNN_E_CUDA. */
+snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *host_dst,
+                          size_t dst_bytes, size_t *needed);
+
+/* Releases every device buffer, graph, event and communicator of the handle. */
+void snn_destroy(snn_sim *sim);
+
+/* The message of the last failed call on sim (or of the last failed
+ * snn_create when sim is NULL).  Valid until the next call on the handle. */
+const char *snn_last_error(const snn_sim *sim);
+
+/* The ABI version the library was built with (SNN_ABI_VERSION). */
+uint32_t snn_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNN_H */

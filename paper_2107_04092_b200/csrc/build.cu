@@ -1,0 +1,231 @@
+// build.cu -- on-GPU construction of the neuron-domain-sliced CSR graph
+// (Sec. III P:185 "constructed only once", Fig. 1
+// P:180 pivots, Sec. III-B P:348 slices, Sec. IV-B P:391 GPU setup).
+//
+// Row i lists, ascending, every target j in this rank's range [tgt_lo, tgt_hi)
+// kept by the Bernoulli draw of reading R22/R23.  Pivots are NOT binary-searched
+// here (the oracle does that): the count pass produces per-(row, slice)
+// counts whose exclusive prefix IS the pivot row -- an independent route to the
+// same table, so the two cross-check each other.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace snn {
+
+constexpr int kBuildThreads = 256;
+
+// Decision for 4 consecutive candidates j0..j0+3 of source row i.
+// Returns a 4-bit mask (bit e = candidate j0+e kept).
+__device__ __forceinline__ uint32_t decide4(const NetDev &net, const uint64_t *thr_tab,
+                                            const uint8_t *autapse_tab, int sp, uint32_t i,
+                                            uint32_t j0, uint32_t jend) {
+    uint32_t mask = 0;
+    int cached_dp = -1;
+    uint32_t cached_q = 0xffffffffu;
+    u32x4 r{0, 0, 0, 0};
+    int dp = find_pop(net, j0 < net.N ? j0 : net.N - 1);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const uint32_t j = j0 + e;
+        if (j >= jend) break;
+        while (dp + 1 < (int)net.npop && j >= net.pop[dp + 1].base) dp++;
+        const uint64_t thr = thr_tab[sp * kMaxPops + dp];
+        if (thr == 0) continue;                       // no projection sp -> dp (or p == 0)
+        if (j == i && !autapse_tab[sp * kMaxPops + dp]) continue;
+        const uint32_t jl = j - net.pop[dp].base;
+        const uint32_t qd = jl >> 2;
+        if (dp != cached_dp || qd != cached_q) {
+            r = philox4x32_10(i, qd, 1u, (uint32_t)dp, net.key0, net.key1);
+            cached_dp = dp;
+            cached_q = qd;
+        }
+        if ((uint64_t)lane_of(r, jl & 3u) < thr) mask |= 1u << e;
+    }
+    return mask;
+}
+
+// Pass 1: per (row, slice) counts -> piv[i][k+1]; piv[i][0] = 0.
+__global__ void __launch_bounds__(kBuildThreads)
+k_count(NetDev net, BuildTabs tabs, uint32_t *piv, uint32_t row0, uint32_t nrows) {
+    const uint32_t i = row0 + blockIdx.x;
+    if (i >= row0 + nrows) return;
+    const int sp = find_pop(net, i);
+    const uint32_t P = net.nslices + 1;
+    uint32_t *prow = piv + (size_t)i * P;
+    __shared__ uint32_t red[kBuildThreads / 32];
+    bool any = false;
+    for (int d = 0; d < (int)net.npop; d++) any |= tabs.thr[sp * kMaxPops + d] != 0;
+    if (threadIdx.x == 0) prow[0] = 0;
+    for (uint32_t k = 0; k < net.nslices; k++) {
+        const uint32_t lo = net.tgt_lo + (k << net.log2C);
+        const uint32_t hi = min(lo + net.C, net.tgt_hi);
+        uint32_t cnt = 0;
+        if (any) {
+            for (uint32_t j0 = lo + 4 * threadIdx.x; j0 < hi; j0 += 4 * kBuildThreads)
+                cnt += __popc(decide4(net, tabs.thr, tabs.autapse, sp, i, j0, hi));
+        }
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t s = 0;
+            for (int w = 0; w < kBuildThreads / 32; w++) s += red[w];
+            prow[k + 1] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// Pass 2: per row, counts -> exclusive prefix (the pivots); row length out.
+__global__ void k_pivot_scan(NetDev net, uint32_t *piv, int64_t *len, uint32_t nrows) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp >= nrows) return;
+    const uint32_t P = net.nslices + 1;
+    uint32_t *prow = piv + (size_t)warp * P;
+    uint32_t carry = 0;
+    for (uint32_t b = 1; b < P; b += 32) {
+        const uint32_t k = b + lane;
+        uint32_t v = k < P ? prow[k] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (k < P) prow[k] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) len[warp] = carry;
+}
+
+// Pass 3: fill targets (sorted by construction) and initial weights.
+__global__ void __launch_bounds__(kBuildThreads)
+k_fill(NetDev net, BuildTabs tabs, const uint32_t *piv, const int64_t *row_ptr, uint32_t *idx,
+       float *w) {
+    typedef cub::BlockScan<uint32_t, kBuildThreads> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    const uint32_t i = blockIdx.x;
+    const int sp = find_pop(net, i);
+    const uint32_t P = net.nslices + 1;
+    const uint32_t *prow = piv + (size_t)i * P;
+    if (prow[net.nslices] == 0) return;
+    const int64_t rbase = row_ptr[i];
+    for (uint32_t k = 0; k < net.nslices; k++) {
+        if (prow[k + 1] == prow[k]) continue;
+        const uint32_t lo = net.tgt_lo + (k << net.log2C);
+        const uint32_t hi = min(lo + net.C, net.tgt_hi);
+        int64_t pos = rbase + prow[k];
+        for (uint32_t jb = lo; jb < hi; jb += 4 * kBuildThreads) {
+            const uint32_t j0 = jb + 4 * threadIdx.x;
+            const uint32_t m = j0 < hi ? decide4(net, tabs.thr, tabs.autapse, sp, i, j0, hi) : 0u;
+            uint32_t off, tot;
+            Scan(tmp).ExclusiveSum((uint32_t)__popc(m), off, tot);
+            uint32_t mm = m;
+            while (mm) {
+                const int e = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const uint32_t j = j0 + e;
+                const int dp = find_pop(net, j);
+                idx[pos + off] = j;
+                w[pos + off] = tabs.weight[sp * kMaxPops + dp];
+                off++;
+            }
+            pos += tot;
+            __syncthreads();
+        }
+    }
+}
+
+// Plastic segment [lo, hi) of each PF_PRE_PLASTIC row: the targets inside the
+// STDP projection's destination population (rows are sorted, so it is one
+// contiguous run, found by binary search).
+__global__ void k_segments(NetDev net, const int64_t *row_ptr, const uint32_t *idx, uint2 *seg) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= net.N) return;
+    const int sp = find_pop(net, i);
+    uint2 s = make_uint2(0, 0);
+    if (net.pop[sp].stdp >= 0) {
+        const PopDev &dp = net.pop[net.stdp[net.pop[sp].stdp].dst_pop];
+        const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+        auto lb = [&](uint32_t v) {
+            int64_t a = b, c = e;
+            while (a < c) {
+                const int64_t m = (a + c) >> 1;
+                if (idx[m] < v) a = m + 1; else c = m;
+            }
+            return (uint32_t)(a - b);
+        };
+        s.x = lb(dp.base);
+        s.y = lb(dp.base + dp.n);
+    }
+    seg[i] = s;
+}
+
+// Initial state: V0 = v_reset + (v_th - v_reset) * u, u = (x >> 8) 2^-24 with
+// x = Philox(i, 0, 3, 0).x; all else 0; tlu = -1 (R4).
+__global__ void k_init_state(NetDev net, StateDev st) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= net.N) return;
+    const PopDev &p = net.pop[find_pop(net, i)];
+    float v = 0.0f;
+    if (p.kind != POP_POISSON) {
+        const u32x4 r = philox4x32_10(i, 0u, 3u, 0u, net.key0, net.key1);
+        const float u = __fmul_rn(__uint2float_rn(r.x >> 8), 0x1p-24f);
+        const float span = __fsub_rn(p.v_th, p.v_reset);
+        v = __fadd_rn(p.v_reset, __fmul_rn(span, u));
+    }
+    st.V[i] = v;
+    st.ge[i] = 0.0f;
+    st.gi[i] = 0.0f;
+    st.xpost[i] = 0.0f;
+    st.ref[i] = 0;
+    st.in_e[i] = 0;
+    st.in_i[i] = 0;
+    st.hist[i] = 0ull;
+    st.nspk[i] = 0u;
+    st.xpre[i] = 0.0f;
+    st.tlu[i] = -1;
+}
+
+// ---------------------------------------------------------------- launchers
+cudaError_t build_count(const NetDev &net, const BuildTabs &tabs, uint32_t *piv, cudaStream_t s) {
+    const uint32_t chunk = 1u << 20;
+    for (uint32_t r0 = 0; r0 < net.N; r0 += chunk) {
+        const uint32_t nr = min(chunk, net.N - r0);
+        k_count<<<nr, kBuildThreads, 0, s>>>(net, tabs, piv, r0, nr);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t build_scan(const NetDev &net, uint32_t *piv, int64_t *len, int64_t *row_ptr,
+                       void *tmp, size_t *tmp_bytes, cudaStream_t s) {
+    if (tmp == nullptr) {
+        return cub::DeviceScan::ExclusiveSum(nullptr, *tmp_bytes, len, row_ptr, (int)net.N + 1, s);
+    }
+    k_pivot_scan<<<(net.N * 32 + 255) / 256, 256, 0, s>>>(net, piv, len, net.N);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // len[N] = 0 was set by the caller; row_ptr = exclusive scan over N+1 entries
+    return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, len, row_ptr, (int)net.N + 1, s);
+}
+
+cudaError_t build_fill(const NetDev &net, const BuildTabs &tabs, const uint32_t *piv,
+                       const int64_t *row_ptr, uint32_t *idx, float *w, cudaStream_t s) {
+    k_fill<<<net.N, kBuildThreads, 0, s>>>(net, tabs, piv, row_ptr, idx, w);
+    return cudaGetLastError();
+}
+
+cudaError_t build_segments(const NetDev &net, const int64_t *row_ptr, const uint32_t *idx,
+                           uint2 *seg, cudaStream_t s) {
+    k_segments<<<(net.N + 255) / 256, 256, 0, s>>>(net, row_ptr, idx, seg);
+    return cudaGetLastError();
+}
+
+cudaError_t init_state(const NetDev &net, const StateDev &st, cudaStream_t s) {
+    k_init_state<<<(net.N + 255) / 256, 256, 0, s>>>(net, st);
+    return cudaGetLastError();
+}
+
+}  // namespace snn

@@ -1,0 +1,106 @@
+// common.cuh -- device-side tables and state of one simulation handle.
+//
+// Part of the product path (libsnn.so).  Shares nothing with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace snn {
+
+constexpr int kMaxPops = 16;
+constexpr int kHistBits = 64;     // H
+constexpr int kRingSlots = 64;    // bitmask ring: slot t % 64 holds step t's spikes
+constexpr uint32_t kArrBit = 0x80000000u;
+
+enum PopKind : uint32_t { POP_POISSON = 0, POP_LIF_DELTA = 1, POP_LIF_CUBA = 2 };
+enum PopFlags : uint32_t {
+    PF_HAS_INPUT = 1u,       // target of at least one projection
+    PF_POST_PLASTIC = 2u,    // target of an STDP projection: keeps hist u64 + x_post
+    PF_PRE_PLASTIC = 4u      // source of an STDP projection: rows carry tlu / x_pre
+};
+
+// Per-population constants, computed once on the host in double and rounded
+// to fp32 (R19).
+struct PopDev {
+    uint32_t base, n, kind, flags;
+    uint64_t thr;        // POISSON: floor(rate*dt*2^32) (2^32 = always)
+    float k_m;           // LIF_DELTA: fp32(1 - dt/tau_m)
+    float a_m;           // LIF_CUBA:  fp32(dt/tau_m)
+    float d_e, d_i;      // LIF_CUBA:  fp32(exp(-dt/tau_e)), fp32(exp(-dt/tau_i))
+    float v_th, v_reset, v_rest;
+    int32_t n_ref;       // refractory steps
+    float d_minus;       // PF_POST_PLASTIC: fp32(exp(-dt/tau_-)) of the x_post trace
+    int32_t stdp;        // PF_PRE_PLASTIC: index into NetDev::stdp, else -1
+    int32_t rcpt_uniform;// receptor used by every projection out of this pop (-1: mixed)
+};
+
+struct StdpDev {
+    uint32_t dst_pop;
+    float a_plus, a_minus, w_max;
+    float dplus[kHistBits + 1];   // fp32(exp(-n dt / tau_+)), n = 0..64 (closed-form skip-ahead)
+};
+
+struct NetDev {
+    uint32_t N;          // neurons
+    uint32_t R;          // neurons [0, R) may receive synapses (slice domain)
+    uint32_t tgt_lo, tgt_hi;  // this rank's target range
+    uint32_t C, log2C, nslices;   // slice width and number of local slices
+    uint32_t nwords;     // 32-bit words per ring slot = ceil(N/32)
+    uint32_t D;          // delay
+    uint32_t npop, nstdp;
+    int32_t F;           // fixed-point fraction bits
+    float scale, inv_scale;       // 2^F, 2^-F
+    uint32_t key0, key1;          // Philox key
+    uint32_t nrcpt;      // accumulator arrays in use (1 or 2)
+    PopDev pop[kMaxPops];
+    int8_t rcpt[kMaxPops][kMaxPops];   // receptor of projection (src, dst), -1 = none
+    StdpDev stdp[4];
+    // plastic source rows: concatenation of the PF_PRE_PLASTIC populations
+    uint32_t n_plastic_rows;
+};
+
+// Tables of the graph builder (per (src pop, dst pop) projection).
+struct BuildTabs {
+    uint64_t thr[kMaxPops * kMaxPops];     // Bernoulli thresholds floor(p 2^32), 0 = none
+    uint8_t autapse[kMaxPops * kMaxPops];
+    float weight[kMaxPops * kMaxPops];     // initial (final, caller-scaled) weight
+};
+
+struct Counters {
+    int64_t t;               // next step to simulate
+    uint32_t nA, nV;         // arrivals / plastic row visits of the current step
+    uint32_t ticket;         // CTA-completion ticket of the delivery kernel
+    uint32_t pad;
+    unsigned long long metric[8];
+};
+
+struct StateDev {
+    // neurons (indexed by global id)
+    float *V, *ge, *gi, *xpost;
+    int32_t *ref, *in_e, *in_i;
+    uint64_t *hist;
+    uint32_t *nspk;
+    uint32_t *ring;          // [kRingSlots][nwords]
+    // source rows
+    float *xpre;
+    int32_t *tlu;
+    // graph (this rank's target range)
+    int64_t *row_ptr;        // [N+1]
+    uint32_t *idx;           // [S + pad]
+    float *w;                // [S + pad]
+    uint32_t *piv;           // [N][nslices+1], row-relative
+    uint2 *seg;              // [N] plastic segment (lo, hi), row-relative
+    // work lists
+    uint32_t *arr_list, *visit_list;
+    Counters *ctr;
+};
+
+__host__ __device__ inline int find_pop(const NetDev &net, uint32_t i) {
+    int p = 0;
+#pragma unroll 1
+    for (int k = 1; k < (int)net.npop; k++)
+        if (i >= net.pop[k].base) p = k;
+    return p;
+}
+
+}  // namespace snn

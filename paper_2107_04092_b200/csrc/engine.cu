@@ -1,0 +1,582 @@
+// engine.cu -- libsnn.so: the C ABI of include/snn.h, the per-handle state, the
+// setup (graph construction) and the step orchestration:
+//   per step t:  k_neuron -> k_worklist -> k_stdp (if plastic) -> k_deliver
+// replayed from a captured CUDA graph of kGraphSteps steps.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/snn.h"
+#include "common.cuh"
+
+namespace snn {
+cudaError_t build_count(const NetDev &, const BuildTabs &, uint32_t *, cudaStream_t);
+cudaError_t build_scan(const NetDev &, uint32_t *, int64_t *, int64_t *, void *, size_t *, cudaStream_t);
+cudaError_t build_fill(const NetDev &, const BuildTabs &, const uint32_t *, const int64_t *, uint32_t *,
+                       float *, cudaStream_t);
+cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, uint2 *, cudaStream_t);
+cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
+cudaError_t launch_neuron(const NetDev &, const StateDev &, uint32_t, uint32_t, cudaStream_t);
+cudaError_t launch_worklist(const NetDev &, const StateDev &, uint32_t, uint32_t, cudaStream_t);
+cudaError_t launch_stdp(const NetDev &, const StateDev &, uint32_t, cudaStream_t);
+cudaError_t launch_stdp_fixed(const NetDev &, const StateDev &, int64_t, uint32_t, cudaStream_t);
+cudaError_t launch_flush_list(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t *,
+                              cudaStream_t);
+size_t deliver_smem_bytes(const NetDev &);
+cudaError_t deliver_configure(const NetDev &);
+cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t);
+cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
+}  // namespace snn
+
+using namespace snn;
+
+namespace {
+
+constexpr uint32_t kGraphSteps = 16;
+std::string g_create_error;
+
+struct HostPop {
+    snn_pop_params prm;
+    uint32_t base, n;
+};
+struct HostProj {
+    uint32_t src, dst;
+    snn_syn_params prm;
+};
+
+}  // namespace
+
+struct snn_sim {
+    snn_config cfg{};
+    std::string err;
+    int state = 0;  // 0 CONFIG, 1 FINALIZED
+    std::vector<HostPop> pops;
+    std::vector<HostProj> projs;
+    NetDev net{};
+    StateDev st{};
+    uint32_t N = 0;
+    int64_t nsyn = 0;
+    int64_t t = 0;  // steps enqueued so far
+    cudaStream_t stream = nullptr, cap_stream = nullptr;
+    cudaGraphExec_t g_many = nullptr, g_one = nullptr;
+    std::vector<void *> allocs;
+    uint32_t pl_lo = 0, pl_hi = 0;
+    uint32_t stdp_grid = 0, deliver_splits = 1;
+    bool plastic = false;
+    uint32_t *d_scratch_u32 = nullptr;
+    uint64_t *d_hist_tmp = nullptr;
+    // phase timing
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::vector<cudaEvent_t>> ev_steps;  // per step: 5 boundary events
+    size_t ev_used = 0;
+    double phase_ms[8] = {0};
+
+    snn_status fail(snn_status code, const char *fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        return code;
+    }
+    void *dalloc(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        bytes = (bytes + 255) & ~(size_t)255;
+        void *p = nullptr;
+        if (cfg.dev_alloc) {
+            p = cfg.dev_alloc(bytes, (void *)stream, cfg.alloc_ctx);
+        } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        if (p) allocs.push_back(p);
+        return p;
+    }
+};
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return sim->fail(SNN_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                             __FILE__, __LINE__);                                             \
+    } while (0)
+
+#define ALLOC(ptr, type, count)                                                            \
+    do {                                                                                   \
+        ptr = (type *)sim->dalloc(sizeof(type) * (size_t)(count));                         \
+        if (!ptr) return sim->fail(SNN_E_OOM, "device allocation of %zu bytes failed",     \
+                                   sizeof(type) * (size_t)(count));                        \
+    } while (0)
+
+static uint64_t bernoulli_thr(double p) {
+    if (!(p > 0.0)) return 0;
+    if (p >= 1.0) return 1ull << 32;
+    return (uint64_t)std::floor(p * 4294967296.0);
+}
+
+// --------------------------------------------------------------------- setup
+static snn_status finalize(snn_sim *sim) {
+    const snn_config &cfg = sim->cfg;
+    if (sim->pops.empty()) return sim->fail(SNN_E_INVALID, "no populations");
+    NetDev &net = sim->net;
+    memset(&net, 0, sizeof net);
+    const double dt = cfg.dt_ms;
+    net.npop = (uint32_t)sim->pops.size();
+    net.N = sim->N;
+    net.D = cfg.delay_steps;
+    net.F = cfg.accum_frac_bits;
+    net.scale = std::ldexp(1.0f, net.F);
+    net.inv_scale = std::ldexp(1.0f, -net.F);
+    net.key0 = (uint32_t)(cfg.seed & 0xffffffffu);
+    net.key1 = (uint32_t)(cfg.seed >> 32);
+    for (int a = 0; a < kMaxPops; a++)
+        for (int b = 0; b < kMaxPops; b++) net.rcpt[a][b] = -1;
+    BuildTabs tabs;
+    memset(&tabs, 0, sizeof tabs);
+    uint32_t R = 0;
+    for (uint32_t k = 0; k < net.npop; k++) {
+        const HostPop &hp = sim->pops[k];
+        PopDev &p = net.pop[k];
+        p.base = hp.base;
+        p.n = hp.n;
+        p.kind = hp.prm.kind;
+        p.stdp = -1;
+        p.rcpt_uniform = -2;  // unset
+        p.thr = bernoulli_thr((double)hp.prm.rate_hz * 1e-3 * dt);
+        p.k_m = (float)(1.0 - dt / (double)hp.prm.tau_m_ms);
+        p.a_m = (float)(dt / (double)hp.prm.tau_m_ms);
+        p.d_e = (float)std::exp(-dt / (double)hp.prm.tau_e_ms);
+        p.d_i = (float)std::exp(-dt / (double)hp.prm.tau_i_ms);
+        p.v_th = hp.prm.v_th_mv;
+        p.v_reset = hp.prm.v_reset_mv;
+        p.v_rest = hp.prm.v_rest_mv;
+        p.n_ref = (int32_t)std::llround((double)hp.prm.tau_ref_ms / dt);
+    }
+    // projections
+    double acc_bound[kMaxPops][2] = {{0}};
+    for (const HostProj &hj : sim->projs) {
+        const snn_syn_params &q = hj.prm;
+        PopDev &sp = net.pop[hj.src];
+        PopDev &dp = net.pop[hj.dst];
+        net.rcpt[hj.src][hj.dst] = (int8_t)q.receptor;
+        sp.rcpt_uniform = (sp.rcpt_uniform == -2 || sp.rcpt_uniform == (int32_t)q.receptor) ? (int32_t)q.receptor : -1;
+        dp.flags |= PF_HAS_INPUT;
+        R = std::max(R, dp.base + dp.n);
+        tabs.thr[hj.src * kMaxPops + hj.dst] = bernoulli_thr(q.p);
+        tabs.autapse[hj.src * kMaxPops + hj.dst] = q.allow_autapses ? 1 : 0;
+        tabs.weight[hj.src * kMaxPops + hj.dst] = q.weight;
+        double wabs = std::fabs((double)q.weight);
+        if (q.kind == SNN_SYN_STDP) {
+            if (net.nstdp >= 4) return sim->fail(SNN_E_UNSUPPORTED, "at most 4 STDP projections");
+            StdpDev &sd = net.stdp[net.nstdp];
+            sd.dst_pop = hj.dst;
+            sd.a_plus = q.a_plus;
+            sd.a_minus = q.a_minus;
+            sd.w_max = q.w_max;
+            for (int n = 0; n <= kHistBits; n++) sd.dplus[n] = (float)std::exp(-(double)n * dt / (double)q.tau_plus_ms);
+            const float dm = (float)std::exp(-dt / (double)q.tau_minus_ms);
+            if ((dp.flags & PF_POST_PLASTIC) && dp.d_minus != dm)
+                return sim->fail(SNN_E_UNSUPPORTED, "STDP projections into one population must share tau_minus");
+            dp.flags |= PF_POST_PLASTIC;
+            dp.d_minus = dm;
+            sp.flags |= PF_PRE_PLASTIC;
+            sp.stdp = (int32_t)net.nstdp++;
+            wabs = std::max(wabs, std::fabs((double)q.w_max));
+        }
+        // fixed-point overflow bound (R18): expected in-degree + 10 sigma
+        const double k = q.p * (double)sim->pops[hj.src].n;
+        const double kmax = std::min((double)sim->pops[hj.src].n, k + 10.0 * std::sqrt(k) + 10.0);
+        acc_bound[hj.dst][q.receptor] += kmax * std::ldexp(wabs, net.F);
+    }
+    for (uint32_t k = 0; k < net.npop; k++) {
+        if (net.pop[k].rcpt_uniform == -2) net.pop[k].rcpt_uniform = 0;
+        for (int r = 0; r < 2; r++)
+            if (acc_bound[k][r] >= 2147483647.0)
+                return sim->fail(SNN_E_INVALID,
+                                 "fixed-point overflow bound: population %u receptor %d may reach %.3g >= 2^31 "
+                                 "(lower accum_frac_bits)", k, r, acc_bound[k][r]);
+    }
+    net.nrcpt = 1;
+    for (const HostProj &hj : sim->projs)
+        if (hj.prm.receptor == SNN_RCPT_INH) net.nrcpt = 2;
+    net.R = R;
+    if (cfg.world > 1) return sim->fail(SNN_E_UNSUPPORTED, "world > 1 not available in this build");
+    net.tgt_lo = 0;
+    net.tgt_hi = R;
+    uint32_t C = cfg.slice_width ? cfg.slice_width : 1024u;
+    net.C = C;
+    net.log2C = 0;
+    while ((1u << net.log2C) < C) net.log2C++;
+    net.nslices = (net.tgt_hi - net.tgt_lo + C - 1) / C;
+    net.nwords = (net.N + 31) / 32;
+    // plastic source rows
+    sim->pl_lo = net.N;
+    sim->pl_hi = 0;
+    for (uint32_t k = 0; k < net.npop; k++)
+        if (net.pop[k].flags & PF_PRE_PLASTIC) {
+            sim->pl_lo = std::min(sim->pl_lo, net.pop[k].base);
+            sim->pl_hi = std::max(sim->pl_hi, net.pop[k].base + net.pop[k].n);
+        }
+    sim->plastic = sim->pl_hi > sim->pl_lo;
+    if (!sim->plastic) sim->pl_lo = sim->pl_hi = 0;
+    net.n_plastic_rows = sim->pl_hi - sim->pl_lo;
+
+    // ---- device buffers
+    const uint32_t N = net.N;
+    StateDev &st = sim->st;
+    ALLOC(st.V, float, N);
+    ALLOC(st.ge, float, N);
+    ALLOC(st.gi, float, N);
+    ALLOC(st.xpost, float, N);
+    ALLOC(st.ref, int32_t, N);
+    ALLOC(st.in_e, int32_t, N);
+    ALLOC(st.in_i, int32_t, N);
+    ALLOC(st.hist, uint64_t, N);
+    ALLOC(st.nspk, uint32_t, N);
+    ALLOC(st.ring, uint32_t, (size_t)kRingSlots * net.nwords);
+    ALLOC(st.xpre, float, N);
+    ALLOC(st.tlu, int32_t, N);
+    ALLOC(st.row_ptr, int64_t, (size_t)N + 1);
+    ALLOC(st.piv, uint32_t, (size_t)N * (net.nslices + 1));
+    ALLOC(st.seg, uint2, N);
+    ALLOC(st.arr_list, uint32_t, N);
+    ALLOC(st.visit_list, uint32_t, N);
+    ALLOC(st.ctr, Counters, 1);
+    ALLOC(sim->d_scratch_u32, uint32_t, 4);
+    cudaStream_t s = sim->stream;
+    CK(cudaMemsetAsync(st.ring, 0, sizeof(uint32_t) * (size_t)kRingSlots * net.nwords, s));
+    CK(cudaMemsetAsync(st.ctr, 0, sizeof(Counters), s));
+
+    // ---- graph (count -> pivots/row_ptr -> fill)
+    int64_t *len = nullptr;
+    ALLOC(len, int64_t, (size_t)N + 1);
+    CK(cudaMemsetAsync(len + N, 0, sizeof(int64_t), s));
+    CK(build_count(net, tabs, st.piv, s));
+    size_t tmp_bytes = 0;
+    CK(build_scan(net, st.piv, len, st.row_ptr, nullptr, &tmp_bytes, s));
+    void *tmp = sim->dalloc(tmp_bytes);
+    if (!tmp) return sim->fail(SNN_E_OOM, "scan scratch");
+    CK(build_scan(net, st.piv, len, st.row_ptr, tmp, &tmp_bytes, s));
+    CK(cudaMemcpyAsync(&sim->nsyn, st.row_ptr + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ALLOC(st.idx, uint32_t, (size_t)sim->nsyn + 8);
+    ALLOC(st.w, float, (size_t)sim->nsyn + 8);
+    CK(cudaMemsetAsync(st.idx + sim->nsyn, 0, 8 * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(st.w + sim->nsyn, 0, 8 * sizeof(float), s));
+    CK(build_fill(net, tabs, st.piv, st.row_ptr, st.idx, st.w, s));
+    CK(build_segments(net, st.row_ptr, st.idx, st.seg, s));
+    CK(init_state(net, st, s));
+
+    // ---- launch shapes
+    CK(deliver_configure(net));
+    const uint32_t target_ctas = 2 * 148;
+    sim->deliver_splits = std::max(1u, (target_ctas + std::max(1u, net.nslices) - 1) / std::max(1u, net.nslices));
+    sim->deliver_splits = std::min(sim->deliver_splits, 16u);
+    sim->stdp_grid = 148 * 8;
+    CK(cudaStreamSynchronize(s));
+    sim->state = 1;
+    return SNN_OK;
+}
+
+// ---------------------------------------------------------------- the step
+static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev) {
+    const NetDev &net = sim->net;
+    const StateDev &st = sim->st;
+    if (ev) CK(cudaEventRecord(ev[0], s));
+    CK(launch_neuron(net, st, 0, net.N, s));                        // (1) P:36
+    if (ev) CK(cudaEventRecord(ev[1], s));
+    CK(launch_worklist(net, st, sim->pl_lo, sim->pl_hi, s));        // A(t), A(t) u F(t)
+    if (ev) CK(cudaEventRecord(ev[2], s));
+    if (sim->plastic) CK(launch_stdp(net, st, sim->stdp_grid, s));  // (2) P:37-39
+    if (ev) CK(cudaEventRecord(ev[3], s));
+    CK(launch_deliver(net, st, sim->deliver_splits, s));           // (3) P:41
+    if (ev) CK(cudaEventRecord(ev[4], s));
+    return SNN_OK;
+}
+
+static snn_status capture(snn_sim *sim, uint32_t nsteps, cudaGraphExec_t *out) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(sim->cap_stream, cudaStreamCaptureModeThreadLocal));
+    for (uint32_t k = 0; k < nsteps; k++) {
+        snn_status r = enqueue_step(sim, sim->cap_stream, nullptr);
+        if (r != SNN_OK) {
+            cudaStreamEndCapture(sim->cap_stream, &g);
+            if (g) cudaGraphDestroy(g);
+            return r;
+        }
+    }
+    CK(cudaStreamEndCapture(sim->cap_stream, &g));
+    CK(cudaGraphInstantiate(out, g, 0));
+    CK(cudaGraphDestroy(g));
+    return SNN_OK;
+}
+
+extern "C" {
+
+uint32_t snn_abi_version(void) { return SNN_ABI_VERSION; }
+
+const char *snn_last_error(const snn_sim *sim) {
+    return sim ? sim->err.c_str() : g_create_error.c_str();
+}
+
+snn_status snn_create(const snn_config *cfg, snn_sim **out) {
+    if (!out) return SNN_E_INVALID;
+    *out = nullptr;
+    g_create_error.clear();
+    if (!cfg || cfg->abi_version != SNN_ABI_VERSION || cfg->struct_size != sizeof(snn_config)) {
+        g_create_error = "snn_config: ABI version / struct size mismatch";
+        return SNN_E_INVALID;
+    }
+    if (!(cfg->dt_ms > 0.0f) || cfg->history_bits != 64 || cfg->delay_steps >= 64 ||
+        cfg->accum_frac_bits < 0 || cfg->accum_frac_bits > 30 || cfg->world < 1 || cfg->rank < 0 ||
+        cfg->rank >= cfg->world) {
+        g_create_error = "snn_config: need dt > 0, history_bits == 64, delay < 64, 0 <= F <= 30, 0 <= rank < world";
+        return SNN_E_INVALID;
+    }
+    const uint32_t C = cfg->slice_width;
+    if (C != 0 && (C < 32 || C > 32768 || (C & (C - 1)) != 0)) {
+        g_create_error = "snn_config: slice_width must be 0 or a power of two in [32, 32768]";
+        return SNN_E_INVALID;
+    }
+    if ((cfg->dev_alloc == nullptr) != (cfg->dev_free == nullptr)) {
+        g_create_error = "snn_config: dev_alloc and dev_free must both be set or both NULL";
+        return SNN_E_INVALID;
+    }
+    if (cfg->world > 1) {
+        g_create_error = "world > 1 not available in this build";
+        return SNN_E_UNSUPPORTED;
+    }
+    cudaError_t e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) {
+        g_create_error = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+        return SNN_E_CUDA;
+    }
+    snn_sim *sim = new snn_sim();
+    sim->cfg = *cfg;
+    sim->stream = (cudaStream_t)cfg->stream;
+    e = cudaStreamCreateWithFlags(&sim->cap_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        g_create_error = std::string("cudaStreamCreate: ") + cudaGetErrorString(e);
+        delete sim;
+        return SNN_E_CUDA;
+    }
+    *out = sim;
+    return SNN_OK;
+}
+
+snn_status snn_add_population(snn_sim *sim, uint32_t n, const snn_pop_params *prm, uint32_t *pop_id) {
+    if (!sim) return SNN_E_INVALID;
+    sim->err.clear();
+    if (sim->state != 0) return sim->fail(SNN_E_STATE, "add_population after finalize");
+    if (!prm || prm->struct_size != sizeof(snn_pop_params)) return sim->fail(SNN_E_INVALID, "snn_pop_params size");
+    if (n == 0) return sim->fail(SNN_E_INVALID, "population size must be > 0");
+    if (prm->kind > SNN_POP_LIF_CUBA) return sim->fail(SNN_E_INVALID, "unknown population kind %u", prm->kind);
+    if (sim->pops.size() >= (size_t)kMaxPops) return sim->fail(SNN_E_UNSUPPORTED, "at most %d populations", kMaxPops);
+    if ((uint64_t)sim->N + n >= 0x7fffffffull) return sim->fail(SNN_E_INVALID, "too many neurons");
+    if (prm->kind != SNN_POP_POISSON) {
+        if (!(prm->tau_m_ms > 0.0f) || !(prm->tau_ref_ms >= 0.0f))
+            return sim->fail(SNN_E_INVALID, "tau_m must be > 0 and tau_ref >= 0");
+        if (prm->kind == SNN_POP_LIF_CUBA && !(prm->tau_e_ms > 0.0f && prm->tau_i_ms > 0.0f))
+            return sim->fail(SNN_E_INVALID, "CUBA needs tau_e, tau_i > 0");
+    } else if (!(prm->rate_hz >= 0.0f)) {
+        return sim->fail(SNN_E_INVALID, "rate must be >= 0");
+    }
+    HostPop hp;
+    hp.prm = *prm;
+    hp.base = sim->N;
+    hp.n = n;
+    sim->pops.push_back(hp);
+    sim->N += n;
+    if (pop_id) *pop_id = (uint32_t)sim->pops.size() - 1;
+    return SNN_OK;
+}
+
+snn_status snn_connect(snn_sim *sim, uint32_t src, uint32_t dst, const snn_syn_params *q) {
+    if (!sim) return SNN_E_INVALID;
+    sim->err.clear();
+    if (sim->state != 0) return sim->fail(SNN_E_STATE, "connect after finalize");
+    if (!q || q->struct_size != sizeof(snn_syn_params)) return sim->fail(SNN_E_INVALID, "snn_syn_params size");
+    if (src >= sim->pops.size() || dst >= sim->pops.size()) return sim->fail(SNN_E_INVALID, "unknown population");
+    if (!(q->p >= 0.0 && q->p <= 1.0)) return sim->fail(SNN_E_INVALID, "p must be in [0, 1]");
+    if (q->kind > SNN_SYN_STDP || q->receptor > SNN_RCPT_INH) return sim->fail(SNN_E_INVALID, "bad kind / receptor");
+    const uint32_t dk = sim->pops[dst].prm.kind;
+    if (dk == SNN_POP_POISSON) return sim->fail(SNN_E_INVALID, "POISSON populations take no input");
+    if (dk == SNN_POP_LIF_DELTA && q->receptor != SNN_RCPT_EXC)
+        return sim->fail(SNN_E_INVALID, "LIF_DELTA has a single (EXC) receptor; use a signed weight");
+    for (const HostProj &hj : sim->projs) {
+        if (hj.src == src && hj.dst == dst) return sim->fail(SNN_E_INVALID, "duplicate projection");
+        if (q->kind == SNN_SYN_STDP && hj.src == src && hj.prm.kind == SNN_SYN_STDP)
+            return sim->fail(SNN_E_UNSUPPORTED, "one STDP projection per source population");
+    }
+    if (q->kind == SNN_SYN_STDP &&
+        !(q->tau_plus_ms > 0.0f && q->tau_minus_ms > 0.0f && q->w_max >= 0.0f && q->weight >= 0.0f))
+        return sim->fail(SNN_E_INVALID, "STDP needs tau_+, tau_- > 0 and 0 <= weight, w_max");
+    HostProj hj;
+    hj.src = src;
+    hj.dst = dst;
+    hj.prm = *q;
+    sim->projs.push_back(hj);
+    return SNN_OK;
+}
+
+snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
+    if (!sim) return SNN_E_INVALID;
+    sim->err.clear();
+    if (sim->state == 0) {
+        snn_status r = finalize(sim);
+        if (r != SNN_OK) return r;
+    }
+    if (n_steps == 0) return SNN_OK;
+    const bool timing = (sim->cfg.flags & SNN_FLAG_PHASE_TIMING) != 0;
+    const bool direct = timing || (sim->cfg.flags & SNN_FLAG_NO_GRAPH) != 0;
+    if (direct) {
+        for (uint32_t k = 0; k < n_steps; k++) {
+            cudaEvent_t *ev = nullptr;
+            if (timing) {
+                if (sim->ev_used == sim->ev_steps.size()) {
+                    std::vector<cudaEvent_t> v(5);
+                    for (auto &e : v) CK(cudaEventCreate(&e));
+                    sim->ev_steps.push_back(v);
+                }
+                ev = sim->ev_steps[sim->ev_used++].data();
+            }
+            snn_status r = enqueue_step(sim, sim->stream, ev);
+            if (r != SNN_OK) return r;
+            sim->t++;
+        }
+        return SNN_OK;
+    }
+    if (!sim->g_many) {
+        snn_status r = capture(sim, kGraphSteps, &sim->g_many);
+        if (r != SNN_OK) return r;
+        r = capture(sim, 1, &sim->g_one);
+        if (r != SNN_OK) return r;
+    }
+    uint32_t k = 0;
+    for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(sim->g_many, sim->stream));
+    for (; k < n_steps; k++) CK(cudaGraphLaunch(sim->g_one, sim->stream));
+    sim->t += n_steps;
+    return SNN_OK;
+}
+
+// Read-out flush (R11): bring every stale plastic row up to t_last, no pre spike.
+static snn_status readout_flush(snn_sim *sim) {
+    if (!sim->plastic || sim->t == 0) return SNN_OK;
+    const int64_t t_last = sim->t - 1;
+    cudaStream_t s = sim->stream;
+    CK(cudaMemsetAsync(sim->d_scratch_u32, 0, sizeof(uint32_t), s));
+    CK(launch_flush_list(sim->net, sim->st, t_last, sim->pl_lo, sim->pl_hi, sim->d_scratch_u32, s));
+    uint32_t n = 0;
+    CK(cudaMemcpyAsync(&n, sim->d_scratch_u32, sizeof n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(launch_stdp_fixed(sim->net, sim->st, t_last, n, s));
+    return SNN_OK;
+}
+
+snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *host_dst, size_t dst_bytes,
+                          size_t *needed) {
+    if (!sim) return SNN_E_INVALID;
+    sim->err.clear();
+    if (field >= SNN_FIELD_COUNT) return sim->fail(SNN_E_INVALID, "unknown field %u", field);
+    if (sim->state == 0 && field != SNN_FIELD_STEP) return sim->fail(SNN_E_STATE, "read_state before finalize");
+    const NetDev &net = sim->net;
+    const StateDev &st = sim->st;
+    uint32_t base = 0, n = sim->N;
+    if (pop_id != 0xffffffffu) {
+        if (pop_id >= sim->pops.size()) return sim->fail(SNN_E_INVALID, "unknown population %u", pop_id);
+        base = sim->pops[pop_id].base;
+        n = sim->pops[pop_id].n;
+    }
+    const void *src = nullptr;
+    size_t bytes = 0;
+    int64_t host_i64[8];
+    unsigned long long host_u64[8];
+    double host_f64[8];
+    const void *host_src = nullptr;
+    switch (field) {
+    case SNN_FIELD_V: src = st.V + base; bytes = 4ull * n; break;
+    case SNN_FIELD_REFRACTORY: src = st.ref + base; bytes = 4ull * n; break;
+    case SNN_FIELD_G_EXC: src = st.ge + base; bytes = 4ull * n; break;
+    case SNN_FIELD_G_INH: src = st.gi + base; bytes = 4ull * n; break;
+    case SNN_FIELD_INPUT_EXC: src = st.in_e + base; bytes = 4ull * n; break;
+    case SNN_FIELD_INPUT_INH: src = st.in_i + base; bytes = 4ull * n; break;
+    case SNN_FIELD_SPIKE_COUNT: src = st.nspk + base; bytes = 4ull * n; break;
+    case SNN_FIELD_XPOST: src = st.xpost + base; bytes = 4ull * n; break;
+    case SNN_FIELD_XPRE_ROW: src = st.xpre + base; bytes = 4ull * n; break;
+    case SNN_FIELD_TLU: src = st.tlu + base; bytes = 4ull * n; break;
+    case SNN_FIELD_HIST: bytes = 8ull * n; break;
+    case SNN_FIELD_ROW_PTR: src = st.row_ptr; bytes = 8ull * (sim->N + 1); break;
+    case SNN_FIELD_IDX: src = st.idx; bytes = 4ull * sim->nsyn; break;
+    case SNN_FIELD_WEIGHTS: src = st.w; bytes = 4ull * sim->nsyn; break;
+    case SNN_FIELD_PIVOTS: src = st.piv; bytes = 4ull * sim->N * (net.nslices + 1); break;
+    case SNN_FIELD_SPIKE_RING: src = st.ring; bytes = 4ull * kRingSlots * net.nwords; break;
+    case SNN_FIELD_STEP: host_i64[0] = sim->t; host_src = host_i64; bytes = 8; break;
+    case SNN_FIELD_METRICS: src = st.ctr->metric; bytes = 8 * 8; break;
+    case SNN_FIELD_PHASE_TIMES: bytes = 8 * 8; break;
+    case SNN_FIELD_INFO:
+        host_i64[0] = sim->N; host_i64[1] = sim->nsyn; host_i64[2] = net.nslices; host_i64[3] = net.C;
+        host_i64[4] = net.R; host_i64[5] = net.tgt_lo; host_i64[6] = net.tgt_hi;
+        host_i64[7] = (int64_t)4 * sim->N * (net.nslices + 1);
+        host_src = host_i64; bytes = 64; break;
+    default: return sim->fail(SNN_E_INVALID, "unknown field %u", field);
+    }
+    if (needed) *needed = bytes;
+    if (!host_dst) return SNN_OK;
+    if (dst_bytes < bytes) return sim->fail(SNN_E_INVALID, "buffer of %zu bytes < %zu needed", dst_bytes, bytes);
+    cudaStream_t s = sim->stream;
+    if (field == SNN_FIELD_WEIGHTS || field == SNN_FIELD_XPRE_ROW || field == SNN_FIELD_TLU) {
+        snn_status r = readout_flush(sim);
+        if (r != SNN_OK) return r;
+    }
+    if (field == SNN_FIELD_HIST) {
+        if (!sim->d_hist_tmp) {
+            sim->d_hist_tmp = (uint64_t *)sim->dalloc(8ull * sim->N);
+            if (!sim->d_hist_tmp) return sim->fail(SNN_E_OOM, "hist scratch");
+        }
+        CK(launch_hist_from_ring(net, st.ring, sim->t - 1, sim->d_hist_tmp, s));
+        src = sim->d_hist_tmp + base;
+    }
+    if (field == SNN_FIELD_PHASE_TIMES) {
+        CK(cudaStreamSynchronize(s));
+        for (size_t k = 0; k < sim->ev_used; k++) {
+            float ms[4];
+            for (int p = 0; p < 4; p++) CK(cudaEventElapsedTime(&ms[p], sim->ev_steps[k][p], sim->ev_steps[k][p + 1]));
+            for (int p = 0; p < 4; p++) sim->phase_ms[p == 3 ? SNN_PHASE_DELIVERY : p] += ms[p];
+            sim->phase_ms[SNN_PHASE_TOTAL] += ms[0] + ms[1] + ms[2] + ms[3];
+        }
+        sim->ev_used = 0;
+        for (int k = 0; k < 8; k++) host_f64[k] = sim->phase_ms[k];
+        host_src = host_f64;
+    }
+    (void)host_u64;
+    if (host_src) {
+        memcpy(host_dst, host_src, bytes);
+        return SNN_OK;
+    }
+    if (bytes) CK(cudaMemcpyAsync(host_dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return SNN_OK;
+}
+
+void snn_destroy(snn_sim *sim) {
+    if (!sim) return;
+    if (sim->stream) cudaStreamSynchronize(sim->stream);
+    cudaDeviceSynchronize();
+    if (sim->g_many) cudaGraphExecDestroy(sim->g_many);
+    if (sim->g_one) cudaGraphExecDestroy(sim->g_one);
+    for (auto &v : sim->ev_steps)
+        for (auto e : v) cudaEventDestroy(e);
+    for (void *p : sim->allocs) {
+        if (sim->cfg.dev_free) sim->cfg.dev_free(p, (void *)sim->stream, sim->cfg.alloc_ctx);
+        else cudaFree(p);
+    }
+    if (sim->cap_stream) cudaStreamDestroy(sim->cap_stream);
+    delete sim;
+}
+
+}  // extern "C"

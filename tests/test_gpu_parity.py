@@ -1,0 +1,228 @@
+"""GPU <-> oracle parity through the C ABI (BASELINE.json north_star bars):
+connectivity, pivots, spike rasters / bitfields bit-exact; V bit-exact for
+static networks (every op identical, integer accumulation); weights and V
+within 1e-4 relative for Brunel+ (DESIGN.md section 5 derives the tolerance)."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(rc, slice_width=0, flags=0):
+    from paper_2107_04092_b200 import Snn
+    g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=slice_width, flags=flags)
+    rc.apply(g)
+    g.finalize()
+    o = O.Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, threads=8)
+    rc.apply(o)
+    o.finalize()
+    return g, o
+
+
+def _check_graph(g, o):
+    assert np.array_equal(g.read_state("ROW_PTR"), o.array("row_ptr"))
+    assert np.array_equal(g.read_state("IDX"), o.array("idx"))
+    assert np.array_equal(g.read_state("WEIGHTS"), o.array("w"))
+    info = g.info()
+    P = info["nslices"] + 1
+    piv = g.read_state("PIVOTS").reshape(-1, P)
+    rp, idx = o.array("row_ptr"), o.array("idx")
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([[0, o.n - 1], rng.integers(0, o.n, 200)]))
+    for i in rows:
+        ref = O.pivots(idx[rp[i]:rp[i + 1]], info["tgt_lo"], info["C"], info["nslices"])
+        assert np.array_equal(piv[i].astype(np.int64), ref), f"pivots of row {i}"
+
+
+# ------------------------------------------------------------------ graph
+@pytest.mark.parametrize("C", [32, 256, 1024])
+def test_connectivity_and_pivots_bit_exact(C):
+    rc = W.brunel(6000, p=0.05, plastic=True, seed=2)
+    g, o = _pair(rc, slice_width=C)
+    _check_graph(g, o)
+
+
+def test_initial_state_bit_exact():
+    rc = W.vogels(4000, seed=5)
+    g, o = _pair(rc)
+    assert np.array_equal(g.read_state("V"), o.array("V"))
+    assert np.all(g.read_state("TLU") == -1)
+
+
+# ------------------------------------------------------------- dynamics
+def _run_compare(g, o, steps, exact_v=True, every=1):
+    for t in range(steps):
+        g.step(1)
+        o.step(1)
+        if t % every and t != steps - 1:
+            continue
+        hg, ho = g.read_state("HIST"), o.array("hist")
+        assert np.array_equal(hg, ho), f"raster / bitfields differ at step {t}: {np.flatnonzero(hg != ho)[:10]}"
+        vg, vo = g.read_state("V"), o.array("V")
+        if exact_v:
+            assert np.array_equal(vg, vo), f"V differs at step {t}"
+            assert np.array_equal(g.read_state("INPUT_EXC"), o.array("in_e"))
+            assert np.array_equal(g.read_state("INPUT_INH"), o.array("in_i"))
+        else:
+            assert np.allclose(vg, vo, rtol=1e-4, atol=1e-4)
+
+
+def test_vogels_cfg1_raster_and_state_bit_exact_300_steps():
+    """BASELINE config 1 (Vogels-Abbott 4,000, p = 0.02, D = 0)."""
+    rc = W.config(1)
+    g, o = _pair(rc)
+    _run_compare(g, o, 300)
+    assert np.array_equal(g.read_state("G_EXC"), o.array("ge"))
+    assert np.array_equal(g.read_state("G_INH"), o.array("gi"))
+    assert np.array_equal(g.read_state("REFRACTORY"), o.array("ref"))
+    assert g.read_state("SPIKE_COUNT").sum() > 0
+
+
+@pytest.mark.parametrize("C", [64, 1024])
+def test_brunel_static_bit_exact(C):
+    rc = W.brunel(12000, p=0.02, plastic=False, seed=4)
+    g, o = _pair(rc, slice_width=C)
+    _run_compare(g, o, 150, every=10)
+    assert g.metrics()["EVENTS"] == o.events
+
+
+def _compare_weights(g, o, rc):
+    wg, wo = g.read_state("WEIGHTS"), o.array("w")
+    wmax = rc.projs[4].stdp["w_max"]
+    err = np.abs(wg.astype(np.float64) - wo)
+    bad = err > 1e-4 * np.maximum(np.abs(wo), 1e-2 * wmax)
+    assert not bad.any(), f"{bad.sum()} weights off, max err {err.max():.3g}"
+    return err.max()
+
+
+@pytest.mark.parametrize("delay", [0, 15])
+def test_brunel_plus_stdp_parity(delay):
+    """Lazy+event STDP (GPU) vs naive STDP (oracle), 400 steps: forced flushes
+    at t = 63, 127, ... and arrivals both exercised; rasters bit-exact."""
+    rc = W.brunel(10000, p=0.05, plastic=True, delay=delay, seed=7)
+    g, o = _pair(rc, slice_width=512)
+    _run_compare(g, o, 400, exact_v=False, every=20)
+    _compare_weights(g, o, rc)
+    xp = g.read_state("XPRE_ROW")
+    rp, idx = o.array("row_ptr"), o.array("idx")
+    xo = o.array("xpre")
+    base_p = rc.pops[0].n + rc.pops[1].n
+    checked = 0
+    for i in range(base_p, base_p + 300):
+        if rp[i + 1] > rp[i] and idx[rp[i]] < rc.pops[0].n:   # row has a plastic (P->E) prefix
+            assert abs(xp[i] - xo[rp[i]]) <= 1e-4 * max(1.0, abs(xo[rp[i]]))
+            checked += 1
+    assert checked > 100
+    m = g.metrics()
+    assert m["FLUSH_ROWS"] > 0 and m["STDP_WTOUCH"] > 0
+
+
+def test_readout_flush_does_not_change_future():
+    """Reading weights mid-run (read-out flush, R11) does not change later
+    results: rasters identical, weights equal up to the rounding of splitting a
+    closed-form decay D+[a+b] into D+[a] D+[b] (relative 1e-5)."""
+    rc = W.brunel(6000, p=0.05, plastic=True, delay=3, seed=8)
+    g1, o = _pair(rc, slice_width=256)
+    from paper_2107_04092_b200 import Snn
+    g2 = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=256)
+    rc.apply(g2)
+    for t in range(200):
+        g1.step(1)
+        g2.step(1)
+        if t % 37 == 5:
+            g1.read_state("WEIGHTS")
+    assert np.array_equal(g1.read_state("HIST"), g2.read_state("HIST"))
+    assert np.allclose(g1.read_state("WEIGHTS"), g2.read_state("WEIGHTS"), rtol=1e-5, atol=0)
+
+
+def test_graph_replay_equals_direct_launches():
+    """CUDA-graph replay (default) == direct launches (SNN_FLAG_NO_GRAPH)."""
+    from paper_2107_04092_b200 import Snn, FLAG_NO_GRAPH
+    rc = W.brunel(8000, p=0.03, plastic=True, delay=15, seed=9)
+    a = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits)
+    b = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, flags=FLAG_NO_GRAPH)
+    rc.apply(a)
+    rc.apply(b)
+    a.step(100)
+    b.step(37)
+    b.step(63)
+    assert np.array_equal(a.read_state("SPIKE_RING"), b.read_state("SPIKE_RING"))
+    assert np.array_equal(a.read_state("WEIGHTS"), b.read_state("WEIGHTS"))
+    assert a.t == b.t == 100
+
+
+def test_from_shared_state_100_steps():
+    """North-star parity: GPU snapshot (after read-out flush) loaded into the
+    oracle, then 100 steps on both: rasters bit-exact, V / w within 1e-4."""
+    rc = W.brunel(10000, p=0.05, plastic=True, delay=15, seed=11)
+    g, o = _pair(rc, slice_width=1024)
+    g.step(250)
+    # snapshot -> oracle
+    for f, name in [("V", "V"), ("REFRACTORY", "ref"), ("G_EXC", "ge"), ("G_INH", "gi"),
+                    ("INPUT_EXC", "in_e"), ("INPUT_INH", "in_i"), ("HIST", "hist"), ("WEIGHTS", "w")]:
+        o.array(name)[:] = g.read_state(f)
+    xpre_row, xpost = g.read_state("XPRE_ROW"), g.read_state("XPOST")
+    rp, idx = o.array("row_ptr"), o.array("idx")
+    src = np.repeat(np.arange(o.n), np.diff(rp))
+    o.array("xpre")[:] = xpre_row[src]
+    o.array("xpost")[:] = xpost[idx]
+    o.t = g.t
+    _run_compare(g, o, 100, exact_v=False, every=10)
+    _compare_weights(g, o, rc)
+
+
+# ------------------------------------------------------------- edge cases
+def test_empty_and_degenerate_networks():
+    from paper_2107_04092_b200 import Snn
+    # p = 0: no synapses at all; Poisson-only network; single neuron
+    rc = W.brunel(3000, p=0.0, plastic=True, seed=1)
+    g, o = _pair(rc)
+    assert g.info()["S"] == 0
+    _run_compare(g, o, 80, every=10)
+    g = Snn(1, 0.1, 0, 20)
+    g.add_population(W.POISSON, 1000, rate_hz=100.0)
+    g.step(50)
+    assert g.read_state("SPIKE_COUNT").sum() > 0
+    g = Snn(1, 0.1, 0, 20)
+    a = g.add_population(W.LIF_DELTA, 1, tau_m=20.0, v_reset=10.0, v_th=20.0)
+    g.connect(a, a, W.STATIC, 0, 1.0, 0.5, autapses=True)
+    g.step(10)
+    assert g.info()["S"] == 1
+
+
+def test_ragged_tail_and_odd_sizes():
+    """N not a multiple of 32 or of C: ragged last slice and ring word."""
+    rc = W.brunel(5003, p=0.04, plastic=True, delay=2, seed=13)
+    g, o = _pair(rc, slice_width=128)
+    _check_graph(g, o)
+    _run_compare(g, o, 130, exact_v=False, every=13)
+    _compare_weights(g, o, rc)
+
+
+def test_invalid_arguments_rejected():
+    from paper_2107_04092_b200 import Snn, SnnError, SNN_E_INVALID, SNN_E_STATE
+    with pytest.raises(SnnError):
+        Snn(1, 0.1, 64, 20)                  # D >= H
+    with pytest.raises(SnnError):
+        Snn(1, 0.1, 0, 20, slice_width=1000)  # not a power of two
+    g = Snn(1, 0.1, 0, 20)
+    with pytest.raises(SnnError) as e:
+        g.add_population(W.LIF_DELTA, 0)
+    assert e.value.code == SNN_E_INVALID
+    a = g.add_population(W.LIF_DELTA, 10, v_th=20.0)
+    with pytest.raises(SnnError):
+        g.connect(a, a, W.STATIC, 0, 1.5, 0.1)
+    g.step(1)
+    with pytest.raises(SnnError) as e:
+        g.add_population(W.LIF_DELTA, 10)
+    assert e.value.code == SNN_E_STATE
+    # fixed-point overflow bound
+    g = Snn(1, 0.1, 0, 30)
+    a = g.add_population(W.LIF_DELTA, 100000, v_th=20.0)
+    g.connect(a, a, W.STATIC, 0, 0.5, 10.0)
+    with pytest.raises(SnnError) as e:
+        g.finalize()
+    assert e.value.code == SNN_E_INVALID
