@@ -237,21 +237,19 @@ def main():
     d = {k: mp1[k] - mp0[k] for k in mp1}
     sp.close()
     nrcpt = 2 if any(pr.receptor == W.INH for pr in rc.projs) else 1
-    # algorithmic HBM bytes per phase
-    bytes_ph = {
-        "STDP": 4 * d["STDP_SYN"] + 8 * d["STDP_WTOUCH"] + 24 * d["STDP_ROWS"],
-        "DELIVERY": 8 * d["EVENTS"] + 8 * d["SPIKES"] * info["nslices"] + 16 * d["SPIKES"]
-                    + 8 * nrcpt * info["R"] * 0,
-        "NEURON": psteps * sum(p.n * (16 if p.kind == W.POISSON else 40) for p in rc.pops) // 1,
-    }
+    # algorithmic HBM bytes of the fused slice kernel:
+    #   static deliveries 8 B (idx + w), plastic visits 4 B (idx) + 8 B where the
+    #   weight is read and written, 8 B per (row, slice) pivot pair, 4 B per
+    #   slice neuron and receptor written back
+    static_el = d["ELEMS"] - d["STDP_SYN"]
+    rows = d["STDP_ROWS"] + (d["SPIKES"] - 0)
+    slice_bytes = (8 * static_el + 4 * d["STDP_SYN"] + 8 * d["STDP_WTOUCH"]
+                   + 8 * d["SEGMENTS"] + 4 * nrcpt * info["R"] * psteps)
     hbm, peak_src = peaks()
-    dom = max(("STDP", "DELIVERY", "NEURON", "WORKLIST"), key=lambda k: ph.get(k, 0.0))
-    dom_bytes = bytes_ph.get(dom, 0)
-    dom_ms = ph[dom]
-    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
-    shares = {k: ph[k] / ph["TOTAL"] for k in ("NEURON", "WORKLIST", "STDP", "DELIVERY")} if ph["TOTAL"] else {}
-    sd_bytes = bytes_ph["STDP"] + bytes_ph["DELIVERY"]
-    sd_ms = ph["STDP"] + ph["DELIVERY"]
+    slice_ms = ph["SLICE"]
+    achieved = slice_bytes / (slice_ms * 1e-3) / 1e9 if slice_ms > 0 else 0.0
+    shares = {k: ph[k] / ph["TOTAL"] for k in ("FRONT", "SLICE")} if ph["TOTAL"] else {}
+    split_group = info["pivot_bytes"]
 
     out = {
         "metric": METRIC, "value": events_per_s, "unit": "events/s", "n_gpus": world, "steps": a.steps,
@@ -265,16 +263,13 @@ def main():
         "wall_s_per_bio_s": wall_per_bio,
         "setup_s": setup_s,
         "rates_hz": rates,
-        "per_step": {"events": dm["EVENTS"] / a.steps, "spikes": dm["SPIKES"] / a.steps,
-                     "stdp_rows": dm["STDP_ROWS"] / a.steps, "stdp_syn": dm["STDP_SYN"] / a.steps,
-                     "stdp_wtouch": dm["STDP_WTOUCH"] / a.steps},
-        "gpu_launches": a.steps * (4 if rc.plastic else 3),
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+        "per_step": {k.lower(): v / a.steps for k, v in dm.items()},
+        "gpu_launches": a.steps * 2,
+        "roofline": {"bound": "hbm", "kernel": "k_slice (STDP + delivery, fused)", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                     "bytes_per_step": slice_bytes / psteps,
                      "phase_ms_per_step": {k: ph[k] / psteps for k in ph}, "phase_share": shares,
-                     "stdp_plus_delivery": {"achieved": sd_bytes / (sd_ms * 1e-3) / 1e9 if sd_ms else 0.0,
-                                            "frac": (sd_bytes / (sd_ms * 1e-3) / 1e9 / hbm) if sd_ms else 0.0,
-                                            "bytes_per_step": sd_bytes / psteps}},
+                     "slice_splits": split_group >> 32, "slot_elems": split_group & 0xffffffff},
         "e2e": e2e,
         "clocks": clk.summary(),
     }

@@ -51,7 +51,7 @@ typedef int32_t snn_status;
 
 enum {
     SNN_OK = 0,
-    SNN_E_INVALID = -1,     /* bad argument: p outside [0,1], n == 0, D >= H,
+    SNN_E_INVALID = -1,     /* bad argument: p outside [0,1], n == 0, D > 62,
                                slice width not a power of two in [32, 32768],
                                fixed-point overflow bound violated, ...      */
     SNN_E_STATE = -2,       /* call not allowed in the handle's lifecycle state */
@@ -86,7 +86,7 @@ typedef struct {
     uint32_t abi_version;    /* must be SNN_ABI_VERSION                          */
     uint32_t struct_size;    /* sizeof(snn_config)                                */
     float dt_ms;             /* step length; 0.1 ms in the paper          */
-    uint32_t delay_steps;    /* network-wide delay D in steps; D < 64     */
+    uint32_t delay_steps;    /* network-wide delay D in steps; D <= 62    */
     uint32_t history_bits;   /* H: 64; only 64 is supported        */
     uint32_t slice_width;    /* C: neurons per slice; power of two
                                 in [32, 32768]; 0 = automatic                      */
@@ -158,7 +158,7 @@ enum {
     SNN_FIELD_PHASE_TIMES = 18, /* [f64 / 8]  ms per phase (SNN_PHASE_*), summed
                                    over steps run with SNN_FLAG_PHASE_TIMING     */
     SNN_FIELD_INFO = 19,        /* [i64 / 8]  N, S, nslices, C, R, tgt_lo, tgt_hi,
-                                   pivot bytes                                    */
+                                   (slice-kernel splits << 32) | lanes per segment */
     SNN_FIELD_COUNT = 20
 };
 
@@ -170,14 +170,16 @@ enum {
     SNN_METRIC_STDP_SYN = 3,     /* plastic synapses visited                       */
     SNN_METRIC_STDP_WTOUCH = 4,  /* plastic synapses whose weight was read+written */
     SNN_METRIC_FLUSH_ROWS = 5,   /* rows visited by a forced flush (R3)            */
-    SNN_METRIC_SEGMENTS = 6,     /* non-empty (row, slice) segments delivered      */
-    SNN_METRIC_RESERVED = 7
+    SNN_METRIC_SEGMENTS = 6,     /* non-empty (row, slice) segments processed      */
+    SNN_METRIC_ELEMS = 7         /* synapse entries (target ids) read by the slice kernel */
 };
 
-/* SNN_FIELD_PHASE_TIMES layout */
+/* SNN_FIELD_PHASE_TIMES layout: the two kernels of a step */
 enum {
-    SNN_PHASE_NEURON = 0, SNN_PHASE_WORKLIST = 1, SNN_PHASE_STDP = 2,
-    SNN_PHASE_DELIVERY = 3, SNN_PHASE_EXCHANGE = 4, SNN_PHASE_TOTAL = 5
+    SNN_PHASE_FRONT = 0,    /* neuron update + firing bits + work lists       */
+    SNN_PHASE_SLICE = 1,    /* lazy+event STDP + sliced delivery (fused)      */
+    SNN_PHASE_EXCHANGE = 2, /* spike-bitmask all-gather (world > 1)           */
+    SNN_PHASE_TOTAL = 3
 };
 
 /* Creates a simulation handle bound to cfg->device / cfg->stream.

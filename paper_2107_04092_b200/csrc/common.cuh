@@ -66,13 +66,28 @@ struct BuildTabs {
     float weight[kMaxPops * kMaxPops];     // initial (final, caller-scaled) weight
 };
 
+constexpr int kFrontThreads = 1024;   // k_front CTA = one list region
+
 struct Counters {
     int64_t t;               // next step to simulate
-    uint32_t nA, nV;         // arrivals / plastic row visits of the current step
-    uint32_t ticket;         // CTA-completion ticket of the delivery kernel
+    uint32_t ticket;         // CTA-completion ticket of the slice kernel
     uint32_t pad;
     unsigned long long metric[8];
 };
+
+// One row to process in the slice kernel, written by the front kernel.
+// meta: bits 0-6 age (1..64), bit 7 arrival, bits 8-9 receptor (3 = per target),
+//       bit 10 plastic row, bits 12-15 STDP projection index.
+struct __align__(16) RowDesc {
+    int64_t start;   // CSR offset of the row
+    uint32_t row;    // source neuron id
+    uint32_t meta;
+    float xp;        // x_pre of the row at its last update (tlu)
+    uint32_t s0, s1; // plastic segment [s0, s1), row-relative
+    uint32_t pad;
+};
+constexpr uint32_t kMetaArr = 1u << 7;
+constexpr uint32_t kMetaPlastic = 1u << 10;
 
 struct StateDev {
     // neurons (indexed by global id)
@@ -90,8 +105,14 @@ struct StateDev {
     float *w;                // [S + pad]
     uint32_t *piv;           // [N][nslices+1], row-relative
     uint2 *seg;              // [N] plastic segment (lo, hi), row-relative
-    // work lists
-    uint32_t *arr_list, *visit_list;
+    // work lists (by step parity), one region of kFrontThreads entries per
+    // k_front CTA (no global atomics): plastic visits and static arrivals
+    RowDesc *vdesc[2], *adesc[2];
+    uint4 *cnt[2];           // per k_front CTA: (visits, static arrivals, arrivals, flushes)
+    RowDesc *rdesc;          // read-out flush rows (same region layout)
+    uint4 *rcnt;
+    uint32_t nblk;           // k_front CTAs = list regions
+    uint32_t *vmask[2];      // [nwords] rows visited at the step of that parity
     Counters *ctr;
 };
 

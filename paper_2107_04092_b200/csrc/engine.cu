@@ -19,15 +19,12 @@ cudaError_t build_fill(const NetDev &, const BuildTabs &, const uint32_t *, cons
                        float *, cudaStream_t);
 cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, uint2 *, cudaStream_t);
 cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
-cudaError_t launch_neuron(const NetDev &, const StateDev &, uint32_t, uint32_t, cudaStream_t);
-cudaError_t launch_worklist(const NetDev &, const StateDev &, uint32_t, uint32_t, cudaStream_t);
-cudaError_t launch_stdp(const NetDev &, const StateDev &, uint32_t, cudaStream_t);
-cudaError_t launch_stdp_fixed(const NetDev &, const StateDev &, int64_t, uint32_t, cudaStream_t);
-cudaError_t launch_flush_list(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t *,
-                              cudaStream_t);
-size_t deliver_smem_bytes(const NetDev &);
-cudaError_t deliver_configure(const NetDev &);
-cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t);
+uint32_t front_blocks(const NetDev &);
+cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t);
+size_t slice_smem_bytes(const NetDev &, uint32_t);
+cudaError_t slice_configure(const NetDev &, uint32_t);
+cudaError_t launch_step_slice(const NetDev &, const StateDev &, uint32_t, uint32_t, cudaStream_t);
+cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, cudaStream_t);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
 }  // namespace snn
 
@@ -63,10 +60,8 @@ struct snn_sim {
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     cudaGraphExec_t g_many = nullptr, g_one = nullptr;
     std::vector<void *> allocs;
-    uint32_t pl_lo = 0, pl_hi = 0;
-    uint32_t stdp_grid = 0, deliver_splits = 1;
+    uint32_t splits = 1, slot_elems = 64;   // slice-kernel launch shape
     bool plastic = false;
-    uint32_t *d_scratch_u32 = nullptr;
     uint64_t *d_hist_tmp = nullptr;
     // phase timing
     std::vector<cudaEvent_t> ev_pool;
@@ -201,30 +196,57 @@ static snn_status finalize(snn_sim *sim) {
                                  "fixed-point overflow bound: population %u receptor %d may reach %.3g >= 2^31 "
                                  "(lower accum_frac_bits)", k, r, acc_bound[k][r]);
     }
-    net.nrcpt = 1;
-    for (const HostProj &hj : sim->projs)
-        if (hj.prm.receptor == SNN_RCPT_INH) net.nrcpt = 2;
     net.R = R;
     if (cfg.world > 1) return sim->fail(SNN_E_UNSUPPORTED, "world > 1 not available in this build");
     net.tgt_lo = 0;
     net.tgt_hi = R;
-    uint32_t C = cfg.slice_width ? cfg.slice_width : 1024u;
+    net.nrcpt = 1;
+    for (const HostProj &hj : sim->projs)
+        if (hj.prm.receptor == SNN_RCPT_INH) net.nrcpt = 2;
+    // slice width C ("delicate, tunable") and the TMA staging slot
+    // of the slice kernel (one (row, slice) segment per slot: mean + 6 sigma of
+    // the binomial segment length, + alignment slack).  Auto C: the largest
+    // power of two <= 8192 that leaves >= 16 slices and 2 CTAs per SM.
+    double syn_est = 0.0;
+    uint64_t rows_out = 0;
+    for (uint32_t k = 0; k < net.npop; k++) {
+        bool has_out = false;
+        for (const HostProj &hj : sim->projs)
+            if (hj.src == k) {
+                has_out = true;
+                syn_est += hj.prm.p * (double)sim->pops[k].n * (double)sim->pops[hj.dst].n;
+            }
+        if (has_out) rows_out += sim->pops[k].n;
+    }
+    const double density = (rows_out && R) ? syn_est / ((double)rows_out * (double)R) : 0.0;
+    auto slot_for = [&](uint32_t c) {
+        const double mu = density * c;
+        uint32_t se = (uint32_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 8.0);
+        se = (se + 31) & ~31u;
+        return std::min(1024u, std::max(64u, se));
+    };
+    uint32_t C = cfg.slice_width;
+    if (C == 0) {
+        C = 8192;
+        while (C > 64) {
+            NetDev probe = net;
+            probe.C = C;
+            probe.nrcpt = 2;
+            const bool ok_slices = (R + C - 1) / C >= 16;
+            const bool ok_smem = slice_smem_bytes(probe, slot_for(C)) <= 110 * 1024;
+            if (ok_slices && ok_smem) break;
+            C >>= 1;
+        }
+    }
     net.C = C;
     net.log2C = 0;
     while ((1u << net.log2C) < C) net.log2C++;
     net.nslices = (net.tgt_hi - net.tgt_lo + C - 1) / C;
+    sim->slot_elems = slot_for(C);
     net.nwords = (net.N + 31) / 32;
-    // plastic source rows
-    sim->pl_lo = net.N;
-    sim->pl_hi = 0;
+    sim->plastic = net.nstdp > 0;
     for (uint32_t k = 0; k < net.npop; k++)
-        if (net.pop[k].flags & PF_PRE_PLASTIC) {
-            sim->pl_lo = std::min(sim->pl_lo, net.pop[k].base);
-            sim->pl_hi = std::max(sim->pl_hi, net.pop[k].base + net.pop[k].n);
-        }
-    sim->plastic = sim->pl_hi > sim->pl_lo;
-    if (!sim->plastic) sim->pl_lo = sim->pl_hi = 0;
-    net.n_plastic_rows = sim->pl_hi - sim->pl_lo;
+        if (net.pop[k].flags & PF_PRE_PLASTIC) net.n_plastic_rows += net.pop[k].n;
 
     // ---- device buffers
     const uint32_t N = net.N;
@@ -244,12 +266,23 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.row_ptr, int64_t, (size_t)N + 1);
     ALLOC(st.piv, uint32_t, (size_t)N * (net.nslices + 1));
     ALLOC(st.seg, uint2, N);
-    ALLOC(st.arr_list, uint32_t, N);
-    ALLOC(st.visit_list, uint32_t, N);
+    st.nblk = front_blocks(net);
+    const size_t nreg = (size_t)st.nblk * kFrontThreads;
+    for (int b = 0; b < 2; b++) {
+        ALLOC(st.vdesc[b], RowDesc, net.nstdp ? nreg : 1);
+        ALLOC(st.adesc[b], RowDesc, nreg);
+        ALLOC(st.cnt[b], uint4, st.nblk);
+        ALLOC(st.vmask[b], uint32_t, net.nwords);
+    }
+    ALLOC(st.rdesc, RowDesc, net.nstdp ? nreg : 1);
+    ALLOC(st.rcnt, uint4, st.nblk);
     ALLOC(st.ctr, Counters, 1);
-    ALLOC(sim->d_scratch_u32, uint32_t, 4);
     cudaStream_t s = sim->stream;
     CK(cudaMemsetAsync(st.ring, 0, sizeof(uint32_t) * (size_t)kRingSlots * net.nwords, s));
+    for (int b = 0; b < 2; b++) {
+        CK(cudaMemsetAsync(st.vmask[b], 0, sizeof(uint32_t) * net.nwords, s));
+        CK(cudaMemsetAsync(st.cnt[b], 0, sizeof(uint4) * st.nblk, s));
+    }
     CK(cudaMemsetAsync(st.ctr, 0, sizeof(Counters), s));
 
     // ---- graph (count -> pivots/row_ptr -> fill)
@@ -272,12 +305,17 @@ static snn_status finalize(snn_sim *sim) {
     CK(build_segments(net, st.row_ptr, st.idx, st.seg, s));
     CK(init_state(net, st, s));
 
-    // ---- launch shapes
-    CK(deliver_configure(net));
-    const uint32_t target_ctas = 2 * 148;
-    sim->deliver_splits = std::max(1u, (target_ctas + std::max(1u, net.nslices) - 1) / std::max(1u, net.nslices));
-    sim->deliver_splits = std::min(sim->deliver_splits, 16u);
-    sim->stdp_grid = 148 * 8;
+    // ---- launch shape of the slice kernel: nslices x splits CTAs, one wave at
+    //      the occupancy the shared memory allows
+    const size_t smem = slice_smem_bytes(net, sim->slot_elems);
+    if (smem > 227 * 1024)
+        return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory (> 227 KB)", C, smem);
+    CK(slice_configure(net, sim->slot_elems));
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg.device);
+    const uint32_t occ = smem <= 113 * 1024 ? 2u : 1u;
+    const uint32_t ns = std::max(1u, net.nslices);
+    sim->splits = std::max(1u, (uint32_t)(occ * nsm) / ns);
     CK(cudaStreamSynchronize(s));
     sim->state = 1;
     return SNN_OK;
@@ -288,14 +326,10 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev) {
     const NetDev &net = sim->net;
     const StateDev &st = sim->st;
     if (ev) CK(cudaEventRecord(ev[0], s));
-    CK(launch_neuron(net, st, 0, net.N, s));                        // (1) P:36
+    CK(launch_front(net, st, s));                                   // (1) P:36 + work lists
     if (ev) CK(cudaEventRecord(ev[1], s));
-    CK(launch_worklist(net, st, sim->pl_lo, sim->pl_hi, s));        // A(t), A(t) u F(t)
+    CK(launch_step_slice(net, st, sim->splits, sim->slot_elems, s));  // (2) P:37-39 + (3) P:41
     if (ev) CK(cudaEventRecord(ev[2], s));
-    if (sim->plastic) CK(launch_stdp(net, st, sim->stdp_grid, s));  // (2) P:37-39
-    if (ev) CK(cudaEventRecord(ev[3], s));
-    CK(launch_deliver(net, st, sim->deliver_splits, s));           // (3) P:41
-    if (ev) CK(cudaEventRecord(ev[4], s));
     return SNN_OK;
 }
 
@@ -332,10 +366,10 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         g_create_error = "snn_config: ABI version / struct size mismatch";
         return SNN_E_INVALID;
     }
-    if (!(cfg->dt_ms > 0.0f) || cfg->history_bits != 64 || cfg->delay_steps >= 64 ||
+    if (!(cfg->dt_ms > 0.0f) || cfg->history_bits != 64 || cfg->delay_steps > 62 ||
         cfg->accum_frac_bits < 0 || cfg->accum_frac_bits > 30 || cfg->world < 1 || cfg->rank < 0 ||
         cfg->rank >= cfg->world) {
-        g_create_error = "snn_config: need dt > 0, history_bits == 64, delay < 64, 0 <= F <= 30, 0 <= rank < world";
+        g_create_error = "snn_config: need dt > 0, history_bits == 64, delay <= 62, 0 <= F <= 30, 0 <= rank < world";
         return SNN_E_INVALID;
     }
     const uint32_t C = cfg->slice_width;
@@ -439,7 +473,7 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
             cudaEvent_t *ev = nullptr;
             if (timing) {
                 if (sim->ev_used == sim->ev_steps.size()) {
-                    std::vector<cudaEvent_t> v(5);
+                    std::vector<cudaEvent_t> v(3);
                     for (auto &e : v) CK(cudaEventCreate(&e));
                     sim->ev_steps.push_back(v);
                 }
@@ -464,17 +498,11 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
     return SNN_OK;
 }
 
-// Read-out flush (R11): bring every stale plastic row up to t_last, no pre spike.
+// Read-out flush (R11): finalise pending row visits and bring every stale
+// plastic row up to t_last without a pre spike.
 static snn_status readout_flush(snn_sim *sim) {
     if (!sim->plastic || sim->t == 0) return SNN_OK;
-    const int64_t t_last = sim->t - 1;
-    cudaStream_t s = sim->stream;
-    CK(cudaMemsetAsync(sim->d_scratch_u32, 0, sizeof(uint32_t), s));
-    CK(launch_flush_list(sim->net, sim->st, t_last, sim->pl_lo, sim->pl_hi, sim->d_scratch_u32, s));
-    uint32_t n = 0;
-    CK(cudaMemcpyAsync(&n, sim->d_scratch_u32, sizeof n, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    CK(launch_stdp_fixed(sim->net, sim->st, t_last, n, s));
+    CK(launch_readout(sim->net, sim->st, sim->t - 1, sim->splits, sim->slot_elems, sim->stream));
     return SNN_OK;
 }
 
@@ -521,7 +549,7 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
     case SNN_FIELD_INFO:
         host_i64[0] = sim->N; host_i64[1] = sim->nsyn; host_i64[2] = net.nslices; host_i64[3] = net.C;
         host_i64[4] = net.R; host_i64[5] = net.tgt_lo; host_i64[6] = net.tgt_hi;
-        host_i64[7] = (int64_t)4 * sim->N * (net.nslices + 1);
+        host_i64[7] = ((int64_t)sim->splits << 32) | sim->slot_elems;
         host_src = host_i64; bytes = 64; break;
     default: return sim->fail(SNN_E_INVALID, "unknown field %u", field);
     }
@@ -544,10 +572,11 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
     if (field == SNN_FIELD_PHASE_TIMES) {
         CK(cudaStreamSynchronize(s));
         for (size_t k = 0; k < sim->ev_used; k++) {
-            float ms[4];
-            for (int p = 0; p < 4; p++) CK(cudaEventElapsedTime(&ms[p], sim->ev_steps[k][p], sim->ev_steps[k][p + 1]));
-            for (int p = 0; p < 4; p++) sim->phase_ms[p == 3 ? SNN_PHASE_DELIVERY : p] += ms[p];
-            sim->phase_ms[SNN_PHASE_TOTAL] += ms[0] + ms[1] + ms[2] + ms[3];
+            float ms[2];
+            for (int p = 0; p < 2; p++) CK(cudaEventElapsedTime(&ms[p], sim->ev_steps[k][p], sim->ev_steps[k][p + 1]));
+            sim->phase_ms[SNN_PHASE_FRONT] += ms[0];
+            sim->phase_ms[SNN_PHASE_SLICE] += ms[1];
+            sim->phase_ms[SNN_PHASE_TOTAL] += ms[0] + ms[1];
         }
         sim->ev_used = 0;
         for (int k = 0; k < 8; k++) host_f64[k] = sim->phase_ms[k];

@@ -83,8 +83,8 @@ def vogels(n_total: int = 4000, p: float = 0.02, seed: int = 1, delay: int = 0,
     """Vogels-Abbott CUBA network: 80 % E / 20 % I, Erdos-Renyi p (BASELINE.json configs 1, 5)."""
     ne = int(round(0.8 * n_total))
     ni = n_total - ne
-    we = VOGELS_WE * VOGELS_KE / (p * ne)
-    wi = VOGELS_WI * VOGELS_KI / (p * ni)
+    we = VOGELS_WE * VOGELS_KE / (p * ne) if p > 0 else VOGELS_WE
+    wi = VOGELS_WI * VOGELS_KI / (p * ni) if p > 0 else VOGELS_WI
     pops = [Pop("E", LIF_CUBA, ne, dict(VOGELS_LIF)), Pop("I", LIF_CUBA, ni, dict(VOGELS_LIF))]
     projs = [Proj(0, 0, STATIC, EXC, p, we), Proj(0, 1, STATIC, EXC, p, we),
              Proj(1, 0, STATIC, INH, p, wi), Proj(1, 1, STATIC, INH, p, wi)]
@@ -105,7 +105,7 @@ def brunel(n_total: int = 100_000, p: float = 0.02, plastic: bool = False, seed:
     ne = int(round(0.4 * n_total))
     ni = int(round(0.1 * n_total))
     npp = n_total - ne - ni
-    J = BRUNEL_J * BRUNEL_KBASE / (p * ne)
+    J = BRUNEL_J * BRUNEL_KBASE / (p * ne) if p > 0 else BRUNEL_J
     w_max = 2.0 * J
     a_plus = 0.01 * w_max
     stdp = dict(tau_plus=20.0, tau_minus=20.0, a_plus=a_plus, a_minus=1.05 * a_plus, w_max=w_max)
