@@ -237,18 +237,25 @@ def main():
     d = {k: mp1[k] - mp0[k] for k in mp1}
     sp.close()
     nrcpt = 2 if any(pr.receptor == W.INH for pr in rc.projs) else 1
-    # algorithmic HBM bytes of the fused slice kernel:
-    #   static deliveries 8 B (idx + w), plastic visits 4 B (idx) + 8 B where the
-    #   weight is read and written, 8 B per (row, slice) pivot pair, 4 B per
-    #   slice neuron and receptor written back
-    static_el = d["ELEMS"] - d["STDP_SYN"]
-    rows = d["STDP_ROWS"] + (d["SPIKES"] - 0)
-    slice_bytes = (8 * static_el + 4 * d["STDP_SYN"] + 8 * d["STDP_WTOUCH"]
-                   + 8 * d["SEGMENTS"] + 4 * nrcpt * info["R"] * psteps)
+    # algorithmic HBM bytes per kernel:
+    #   k_stdp:    4 B target id per visited plastic synapse, 8 B where the weight
+    #              is read and written, 16 B per visited row (x_pre, tlu, row_ptr, seg)
+    #   k_deliver: 8 B per delivered event (id + weight), 8 B per (arriving row,
+    #              slice) pivot pair, 4 B per slice neuron and receptor written back
+    kb = {
+        "STDP": 4 * d["STDP_SYN"] + 8 * d["STDP_WTOUCH"] + 16 * d["STDP_ROWS"],
+        "DELIVERY": 8 * d["EVENTS"] + 8 * d["SPIKES"] * info["nslices"] + 4 * nrcpt * info["R"] * psteps,
+    }
     hbm, peak_src = peaks()
-    slice_ms = ph["SLICE"]
-    achieved = slice_bytes / (slice_ms * 1e-3) / 1e9 if slice_ms > 0 else 0.0
-    shares = {k: ph[k] / ph["TOTAL"] for k in ("FRONT", "SLICE")} if ph["TOTAL"] else {}
+    kern = {}
+    for k2, by in kb.items():
+        ms_k = ph[k2]
+        kern[k2] = {"bytes_per_step": by / psteps, "ms_per_step": ms_k / psteps,
+                    "achieved_gbs": by / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0}
+    dom = max(kern, key=lambda k2: kern[k2]["ms_per_step"])
+    achieved = kern[dom]["achieved_gbs"]
+    shares = {k: ph[k] / ph["TOTAL"] for k in ("FRONT", "STDP", "DELIVERY")} if ph["TOTAL"] else {}
+    sd_bytes, sd_ms = kb["STDP"] + kb["DELIVERY"], ph["STDP"] + ph["DELIVERY"]
     split_group = info["pivot_bytes"]
 
     out = {
@@ -264,12 +271,14 @@ def main():
         "setup_s": setup_s,
         "rates_hz": rates,
         "per_step": {k.lower(): v / a.steps for k, v in dm.items()},
-        "gpu_launches": a.steps * 2,
-        "roofline": {"bound": "hbm", "kernel": "k_slice (STDP + delivery, fused)", "achieved": achieved,
-                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
-                     "bytes_per_step": slice_bytes / psteps,
+        "gpu_launches": a.steps * (3 if rc.plastic else 2),
+        "roofline": {"bound": "hbm", "kernel": {"STDP": "k_stdp", "DELIVERY": "k_deliver"}[dom],
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "peak_source": peak_src, "kernels": kern,
+                     "stdp_plus_delivery": {"achieved_gbs": sd_bytes / (sd_ms * 1e-3) / 1e9 if sd_ms else 0.0,
+                                            "frac": sd_bytes / (sd_ms * 1e-3) / 1e9 / hbm if sd_ms else 0.0},
                      "phase_ms_per_step": {k: ph[k] / psteps for k in ph}, "phase_share": shares,
-                     "slice_splits": split_group >> 32, "slot_elems": split_group & 0xffffffff},
+                     "deliver_splits": split_group >> 32, "stdp_grid": split_group & 0xffffffff},
         "e2e": e2e,
         "clocks": clk.summary(),
     }

@@ -77,9 +77,12 @@ enum { SNN_RCPT_EXC = 0, SNN_RCPT_INH = 1 };
 enum {
     SNN_FLAG_NO_GRAPH = 1u << 0,     /* launch kernels directly instead of replaying
                                         a captured CUDA graph of the step          */
-    SNN_FLAG_PHASE_TIMING = 1u << 1  /* record CUDA events around every phase of
+    SNN_FLAG_PHASE_TIMING = 1u << 1, /* record CUDA events around every phase of
                                         every step (implies NO_GRAPH); read with
                                         SNN_FIELD_PHASE_TIMES                       */
+    SNN_FLAG_TRACE = 1u << 2         /* debug: per-CTA %globaltimer phase marks of
+                                        the last step (implies NO_GRAPH); read with
+                                        SNN_FIELD_TRACE                             */
 };
 
 typedef struct {
@@ -158,8 +161,11 @@ enum {
     SNN_FIELD_PHASE_TIMES = 18, /* [f64 / 8]  ms per phase (SNN_PHASE_*), summed
                                    over steps run with SNN_FLAG_PHASE_TIMING     */
     SNN_FIELD_INFO = 19,        /* [i64 / 8]  N, S, nslices, C, R, tgt_lo, tgt_hi,
-                                   (slice-kernel splits << 32) | lanes per segment */
-    SNN_FIELD_COUNT = 20
+                                   (delivery splits << 32) | STDP grid          */
+    SNN_FIELD_TRACE = 20,       /* [u64 / 3*4096*4] debug phase marks (ns) of the
+                                   last step: [kernel][cta][phase], kernels
+                                   front / stdp / deliver                        */
+    SNN_FIELD_COUNT = 21
 };
 
 /* SNN_FIELD_METRICS layout (device counters, cumulative over steps) */
@@ -171,15 +177,16 @@ enum {
     SNN_METRIC_STDP_WTOUCH = 4,  /* plastic synapses whose weight was read+written */
     SNN_METRIC_FLUSH_ROWS = 5,   /* rows visited by a forced flush (R3)            */
     SNN_METRIC_SEGMENTS = 6,     /* non-empty (row, slice) segments processed      */
-    SNN_METRIC_ELEMS = 7         /* synapse entries (target ids) read by the slice kernel */
+    SNN_METRIC_ELEMS = 7         /* synapse entries read by the delivery kernel    */
 };
 
-/* SNN_FIELD_PHASE_TIMES layout: the two kernels of a step */
+/* SNN_FIELD_PHASE_TIMES layout: the kernels of a step */
 enum {
     SNN_PHASE_FRONT = 0,    /* neuron update + firing bits + work lists       */
-    SNN_PHASE_SLICE = 1,    /* lazy+event STDP + sliced delivery (fused)      */
-    SNN_PHASE_EXCHANGE = 2, /* spike-bitmask all-gather (world > 1)           */
-    SNN_PHASE_TOTAL = 3
+    SNN_PHASE_STDP = 1,     /* lazy + event-driven STDP                       */
+    SNN_PHASE_DELIVERY = 2, /* sliced shared-atomic delivery                  */
+    SNN_PHASE_EXCHANGE = 3, /* spike-bitmask all-gather (world > 1)           */
+    SNN_PHASE_TOTAL = 4
 };
 
 /* Creates a simulation handle bound to cfg->device / cfg->stream.

@@ -113,8 +113,26 @@ struct StateDev {
     uint4 *rcnt;
     uint32_t nblk;           // k_front CTAs = list regions
     uint32_t *vmask[2];      // [nwords] rows visited at the step of that parity
+    uint32_t *recent;        // [nwords] bit i: post-plastic neuron i fired in the last 64 steps
     Counters *ctr;
+    unsigned long long *trace;   // optional (SNN_FLAG_TRACE): per-CTA phase timestamps
 };
+
+// Phase trace (debug, SNN_FLAG_TRACE): thread 0 of each CTA stores %globaltimer
+// at phase boundaries: trace[(kernel * kTraceCtas + cta) * 4 + phase].
+constexpr int kTraceCtas = 4096;
+__device__ __forceinline__ void trace_mark(unsigned long long *tr, int kernel, int phase) {
+#ifdef __CUDA_ARCH__
+    if (tr && threadIdx.x == 0) {
+        const uint32_t cta = blockIdx.y * gridDim.x + blockIdx.x;
+        if (cta < (uint32_t)kTraceCtas) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            tr[((size_t)kernel * kTraceCtas + cta) * 4 + phase] = g;
+        }
+    }
+#endif
+}
 
 __host__ __device__ inline int find_pop(const NetDev &net, uint32_t i) {
     int p = 0;

@@ -21,10 +21,12 @@ cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, ui
 cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
 uint32_t front_blocks(const NetDev &);
 cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t);
-size_t slice_smem_bytes(const NetDev &, uint32_t);
-cudaError_t slice_configure(const NetDev &, uint32_t);
-cudaError_t launch_step_slice(const NetDev &, const StateDev &, uint32_t, uint32_t, cudaStream_t);
-cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, cudaStream_t);
+size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
+size_t deliver_smem_bytes(const NetDev &);
+cudaError_t kernels_configure(const NetDev &, uint32_t, uint32_t);
+cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
+cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t);
+cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
 }  // namespace snn
 
@@ -60,7 +62,9 @@ struct snn_sim {
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     cudaGraphExec_t g_many = nullptr, g_one = nullptr;
     std::vector<void *> allocs;
-    uint32_t splits = 1, slot_elems = 64;   // slice-kernel launch shape
+    uint32_t splits = 1;                 // k_deliver CTAs per slice
+    uint32_t stdp_grid = 1;              // k_stdp CTAs
+    uint32_t pp_lo = 0, pp_hi = 0;       // post-plastic neuron range (bitmap span)
     bool plastic = false;
     uint64_t *d_hist_tmp = nullptr;
     // phase timing
@@ -203,46 +207,18 @@ static snn_status finalize(snn_sim *sim) {
     net.nrcpt = 1;
     for (const HostProj &hj : sim->projs)
         if (hj.prm.receptor == SNN_RCPT_INH) net.nrcpt = 2;
-    // slice width C ("delicate, tunable") and the TMA staging slot
-    // of the slice kernel (one (row, slice) segment per slot: mean + 6 sigma of
-    // the binomial segment length, + alignment slack).  Auto C: the largest
-    // power of two <= 8192 that leaves >= 16 slices and 2 CTAs per SM.
-    double syn_est = 0.0;
-    uint64_t rows_out = 0;
-    for (uint32_t k = 0; k < net.npop; k++) {
-        bool has_out = false;
-        for (const HostProj &hj : sim->projs)
-            if (hj.src == k) {
-                has_out = true;
-                syn_est += hj.prm.p * (double)sim->pops[k].n * (double)sim->pops[hj.dst].n;
-            }
-        if (has_out) rows_out += sim->pops[k].n;
-    }
-    const double density = (rows_out && R) ? syn_est / ((double)rows_out * (double)R) : 0.0;
-    auto slot_for = [&](uint32_t c) {
-        const double mu = density * c;
-        uint32_t se = (uint32_t)std::ceil(mu + 6.0 * std::sqrt(mu) + 8.0);
-        se = (se + 31) & ~31u;
-        return std::min(1024u, std::max(64u, se));
-    };
+    // slice width C of the delivery ("delicate, tunable"): the
+    // paper's 1024 by default, shrunk so that there are at least ~1 slice per SM
+    // when the target range is small
     uint32_t C = cfg.slice_width;
     if (C == 0) {
-        C = 8192;
-        while (C > 64) {
-            NetDev probe = net;
-            probe.C = C;
-            probe.nrcpt = 2;
-            const bool ok_slices = (R + C - 1) / C >= 16;
-            const bool ok_smem = slice_smem_bytes(probe, slot_for(C)) <= 110 * 1024;
-            if (ok_slices && ok_smem) break;
-            C >>= 1;
-        }
+        C = 1024;
+        while (C > 128 && (R + C - 1) / C < 64) C >>= 1;
     }
     net.C = C;
     net.log2C = 0;
     while ((1u << net.log2C) < C) net.log2C++;
     net.nslices = (net.tgt_hi - net.tgt_lo + C - 1) / C;
-    sim->slot_elems = slot_for(C);
     net.nwords = (net.N + 31) / 32;
     sim->plastic = net.nstdp > 0;
     for (uint32_t k = 0; k < net.npop; k++)
@@ -276,9 +252,16 @@ static snn_status finalize(snn_sim *sim) {
     }
     ALLOC(st.rdesc, RowDesc, net.nstdp ? nreg : 1);
     ALLOC(st.rcnt, uint4, st.nblk);
+    ALLOC(st.recent, uint32_t, net.nwords);
+    st.trace = nullptr;
+    if (cfg.flags & SNN_FLAG_TRACE) {
+        ALLOC(st.trace, unsigned long long, 3ull * kTraceCtas * 4);
+        CK(cudaMemsetAsync(st.trace, 0, 8ull * 3 * kTraceCtas * 4, sim->stream));
+    }
     ALLOC(st.ctr, Counters, 1);
     cudaStream_t s = sim->stream;
     CK(cudaMemsetAsync(st.ring, 0, sizeof(uint32_t) * (size_t)kRingSlots * net.nwords, s));
+    CK(cudaMemsetAsync(st.recent, 0, sizeof(uint32_t) * net.nwords, s));
     for (int b = 0; b < 2; b++) {
         CK(cudaMemsetAsync(st.vmask[b], 0, sizeof(uint32_t) * net.nwords, s));
         CK(cudaMemsetAsync(st.cnt[b], 0, sizeof(uint4) * st.nblk, s));
@@ -305,17 +288,26 @@ static snn_status finalize(snn_sim *sim) {
     CK(build_segments(net, st.row_ptr, st.idx, st.seg, s));
     CK(init_state(net, st, s));
 
-    // ---- launch shape of the slice kernel: nslices x splits CTAs, one wave at
-    //      the occupancy the shared memory allows
-    const size_t smem = slice_smem_bytes(net, sim->slot_elems);
-    if (smem > 227 * 1024)
-        return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory (> 227 KB)", C, smem);
-    CK(slice_configure(net, sim->slot_elems));
+    // ---- launch shapes: k_deliver = nslices x splits CTAs (~1 wave at 2 per
+    //      SM); k_stdp = 4 CTAs per SM, grid-striding over the visited rows
+    sim->pp_lo = net.N;
+    sim->pp_hi = 0;
+    for (uint32_t k = 0; k < net.npop; k++)
+        if (net.pop[k].flags & PF_POST_PLASTIC) {
+            sim->pp_lo = std::min(sim->pp_lo, net.pop[k].base);
+            sim->pp_hi = std::max(sim->pp_hi, net.pop[k].base + net.pop[k].n);
+        }
+    if (sim->pp_hi <= sim->pp_lo) sim->pp_lo = sim->pp_hi = 0;
+    if (deliver_smem_bytes(net) > 200 * 1024)
+        return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory", C, deliver_smem_bytes(net));
+    if (stdp_smem_bytes(net, sim->pp_lo, sim->pp_hi) > 200 * 1024)
+        return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for the shared bitmap");
+    CK(kernels_configure(net, sim->pp_lo, sim->pp_hi));
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg.device);
-    const uint32_t occ = smem <= 113 * 1024 ? 2u : 1u;
     const uint32_t ns = std::max(1u, net.nslices);
-    sim->splits = std::max(1u, (uint32_t)(occ * nsm) / ns);
+    sim->splits = std::max(1u, (uint32_t)(2 * nsm) / ns);
+    sim->stdp_grid = 3 * (uint32_t)nsm;
     CK(cudaStreamSynchronize(s));
     sim->state = 1;
     return SNN_OK;
@@ -328,8 +320,11 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev) {
     if (ev) CK(cudaEventRecord(ev[0], s));
     CK(launch_front(net, st, s));                                   // (1) P:36 + work lists
     if (ev) CK(cudaEventRecord(ev[1], s));
-    CK(launch_step_slice(net, st, sim->splits, sim->slot_elems, s));  // (2) P:37-39 + (3) P:41
+    if (sim->plastic)                                               // (2) P:37-39
+        CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s));
     if (ev) CK(cudaEventRecord(ev[2], s));
+    CK(launch_deliver(net, st, sim->splits, s));                    // (3) P:41
+    if (ev) CK(cudaEventRecord(ev[3], s));
     return SNN_OK;
 }
 
@@ -467,13 +462,13 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
     }
     if (n_steps == 0) return SNN_OK;
     const bool timing = (sim->cfg.flags & SNN_FLAG_PHASE_TIMING) != 0;
-    const bool direct = timing || (sim->cfg.flags & SNN_FLAG_NO_GRAPH) != 0;
+    const bool direct = timing || (sim->cfg.flags & (SNN_FLAG_NO_GRAPH | SNN_FLAG_TRACE)) != 0;
     if (direct) {
         for (uint32_t k = 0; k < n_steps; k++) {
             cudaEvent_t *ev = nullptr;
             if (timing) {
                 if (sim->ev_used == sim->ev_steps.size()) {
-                    std::vector<cudaEvent_t> v(3);
+                    std::vector<cudaEvent_t> v(4);
                     for (auto &e : v) CK(cudaEventCreate(&e));
                     sim->ev_steps.push_back(v);
                 }
@@ -502,7 +497,7 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
 // plastic row up to t_last without a pre spike.
 static snn_status readout_flush(snn_sim *sim) {
     if (!sim->plastic || sim->t == 0) return SNN_OK;
-    CK(launch_readout(sim->net, sim->st, sim->t - 1, sim->splits, sim->slot_elems, sim->stream));
+    CK(launch_readout(sim->net, sim->st, sim->t - 1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, sim->stream));
     return SNN_OK;
 }
 
@@ -546,10 +541,13 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
     case SNN_FIELD_STEP: host_i64[0] = sim->t; host_src = host_i64; bytes = 8; break;
     case SNN_FIELD_METRICS: src = st.ctr->metric; bytes = 8 * 8; break;
     case SNN_FIELD_PHASE_TIMES: bytes = 8 * 8; break;
+    case SNN_FIELD_TRACE:
+        if (!st.trace) return sim->fail(SNN_E_STATE, "trace needs SNN_FLAG_TRACE");
+        src = st.trace; bytes = 8ull * 3 * kTraceCtas * 4; break;
     case SNN_FIELD_INFO:
         host_i64[0] = sim->N; host_i64[1] = sim->nsyn; host_i64[2] = net.nslices; host_i64[3] = net.C;
         host_i64[4] = net.R; host_i64[5] = net.tgt_lo; host_i64[6] = net.tgt_hi;
-        host_i64[7] = ((int64_t)sim->splits << 32) | sim->slot_elems;
+        host_i64[7] = ((int64_t)sim->splits << 32) | sim->stdp_grid;
         host_src = host_i64; bytes = 64; break;
     default: return sim->fail(SNN_E_INVALID, "unknown field %u", field);
     }
@@ -572,11 +570,12 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
     if (field == SNN_FIELD_PHASE_TIMES) {
         CK(cudaStreamSynchronize(s));
         for (size_t k = 0; k < sim->ev_used; k++) {
-            float ms[2];
-            for (int p = 0; p < 2; p++) CK(cudaEventElapsedTime(&ms[p], sim->ev_steps[k][p], sim->ev_steps[k][p + 1]));
+            float ms[3];
+            for (int p = 0; p < 3; p++) CK(cudaEventElapsedTime(&ms[p], sim->ev_steps[k][p], sim->ev_steps[k][p + 1]));
             sim->phase_ms[SNN_PHASE_FRONT] += ms[0];
-            sim->phase_ms[SNN_PHASE_SLICE] += ms[1];
-            sim->phase_ms[SNN_PHASE_TOTAL] += ms[0] + ms[1];
+            sim->phase_ms[SNN_PHASE_STDP] += ms[1];
+            sim->phase_ms[SNN_PHASE_DELIVERY] += ms[2];
+            sim->phase_ms[SNN_PHASE_TOTAL] += ms[0] + ms[1] + ms[2];
         }
         sim->ev_used = 0;
         for (int k = 0; k < 8; k++) host_f64[k] = sim->phase_ms[k];

@@ -1,19 +1,23 @@
-// step.cu -- the per-step hot path, two kernels per step:
+// step.cu -- the per-step hot path, three kernels per step:
 //
-//   k_front  (a1)+(a2)  neuron / Poisson update, firing bits -> bitmask ring,
-//                       64-bit history push, and the step's work lists:
-//                       plastic row visits A(t) u F(t) (arrivals + forced
-//                       flushes, R3) and static arrivals, compacted per CTA
-//                       into that CTA's own list region (no global atomics);
-//                       also finalises the per-row STDP state (x_pre, tlu) of
-//                       rows visited at t-1.
-//   k_slice  (a3)+(a4)  one CTA group per neuron slice (Fig. 3b):
-//                       stages the slice's 64-bit histories and post traces in
-//                       shared memory, runs lazy + event-driven STDP (Fig. 2c,
-//                       P:233-246) on every visited row's segment in the slice
-//                       and delivers every arriving row's segment into int32
-//                       shared-memory accumulators (native ATOMS.ADD), then adds
-//                       them to the global input arrays in one coalesced pass.
+//   k_front    (a1)+(a2)  neuron / Poisson update, firing bits -> bitmask ring,
+//                         64-bit history push, "fired in the last 64
+//                         steps" bitmap of post-synaptic neurons, and the work
+//                         lists: plastic row visits A(t) u F(t) (arrivals +
+//                         forced flushes, R3) and arrivals A(t), compacted per
+//                         CTA into that CTA's list region (no global atomics);
+//                         also finalises the per-row STDP state (x_pre, tlu) of
+//                         rows visited at t-1.
+//   k_stdp     (a3)       lazy + event-driven STDP (Fig. 2c) over the
+//                         visited rows: one warp streams a row's plastic span
+//                         with 16-byte loads; the shared-memory bitmap filters
+//                         the targets whose 64-bit history can hold a post spike,
+//                         only those histories are gathered.
+//   k_deliver  (a4)       neuron-domain-sliced delivery (Fig. 3b, P:313-331,
+//                         P:348-355): one CTA per slice accumulates every
+//                         arriving spike's segment in int32 shared memory with
+//                         native atomics (ATOMS.ADD), then one coalesced
+//                         write-back; a warp per 32 spikes, lanes over targets.
 //
 // Floating point: every fp32 op is an explicit __f*_rn intrinsic, so there is no
 // FMA contraction (R19); accumulators are int32 fixed point (R18).
@@ -77,6 +81,7 @@ __device__ __forceinline__ void compact2(Compact2 &sm, bool a, bool b, uint32_t 
 __global__ void __launch_bounds__(kFrontThreads)
 k_front(NetDev net, StateDev st) {
     __shared__ Compact2 cs;
+    trace_mark(st.trace, 0, 0);
     const int64_t t = st.ctr->t;
     const uint32_t par = (uint32_t)(t & 1);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -84,7 +89,7 @@ k_front(NetDev net, StateDev st) {
     const bool valid = i < net.N;
     const int pi = valid ? find_pop(net, i) : 0;
     const PopDev &p = net.pop[pi];
-    bool fired = false;
+    bool fired = false, recent = false;
     // ---- (1) neuron dynamics (App. B op order)
     if (valid) {
         if (p.kind == POP_POISSON) {
@@ -137,14 +142,20 @@ k_front(NetDev net, StateDev st) {
             st.gi[i] = gi;
         }
         if (p.flags & PF_POST_PLASTIC) {
-            st.hist[i] = (st.hist[i] << 1) | (uint64_t)fired;
+            const uint64_t h = (st.hist[i] << 1) | (uint64_t)fired;
+            st.hist[i] = h;
+            recent = h != 0ull;
             const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
             st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
         }
         if (fired) st.nspk[i] += 1u;
     }
     const uint32_t fword = __ballot_sync(0xffffffffu, fired);
-    if (lane == 0 && valid) st.ring[(size_t)(t & (kRingSlots - 1)) * net.nwords + (i >> 5)] = fword;
+    const uint32_t rword = __ballot_sync(0xffffffffu, recent);
+    if (lane == 0 && valid) {
+        st.ring[(size_t)(t & (kRingSlots - 1)) * net.nwords + (i >> 5)] = fword;
+        if (net.nstdp) st.recent[i >> 5] = rword;
+    }
 
     // ---- (2) arrival of row i at step t: its spike of step t - D (hist[delay])
     bool arr = false;
@@ -159,7 +170,7 @@ k_front(NetDev net, StateDev st) {
         const StdpDev &sd = net.stdp[p.stdp];
         int32_t tl = st.tlu[i];
         float xp = st.xpre[i];
-        // finalise a visit of step t-1 (its synapses were updated by k_slice(t-1))
+        // finalise a visit of step t-1 (its synapses were updated by k_stdp(t-1))
         if (t >= 1 && ((st.vmask[par ^ 1u][i >> 5] >> (i & 31)) & 1u)) {
             const bool arr_prev = (t - 1 >= (int64_t)net.D) && ring_bit(st.ring, net.nwords, t - 1 - net.D, i);
             xp = xpre_after(sd, xp, (int)(t - 1 - tl), arr_prev);
@@ -183,16 +194,16 @@ k_front(NetDev net, StateDev st) {
     }
     const uint32_t vword = __ballot_sync(0xffffffffu, visit);
     if (net.nstdp && lane == 0 && valid) st.vmask[par][i >> 5] = vword;
-    const bool sarr = arr && !plastic_row;          // static arrivals (rows without STDP)
     uint32_t sv, sa, nv, na;
-    compact2(cs, visit, sarr, sv, sa, nv, na);
+    compact2(cs, visit, arr, sv, sa, nv, na);
     const size_t region = (size_t)blockIdx.x * kFrontThreads;
     if (visit) st.vdesc[par][region + sv] = d;
-    if (sarr) {
+    if (arr) {                                       // every arriving row is delivered
         RowDesc a;
         a.start = st.row_ptr[i];
         a.row = i;
         a.meta = kMetaArr | ((uint32_t)(p.rcpt_uniform & 3) << 8);
+        if (p.rcpt_uniform < 0) a.meta |= (uint32_t)pi << 16;
         a.xp = 0.0f;
         a.s0 = a.s1 = 0;
         a.pad = 0;
@@ -202,401 +213,429 @@ k_front(NetDev net, StateDev st) {
     const uint32_t na_all = __syncthreads_count(arr);
     const uint32_t nflush = __syncthreads_count(visit && !arr);
     if (threadIdx.x == 0) st.cnt[par][blockIdx.x] = make_uint4(nv, na, na_all, nflush);
+    trace_mark(st.trace, 0, 3);
 }
 
-// ------------------------------------------------------------------ k_slice
-constexpr int kSliceThreads = 512;
-constexpr int kSliceWarps = kSliceThreads / 32;
-constexpr int kMaxPieces = 512;     // piece table entries per round
+// ------------------------------------------------------- list region prefix
+// Per-CTA list regions (k_front) -> exclusive prefix over the regions of the
+// selected count (0 = visits, 1 = arrivals), into pre[0..nblk].
+template <int kThreads>
+__device__ __forceinline__ void region_prefix(const uint4 *cnt, uint32_t nblk, int which, uint32_t *pre,
+                                              uint32_t *wsum) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t per = (nblk + kThreads - 1) / kThreads;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t sv = 0;
+    for (uint32_t b = b0; b < min(b0 + per, nblk); b++) sv += which ? cnt[b].y : cnt[b].x;
+    uint32_t iv = sv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, iv, o);
+        if (lane >= o) iv += x;
+    }
+    if (lane == 31) wsum[warp] = iv;
+    __syncthreads();
+    uint32_t ov = 0;
+    for (uint32_t w2 = 0; w2 < warp; w2++) ov += wsum[w2];
+    uint32_t rv = ov + iv - sv;
+    for (uint32_t b = b0; b < min(b0 + per, nblk); b++) {
+        pre[b] = rv;
+        rv += which ? cnt[b].y : cnt[b].x;
+    }
+    if (threadIdx.x == kThreads - 1) pre[nblk] = rv;
+}
 
-// Map a flattened row index r (over the per-CTA regions) to its descriptor.
-__device__ __forceinline__ RowDesc fetch_row(const uint32_t *pre_v, const uint32_t *pre_a, uint32_t nblk, uint32_t nV,
-                                             const RowDesc *V, const RowDesc *A, uint32_t r) {
-    const uint32_t *pre = r < nV ? pre_v : pre_a;
-    const uint32_t x = r < nV ? r : r - nV;
-    uint32_t lo = 0, hi = nblk;          // largest b with pre[b] <= x
+// Row index r over the per-CTA regions -> position in the region array.
+__device__ __forceinline__ size_t region_index(const uint32_t *pre, uint32_t nblk, uint32_t r) {
+    uint32_t lo = 0, hi = nblk;          // largest b with pre[b] <= r
     while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (pre[mid] <= x) lo = mid; else hi = mid;
+        if (pre[mid] <= r) lo = mid; else hi = mid;
     }
-    const size_t idx = (size_t)lo * kFrontThreads + (x - pre[lo]);
-    return r < nV ? V[idx] : A[idx];
+    return (size_t)lo * kFrontThreads + (r - pre[lo]);
 }
 
-// One plastic synapse update (Fig. 2c with the closed-form skip-ahead of R7):
-// potentiation for every post spike in the window, oldest first (P:284
-// "__clz"), then the depression of an arriving pre spike.
-__device__ __forceinline__ float stdp_update(const StdpDev &sd, float w, uint64_t m, float xp, int age, bool arr,
-                                             float xpost) {
+// ---------------------------------------------------- CTA row-table helpers
+// Block-wide inclusive scan of one u32 per thread (kThreads <= 1024).
+template <int kThreads>
+__device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t *wsum, uint32_t &total) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += x;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t off = 0, tot = 0;
+    for (int w2 = 0; w2 < kThreads / 32; w2++) {
+        const uint32_t x = wsum[w2];
+        if (w2 < (int)warp) off += x;
+        tot += x;
+    }
+    total = tot;
+    return off + inc;
+}
+
+// Index of the row whose [incl - len, incl) range holds e (incl ascending).
+__device__ __forceinline__ uint32_t owner_search(const uint32_t *incl, uint32_t n, uint32_t e) {
+    uint32_t lo = 0, hi = n;            // first r with incl[r] > e
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (incl[mid] <= e) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// ------------------------------------------------------------------ k_stdp
+constexpr int kStdpThreads = 256;
+constexpr int kStdpWarps = kStdpThreads / 32;
+constexpr int kStdpRows = kStdpThreads;   // row table per round (one row per thread)
+constexpr int kStdpU = 2;                 // 16-byte chunks in flight per lane
+
+struct __align__(16) StdpRow {   // one visited row of this CTA (shared memory)
+    int64_t cb;           // 16-byte aligned CSR offset of its plastic span
+    uint32_t lo, hi;      // valid elements [lo, hi) relative to cb
+    float xp;             // x_pre at tlu
+    uint32_t meta;
+    uint32_t first;       // flattened index of its first 16-byte chunk
+    uint32_t pad;
+};
+
+// Potentiation by the post spikes in m (oldest first, "__clz") with the
+// closed-form skip-ahead of R7: w = min(w + A+ (x_pre D+[age - p]), w_max).
+__device__ __forceinline__ float potentiate(float w, uint64_t m, float xp, int age, const float *dp, float a_plus,
+                                            float w_max) {
     while (m) {
         const int pb = 63 - __clzll((long long)m);
         m &= ~(1ull << pb);
-        const float x = __fmul_rn(xp, sd.dplus[age - pb]);
-        const float nw = __fadd_rn(w, __fmul_rn(sd.a_plus, x));
-        w = nw < sd.w_max ? nw : sd.w_max;
-    }
-    if (arr) {
-        const float nw = __fsub_rn(w, __fmul_rn(sd.a_minus, xpost));
-        w = nw > 0.0f ? nw : 0.0f;
+        const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, dp[age - pb])));
+        w = nw < w_max ? nw : w_max;
     }
     return w;
 }
 
-// ---- TMA bulk copy + mbarrier helpers (sm_90+ async proxy; SASS UBLKCP / SYNCS)
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
+// Lazy + event-driven STDP over the visited rows (Fig. 2c).  For each plastic
+// synapse (i -> j):
+//   m = hist[j] & window(age)        post spikes in steps (tlu, t]   (R2)
+//   for set bits p, oldest first:    w = min(w + A+ (x_pre D+[age-p]), w_max)
+//   on an arrival:                   w = max(w - A- x_post[j], 0)
+// The CTA takes a contiguous share of the visited rows, tabulates them in
+// shared memory, and its warps split the flattened 16-byte chunks of all those
+// rows evenly (a lane keeps its current row's fields in registers).  hist[j] is
+// gathered only when the shared bitmap says j fired in the last 64 steps (a
+// superset of every window), x_post[j] only on arrivals; all gathers of a pass
+// are issued before any is consumed.
+__global__ void __launch_bounds__(kStdpThreads, 3)
+k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t wsum[kStdpWarps];
+    __shared__ float dplus_s[4 * (kHistBits + 1)];
+    __shared__ StdpRow rows_s[kStdpRows];
+    __shared__ uint32_t incl_s[kStdpRows];
+    const uint32_t nblk = st.nblk;
+    const bool readout = t_fixed >= 0;
+    const int64_t t = readout ? t_fixed : st.ctr->t;
+    const uint32_t par = (uint32_t)(t & 1);
+    const RowDesc *Vl = readout ? st.rdesc : st.vdesc[par];
+    const uint4 *cnt = readout ? st.rcnt : st.cnt[par];
+    const uint32_t w_lo = (pp_lo >> 7) << 2, w_hi = (pp_hi + 31) >> 5;     // 16-byte aligned start
+    uint32_t *pre = reinterpret_cast<uint32_t *>(smem);                       // [nblk + 1]
+    uint32_t *recent_s = pre + ((nblk + 1 + 3) & ~3u);                        // [w_hi - w_lo]
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (!readout) trace_mark(st.trace, 1, 0);
+
+    {   // bitmap of recently fired post-synaptic neurons: 16-byte loads, all issued first
+        const uint32_t n4 = (w_hi - w_lo + 3) >> 2;
+        const uint4 *src = reinterpret_cast<const uint4 *>(st.recent + w_lo);
+        uint4 *dst = reinterpret_cast<uint4 *>(recent_s);
+        constexpr int kMaxU = 16;
+        uint4 v[kMaxU];
+#pragma unroll
+        for (int u = 0; u < kMaxU; u++) {
+            const uint32_t x = threadIdx.x + u * kStdpThreads;
+            if (x < n4) v[u] = src[x];
+        }
+#pragma unroll
+        for (int u = 0; u < kMaxU; u++) {
+            const uint32_t x = threadIdx.x + u * kStdpThreads;
+            if (x < n4) dst[x] = v[u];
+        }
+        for (uint32_t x = threadIdx.x + kMaxU * kStdpThreads; x < n4; x += kStdpThreads) dst[x] = src[x];
+    }
+    for (uint32_t x = threadIdx.x; x < net.nstdp * (kHistBits + 1); x += kStdpThreads)
+        dplus_s[x] = net.stdp[x / (kHistBits + 1)].dplus[x % (kHistBits + 1)];
+    region_prefix<kStdpThreads>(cnt, nblk, 0, pre, wsum);
+    __syncthreads();
+    const uint32_t nV = pre[nblk];
+    if (!readout) trace_mark(st.trace, 1, 1);
+    const uint32_t r_begin = (uint32_t)(((uint64_t)nV * blockIdx.x) / gridDim.x);
+    const uint32_t r_end = (uint32_t)(((uint64_t)nV * (blockIdx.x + 1)) / gridDim.x);
+    uint32_t n_syn = 0, n_w = 0;
+    for (uint32_t r0 = r_begin; r0 < r_end; r0 += kStdpRows) {
+        // ---- tabulate up to kStdpRows rows (one per thread), chunk prefix
+        const uint32_t r = r0 + threadIdx.x;
+        uint32_t nch = 0;
+        StdpRow rw;
+        rw.cb = 0;
+        rw.lo = rw.hi = 0;
+        rw.xp = 0.0f;
+        rw.meta = 0;
+        if (r < r_end) {
+            const RowDesc d = Vl[region_index(pre, nblk, r)];
+            const bool arr = (d.meta & kMetaArr) != 0;
+            const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
+            // a flush with x_pre == 0 changes no weight (potentiation adds 0)
+            if (cs < ce && (arr || d.xp != 0.0f)) {
+                rw.cb = cs & ~3ll;
+                rw.lo = (uint32_t)(cs - rw.cb);
+                rw.hi = (uint32_t)(ce - rw.cb);
+                rw.xp = d.xp;
+                rw.meta = d.meta;
+                nch = (rw.hi + 3) >> 2;
+                n_syn += (uint32_t)(ce - cs);
+            }
+        }
+        __syncthreads();                           // previous round done with the table
+        uint32_t T = 0;
+        const uint32_t inc = block_incl_scan<kStdpThreads>(nch, wsum, T);
+        rw.first = inc - nch;
+        rw.pad = 0;
+        rows_s[threadIdx.x] = rw;
+        incl_s[threadIdx.x] = inc;
+        const uint32_t nrows = min(r_end - r0, (uint32_t)kStdpRows);
+        __syncthreads();
+        if (!readout) trace_mark(st.trace, 1, 2);
+        // ---- warps split the T chunks evenly; lane = one 16-byte chunk per slot
+        const uint32_t c_begin = (uint32_t)(((uint64_t)T * warp) / kStdpWarps);
+        const uint32_t c_end = (uint32_t)(((uint64_t)T * (warp + 1)) / kStdpWarps);
+        if (c_begin >= c_end) continue;
+        // current row of this lane (refreshed when its chunk passes the row end)
+        uint32_t o = owner_search(incl_s, nrows, min(c_begin + lane, c_end - 1));
+        StdpRow cur = rows_s[o];
+        uint32_t o_end = incl_s[o];
+        for (uint32_t base = c_begin; base < c_end; base += 32 * kStdpU) {
+            uint4 j4[kStdpU];
+            float4 w4[kStdpU];
+            int64_t cc[kStdpU];
+            uint32_t lo4[kStdpU], hi4[kStdpU];      // valid elements of the chunk: [lo4, hi4)
+            uint32_t meta4[kStdpU];
+            float xp4[kStdpU];
+#pragma unroll
+            for (int u = 0; u < kStdpU; u++) {
+                const uint32_t ch = base + 32 * u + lane;
+                lo4[u] = hi4[u] = 0;
+                meta4[u] = 0;
+                xp4[u] = 0.0f;
+                cc[u] = 0;
+                if (ch < c_end) {
+                    while (ch >= o_end) {
+                        o++;
+                        cur = rows_s[o];
+                        o_end = incl_s[o];
+                    }
+                    const uint32_t x0 = 4 * (ch - cur.first);
+                    cc[u] = cur.cb + x0;
+                    lo4[u] = cur.lo > x0 ? cur.lo - x0 : 0u;
+                    hi4[u] = min(cur.hi - x0, 4u);
+                    meta4[u] = cur.meta;
+                    xp4[u] = cur.xp;
+                    j4[u] = __ldg(reinterpret_cast<const uint4 *>(st.idx + cc[u]));
+                    w4[u] = *reinterpret_cast<const float4 *>(st.w + cc[u]);
+                }
+            }
+            // gathers: every history / post trace this pass needs, before any use
+            uint64_t h[kStdpU * 4];
+            float xq[kStdpU * 4];
+#pragma unroll
+            for (int u = 0; u < kStdpU; u++) {
+                const uint32_t jj[4] = {j4[u].x, j4[u].y, j4[u].z, j4[u].w};
+                const bool arr = (meta4[u] & kMetaArr) != 0;
+                const bool pot = xp4[u] != 0.0f;
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const bool in = e >= (int)lo4[u] && e < (int)hi4[u];
+                    const uint32_t j = jj[e];
+                    const bool rec = in && pot && ((recent_s[(j >> 5) - w_lo] >> (j & 31)) & 1u);
+                    h[4 * u + e] = rec ? __ldg(st.hist + j) : 0ull;
+                    xq[4 * u + e] = (in && arr) ? __ldg(st.xpost + j) : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kStdpU; u++) {
+                const bool arr = (meta4[u] & kMetaArr) != 0;
+                const int age = (int)(meta4[u] & 0x7fu);
+                const uint64_t wmask = age >= 64 ? ~0ull : ((1ull << age) - 1ull);
+                const uint32_t si = (meta4[u] >> 12) & 0xfu;
+                const float *dp = dplus_s + si * (kHistBits + 1);
+                const StdpDev &sd = net.stdp[si];
+                const float ww[4] = {w4[u].x, w4[u].y, w4[u].z, w4[u].w};
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const bool in = e >= (int)lo4[u] && e < (int)hi4[u];
+                    const uint64_t m = h[4 * u + e] & wmask;     // post spikes in (tlu, t], R2
+                    if (!in || (m == 0ull && !arr)) continue;
+                    float w = potentiate(ww[e], m, xp4[u], age, dp, sd.a_plus, sd.w_max);
+                    if (arr) {                                    // pre spike at t, after the posts
+                        const float nw = __fsub_rn(w, __fmul_rn(sd.a_minus, xq[4 * u + e]));
+                        w = nw > 0.0f ? nw : 0.0f;
+                    }
+                    if (__float_as_uint(w) != __float_as_uint(ww[e])) {
+                        st.w[cc[u] + e] = w;
+                        n_w++;
+                    }
+                }
+            }
+        }
+    }
+    n_syn = __reduce_add_sync(0xffffffffu, n_syn);
+    n_w = __reduce_add_sync(0xffffffffu, n_w);
+    if (lane == 0) {
+        if (n_syn) atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
+        if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
+    }
+    if (!readout && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&st.ctr->metric[2], (unsigned long long)nV);
+    if (!readout) {
+        __syncthreads();
+        trace_mark(st.trace, 1, 3);
     }
 }
 
-// A piece = one (row, slice) segment (or a part of a long one): the 16-byte
-// aligned span [cb, cb + 4*n4) of the CSR arrays staged by one bulk copy each
-// for the target ids and the weights.
-struct __align__(16) Piece {
-    int64_t cb;          // aligned CSR offset of the span
-    uint32_t lohi;       // valid elements [lo, hi) relative to cb (16 + 16 bit)
-    uint32_t prange;     // plastic elements [p0, p1) relative to cb (16 + 16 bit)
-    uint32_t meta;       // RowDesc meta; bits 16-19 = source population
-    float xp;
-    uint32_t n4;         // 4-element chunks staged
-    uint32_t pad;
-};
+// --------------------------------------------------------------- k_deliver
+constexpr int kDelThreads = 512;
+constexpr int kDelWarps = kDelThreads / 32;
+constexpr int kDelRows = 1024;     // row table per round (two rows per thread)
+constexpr int kDelU = 8;           // elements in flight per lane
 
-// One CTA = (slice k, split s).  Round structure:
-//   1. all threads: each takes one of this CTA's rows (per-CTA list regions,
-//      k_front) -> descriptor + pivot pair (Fig. 1 / P:348) -> the pieces of its
-//      segment, block-compacted into the shared piece table;
-//   2. every warp runs its own TMA pipeline over pieces warp, warp+16, ...:
-//      kStages bulk copies in flight, each piece processed from shared memory
-//      32 lanes wide (STDP update, changed weights stored back, delivery by
-//      int32 shared atomics).
-template <int kStages>
-__global__ void __launch_bounds__(kSliceThreads, 2)
-k_slice(NetDev net, StateDev st, int64_t t_fixed, uint32_t slot_elems) {
-    extern __shared__ __align__(128) unsigned char smem[];
+// One CTA per (slice k, split s) (Fig. 3b): the CTA tabulates the
+// (row, slice) segments of its share of the arriving rows (descriptor + pivot
+// pair) in shared memory, its warps split the flattened elements evenly
+// and walk them 32 lanes wide with kDelU loads in flight per lane; each element
+// adds q(w) = RNE(w 2^F) to the slice accumulator with a shared atomic.
+__global__ void __launch_bounds__(kDelThreads, 2)
+k_deliver(NetDev net, StateDev st) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t wsum[kDelWarps];
+    __shared__ int64_t s_c0[kDelRows];       // CSR offset of element 0 of the flattened range of row r
+    __shared__ uint32_t s_inc[kDelRows];
+    __shared__ uint32_t s_rc[kDelRows];
     const uint32_t C = net.C;
     const uint32_t nblk = st.nblk;
-    // t_fixed < 0: step t = ctr->t with the lists of parity t & 1;
-    // t_fixed >= 0: read-out flush at t_fixed, no delivery.
-    const bool deliver = t_fixed < 0;
-    const int64_t t = deliver ? st.ctr->t : t_fixed;
+    const int64_t t = st.ctr->t;
     const uint32_t par = (uint32_t)(t & 1);
-    const RowDesc *Vl = deliver ? st.vdesc[par] : st.rdesc;
     const RowDesc *Al = st.adesc[par];
-    const uint4 *cnt = deliver ? st.cnt[par] : st.rcnt;
-
-    // shared memory carve-up (all offsets 16-byte multiples)
-    const uint32_t npre = (nblk + 1 + 3) & ~3u;
-    unsigned char *p = smem;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(p);            p += 16 * kSliceWarps * kStages / 2 * 1;  // [warps][stages]
-    Piece *pieces = reinterpret_cast<Piece *>(p);                p += sizeof(Piece) * kMaxPieces;
-    uint32_t *slots = reinterpret_cast<uint32_t *>(p);           p += 8ull * slot_elems * kSliceWarps * kStages;
-    int32_t *acc = reinterpret_cast<int32_t *>(p);               p += 4ull * net.nrcpt * C;
-    uint64_t *hist_s = reinterpret_cast<uint64_t *>(p);          p += net.nstdp ? 8ull * C : 0;
-    float *xpost_s = reinterpret_cast<float *>(p);               p += net.nstdp ? 4ull * C : 0;
-    uint32_t *pre_v = reinterpret_cast<uint32_t *>(p);           p += 4ull * npre;
-    uint32_t *pre_a = reinterpret_cast<uint32_t *>(p);          p += 4ull * npre;
-    float *dplus_s = reinterpret_cast<float *>(p);              // [nstdp][65]
-
+    const uint4 *cnt = st.cnt[par];
+    uint32_t *pre = reinterpret_cast<uint32_t *>(smem);                         // [nblk + 1]
+    int32_t *acc = reinterpret_cast<int32_t *>(pre + ((nblk + 1 + 3) & ~3u));  // [nrcpt][C]
     const uint32_t k = blockIdx.x;
     const uint32_t nsplit = gridDim.y, split = blockIdx.y;
     const uint32_t slo = net.tgt_lo + (k << net.log2C);
     const uint32_t shi = min(slo + C, net.tgt_hi);
     const uint32_t width = shi > slo ? shi - slo : 0u;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    trace_mark(st.trace, 2, 0);
 
-    __shared__ uint32_t wsum[2][kSliceWarps];
-    __shared__ uint32_t s_round[2];
-    // ---- barriers
-    if (threadIdx.x < kSliceWarps * kStages) mbar_init(&bars[threadIdx.x], 1);
-    // ---- per-CTA list regions -> exclusive prefix sums (visits, static arrivals)
-    {
-        const uint32_t per = (nblk + kSliceThreads - 1) / kSliceThreads;
-        const uint32_t b0 = threadIdx.x * per;
-        uint32_t sv = 0, sa = 0;
-        for (uint32_t b = b0; b < min(b0 + per, nblk); b++) {
-            const uint4 c4 = cnt[b];
-            sv += c4.x;
-            sa += deliver ? c4.y : 0u;
-        }
-        uint32_t iv = sv, ia = sa;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t xv = __shfl_up_sync(0xffffffffu, iv, o), xa = __shfl_up_sync(0xffffffffu, ia, o);
-            if (lane >= o) {
-                iv += xv;
-                ia += xa;
-            }
-        }
-        if (lane == 31) {
-            wsum[0][warp] = iv;
-            wsum[1][warp] = ia;
-        }
-        __syncthreads();
-        uint32_t ov = 0, oa = 0;
-        for (uint32_t w2 = 0; w2 < warp; w2++) {
-            ov += wsum[0][w2];
-            oa += wsum[1][w2];
-        }
-        uint32_t rv = ov + iv - sv, ra = oa + ia - sa;
-        for (uint32_t b = b0; b < min(b0 + per, nblk); b++) {
-            pre_v[b] = rv;
-            pre_a[b] = ra;
-            const uint4 c4 = cnt[b];
-            rv += c4.x;
-            ra += deliver ? c4.y : 0u;
-        }
-        if (threadIdx.x == kSliceThreads - 1) {
-            pre_v[nblk] = rv;
-            pre_a[nblk] = ra;
-        }
-    }
-    for (uint32_t x = threadIdx.x; x < net.nstdp * (kHistBits + 1); x += blockDim.x)
-        dplus_s[x] = net.stdp[x / (kHistBits + 1)].dplus[x % (kHistBits + 1)];
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // ---- stage: zero accumulators, load the slice's histories / post traces
-    if (deliver)
-        for (uint32_t x = threadIdx.x; x < net.nrcpt * C; x += blockDim.x) acc[x] = 0;
-    bool post_plastic = false;
-    for (uint32_t q = 0; q < net.npop; q++) {
-        const PopDev &pp = net.pop[q];
-        if ((pp.flags & PF_POST_PLASTIC) && pp.base < shi && pp.base + pp.n > slo) post_plastic = true;
-    }
+    region_prefix<kDelThreads>(cnt, nblk, 1, pre, wsum);
+    for (uint32_t x = threadIdx.x; x < net.nrcpt * C; x += kDelThreads) acc[x] = 0;
     __syncthreads();
-    const uint32_t nV = pre_v[nblk];
-    const uint32_t nA = pre_a[nblk];
-    if (post_plastic && nV > 0) {
-        for (uint32_t x = threadIdx.x; x < width; x += blockDim.x) {
-            hist_s[x] = st.hist[slo + x];
-            xpost_s[x] = st.xpost[slo + x];
-        }
-    }
-    // (the first __syncthreads of the round loop publishes the staging)
-
+    const uint32_t nA = k < net.nslices ? pre[nblk] : 0u;
+    const uint32_t r_begin = (uint32_t)(((uint64_t)nA * split) / nsplit);
+    const uint32_t r_end = (uint32_t)(((uint64_t)nA * (split + 1)) / nsplit);
     const uint32_t P = net.nslices + 1;
     const float scale = net.scale;
-    uint32_t n_syn = 0, n_w = 0, n_ev = 0, n_seg = 0, n_el = 0;
-    const uint32_t total = nV + nA;
-    const uint32_t r_begin = (uint32_t)(((uint64_t)total * split) / nsplit);
-    const uint32_t r_end = (uint32_t)(((uint64_t)total * (split + 1)) / nsplit);
-    uint64_t *mybars = bars + warp * kStages;
-    uint32_t *myslots = slots + (size_t)warp * kStages * 2 * slot_elems;
-    uint32_t uses = 0;     // pieces this warp has consumed so far (barrier phase tracking)
-    for (uint32_t r0 = r_begin; r0 < r_end;) {
-        // ---- 1. rows -> pieces
-        const uint32_t r = r0 + threadIdx.x;
-        uint32_t np = 0, chunks = 0;
-        int64_t cb0 = 0;
-        uint32_t lo = 0, hi = 0, cp0 = 0, cp1 = 0, meta = 0;
-        uint32_t c_syn = 0, c_ev = 0;
-        float xp = 0.0f;
-        if (r < r_end) {
-            const RowDesc d = fetch_row(pre_v, pre_a, nblk, nV, Vl, Al, r);
-            const uint32_t *pv = st.piv + (size_t)d.row * P + k;
-            const uint32_t q0 = pv[0], q1 = pv[1];
-            const bool arr = (d.meta & kMetaArr) != 0;
-            uint32_t ps0 = 0, ps1 = 0;
-            if (d.meta & kMetaPlastic) {
-                ps0 = min(max(d.s0, q0), q1) - q0;
-                ps1 = max(min(d.s1, q1), q0) - q0;
-            }
-            xp = d.xp;
-            const bool pot = xp != 0.0f;       // potentiation adds A+ x_pre D+[n] = 0 otherwise
-            const bool active = q1 > q0 && (arr || (pot && ps1 > ps0));   // a flush that changes no weight is skipped
-            if (active) {
-                const int64_t rs = d.start + q0;
-                const int64_t cs = rs + (arr ? 0 : ps0);
-                const int64_t ce = rs + (arr ? (q1 - q0) : ps1);
-                cb0 = cs & ~3ll;
-                lo = (uint32_t)(cs - cb0);
-                hi = (uint32_t)(ce - cb0);
-                cp0 = (uint32_t)(rs + ps0 - cb0 < 0 ? 0 : rs + ps0 - cb0);
-                cp1 = (uint32_t)(rs + ps1 - cb0 < 0 ? 0 : rs + ps1 - cb0);
-                chunks = (hi + 3) >> 2;
-                np = (chunks * 4 + slot_elems - 1) / slot_elems;
-                meta = d.meta & 0xffffu;
-                if (((d.meta >> 8) & 3u) == 3u) meta |= (uint32_t)find_pop(net, d.row) << 16;
-                c_syn = ps1 - ps0;
-                c_ev = arr ? (q1 - q0) : 0u;
-            }
-        }
-        // block exclusive scan of np; rows whose pieces overflow the table wait
-        uint32_t inc = np;
+    uint32_t n_ev = 0, n_seg = 0;
+    for (uint32_t r0 = r_begin; r0 < r_end; r0 += kDelRows) {
+        // ---- tabulate (two rows per thread): descriptor + pivot pair
+        uint32_t len2[2] = {0, 0};
+        RowDesc d2[2];
+        uint2 pp[2];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += x;
+        for (int q = 0; q < 2; q++) {                 // both rows' loads in flight together
+            const uint32_t r = r0 + threadIdx.x * 2 + q;
+            if (r < r_end) d2[q] = Al[region_index(pre, nblk, r)];
         }
-        __syncthreads();                       // previous round fully consumed
-        if (lane == 31) wsum[0][warp] = inc;
-        __syncthreads();
-        uint32_t off = 0;
-        for (uint32_t w2 = 0; w2 < warp; w2++) off += wsum[0][w2];
-        const uint32_t excl = off + inc - np;
-        const bool fits = excl + np <= kMaxPieces;
-        if (fits && np) {
-            n_syn += c_syn;
-            n_ev += c_ev;
-            n_el += hi - lo;
-            n_seg += 1;
-            const uint32_t per = slot_elems / 4;   // chunks per piece
-            for (uint32_t q = 0; q < np; q++) {
-                Piece pc;
-                pc.cb = cb0 + 4ll * per * q;
-                const uint32_t base = 4 * per * q;
-                const uint32_t n4 = min(per, chunks - per * q);
-                const uint32_t vlo = lo > base ? lo - base : 0u;
-                const uint32_t vhi = min(hi - base, 4 * n4);
-                const uint32_t plo = cp0 > base ? min(cp0 - base, 4 * n4) : 0u;
-                const uint32_t phi = cp1 > base ? min(cp1 - base, 4 * n4) : 0u;
-                pc.lohi = vlo | (vhi << 16);
-                pc.prange = plo | (phi << 16);
-                pc.meta = meta;
-                pc.xp = xp;
-                pc.n4 = n4;
-                pc.pad = 0;
-                pieces[excl + q] = pc;
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            const uint32_t r = r0 + threadIdx.x * 2 + q;
+            if (r < r_end) {
+                const uint32_t *pv = st.piv + (size_t)d2[q].row * P + k;
+                pp[q] = make_uint2(pv[0], pv[1]);
             }
         }
-        // rows consumed this round: the prefix of rows whose pieces fit
-        if (threadIdx.x == 0) s_round[0] = 0;
-        const uint32_t fitcount = __syncthreads_count(fits && r < r_end);
-        if (fits && np) atomicMax(&s_round[0], excl + np);
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            const uint32_t r = r0 + threadIdx.x * 2 + q;
+            if (r >= r_end) continue;
+            len2[q] = pp[q].y - pp[q].x;
+            uint32_t rc = (d2[q].meta >> 8) & 3u;
+            if (rc == 3u) rc = 3u | (((d2[q].meta >> 16) & 0xfu) << 2);
+            s_rc[threadIdx.x * 2 + q] = rc;
+            s_c0[threadIdx.x * 2 + q] = d2[q].start + pp[q].x;
+        }
+        n_ev += len2[0] + len2[1];
+        n_seg += (len2[0] != 0) + (len2[1] != 0);
+        uint32_t T = 0;
+        const uint32_t inc = block_incl_scan<kDelThreads>(len2[0] + len2[1], wsum, T);
+        s_inc[threadIdx.x * 2] = inc - len2[1];
+        s_inc[threadIdx.x * 2 + 1] = inc;
+        s_c0[threadIdx.x * 2] -= (int64_t)(inc - len2[1] - len2[0]);   // element e at s_c0[o] + e
+        s_c0[threadIdx.x * 2 + 1] -= (int64_t)(inc - len2[1]);
+        const uint32_t nrows = min(r_end - r0, (uint32_t)kDelRows);
         __syncthreads();
-        const uint32_t npieces = s_round[0];
-        r0 += fitcount;
-
-        // ---- 2. per-warp TMA pipeline over pieces warp, warp + 16, ...
-        auto issue = [&](uint32_t pi, uint32_t stage) {
-            const Piece &pc = pieces[pi];
-            uint32_t *dst = myslots + stage * 2 * slot_elems;
-            const uint32_t bytes = pc.n4 * 16u;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&mybars[stage], 2 * bytes);
-            bulk_g2s(dst, st.idx + pc.cb, bytes, &mybars[stage]);
-            bulk_g2s(dst + slot_elems, st.w + pc.cb, bytes, &mybars[stage]);
-        };
-        const uint32_t mine = warp < npieces ? (npieces - warp + kSliceWarps - 1) / kSliceWarps : 0u;
-        if (lane == 0)
-            for (uint32_t q = 0; q < min(mine, (uint32_t)kStages); q++) issue(warp + q * kSliceWarps, (uses + q) % kStages);
-        __syncwarp();
-        for (uint32_t q = 0; q < mine; q++) {
-            const uint32_t pi = warp + q * kSliceWarps;
-            const uint32_t stage = (uses + q) % kStages;
-            const uint32_t phase = ((uses + q) / kStages) & 1u;
-            mbar_wait(&mybars[stage], phase);
-            const Piece pc = pieces[pi];
-            const uint32_t *jv = myslots + stage * 2 * slot_elems;
-            const float *wv = reinterpret_cast<const float *>(jv + slot_elems);
-            const uint32_t vlo = pc.lohi & 0xffffu, vhi = pc.lohi >> 16;
-            const uint32_t plo = pc.prange & 0xffffu, phi = pc.prange >> 16;
-            const int age = (int)(pc.meta & 0x7fu);
-            const uint64_t wmask = age >= 64 ? ~0ull : ((1ull << age) - 1ull);
-            const float xp = pc.xp;
-            const uint32_t si = (pc.meta >> 12) & 0xfu;
-            const float a_plus = net.stdp[si].a_plus, a_minus = net.stdp[si].a_minus, w_max = net.stdp[si].w_max;
-            const float *dp = dplus_s + si * (kHistBits + 1);
-            float *wg = st.w + pc.cb;
-            if (!(pc.meta & kMetaArr)) {
-                // forced flush (R3): only the plastic span, potentiation only
-                for (uint32_t x = vlo + lane; x < vhi; x += 32) {
-                    uint64_t m = hist_s[jv[x] - slo] & wmask;       // post spikes in (tlu, t], R2
-                    if (m) {
-                        float w = wv[x];
-                        do {                                         // oldest first, "__clz"
-                            const int pb = 63 - __clzll((long long)m);
-                            m &= ~(1ull << pb);
-                            const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, dp[age - pb])));
-                            w = nw < w_max ? nw : w_max;
-                        } while (m);
-                        wg[x] = w;
-                        n_w++;
-                    }
-                }
-            } else {
-                // arrival: STDP on the plastic span (posts, then the pre spike at t),
-                // then delivery of every element of the segment
-                const bool pot = xp != 0.0f;
-                const int rc = (int)((pc.meta >> 8) & 3u);
-                int32_t *accr = acc + (rc == 3 ? 0 : rc) * C;
-                for (uint32_t x = vlo + lane; x < vhi; x += 32) {
-                    const uint32_t j = jv[x];
-                    const uint32_t jl = j - slo;
-                    float w = wv[x];
-                    if (x >= plo && x < phi) {
-                        uint64_t m = pot ? (hist_s[jl] & wmask) : 0ull;
-                        while (m) {
-                            const int pb = 63 - __clzll((long long)m);
-                            m &= ~(1ull << pb);
-                            const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, dp[age - pb])));
-                            w = nw < w_max ? nw : w_max;
-                        }
-                        const float nw = __fsub_rn(w, __fmul_rn(a_minus, xpost_s[jl]));
-                        w = nw > 0.0f ? nw : 0.0f;
-                        wg[x] = w;
-                        n_w++;
-                    }
-                    if (deliver) {
-                        int32_t *a = accr;
-                        if (rc == 3) a = acc + net.rcpt[(pc.meta >> 16) & 0xfu][find_pop(net, j)] * C;
-                        atomicAdd(a + jl, __float2int_rn(__fmul_rn(w, scale)));
-                    }
+        trace_mark(st.trace, 2, 1);
+        // ---- warps split the T elements evenly
+        const uint32_t e_begin = (uint32_t)(((uint64_t)T * warp) / kDelWarps);
+        const uint32_t e_end = (uint32_t)(((uint64_t)T * (warp + 1)) / kDelWarps);
+        uint32_t o = e_begin < e_end ? owner_search(s_inc, nrows, e_begin + lane) : 0u;
+        for (uint32_t base = e_begin; base < e_end; base += 32 * kDelU) {
+            uint32_t jj[kDelU], oo[kDelU];
+            float ww[kDelU];
+#pragma unroll
+            for (int u = 0; u < kDelU; u++) {
+                const uint32_t e = base + u * 32 + lane;
+                oo[u] = 0xffffffffu;
+                if (e < e_end) {
+                    while (e >= s_inc[o]) o++;
+                    const int64_t c = s_c0[o] + e;
+                    jj[u] = __ldg(st.idx + c);
+                    ww[u] = st.w[c];
+                    oo[u] = o;
                 }
             }
-            __syncwarp();
-            const uint32_t nq = q + kStages;
-            if (lane == 0 && nq < mine) issue(warp + nq * kSliceWarps, stage);
-            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < kDelU; u++) {
+                if (oo[u] == 0xffffffffu) continue;
+                uint32_t rr = s_rc[oo[u]];
+                if (rr >= 3u) rr = (uint32_t)net.rcpt[rr >> 2][find_pop(net, jj[u])];
+                atomicAdd(&acc[rr * C + (jj[u] - slo)], __float2int_rn(__fmul_rn(ww[u], scale)));
+            }
         }
-        uses += mine;
+        __syncthreads();                           // table reused next round
     }
+    trace_mark(st.trace, 2, 2);
     // ---- write-back (one coalesced pass; several CTAs may share a slice)
-    __syncthreads();
-    if (deliver) {
-        for (uint32_t rr = 0; rr < net.nrcpt; rr++) {
-            int32_t *dst = rr == 0 ? st.in_e : st.in_i;
-            for (uint32_t x = threadIdx.x; x < width; x += blockDim.x) {
-                const int32_t v = acc[rr * C + x];
-                if (v != 0) atomicAdd(dst + slo + x, v);
-            }
+    for (uint32_t rr = 0; rr < net.nrcpt; rr++) {
+        int32_t *dst = rr == 0 ? st.in_e : st.in_i;
+        for (uint32_t x = threadIdx.x; x < width; x += kDelThreads) {
+            const int32_t v = acc[rr * C + x];
+            if (v != 0) atomicAdd(dst + slo + x, v);
         }
     }
-    // ---- counters
-    n_syn = __reduce_add_sync(0xffffffffu, n_syn);
-    n_w = __reduce_add_sync(0xffffffffu, n_w);
     n_ev = __reduce_add_sync(0xffffffffu, n_ev);
     n_seg = __reduce_add_sync(0xffffffffu, n_seg);
-    n_el = __reduce_add_sync(0xffffffffu, n_el);
     if (lane == 0) {
-        if (n_el) atomicAdd(&st.ctr->metric[7], (unsigned long long)n_el);
-        if (n_syn) atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
-        if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
-        if (n_ev) atomicAdd(&st.ctr->metric[0], (unsigned long long)n_ev);
+        if (n_ev) {
+            atomicAdd(&st.ctr->metric[0], (unsigned long long)n_ev);
+            atomicAdd(&st.ctr->metric[7], (unsigned long long)n_ev);
+        }
         if (n_seg) atomicAdd(&st.ctr->metric[6], (unsigned long long)n_seg);
     }
-    if (!deliver) return;
     // ---- step completion: the last CTA books the list counts and advances t
-    __threadfence();
     __syncthreads();
+    trace_mark(st.trace, 2, 3);
     if (threadIdx.x == 0) {
+        __threadfence();
         const uint32_t nb = gridDim.x * gridDim.y;
         const uint32_t tk = atomicAdd(&st.ctr->ticket, 1u);
         if (tk == nb - 1) {
@@ -607,7 +646,6 @@ k_slice(NetDev net, StateDev st, int64_t t_fixed, uint32_t slot_elems) {
                 flushes += c4.w;
             }
             st.ctr->metric[1] += spikes;
-            st.ctr->metric[2] += nV;
             st.ctr->metric[5] += flushes;
             st.ctr->ticket = 0;
             __threadfence();
@@ -660,7 +698,7 @@ k_readout_prepare(NetDev net, StateDev st, int64_t t_last) {
     if (threadIdx.x == 0) st.rcnt[blockIdx.x] = make_uint4(n0, 0u, 0u, 0u);
 }
 
-// (3) after k_slice ran the flush on the listed rows: their x_pre / tlu.
+// (3) after k_stdp ran the flush on the listed rows: their x_pre / tlu.
 __global__ void __launch_bounds__(kFrontThreads)
 k_readout_finish(NetDev net, StateDev st, int64_t t_last) {
     if (threadIdx.x >= st.rcnt[blockIdx.x].x) return;
@@ -692,44 +730,42 @@ cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s) 
     return cudaGetLastError();
 }
 
-constexpr int kStagesDefault = 4;
-
-size_t slice_smem_bytes(const NetDev &net, uint32_t slot_elems) {
+size_t stdp_smem_bytes(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
     const size_t nblk = front_blocks(net);
-    size_t b = 16ull * kSliceWarps * kStagesDefault / 2;          // mbarriers
-    b += sizeof(Piece) * kMaxPieces;
-    b += 8ull * slot_elems * kSliceWarps * kStagesDefault;         // staged ids + weights
-    b += 4ull * net.nrcpt * net.C;
-    if (net.nstdp) b += 12ull * net.C;
-    b += 8 * ((nblk + 1 + 3) & ~(size_t)3);
-    b += 4ull * 4 * (kHistBits + 1);                               // D+ tables
-    return b;
+    return 4 * ((nblk + 1 + 3) & ~(size_t)3) + 4ull * (((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 4);
 }
 
-cudaError_t slice_configure(const NetDev &net, uint32_t slot_elems) {
-    return cudaFuncSetAttribute(k_slice<kStagesDefault>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)slice_smem_bytes(net, slot_elems));
+size_t deliver_smem_bytes(const NetDev &net) {
+    const size_t nblk = front_blocks(net);
+    return 4 * ((nblk + 1 + 3) & ~(size_t)3) + 4ull * net.nrcpt * net.C;
 }
 
-static cudaError_t launch_slice(const NetDev &net, const StateDev &st, int64_t t_fixed, uint32_t splits,
-                                uint32_t slot_elems, cudaStream_t s) {
-    dim3 grid(net.nslices > 0 ? net.nslices : 1, splits);
-    k_slice<kStagesDefault><<<grid, kSliceThreads, slice_smem_bytes(net, slot_elems), s>>>(net, st, t_fixed,
-                                                                                        slot_elems);
+cudaError_t kernels_configure(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
+    cudaError_t e = cudaFuncSetAttribute(k_deliver, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)deliver_smem_bytes(net));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_stdp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)stdp_smem_bytes(net, pp_lo, pp_hi));
+}
+
+cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, uint32_t grid, uint32_t pp_lo,
+                        uint32_t pp_hi, cudaStream_t s) {
+    k_stdp<<<grid, kStdpThreads, stdp_smem_bytes(net, pp_lo, pp_hi), s>>>(net, st, t_fixed, pp_lo, pp_hi);
     return cudaGetLastError();
 }
 
-cudaError_t launch_step_slice(const NetDev &net, const StateDev &st, uint32_t splits, uint32_t slot_elems,
-                              cudaStream_t s) {
-    return launch_slice(net, st, -1, splits, slot_elems, s);
+cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s) {
+    dim3 grid(net.nslices > 0 ? net.nslices : 1, splits);
+    k_deliver<<<grid, kDelThreads, deliver_smem_bytes(net), s>>>(net, st);
+    return cudaGetLastError();
 }
 
-cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last, uint32_t splits,
-                           uint32_t slot_elems, cudaStream_t s) {
+cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last, uint32_t grid, uint32_t pp_lo,
+                           uint32_t pp_hi, cudaStream_t s) {
     k_readout_prepare<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if ((e = launch_slice(net, st, t_last, splits, slot_elems, s)) != cudaSuccess) return e;
+    if ((e = launch_stdp(net, st, t_last, grid, pp_lo, pp_hi, s)) != cudaSuccess) return e;
     k_readout_finish<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
     return cudaGetLastError();
 }

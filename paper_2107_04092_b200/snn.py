@@ -27,19 +27,20 @@ SNN_OK, SNN_E_INVALID, SNN_E_STATE, SNN_E_OOM, SNN_E_CUDA, SNN_E_NCCL, SNN_E_UNS
 POISSON, LIF_DELTA, LIF_CUBA = 0, 1, 2
 STATIC, STDP = 0, 1
 EXC, INH = 0, 1
-FLAG_NO_GRAPH, FLAG_PHASE_TIMING = 1, 2
+FLAG_NO_GRAPH, FLAG_PHASE_TIMING, FLAG_TRACE = 1, 2, 4
 ALL = 0xFFFFFFFF
 
 FIELD = dict(V=0, REFRACTORY=1, G_EXC=2, G_INH=3, INPUT_EXC=4, INPUT_INH=5, HIST=6, SPIKE_COUNT=7,
              XPOST=8, XPRE_ROW=9, TLU=10, ROW_PTR=11, IDX=12, WEIGHTS=13, PIVOTS=14, STEP=15,
-             METRICS=16, SPIKE_RING=17, PHASE_TIMES=18, INFO=19)
+             METRICS=16, SPIKE_RING=17, PHASE_TIMES=18, INFO=19, TRACE=20)
 FIELD_DTYPE = dict(V=np.float32, REFRACTORY=np.int32, G_EXC=np.float32, G_INH=np.float32,
                    INPUT_EXC=np.int32, INPUT_INH=np.int32, HIST=np.uint64, SPIKE_COUNT=np.uint32,
                    XPOST=np.float32, XPRE_ROW=np.float32, TLU=np.int32, ROW_PTR=np.int64,
                    IDX=np.uint32, WEIGHTS=np.float32, PIVOTS=np.uint32, STEP=np.int64,
-                   METRICS=np.uint64, SPIKE_RING=np.uint32, PHASE_TIMES=np.float64, INFO=np.int64)
+                   METRICS=np.uint64, SPIKE_RING=np.uint32, PHASE_TIMES=np.float64, INFO=np.int64,
+                   TRACE=np.uint64)
 METRIC = dict(EVENTS=0, SPIKES=1, STDP_ROWS=2, STDP_SYN=3, STDP_WTOUCH=4, FLUSH_ROWS=5, SEGMENTS=6, ELEMS=7)
-PHASE = dict(FRONT=0, SLICE=1, EXCHANGE=2, TOTAL=3)
+PHASE = dict(FRONT=0, STDP=1, DELIVERY=2, EXCHANGE=3, TOTAL=4)
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
@@ -183,7 +184,8 @@ class Snn:
                     return None
 
             def _free(ptr, strm, ctx):
-                torch.cuda.caching_allocator_delete(ptr)
+                if torch is not None and torch.cuda is not None:   # not at interpreter teardown
+                    torch.cuda.caching_allocator_delete(ptr)
 
             self._keep += [ALLOC_FN(_alloc), FREE_FN(_free)]
             cfg.dev_alloc, cfg.dev_free = self._keep

@@ -1,0 +1,29 @@
+"""Per-CTA phase trace of one simulation step (debug, SNN_FLAG_TRACE)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import workloads as W
+from paper_2107_04092_b200 import Snn, FLAG_TRACE
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+C = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+rc = W.config(cfg)
+g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, flags=FLAG_TRACE)
+rc.apply(g)
+g.step(1500)
+torch.cuda.synchronize()
+for rep in range(3):
+    g.step(1)
+    tr = g.read_state("TRACE").reshape(3, 4096, 4).astype(np.int64)
+    t0 = tr[0][tr[0][:, 0] > 0][:, 0].min()
+    for k, name in enumerate(["front", "stdp", "deliver"]):
+        a = tr[k]
+        a = a[a[:, 0] > 0]
+        if len(a) == 0:
+            continue
+        rel = (a - t0) / 1000.0
+        print(f"{name:8s} ctas={len(a):4d} start[min/med/max]={rel[:,0].min():7.2f}/{np.median(rel[:,0]):7.2f}/{rel[:,0].max():7.2f} "
+              + " ".join(f"ph{p}[med/max]={np.median(rel[:,p]-rel[:,0]):6.2f}/{(rel[:,p]-rel[:,0]).max():6.2f}" for p in (1, 2, 3))
+              + f" end_max={rel[:,3].max():7.2f}")
+    print(g.metrics())
