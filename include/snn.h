@@ -80,9 +80,11 @@ enum {
     SNN_FLAG_PHASE_TIMING = 1u << 1, /* record CUDA events around every phase of
                                         every step (implies NO_GRAPH); read with
                                         SNN_FIELD_PHASE_TIMES                       */
-    SNN_FLAG_TRACE = 1u << 2         /* debug: per-CTA %globaltimer phase marks of
+    SNN_FLAG_TRACE = 1u << 2,        /* debug: per-CTA %globaltimer phase marks of
                                         the last step (implies NO_GRAPH); read with
                                         SNN_FIELD_TRACE                             */
+    SNN_FLAG_NO_PDL = 1u << 3        /* no programmatic dependent launch between
+                                        the kernels of a step                       */
 };
 
 typedef struct {

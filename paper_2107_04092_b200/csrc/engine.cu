@@ -20,12 +20,12 @@ cudaError_t build_fill(const NetDev &, const BuildTabs &, const uint32_t *, cons
 cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, uint2 *, cudaStream_t);
 cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
 uint32_t front_blocks(const NetDev &);
-cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t);
+cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool);
 size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
 size_t deliver_smem_bytes(const NetDev &);
 cudaError_t kernels_configure(const NetDev &, uint32_t, uint32_t);
-cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
-cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t);
+cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
+cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
 }  // namespace snn
@@ -314,16 +314,19 @@ static snn_status finalize(snn_sim *sim) {
 }
 
 // ---------------------------------------------------------------- the step
-static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev) {
+static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bool first) {
     const NetDev &net = sim->net;
     const StateDev &st = sim->st;
+    // programmatic dependent launch between the kernels of the graph (not
+    // across event records, whose timing would then overlap)
+    const bool pdl = ev == nullptr && !(sim->cfg.flags & SNN_FLAG_NO_PDL);
     if (ev) CK(cudaEventRecord(ev[0], s));
-    CK(launch_front(net, st, s));                                   // (1) P:36 + work lists
+    CK(launch_front(net, st, s, pdl && !first));                    // (1) P:36 + work lists
     if (ev) CK(cudaEventRecord(ev[1], s));
     if (sim->plastic)                                               // (2) P:37-39
-        CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s));
+        CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
     if (ev) CK(cudaEventRecord(ev[2], s));
-    CK(launch_deliver(net, st, sim->splits, s));                    // (3) P:41
+    CK(launch_deliver(net, st, sim->splits, s, pdl));               // (3) P:41
     if (ev) CK(cudaEventRecord(ev[3], s));
     return SNN_OK;
 }
@@ -332,7 +335,7 @@ static snn_status capture(snn_sim *sim, uint32_t nsteps, cudaGraphExec_t *out) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(sim->cap_stream, cudaStreamCaptureModeThreadLocal));
     for (uint32_t k = 0; k < nsteps; k++) {
-        snn_status r = enqueue_step(sim, sim->cap_stream, nullptr);
+        snn_status r = enqueue_step(sim, sim->cap_stream, nullptr, k == 0);
         if (r != SNN_OK) {
             cudaStreamEndCapture(sim->cap_stream, &g);
             if (g) cudaGraphDestroy(g);
@@ -474,7 +477,7 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
                 }
                 ev = sim->ev_steps[sim->ev_used++].data();
             }
-            snn_status r = enqueue_step(sim, sim->stream, ev);
+            snn_status r = enqueue_step(sim, sim->stream, ev, true);
             if (r != SNN_OK) return r;
             sim->t++;
         }

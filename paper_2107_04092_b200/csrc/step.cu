@@ -26,6 +26,12 @@
 
 namespace snn {
 
+// Programmatic dependent launch (PDL): the next kernel of the step is launched
+// early and parks at pdl_wait() until this grid has completed and flushed;
+// pdl_launch() lets the dependent grid start.  No-ops without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t ring_bit(const uint32_t *ring, uint32_t nwords, int64_t step, uint32_t i) {
     return (ring[(size_t)(step & (kRingSlots - 1)) * nwords + (i >> 5)] >> (i & 31)) & 1u;
 }
@@ -81,6 +87,8 @@ __device__ __forceinline__ void compact2(Compact2 &sm, bool a, bool b, uint32_t 
 __global__ void __launch_bounds__(kFrontThreads)
 k_front(NetDev net, StateDev st) {
     __shared__ Compact2 cs;
+    pdl_wait();            // k_deliver(t-1): inputs, step counter
+    pdl_launch();
     trace_mark(st.trace, 0, 0);
     const int64_t t = st.ctr->t;
     const uint32_t par = (uint32_t)(t & 1);
@@ -289,6 +297,60 @@ __device__ __forceinline__ uint32_t owner_search(const uint32_t *incl, uint32_t 
 }
 
 // ------------------------------------------------------------------ k_stdp
+// Shared / predicated global loads written out in PTX so that the compiler
+// neither re-derives the shared window per access nor branches around a load.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint64_t ldg_u64_if(const uint64_t *p, uint32_t pred) {
+    uint64_t v;
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.b64 %0, 0;\n @q ld.global.nc.u64 %0, [%1];\n}\n"
+                 : "=l"(v) : "l"(p), "r"(pred));
+    return v;
+}
+__device__ __forceinline__ float ldg_f32_if(const float *p, uint32_t pred) {
+    float v;
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.b32 %0, 0f00000000;\n @q ld.global.nc.f32 %0, [%1];\n}\n"
+                 : "=f"(v) : "l"(p), "r"(pred));
+    return v;
+}
+__device__ __forceinline__ void stg_f32_if(float *p, float v, uint32_t pred) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}\n"
+                 :: "l"(p), "f"(v), "r"(pred) : "memory");
+}
+
+// One plastic synapse (Fig. 2c, R7), written branch-free for the common cases:
+// potentiation by the post spikes in m, oldest first ("__clz") with the
+// closed-form skip-ahead w = min(w + A+ (x_pre D+[age - p]), w_max) -- the
+// first spike by selects, further ones (rare) in a loop -- then, on an
+// arrival, the depression w = max(w - A- x_post, 0).  dp = shared address of
+// the D+ table of the projection.
+__device__ __forceinline__ float stdp_synapse(float w, uint64_t m, bool arr, float xq, float xp, int age,
+                                              uint32_t dp, float a_plus, float a_minus, float w_max) {
+    const bool has = m != 0ull;
+    const int pb = 63 - __clzll((long long)m);
+    const float d = lds_f32(dp + 4u * (uint32_t)(has ? age - pb : 0));
+    const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, d)));
+    w = has ? (nw < w_max ? nw : w_max) : w;
+    m = has ? (m & ~(1ull << (pb & 63))) : 0ull;
+    while (m) {
+        const int pb2 = 63 - __clzll((long long)m);
+        m &= ~(1ull << pb2);
+        const float nw2 = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, lds_f32(dp + 4u * (uint32_t)(age - pb2)))));
+        w = nw2 < w_max ? nw2 : w_max;
+    }
+    const float dw = __fsub_rn(w, __fmul_rn(a_minus, xq));
+    return arr ? (dw > 0.0f ? dw : 0.0f) : w;
+}
+
 constexpr int kStdpThreads = 256;
 constexpr int kStdpWarps = kStdpThreads / 32;
 constexpr int kStdpRows = kStdpThreads;   // row table per round (one row per thread)
@@ -302,19 +364,6 @@ struct __align__(16) StdpRow {   // one visited row of this CTA (shared memory)
     uint32_t first;       // flattened index of its first 16-byte chunk
     uint32_t pad;
 };
-
-// Potentiation by the post spikes in m (oldest first, "__clz") with the
-// closed-form skip-ahead of R7: w = min(w + A+ (x_pre D+[age - p]), w_max).
-__device__ __forceinline__ float potentiate(float w, uint64_t m, float xp, int age, const float *dp, float a_plus,
-                                            float w_max) {
-    while (m) {
-        const int pb = 63 - __clzll((long long)m);
-        m &= ~(1ull << pb);
-        const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, dp[age - pb])));
-        w = nw < w_max ? nw : w_max;
-    }
-    return w;
-}
 
 // Lazy + event-driven STDP over the visited rows (Fig. 2c).  For each plastic
 // synapse (i -> j):
@@ -344,6 +393,10 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     uint32_t *pre = reinterpret_cast<uint32_t *>(smem);                       // [nblk + 1]
     uint32_t *recent_s = pre + ((nblk + 1 + 3) & ~3u);                        // [w_hi - w_lo]
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t *__restrict__ ghist = st.hist;
+    const float *__restrict__ gxpost = st.xpost;
+    pdl_wait();            // k_front(t): lists, histories, bitmap
+    pdl_launch();          // k_deliver may start its prologue (k_front is complete)
     if (!readout) trace_mark(st.trace, 1, 0);
 
     {   // bitmap of recently fired post-synaptic neurons: 16-byte loads, all issued first
@@ -369,6 +422,9 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     region_prefix<kStdpThreads>(cnt, nblk, 0, pre, wsum);
     __syncthreads();
     const uint32_t nV = pre[nblk];
+    // 32-bit shared addresses: bitmap word of neuron j at rs_addr + 4 (j >> 5); D+ tables
+    const uint32_t rs_addr = smem_u32(recent_s) - 4u * w_lo;
+    const uint32_t dp_addr = smem_u32(dplus_s);
     if (!readout) trace_mark(st.trace, 1, 1);
     const uint32_t r_begin = (uint32_t)(((uint64_t)nV * blockIdx.x) / gridDim.x);
     const uint32_t r_end = (uint32_t)(((uint64_t)nV * (blockIdx.x + 1)) / gridDim.x);
@@ -446,6 +502,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 }
             }
             // gathers: every history / post trace this pass needs, before any use
+            // (branch-free: bitmap probe at a clamped index, predicated loads)
             uint64_t h[kStdpU * 4];
             float xq[kStdpU * 4];
 #pragma unroll
@@ -456,10 +513,11 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
                     const bool in = e >= (int)lo4[u] && e < (int)hi4[u];
-                    const uint32_t j = jj[e];
-                    const bool rec = in && pot && ((recent_s[(j >> 5) - w_lo] >> (j & 31)) & 1u);
-                    h[4 * u + e] = rec ? __ldg(st.hist + j) : 0ull;
-                    xq[4 * u + e] = (in && arr) ? __ldg(st.xpost + j) : 0.0f;
+                    const uint32_t j = in ? jj[e] : pp_lo;
+                    const uint32_t word = lds_u32(rs_addr + ((j >> 5) << 2));
+                    const uint32_t rec = (in && pot) ? ((word >> (j & 31)) & 1u) : 0u;
+                    h[4 * u + e] = ldg_u64_if(ghist + j, rec);
+                    xq[4 * u + e] = ldg_f32_if(gxpost + j, (in && arr) ? 1u : 0u);
                 }
             }
 #pragma unroll
@@ -468,23 +526,18 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 const int age = (int)(meta4[u] & 0x7fu);
                 const uint64_t wmask = age >= 64 ? ~0ull : ((1ull << age) - 1ull);
                 const uint32_t si = (meta4[u] >> 12) & 0xfu;
-                const float *dp = dplus_s + si * (kHistBits + 1);
+                const uint32_t dp = dp_addr + si * 4u * (kHistBits + 1);
                 const StdpDev &sd = net.stdp[si];
                 const float ww[4] = {w4[u].x, w4[u].y, w4[u].z, w4[u].w};
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
                     const bool in = e >= (int)lo4[u] && e < (int)hi4[u];
-                    const uint64_t m = h[4 * u + e] & wmask;     // post spikes in (tlu, t], R2
-                    if (!in || (m == 0ull && !arr)) continue;
-                    float w = potentiate(ww[e], m, xp4[u], age, dp, sd.a_plus, sd.w_max);
-                    if (arr) {                                    // pre spike at t, after the posts
-                        const float nw = __fsub_rn(w, __fmul_rn(sd.a_minus, xq[4 * u + e]));
-                        w = nw > 0.0f ? nw : 0.0f;
-                    }
-                    if (__float_as_uint(w) != __float_as_uint(ww[e])) {
-                        st.w[cc[u] + e] = w;
-                        n_w++;
-                    }
+                    const uint64_t m = in ? (h[4 * u + e] & wmask) : 0ull;     // post spikes in (tlu, t], R2
+                    const float w = stdp_synapse(ww[e], m, arr, xq[4 * u + e], xp4[u], age, dp, sd.a_plus,
+                                                 sd.a_minus, sd.w_max);
+                    const uint32_t chg = (in && __float_as_uint(w) != __float_as_uint(ww[e])) ? 1u : 0u;
+                    stg_f32_if(st.w + cc[u] + e, w, chg);
+                    n_w += chg;
                 }
             }
         }
@@ -536,6 +589,9 @@ k_deliver(NetDev net, StateDev st) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     trace_mark(st.trace, 2, 0);
 
+    // prologue: reads only k_front(t)'s lists -- complete before k_stdp(t)
+    // triggered this launch; without STDP the primary IS k_front(t), so wait
+    if (net.nstdp == 0) pdl_wait();
     region_prefix<kDelThreads>(cnt, nblk, 1, pre, wsum);
     for (uint32_t x = threadIdx.x; x < net.nrcpt * C; x += kDelThreads) acc[x] = 0;
     __syncthreads();
@@ -583,6 +639,10 @@ k_deliver(NetDev net, StateDev st) {
         s_c0[threadIdx.x * 2 + 1] -= (int64_t)(inc - len2[1]);
         const uint32_t nrows = min(r_end - r0, (uint32_t)kDelRows);
         __syncthreads();
+        if (r0 == r_begin) {
+            pdl_wait();    // k_stdp(t): updated weights of plastic arrivals
+            pdl_launch();
+        }
         trace_mark(st.trace, 2, 1);
         // ---- warps split the T elements evenly
         const uint32_t e_begin = (uint32_t)(((uint64_t)T * warp) / kDelWarps);
@@ -612,6 +672,10 @@ k_deliver(NetDev net, StateDev st) {
             }
         }
         __syncthreads();                           // table reused next round
+    }
+    if (r_begin >= r_end) {        // no rows: still order the write-back after k_stdp(t)
+        pdl_wait();
+        pdl_launch();
     }
     trace_mark(st.trace, 2, 2);
     // ---- write-back (one coalesced pass; several CTAs may share a slice)
@@ -725,9 +789,25 @@ __global__ void k_hist_from_ring(NetDev net, const uint32_t *ring, int64_t t_las
 // ---------------------------------------------------------------- launchers
 uint32_t front_blocks(const NetDev &net) { return (net.N + kFrontThreads - 1) / kFrontThreads; }
 
-cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s) {
-    k_front<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st);
-    return cudaGetLastError();
+// Launch with the programmatic-stream-serialization attribute (PDL).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, bool pdl) {
+    return launch_pdl(k_front, dim3(front_blocks(net)), dim3(kFrontThreads), 0, s, pdl, net, st);
 }
 
 size_t stdp_smem_bytes(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
@@ -749,15 +829,14 @@ cudaError_t kernels_configure(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi)
 }
 
 cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, uint32_t grid, uint32_t pp_lo,
-                        uint32_t pp_hi, cudaStream_t s) {
-    k_stdp<<<grid, kStdpThreads, stdp_smem_bytes(net, pp_lo, pp_hi), s>>>(net, st, t_fixed, pp_lo, pp_hi);
-    return cudaGetLastError();
+                        uint32_t pp_hi, cudaStream_t s, bool pdl) {
+    return launch_pdl(k_stdp, dim3(grid), dim3(kStdpThreads), stdp_smem_bytes(net, pp_lo, pp_hi), s, pdl, net, st,
+                      t_fixed, pp_lo, pp_hi);
 }
 
-cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s) {
+cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s, bool pdl) {
     dim3 grid(net.nslices > 0 ? net.nslices : 1, splits);
-    k_deliver<<<grid, kDelThreads, deliver_smem_bytes(net), s>>>(net, st);
-    return cudaGetLastError();
+    return launch_pdl(k_deliver, grid, dim3(kDelThreads), deliver_smem_bytes(net), s, pdl, net, st);
 }
 
 cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last, uint32_t grid, uint32_t pp_lo,
@@ -765,7 +844,7 @@ cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last
     k_readout_prepare<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if ((e = launch_stdp(net, st, t_last, grid, pp_lo, pp_hi, s)) != cudaSuccess) return e;
+    if ((e = launch_stdp(net, st, t_last, grid, pp_lo, pp_hi, s, false)) != cudaSuccess) return e;
     k_readout_finish<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
     return cudaGetLastError();
 }
