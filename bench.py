@@ -157,18 +157,43 @@ def main():
         return
 
     import torch
-    if world > 1:
-        raise SystemExit("multi-GPU bench: see DESIGN.md section 7 (not in this build yet)")
+    import torch.distributed as dist
     from paper_2107_04092_b200 import Snn, FLAG_PHASE_TIMING
+    from paper_2107_04092_b200 import dist as pdist
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
+    if world > 1:
+        # one process per GPU; torch.distributed bootstraps the library's NCCL
+        # communicator (the spike exchange runs inside libsnn.so), times reduce
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     rc = W.config(a.config, seed=a.seed, gpus=world)
     stream = torch.cuda.Stream(dev)
 
+    def make(flags=0):
+        uid = pdist.nccl_unique_id() if world > 1 else None
+        s = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream,
+                flags=flags, rank=rank, world=world, nccl_unique_id=uid)
+        rc.apply(s)
+        return s
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def reduce(x, op):
+        if world == 1:
+            return x
+        v = torch.tensor([float(x)], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(v, op=op)
+        return float(v.item())
+
+    MAX = dist.ReduceOp.MAX if world > 1 else None
+    SUM = dist.ReduceOp.SUM if world > 1 else None
+
     # ---------------------------------------------------------- device-timed
-    sim = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream)
-    rc.apply(sim)
+    sim = make()
     t0 = time.perf_counter()
     sim.finalize()
     torch.cuda.synchronize()
@@ -176,17 +201,17 @@ def main():
     info = sim.info()
     with ClockSampler(dev) as clk:
         sim.step(a.warmup)
-        torch.cuda.synchronize()
+        barrier()
         m0 = sim.metrics()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
+        barrier()
         ev0.record(stream)
         sim.step(a.steps)
         ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+        barrier()
+    ms = reduce(ev0.elapsed_time(ev1), MAX)                   # max over ranks
     m1 = sim.metrics()
-    dm = {k: m1[k] - m0[k] for k in m1}
+    dm = {k: int(reduce(m1[k] - m0[k], SUM)) for k in m1}     # work of all ranks
     spikes = sim.read_state("SPIKE_COUNT")
     t_total = (a.warmup + a.steps) * rc.dt_ms * 1e-3
     rates = {p.name: float(spikes[b:b + p.n].sum()) / p.n / t_total
@@ -202,7 +227,7 @@ def main():
         chunk = 64
         ring = np.empty(64 * ((info["N"] + 31) // 32), dtype=np.uint32)
         m0e = sim.metrics()
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         done = 0
         while done < a.steps:
@@ -212,9 +237,11 @@ def main():
             done += n
         t1 = time.perf_counter()
         m1e = sim.metrics()
-        e2e = {"value": (m1e["EVENTS"] - m0e["EVENTS"]) / (t1 - t0), "unit": "events/s",
+        wall = reduce(t1 - t0, MAX)
+        evs = reduce(m1e["EVENTS"] - m0e["EVENTS"], SUM)
+        e2e = {"value": evs / wall, "unit": "events/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(ring.nbytes / chunk),
-               "wall_s_per_bio_s": (t1 - t0) / (a.steps * rc.dt_ms * 1e-3),
+               "wall_s_per_bio_s": wall / (a.steps * rc.dt_ms * 1e-3),
                "note": "snn_step(64) + snn_read_state(SPIKE_RING) per 64 steps; an SNN step has no host input "
                        "(Poisson drive is counter-based on device), so h2d = 0"}
     sim.close()
@@ -223,9 +250,7 @@ def main():
 
     # ------------------------------------------- per-phase timing (roofline)
     psteps = a.phase_steps or a.steps
-    sp = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream,
-             flags=FLAG_PHASE_TIMING)
-    rc.apply(sp)
+    sp = make(FLAG_PHASE_TIMING)
     sp.step(a.warmup)
     sp.phase_times()   # drain warm-up events
     base = sp.phase_times()
@@ -233,8 +258,8 @@ def main():
     sp.step(psteps)
     ph = sp.phase_times()
     mp1 = sp.metrics()
-    ph = {k: ph[k] - base[k] for k in ph}
-    d = {k: mp1[k] - mp0[k] for k in mp1}
+    ph = {k: reduce(ph[k] - base[k], MAX) for k in ph}
+    d = {k: int(reduce(mp1[k] - mp0[k], SUM)) for k in mp1}
     sp.close()
     nrcpt = 2 if any(pr.receptor == W.INH for pr in rc.projs) else 1
     # algorithmic HBM bytes per kernel:
@@ -260,11 +285,13 @@ def main():
 
     out = {
         "metric": METRIC, "value": events_per_s, "unit": "events/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if a.config in (2, 3, 4) else "weak",
         "vs_baseline": None, "dtype": "f32 (int32 fixed-point accumulators)", "data": "synthetic",
         "config": {"workload": f"BASELINE config {a.config}: {rc.name}", "neurons": info["N"],
                    "synapses": info["S"], "plastic": rc.plastic, "dt_ms": rc.dt_ms, "delay_steps": rc.delay,
                    "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
+                   "parallelism": f"target-range partition x{world}, NCCL spike-word all-gather" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2: %.1f GB of graph, each step touches the rows of that step's spikes"
                          % (info["S"] * 8 / 1e9)},
         "wall_s_per_bio_s": wall_per_bio,
@@ -282,11 +309,14 @@ def main():
         "e2e": e2e,
         "clocks": clk.summary(),
     }
-    if not a.no_cpu_baseline and rank == 0:
+    if not a.no_cpu_baseline and rank == 0 and world == 1:
         r = run_oracle(a.config, a.seed, 2000, 50, budget_s=15.0)
         out["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
         out["cpu_baseline"]["wall_s_per_bio_s"] = r["wall_s_per_bio_s"]
-    print(json.dumps(out))
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -59,7 +59,8 @@ enum {
     SNN_E_CUDA = -4,        /* a CUDA runtime error (text in snn_last_error)   */
     SNN_E_NCCL = -5,        /* an NCCL error                                   */
     SNN_E_UNSUPPORTED = -6  /* valid but not implemented (e.g. 2 STDP
-                               projections from one source population)        */
+                               projections from one source population, or
+                               world > 1 with delay 0)                         */
 };
 
 /* population kinds (R9): */
@@ -108,8 +109,15 @@ typedef struct {
     void (*dev_free)(void *ptr, void *stream, void *ctx);
     void *alloc_ctx;
     /* world > 1: the 128-byte ncclUniqueId, identical on all ranks (the caller
-       broadcasts it, e.g. with torch.distributed).  Ignored when world == 1.   */
+       broadcasts it, e.g. with torch.distributed); the library then exchanges
+       the spike words with ncclAllGather (libnccl.so.2 is loaded at run time).
+       Ignored when world == 1.                                                  */
     const void *nccl_unique_id;
+    /* world > 1 without NCCL: a non-zero key shared by the `world` handles of
+       one process, which then exchange by device copies on the same GPU (a
+       test transport: partitions of one network on one GPU, stepped in
+       lockstep by the caller).                                                 */
+    uint64_t group_key;
 } snn_config;
 
 typedef struct {
@@ -238,6 +246,14 @@ const char *snn_last_error(const snn_sim *sim);
 
 /* The ABI version the library was built with (SNN_ABI_VERSION). */
 uint32_t snn_abi_version(void);
+
+/* Host-only helper (no device work): the target range [*lo, *hi) of `rank`
+ * among `world` ranks for n_targets neurons with inputs and slice width C --
+ * C-aligned equal shares, the last one truncated (the
+ * partition of the neuron domain of P:48 / P:348).  Errors: SNN_E_INVALID
+ * (world == 0, rank >= world, C not a power of two, NULL outputs). */
+snn_status snn_partition(uint32_t n_targets, uint32_t slice_width, uint32_t world, uint32_t rank, uint32_t *lo,
+                         uint32_t *hi);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,17 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "--fmad=false", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
+def nccl_include() -> str:
+    """nccl.h of the NCCL wheel torch ships (types only; libnccl is dlopen'ed)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    for p in (spec.submodule_search_locations or []) if spec else []:
+        inc = os.path.join(p, "include")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -30,7 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", nccl_include(), "-c",
+               os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -39,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-           "-Xcompiler", "-fPIC", "-lcudart"]
+           "-Xcompiler", "-fPIC", "-lcudart", "-ldl"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

@@ -45,7 +45,11 @@ struct NetDev {
     uint32_t R;          // neurons [0, R) may receive synapses (slice domain)
     uint32_t tgt_lo, tgt_hi;  // this rank's target range
     uint32_t C, log2C, nslices;   // slice width and number of local slices
-    uint32_t nwords;     // 32-bit words per ring slot = ceil(N/32)
+    uint32_t nwords;     // 32-bit words of spike bits per step = ceil(N/32)
+    uint32_t ring_stride;// words per ring slot (nwords + exchange padding)
+    uint32_t world, rank;        // ranks sharing the target range
+    uint32_t share_w;            // words per rank share (rank r owns words [r share_w, ...))
+    uint32_t wmax;               // words exchanged per rank and step
     uint32_t D;          // delay
     uint32_t npop, nstdp;
     int32_t F;           // fixed-point fraction bits
@@ -95,7 +99,7 @@ struct StateDev {
     int32_t *ref, *in_e, *in_i;
     uint64_t *hist;
     uint32_t *nspk;
-    uint32_t *ring;          // [kRingSlots][nwords]
+    uint32_t *ring;          // [kRingSlots][ring_stride]
     // source rows
     float *xpre;
     int32_t *tlu;
@@ -114,6 +118,8 @@ struct StateDev {
     uint32_t nblk;           // k_front CTAs = list regions
     uint32_t *vmask[2];      // [nwords] rows visited at the step of that parity
     uint32_t *recent;        // [nwords] bit i: post-plastic neuron i fired in the last 64 steps
+    uint32_t *sendbuf;       // [wmax] this rank's spike words of the step (world > 1)
+    uint32_t *gath;          // [2][world][wmax] all ranks' words (NCCL: slot 0; local group: by step parity)
     Counters *ctr;
     unsigned long long *trace;   // optional (SNN_FLAG_TRACE): per-CTA phase timestamps
 };

@@ -2,7 +2,13 @@
 // setup (graph construction) and the step orchestration:
 //   per step t:  k_neuron -> k_worklist -> k_stdp (if plastic) -> k_deliver
 // replayed from a captured CUDA graph of kGraphSteps steps.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <cmath>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -28,6 +34,7 @@ cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uin
 cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
+cudaError_t launch_unpack(const NetDev &, const StateDev &, const uint32_t *, int64_t, cudaStream_t);
 }  // namespace snn
 
 using namespace snn;
@@ -36,6 +43,42 @@ namespace {
 
 constexpr uint32_t kGraphSteps = 16;
 std::string g_create_error;
+
+// NCCL, loaded at run time (only world > 1 with an ncclUniqueId needs it)
+struct NcclApi {
+    void *lib = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*errorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_mu;
+std::map<uint64_t, std::vector<snn_sim *>> g_groups;   // local-group transport
+
+bool load_nccl(std::string &err) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_nccl.lib) return true;
+    const char *names[] = {getenv("SNN_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    for (const char *n : names) {
+        if (!n) continue;
+        g_nccl.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+        if (g_nccl.lib) break;
+    }
+    if (!g_nccl.lib) {
+        err = "cannot load libnccl.so.2 (set SNN_NCCL_LIB or import torch first)";
+        return false;
+    }
+    g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(g_nccl.lib, "ncclCommInitRank");
+    g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(g_nccl.lib, "ncclAllGather");
+    g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(g_nccl.lib, "ncclCommDestroy");
+    g_nccl.errorString = (decltype(g_nccl.errorString))dlsym(g_nccl.lib, "ncclGetErrorString");
+    if (!g_nccl.commInitRank || !g_nccl.allGather || !g_nccl.commDestroy || !g_nccl.errorString) {
+        err = "libnccl is missing symbols";
+        return false;
+    }
+    return true;
+}
 
 struct HostPop {
     snn_pop_params prm;
@@ -67,6 +110,10 @@ struct snn_sim {
     uint32_t pp_lo = 0, pp_hi = 0;       // post-plastic neuron range (bitmap span)
     bool plastic = false;
     uint64_t *d_hist_tmp = nullptr;
+    // exchange (world > 1)
+    uint32_t wmax = 0;
+    ncclComm_t comm = nullptr;
+    bool local_group = false;
     // phase timing
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::vector<cudaEvent_t>> ev_steps;  // per step: 5 boundary events
@@ -116,6 +163,53 @@ static uint64_t bernoulli_thr(double p) {
     if (!(p > 0.0)) return 0;
     if (p >= 1.0) return 1ull << 32;
     return (uint64_t)std::floor(p * 4294967296.0);
+}
+
+// ------------------------------------------------------------------ exchange
+static snn_status exchange_setup(snn_sim *sim) {
+    const snn_config &cfg = sim->cfg;
+    if (cfg.nccl_unique_id) {
+        std::string err;
+        if (!load_nccl(err)) return sim->fail(SNN_E_NCCL, "%s", err.c_str());
+        ncclUniqueId id;
+        memcpy(&id, cfg.nccl_unique_id, sizeof id);
+        const ncclResult_t r = g_nccl.commInitRank(&sim->comm, cfg.world, id, cfg.rank);
+        if (r != ncclSuccess) return sim->fail(SNN_E_NCCL, "ncclCommInitRank: %s", g_nccl.errorString(r));
+        return SNN_OK;
+    }
+    sim->local_group = true;
+    return SNN_OK;
+}
+
+// The step's exchange: this rank's share of spike words to every rank.
+// NCCL: all-gather into gath[0] and unpack into the ring within the step (the
+// ranks run concurrently; graph-capturable, fixed addresses).  Local group:
+// copy into every peer's gath[t & 1]; each peer unpacks it at the start of its
+// step t + 1 (the caller steps the peers in lockstep, so the parity double
+// buffer keeps step t's words until then).
+static snn_status exchange_enqueue(snn_sim *sim, cudaStream_t s, int64_t t) {
+    const StateDev &st = sim->st;
+    const snn_config &cfg = sim->cfg;
+    if (sim->comm) {
+        const ncclResult_t r = g_nccl.allGather(st.sendbuf, st.gath, sim->wmax, ncclUint32, sim->comm, s);
+        if (r != ncclSuccess) return sim->fail(SNN_E_NCCL, "ncclAllGather: %s", g_nccl.errorString(r));
+        CK(launch_unpack(sim->net, st, st.gath, -1, s));
+        return SNN_OK;
+    }
+    std::vector<snn_sim *> peers;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        peers = g_groups[cfg.group_key];
+    }
+    if ((int)peers.size() != cfg.world)
+        return sim->fail(SNN_E_STATE, "local group %llu has %zu of %d ranks", (unsigned long long)cfg.group_key,
+                         peers.size(), cfg.world);
+    for (snn_sim *p : peers) {
+        if (p->state == 0 || !p->st.gath) return sim->fail(SNN_E_STATE, "local group peer not finalized");
+        CK(cudaMemcpyAsync(p->st.gath + ((size_t)(t & 1) * cfg.world + cfg.rank) * sim->wmax, st.sendbuf,
+                           4ull * sim->wmax, cudaMemcpyDeviceToDevice, s));
+    }
+    return SNN_OK;
 }
 
 // --------------------------------------------------------------------- setup
@@ -201,23 +295,32 @@ static snn_status finalize(snn_sim *sim) {
                                  "(lower accum_frac_bits)", k, r, acc_bound[k][r]);
     }
     net.R = R;
-    if (cfg.world > 1) return sim->fail(SNN_E_UNSUPPORTED, "world > 1 not available in this build");
-    net.tgt_lo = 0;
-    net.tgt_hi = R;
     net.nrcpt = 1;
     for (const HostProj &hj : sim->projs)
         if (hj.prm.receptor == SNN_RCPT_INH) net.nrcpt = 2;
     // slice width C of the delivery ("delicate, tunable"): the
-    // paper's 1024 by default, shrunk so that there are at least ~1 slice per SM
-    // when the target range is small
+    // paper's 1024 by default, shrunk so that each rank keeps >= ~64 slices
+    // when its target range is small
     uint32_t C = cfg.slice_width;
     if (C == 0) {
         C = 1024;
-        while (C > 128 && (R + C - 1) / C < 64) C >>= 1;
+        while (C > 128 && (R / (uint32_t)cfg.world + C - 1) / C < 64) C >>= 1;
     }
     net.C = C;
     net.log2C = 0;
     while ((1u << net.log2C) < C) net.log2C++;
+    // this rank's target range: C-aligned equal shares of [0, R)
+    uint32_t lo = 0, hi = R;
+    snn_partition(R, C, (uint32_t)cfg.world, (uint32_t)cfg.rank, &lo, &hi);
+    if (cfg.world > 1) {
+        for (uint32_t k = 0; k < net.npop; k++)
+            if (net.pop[k].base < R && !(net.pop[k].flags & PF_HAS_INPUT))
+                return sim->fail(SNN_E_INVALID, "world > 1: add populations that receive synapses first");
+        if (cfg.delay_steps == 0)
+            return sim->fail(SNN_E_UNSUPPORTED, "world > 1 needs delay >= 1 (the exchange of step t overlaps step t+1)");
+    }
+    net.tgt_lo = lo;
+    net.tgt_hi = hi;
     net.nslices = (net.tgt_hi - net.tgt_lo + C - 1) / C;
     net.nwords = (net.N + 31) / 32;
     sim->plastic = net.nstdp > 0;
@@ -236,7 +339,20 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.in_i, int32_t, N);
     ALLOC(st.hist, uint64_t, N);
     ALLOC(st.nspk, uint32_t, N);
-    ALLOC(st.ring, uint32_t, (size_t)kRingSlots * net.nwords);
+    // exchange geometry: rank r owns words [r share_w, ...), at most share_w + 1
+    // of them (the word straddling R); ring slots padded for the unpack
+    net.world = (uint32_t)cfg.world;
+    net.rank = (uint32_t)cfg.rank;
+    {
+        const uint32_t W = (uint32_t)cfg.world;
+        const uint64_t share = ((uint64_t)(R + W - 1) / W + C - 1) / C * C;
+        net.share_w = (uint32_t)std::max<uint64_t>(1, share / 32);
+        net.wmax = net.share_w + 1;
+        sim->wmax = net.wmax;
+    }
+    net.ring_stride = net.nwords + (cfg.world > 1 ? net.wmax : 0);
+    ALLOC(st.ring, uint32_t, (size_t)kRingSlots * net.ring_stride);
+    st.sendbuf = st.gath = nullptr;
     ALLOC(st.xpre, float, N);
     ALLOC(st.tlu, int32_t, N);
     ALLOC(st.row_ptr, int64_t, (size_t)N + 1);
@@ -260,7 +376,15 @@ static snn_status finalize(snn_sim *sim) {
     }
     ALLOC(st.ctr, Counters, 1);
     cudaStream_t s = sim->stream;
-    CK(cudaMemsetAsync(st.ring, 0, sizeof(uint32_t) * (size_t)kRingSlots * net.nwords, s));
+    CK(cudaMemsetAsync(st.ring, 0, sizeof(uint32_t) * (size_t)kRingSlots * net.ring_stride, s));
+    if (cfg.world > 1) {
+        ALLOC(st.sendbuf, uint32_t, net.wmax);
+        ALLOC(st.gath, uint32_t, 2ull * net.wmax * cfg.world);
+        CK(cudaMemsetAsync(st.sendbuf, 0, 4ull * net.wmax, s));
+        CK(cudaMemsetAsync(st.gath, 0, 8ull * net.wmax * cfg.world, s));
+        snn_status r = exchange_setup(sim);
+        if (r != SNN_OK) return r;
+    }
     CK(cudaMemsetAsync(st.recent, 0, sizeof(uint32_t) * net.nwords, s));
     for (int b = 0; b < 2; b++) {
         CK(cudaMemsetAsync(st.vmask[b], 0, sizeof(uint32_t) * net.nwords, s));
@@ -306,7 +430,8 @@ static snn_status finalize(snn_sim *sim) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg.device);
     const uint32_t ns = std::max(1u, net.nslices);
-    sim->splits = std::max(1u, (uint32_t)(2 * nsm) / ns);
+    sim->splits = std::max(1u, (uint32_t)(2 * nsm) / ns);   // ~2 CTAs per SM, one wave
+    if (const char *sp = getenv("SNN_DELIVER_SPLITS")) sim->splits = std::max(1, atoi(sp));  // tuning knob
     sim->stdp_grid = 3 * (uint32_t)nsm;
     CK(cudaStreamSynchronize(s));
     sim->state = 1;
@@ -314,14 +439,22 @@ static snn_status finalize(snn_sim *sim) {
 }
 
 // ---------------------------------------------------------------- the step
-static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bool first) {
+static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bool first, int64_t step_k = 0) {
     const NetDev &net = sim->net;
     const StateDev &st = sim->st;
     // programmatic dependent launch between the kernels of the graph (not
     // across event records, whose timing would then overlap)
-    const bool pdl = ev == nullptr && !(sim->cfg.flags & SNN_FLAG_NO_PDL);
+    const bool multi = sim->cfg.world > 1;
+    const bool pdl = ev == nullptr && !(sim->cfg.flags & SNN_FLAG_NO_PDL) && !multi;
     if (ev) CK(cudaEventRecord(ev[0], s));
+    const int64_t t = sim->t + step_k;                              // host copy (direct mode only)
+    if (multi && sim->local_group && t > 0)                         // peers' spikes of t-1 -> ring
+        CK(launch_unpack(net, st, st.gath + (size_t)((t - 1) & 1) * sim->cfg.world * sim->wmax, t - 1, s));
     CK(launch_front(net, st, s, pdl && !first));                    // (1) P:36 + work lists
+    if (multi) {                                                    // spike words of t -> peers
+        snn_status r = exchange_enqueue(sim, s, t);
+        if (r != SNN_OK) return r;
+    }
     if (ev) CK(cudaEventRecord(ev[1], s));
     if (sim->plastic)                                               // (2) P:37-39
         CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
@@ -379,9 +512,9 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         g_create_error = "snn_config: dev_alloc and dev_free must both be set or both NULL";
         return SNN_E_INVALID;
     }
-    if (cfg->world > 1) {
-        g_create_error = "world > 1 not available in this build";
-        return SNN_E_UNSUPPORTED;
+    if (cfg->world > 1 && !cfg->nccl_unique_id && cfg->group_key == 0) {
+        g_create_error = "world > 1 needs an nccl_unique_id or a local group_key";
+        return SNN_E_INVALID;
     }
     cudaError_t e = cudaSetDevice(cfg->device);
     if (e != cudaSuccess) {
@@ -396,6 +529,18 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         g_create_error = std::string("cudaStreamCreate: ") + cudaGetErrorString(e);
         delete sim;
         return SNN_E_CUDA;
+    }
+    if (cfg->world > 1 && !cfg->nccl_unique_id) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        std::vector<snn_sim *> &g = g_groups[cfg->group_key];
+        for (snn_sim *p : g)
+            if (p->cfg.rank == cfg->rank || p->cfg.world != cfg->world) {
+                g_create_error = "local group: duplicate rank or mismatched world";
+                cudaStreamDestroy(sim->cap_stream);
+                delete sim;
+                return SNN_E_INVALID;
+            }
+        g.push_back(sim);
     }
     *out = sim;
     return SNN_OK;
@@ -465,7 +610,7 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
     }
     if (n_steps == 0) return SNN_OK;
     const bool timing = (sim->cfg.flags & SNN_FLAG_PHASE_TIMING) != 0;
-    const bool direct = timing || (sim->cfg.flags & (SNN_FLAG_NO_GRAPH | SNN_FLAG_TRACE)) != 0;
+    const bool direct = timing || (sim->cfg.flags & (SNN_FLAG_NO_GRAPH | SNN_FLAG_TRACE)) != 0 || sim->local_group;
     if (direct) {
         for (uint32_t k = 0; k < n_steps; k++) {
             cudaEvent_t *ev = nullptr;
@@ -562,6 +707,15 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
         snn_status r = readout_flush(sim);
         if (r != SNN_OK) return r;
     }
+    if (sim->local_group && sim->t > 0 && (field == SNN_FIELD_HIST || field == SNN_FIELD_SPIKE_RING))
+        CK(launch_unpack(net, st, st.gath + (size_t)((sim->t - 1) & 1) * sim->cfg.world * sim->wmax, sim->t - 1,
+                         s));                                      // the last step's remote words
+    if (field == SNN_FIELD_SPIKE_RING && net.ring_stride != net.nwords) {
+        CK(cudaMemcpy2DAsync(host_dst, 4ull * net.nwords, st.ring, 4ull * net.ring_stride, 4ull * net.nwords,
+                             kRingSlots, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return SNN_OK;
+    }
     if (field == SNN_FIELD_HIST) {
         if (!sim->d_hist_tmp) {
             sim->d_hist_tmp = (uint64_t *)sim->dalloc(8ull * sim->N);
@@ -594,8 +748,28 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
     return SNN_OK;
 }
 
+snn_status snn_partition(uint32_t n_targets, uint32_t slice_width, uint32_t world, uint32_t rank, uint32_t *lo,
+                         uint32_t *hi) {
+    if (world == 0 || rank >= world || !lo || !hi || slice_width == 0 || (slice_width & (slice_width - 1)))
+        return SNN_E_INVALID;
+    const uint64_t share = ((uint64_t)(n_targets + world - 1) / world + slice_width - 1) / slice_width * slice_width;
+    *lo = (uint32_t)std::min<uint64_t>((uint64_t)rank * share, n_targets);
+    *hi = (uint32_t)std::min<uint64_t>((uint64_t)(rank + 1) * share, n_targets);
+    return SNN_OK;
+}
+
 void snn_destroy(snn_sim *sim) {
     if (!sim) return;
+    if (sim->cfg.world > 1 && !sim->cfg.nccl_unique_id) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        std::vector<snn_sim *> &g = g_groups[sim->cfg.group_key];
+        for (size_t k = 0; k < g.size(); k++)
+            if (g[k] == sim) {
+                g.erase(g.begin() + k);
+                break;
+            }
+    }
+    if (sim->comm) g_nccl.commDestroy(sim->comm);
     if (sim->stream) cudaStreamSynchronize(sim->stream);
     cudaDeviceSynchronize();
     if (sim->g_many) cudaGraphExecDestroy(sim->g_many);

@@ -32,8 +32,8 @@ namespace snn {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-__device__ __forceinline__ uint32_t ring_bit(const uint32_t *ring, uint32_t nwords, int64_t step, uint32_t i) {
-    return (ring[(size_t)(step & (kRingSlots - 1)) * nwords + (i >> 5)] >> (i & 31)) & 1u;
+__device__ __forceinline__ uint32_t ring_bit(const uint32_t *ring, uint32_t stride, int64_t step, uint32_t i) {
+    return (ring[(size_t)(step & (kRingSlots - 1)) * stride + (i >> 5)] >> (i & 31)) & 1u;
 }
 
 // x_pre after a row update: x_pre * D+[age] (+1 on a pre spike), R7 closed form.
@@ -98,8 +98,12 @@ k_front(NetDev net, StateDev st) {
     const int pi = valid ? find_pop(net, i) : 0;
     const PopDev &p = net.pop[pi];
     bool fired = false, recent = false;
+    // this rank updates its own target range and every neuron without inputs
+    // (Poisson: counter-based, identical on all ranks); the spike bits of the
+    // other input neurons arrive by the exchange
+    const bool owned = i >= net.R || (i >= net.tgt_lo && i < net.tgt_hi);
     // ---- (1) neuron dynamics (App. B op order)
-    if (valid) {
+    if (valid && owned) {
         if (p.kind == POP_POISSON) {
             const u32x4 r = philox4x32_10(i, (uint32_t)t, 2u, 0u, net.key0, net.key1);
             fired = (uint64_t)r.x < p.thr;
@@ -160,16 +164,23 @@ k_front(NetDev net, StateDev st) {
     }
     const uint32_t fword = __ballot_sync(0xffffffffu, fired);
     const uint32_t rword = __ballot_sync(0xffffffffu, recent);
-    if (lane == 0 && valid) {
-        st.ring[(size_t)(t & (kRingSlots - 1)) * net.nwords + (i >> 5)] = fword;
+    // ring word of ids [i, i + 32): written by the rank owning its input
+    // neurons (the word straddling R by the last rank), by all if it has none
+    const bool wown = i >= net.R ? true : (i + 32 <= net.R ? (i >= net.tgt_lo && i + 32 <= net.tgt_hi)
+                                                           : (i >= net.tgt_lo && net.tgt_hi == net.R));
+    if (lane == 0 && valid && wown) {
+        st.ring[(size_t)(t & (kRingSlots - 1)) * net.ring_stride + (i >> 5)] = fword;
         if (net.nstdp) st.recent[i >> 5] = rword;
+        // this rank's share of the step's input-neuron words, for the exchange
+        const uint32_t w = i >> 5, w0 = net.rank * net.share_w;
+        if (net.world > 1 && i < net.R && w >= w0 && w < w0 + net.wmax) st.sendbuf[w - w0] = fword;
     }
 
     // ---- (2) arrival of row i at step t: its spike of step t - D (hist[delay])
     bool arr = false;
     if (valid) {
         if (net.D == 0) arr = fired;
-        else if (t >= (int64_t)net.D) arr = ring_bit(st.ring, net.nwords, t - net.D, i);
+        else if (t >= (int64_t)net.D) arr = ring_bit(st.ring, net.ring_stride, t - net.D, i);
     }
     const bool plastic_row = valid && (p.flags & PF_PRE_PLASTIC);
     bool visit = false;
@@ -180,7 +191,7 @@ k_front(NetDev net, StateDev st) {
         float xp = st.xpre[i];
         // finalise a visit of step t-1 (its synapses were updated by k_stdp(t-1))
         if (t >= 1 && ((st.vmask[par ^ 1u][i >> 5] >> (i & 31)) & 1u)) {
-            const bool arr_prev = (t - 1 >= (int64_t)net.D) && ring_bit(st.ring, net.nwords, t - 1 - net.D, i);
+            const bool arr_prev = (t - 1 >= (int64_t)net.D) && ring_bit(st.ring, net.ring_stride, t - 1 - net.D, i);
             xp = xpre_after(sd, xp, (int)(t - 1 - tl), arr_prev);
             tl = (int32_t)(t - 1);
             st.xpre[i] = xp;
@@ -736,7 +747,7 @@ k_readout_prepare(NetDev net, StateDev st, int64_t t_last) {
         int32_t tl = st.tlu[i];
         float xp = st.xpre[i];
         if ((st.vmask[par][i >> 5] >> (i & 31)) & 1u) {
-            const bool arr_prev = (t_last >= (int64_t)net.D) && ring_bit(st.ring, net.nwords, t_last - net.D, i);
+            const bool arr_prev = (t_last >= (int64_t)net.D) && ring_bit(st.ring, net.ring_stride, t_last - net.D, i);
             xp = xpre_after(sd, xp, (int)(t_last - tl), arr_prev);
             tl = (int32_t)t_last;
             st.xpre[i] = xp;
@@ -772,6 +783,29 @@ k_readout_finish(NetDev net, StateDev st, int64_t t_last) {
     st.tlu[d.row] = (int32_t)t_last;
 }
 
+// Exchange (world > 1): the other ranks' spike words of step tp, gathered in
+// `gath` (one share of wmax words per rank), into ring slot tp.  t_fixed < 0:
+// tp = the current step (NCCL: unpack right after the all-gather of the step).
+__global__ void k_unpack(NetDev net, StateDev st, const uint32_t *gath, int64_t t_fixed) {
+    const int64_t tp = t_fixed >= 0 ? t_fixed : st.ctr->t;
+    if (tp < 0) return;
+    const uint32_t nwR = (net.R + 31) >> 5;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwR; w += gridDim.x * blockDim.x) {
+        const uint32_t r = min(w / net.share_w, net.world - 1);
+        if (r == net.rank) continue;
+        st.ring[(size_t)(tp & (kRingSlots - 1)) * net.ring_stride + w] =
+            gath[(size_t)r * net.wmax + (w - r * net.share_w)];
+    }
+}
+
+cudaError_t launch_unpack(const NetDev &net, const StateDev &st, const uint32_t *gath, int64_t t_fixed,
+                          cudaStream_t s) {
+    const uint32_t nwR = (net.R + 31) >> 5;
+    const uint32_t blocks = (nwR + 255) / 256 < 296 ? (nwR + 255) / 256 : 296;
+    k_unpack<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(net, st, gath, t_fixed);
+    return cudaGetLastError();
+}
+
 // History reconstruction from the bitmask ring (read-out of SNN_FIELD_HIST):
 // bit s of hist[i] = spike of i at step t_last - s.
 __global__ void k_hist_from_ring(NetDev net, const uint32_t *ring, int64_t t_last, uint64_t *out) {
@@ -781,7 +815,7 @@ __global__ void k_hist_from_ring(NetDev net, const uint32_t *ring, int64_t t_las
     for (int s = kHistBits - 1; s >= 0; s--) {
         h <<= 1;
         const int64_t u = t_last - s;
-        if (u >= 0) h |= ring_bit(ring, net.nwords, u, i);
+        if (u >= 0) h |= ring_bit(ring, net.ring_stride, u, i);
     }
     out[i] = h;
 }

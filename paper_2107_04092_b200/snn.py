@@ -54,7 +54,7 @@ class snn_config(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("device", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
-                ("nccl_unique_id", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p), ("group_key", ctypes.c_uint64)]
 
 
 class snn_pop_params(ctypes.Structure):
@@ -89,9 +89,12 @@ _lib.snn_last_error.restype = ctypes.c_char_p
 _lib.snn_last_error.argtypes = [ctypes.c_void_p]
 _lib.snn_abi_version.restype = ctypes.c_uint32
 _lib.snn_abi_version.argtypes = []
+_lib.snn_partition.restype = ctypes.c_int32
+_lib.snn_partition.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                               _P(ctypes.c_uint32), _P(ctypes.c_uint32)]
 
 EXPORTS = ["snn_create", "snn_add_population", "snn_connect", "snn_step", "snn_read_state",
-           "snn_destroy", "snn_last_error", "snn_abi_version"]
+           "snn_destroy", "snn_last_error", "snn_abi_version", "snn_partition"]
 
 
 class SnnError(RuntimeError):
@@ -112,6 +115,13 @@ def _check(code, sim):
 
 def snn_abi_version() -> int:
     return _lib.snn_abi_version()
+
+
+def snn_partition(n_targets: int, slice_width: int, world: int, rank: int):
+    """Target range [lo, hi) of `rank` (host only, no device work)."""
+    lo, hi = ctypes.c_uint32(), ctypes.c_uint32()
+    _check(_lib.snn_partition(n_targets, slice_width, world, rank, ctypes.byref(lo), ctypes.byref(hi)), None)
+    return lo.value, hi.value
 
 
 def snn_create(cfg: snn_config):
@@ -152,7 +162,8 @@ class Snn:
 
     def __init__(self, seed: int, dt_ms: float = 0.1, delay: int = 0, frac_bits: int = 20,
                  slice_width: int = 0, device: int = 0, stream=None, flags: int = 0, rank: int = 0,
-                 world: int = 1, nccl_unique_id: bytes | None = None, torch_allocator: bool = True):
+                 world: int = 1, nccl_unique_id: bytes | None = None, group_key: int = 0,
+                 torch_allocator: bool = True):
         import torch  # plumbing: device memory and streams
         self._torch = torch
         self.device = device
@@ -172,6 +183,7 @@ class Snn:
         cfg.device = device
         cfg.rank = rank
         cfg.world = world
+        cfg.group_key = group_key
         cfg.stream = ctypes.c_void_p(stream.cuda_stream)
         self._keep = []
         if torch_allocator:

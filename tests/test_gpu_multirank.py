@@ -1,0 +1,67 @@
+"""The partitioned (multi-GPU) path, run as `world` partitions of one network
+on ONE GPU (local-group transport: the spike words of each step are copied
+into every partition's gather buffer, exactly what ncclAllGather does across
+GPUs).  The partitioned run must equal the single-partition run bit-exactly
+(integer accumulation, identical per-synapse arithmetic) -- SURVEY 8(e)."""
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(rc, world, steps, C=0):
+    from paper_2107_04092_b200 import Snn
+    key = 0x5EED0000 + world
+    sims = []
+    for r in range(world):
+        g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, rank=r, world=world,
+                group_key=key if world > 1 else 0)
+        rc.apply(g)
+        sims.append(g)
+    for g in sims:
+        g.finalize()
+    for t in range(steps):
+        for g in sims:          # lockstep: every partition finishes step t before step t+1
+            g.step(1)
+    return sims
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("plastic", [False, True])
+def test_partitioned_equals_single(world, plastic):
+    rc = W.brunel(9000, p=0.05, plastic=plastic, delay=15, seed=21)
+    ref = _run(rc, 1, 200)[0]
+    parts = _run(rc, world, 200)
+    h_ref = ref.read_state("HIST")
+    v_ref = ref.read_state("V")
+    ev = 0
+    rp_ref, idx_ref = ref.read_state("ROW_PTR"), ref.read_state("IDX")
+    w_ref = ref.read_state("WEIGHTS")
+    for g in parts:
+        info = g.info()
+        lo, hi = info["tgt_lo"], info["tgt_hi"]
+        assert np.array_equal(g.read_state("HIST"), h_ref)          # every neuron's spikes
+        assert np.array_equal(g.read_state("V")[lo:hi], v_ref[lo:hi])  # owned neurons
+        ev += g.metrics()["EVENTS"]
+        # local CSR = the global rows restricted to [lo, hi); weights bit-exact
+        rp, idx, w = g.read_state("ROW_PTR"), g.read_state("IDX"), g.read_state("WEIGHTS")
+        for i in list(range(0, info["N"], 97)) + [info["N"] - 1]:
+            full = idx_ref[rp_ref[i]:rp_ref[i + 1]]
+            sel = (full >= lo) & (full < hi)
+            assert np.array_equal(idx[rp[i]:rp[i + 1]], full[sel])
+            assert np.array_equal(w[rp[i]:rp[i + 1]], w_ref[rp_ref[i]:rp_ref[i + 1]][sel])
+    assert ev == ref.metrics()["EVENTS"]
+
+
+def test_world_gt1_needs_delay():
+    from paper_2107_04092_b200 import Snn, SnnError, SNN_E_UNSUPPORTED
+    rc = W.vogels(2000, seed=2)        # D = 0
+    g0 = Snn(1, 0.1, 0, 20, rank=0, world=2, group_key=77)
+    g1 = Snn(1, 0.1, 0, 20, rank=1, world=2, group_key=77)
+    rc.apply(g0)
+    with pytest.raises(SnnError) as e:
+        g0.finalize()
+    assert e.value.code == SNN_E_UNSUPPORTED
+    g1.close()
