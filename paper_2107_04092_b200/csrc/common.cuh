@@ -48,6 +48,7 @@ struct NetDev {
     uint32_t nwords;     // 32-bit words of spike bits per step = ceil(N/32)
     uint32_t ring_stride;// words per ring slot (nwords + exchange padding)
     uint32_t world, rank;        // ranks sharing the target range
+    uint32_t debug;              // SNN_DEBUG_KERNELS bits (experiments only; 0 in normal runs)
     uint32_t share_w;            // words per rank share (rank r owns words [r share_w, ...))
     uint32_t wmax;               // words exchanged per rank and step
     uint32_t D;          // delay

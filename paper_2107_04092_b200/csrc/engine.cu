@@ -430,7 +430,7 @@ static snn_status finalize(snn_sim *sim) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg.device);
     const uint32_t ns = std::max(1u, net.nslices);
-    sim->splits = std::max(1u, (uint32_t)(2 * nsm) / ns);   // ~2 CTAs per SM, one wave
+    sim->splits = std::max(1u, (uint32_t)(2 * nsm) / ns);   // <= 2 CTAs per SM, one wave
     if (const char *sp = getenv("SNN_DELIVER_SPLITS")) sim->splits = std::max(1, atoi(sp));  // tuning knob
     sim->stdp_grid = 3 * (uint32_t)nsm;
     CK(cudaStreamSynchronize(s));
@@ -440,7 +440,9 @@ static snn_status finalize(snn_sim *sim) {
 
 // ---------------------------------------------------------------- the step
 static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bool first, int64_t step_k = 0) {
-    const NetDev &net = sim->net;
+    NetDev net = sim->net;
+    if ((sim->cfg.flags & SNN_FLAG_TRACE) && getenv("SNN_DEBUG_KERNELS"))   // kernel experiments (trace runs only)
+        net.debug = (uint32_t)atoi(getenv("SNN_DEBUG_KERNELS"));
     const StateDev &st = sim->st;
     // programmatic dependent launch between the kernels of the graph (not
     // across event records, whose timing would then overlap)

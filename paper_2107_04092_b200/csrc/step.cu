@@ -512,7 +512,64 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                     w4[u] = *reinterpret_cast<const float4 *>(st.w + cc[u]);
                 }
             }
-            // gathers: every history / post trace this pass needs, before any use
+            // ---- lean path: every chunk of this pass belongs to a forced flush
+            // (R3; ~90 % of the visits): potentiation only, w updated where a
+            // probed target fired -- 4-bit probe masks, predicated gathers,
+            // the first spike branch-free, predicated stores
+            bool fl = true;
+#pragma unroll
+            for (int u = 0; u < kStdpU; u++) fl &= (meta4[u] & kMetaArr) == 0;
+            if (__all_sync(0xffffffffu, fl)) {
+                uint32_t pm[kStdpU];
+                uint64_t hh[kStdpU * 4];
+#pragma unroll
+                for (int u = 0; u < kStdpU; u++) {
+                    const uint32_t jj[4] = {j4[u].x, j4[u].y, j4[u].z, j4[u].w};
+                    pm[u] = 0;
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const uint32_t j = (e >= (int)lo4[u] && e < (int)hi4[u]) ? jj[e] : pp_lo;
+                        const uint32_t word = lds_u32(rs_addr + ((j >> 5) << 2));
+                        pm[u] |= ((word >> (j & 31)) & 1u) << e;
+                    }
+                    const uint32_t vm = ((1u << hi4[u]) - 1u) & ~((1u << lo4[u]) - 1u);
+                    pm[u] = xp4[u] != 0.0f ? (pm[u] & vm) : 0u;
+#pragma unroll
+                    for (int e = 0; e < 4; e++) hh[4 * u + e] = ldg_u64_if(ghist + jj[e], (pm[u] >> e) & 1u);
+                }
+#pragma unroll
+                for (int u = 0; u < kStdpU; u++) {
+                    if (pm[u] == 0u) continue;
+                    const int age = (int)(meta4[u] & 0x7fu);
+                    const uint64_t wmask = age >= 64 ? ~0ull : ((1ull << age) - 1ull);
+                    const uint32_t si = (meta4[u] >> 12) & 0xfu;
+                    const uint32_t dp = dp_addr + si * 4u * (kHistBits + 1);
+                    const float a_plus = net.stdp[si].a_plus, w_max = net.stdp[si].w_max;
+                    const float ww[4] = {w4[u].x, w4[u].y, w4[u].z, w4[u].w};
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        uint64_t m = ((pm[u] >> e) & 1u) ? (hh[4 * u + e] & wmask) : 0ull;   // R2 window
+                        const bool has = m != 0ull;
+                        const int pb = 63 - __clzll((long long)m);
+                        const float d = lds_f32(dp + 4u * (uint32_t)(has ? age - pb : 0));
+                        const float nw = __fadd_rn(ww[e], __fmul_rn(a_plus, __fmul_rn(xp4[u], d)));
+                        float w = nw < w_max ? nw : w_max;
+                        m &= ~(1ull << (pb & 63));
+                        while (has && m) {                      // further spikes (rare), oldest first
+                            const int p2 = 63 - __clzll((long long)m);
+                            m &= ~(1ull << p2);
+                            const float n2 =
+                                __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp4[u], lds_f32(dp + 4u * (uint32_t)(age - p2)))));
+                            w = n2 < w_max ? n2 : w_max;
+                        }
+                        const uint32_t chg = (has && __float_as_uint(w) != __float_as_uint(ww[e])) ? 1u : 0u;
+                        stg_f32_if(st.w + cc[u] + e, w, chg);
+                        n_w += chg;
+                    }
+                }
+                continue;
+            }
+            // ---- generic path (arrivals): gathers first, then the updates
             // (branch-free: bitmap probe at a clamped index, predicated loads)
             uint64_t h[kStdpU * 4];
             float xq[kStdpU * 4];
@@ -570,12 +627,12 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
 constexpr int kDelThreads = 512;
 constexpr int kDelWarps = kDelThreads / 32;
 constexpr int kDelRows = 1024;     // row table per round (two rows per thread)
-constexpr int kDelU = 8;           // elements in flight per lane
+constexpr int kDelU4 = 2;          // 4-element slots in flight per lane (8 elements)
 
 // One CTA per (slice k, split s) (Fig. 3b): the CTA tabulates the
 // (row, slice) segments of its share of the arriving rows (descriptor + pivot
 // pair) in shared memory, its warps split the flattened elements evenly
-// and walk them 32 lanes wide with kDelU loads in flight per lane; each element
+// and walk them 32 lanes wide, 8 elements in flight per lane; each element
 // adds q(w) = RNE(w 2^F) to the slice accumulator with a shared atomic.
 __global__ void __launch_bounds__(kDelThreads, 2)
 k_deliver(NetDev net, StateDev st) {
@@ -655,31 +712,60 @@ k_deliver(NetDev net, StateDev st) {
             pdl_launch();
         }
         trace_mark(st.trace, 2, 1);
-        // ---- warps split the T elements evenly
+        // ---- warps split the T elements evenly; a lane takes 4 consecutive
+        // elements per slot (its segment's fields stay in registers)
         const uint32_t e_begin = (uint32_t)(((uint64_t)T * warp) / kDelWarps);
         const uint32_t e_end = (uint32_t)(((uint64_t)T * (warp + 1)) / kDelWarps);
-        uint32_t o = e_begin < e_end ? owner_search(s_inc, nrows, e_begin + lane) : 0u;
-        for (uint32_t base = e_begin; base < e_end; base += 32 * kDelU) {
-            uint32_t jj[kDelU], oo[kDelU];
-            float ww[kDelU];
+        uint32_t o = e_begin < e_end ? owner_search(s_inc, nrows, min(e_begin + 4 * lane, e_end - 1)) : 0u;
+        uint32_t o_end = s_inc[o], o_rc = s_rc[o];
+        int64_t o_c0 = s_c0[o];
+        for (uint32_t base = e_begin; base < e_end; base += 128 * kDelU4) {
+            uint32_t jj[kDelU4][4], rr[kDelU4][4];
+            float ww[kDelU4][4];
 #pragma unroll
-            for (int u = 0; u < kDelU; u++) {
-                const uint32_t e = base + u * 32 + lane;
-                oo[u] = 0xffffffffu;
-                if (e < e_end) {
-                    while (e >= s_inc[o]) o++;
-                    const int64_t c = s_c0[o] + e;
-                    jj[u] = __ldg(st.idx + c);
-                    ww[u] = st.w[c];
-                    oo[u] = o;
+            for (int u = 0; u < kDelU4; u++) {
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint32_t e = base + 128 * u + 4 * lane + k;
+                    rr[u][k] = 0xffffffffu;
+                    if (e < e_end) {
+                        while (e >= o_end) {
+                            o++;
+                            o_end = s_inc[o];
+                            o_rc = s_rc[o];
+                            o_c0 = s_c0[o];
+                        }
+                        const int64_t c = o_c0 + e;
+                        if (net.debug & 2u) {  // experiment: no global loads
+                            jj[u][k] = slo + (e & (C - 1));
+                            ww[u][k] = 0.001f;
+                        } else {
+                            jj[u][k] = __ldg(st.idx + c);
+                            ww[u][k] = __ldg(st.w + c);
+                        }
+                        rr[u][k] = o_rc;
+                    }
                 }
             }
+            if (net.debug & 1u) {          // experiment: no shared atomics
+                uint32_t sink = 0;
 #pragma unroll
-            for (int u = 0; u < kDelU; u++) {
-                if (oo[u] == 0xffffffffu) continue;
-                uint32_t rr = s_rc[oo[u]];
-                if (rr >= 3u) rr = (uint32_t)net.rcpt[rr >> 2][find_pop(net, jj[u])];
-                atomicAdd(&acc[rr * C + (jj[u] - slo)], __float2int_rn(__fmul_rn(ww[u], scale)));
+                for (int u = 0; u < kDelU4; u++)
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        if (rr[u][k] != 0xffffffffu) sink += jj[u][k] + __float2int_rn(__fmul_rn(ww[u][k], scale));
+                if (sink == 0x7fffffffu) acc[0] = 1;
+                continue;
+            }
+#pragma unroll
+            for (int u = 0; u < kDelU4; u++) {
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    uint32_t r2 = rr[u][k];
+                    if (r2 == 0xffffffffu) continue;
+                    if (r2 >= 3u) r2 = (uint32_t)net.rcpt[r2 >> 2][find_pop(net, jj[u][k])];
+                    atomicAdd(&acc[r2 * C + (jj[u][k] - slo)], __float2int_rn(__fmul_rn(ww[u][k], scale)));
+                }
             }
         }
         __syncthreads();                           // table reused next round

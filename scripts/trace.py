@@ -13,8 +13,12 @@ g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, flags=FLAG_TRA
 rc.apply(g)
 g.step(1500)
 torch.cuda.synchronize()
+dbg = os.environ.pop("SNN_TRACE_DEBUG", None)
 for rep in range(3):
+    if dbg is not None:
+        os.environ["SNN_DEBUG_KERNELS"] = dbg     # kernel experiment on the traced steps only
     g.step(1)
+    os.environ.pop("SNN_DEBUG_KERNELS", None)
     tr = g.read_state("TRACE").reshape(3, 4096, 4).astype(np.int64)
     t0 = tr[0][tr[0][:, 0] > 0][:, 0].min()
     for k, name in enumerate(["front", "stdp", "deliver"]):
