@@ -627,20 +627,113 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
 constexpr int kDelThreads = 512;
 constexpr int kDelWarps = kDelThreads / 32;
 constexpr int kDelRows = 1024;     // row table per round (two rows per thread)
-constexpr int kDelU4 = 2;          // 4-element slots in flight per lane (8 elements)
+constexpr int kDelWin = 32 * kDelThreads;   // flattened elements per owner window (one bitmap word per thread)
+constexpr int kDelU = 8;           // elements in flight per thread
 
-// One CTA per (slice k, split s) (Fig. 3b): the CTA tabulates the
-// (row, slice) segments of its share of the arriving rows (descriptor + pivot
-// pair) in shared memory, its warps split the flattened elements evenly
-// and walk them 32 lanes wide, 8 elements in flight per lane; each element
-// adds q(w) = RNE(w 2^F) to the slice accumulator with a shared atomic.
+// Block-wide inclusive scan of a packed pair (low 32 bits: elements, high 32:
+// segments) per thread.
+__device__ __forceinline__ unsigned long long block_incl_scan64(unsigned long long v, unsigned long long *wsum,
+                                                                unsigned long long &total) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long x = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += x;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    unsigned long long off = 0, tot = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kDelWarps; w2++) {
+        const unsigned long long x = wsum[w2];
+        if (w2 < (int)warp) off += x;
+        tot += x;
+    }
+    total = tot;
+    return off + inc;
+}
+
+// Delivery helpers: 32-bit shared addresses, read-only global loads.
+__device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void red_shared_add(uint32_t addr, int32_t v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ldg_nc_u32(uint64_t a) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(a));
+    return v;
+}
+__device__ __forceinline__ float ldg_nc_f32(uint64_t a) {
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
+    return v;
+}
+
+// Owner-window pass (k_deliver): thread x takes elements w0 + x + 512 u of the
+// window.  Segment of element x: bw.y + popc(start bits <= x) (s_bw word).
+// s_ptr holds per segment the byte address of idx[c] for flattened element 0.
+template <bool kMulti, bool kCheck>
+__device__ __forceinline__ void deliver_pass(const NetDev &net, uint32_t x0, uint32_t wlen, uint32_t w0,
+                                             uint32_t bw_a, uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a,
+                                             uint64_t dw, float scale) {
+    uint32_t jj[kDelU], rr[kDelU];
+    float ww[kDelU];
+#pragma unroll
+    for (int u = 0; u < kDelU; u++) {
+        // ragged pass: a thread past the end re-reads the last element (no
+        // branch around the loads, so they stay in flight together) and skips
+        // its atomic below
+        const uint32_t x = kCheck ? min(x0 + u * kDelThreads + threadIdx.x, wlen - 1u)
+                                  : x0 + u * kDelThreads + threadIdx.x;
+        const uint2 bw = lds_u2(bw_a + ((x >> 5) << 3));
+        const uint32_t gi = bw.y + __popc(bw.x & (0xffffffffu >> (31u - (x & 31u))));
+        const uint64_t a = lds_u64(ptr_a + (gi << 3)) + 4ull * (w0 + x);
+        jj[u] = ldg_nc_u32(a);
+        ww[u] = ldg_nc_f32(a + dw);
+        rr[u] = kMulti ? lds_u8(rc_a + gi) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kDelU; u++) {
+        const uint32_t x = x0 + u * kDelThreads + threadIdx.x;
+        if (!kCheck || x < wlen) {
+            uint32_t r2 = rr[u];
+            if (kMulti && r2 >= 3u) r2 = (uint32_t)net.rcpt[r2 >> 2][find_pop(net, jj[u])];
+            red_shared_add(acc_a + ((r2 * net.C + jj[u]) << 2), __float2int_rn(__fmul_rn(ww[u], scale)));
+        }
+    }
+}
+
+// One CTA per (slice k, split s) (Fig. 3b).  The CTA tabulates the
+// non-empty (row, slice) segments of its share of the arriving rows
+// (descriptor + pivot pair) in shared memory and concatenates them into
+// one flattened element range.  A bitmap marks the first element of every
+// segment, so the segment of element e is a popcount (no search, no loop);
+// the threads then stride the range 512 wide -- consecutive threads read
+// consecutive synapses -- and each element adds q(w) = RNE(w 2^F) to the slice
+// accumulator with a shared atomic.
 __global__ void __launch_bounds__(kDelThreads, 2)
 k_deliver(NetDev net, StateDev st) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t wsum[kDelWarps];
-    __shared__ int64_t s_c0[kDelRows];       // CSR offset of element 0 of the flattened range of row r
-    __shared__ uint32_t s_inc[kDelRows];
-    __shared__ uint32_t s_rc[kDelRows];
+    __shared__ unsigned long long wsum64[kDelWarps];
+    __shared__ uint64_t s_ptr[kDelRows];     // segment g: byte address of idx[c] of flattened element 0
+    __shared__ uint8_t s_rc[kDelRows];       // segment g: receptor code
+    __shared__ uint2 s_bw[kDelWin / 32];     // window word: (segment-start bits, segments begun before it - 1)
     const uint32_t C = net.C;
     const uint32_t nblk = st.nblk;
     const int64_t t = st.ctr->t;
@@ -654,7 +747,7 @@ k_deliver(NetDev net, StateDev st) {
     const uint32_t slo = net.tgt_lo + (k << net.log2C);
     const uint32_t shi = min(slo + C, net.tgt_hi);
     const uint32_t width = shi > slo ? shi - slo : 0u;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
     trace_mark(st.trace, 2, 0);
 
     // prologue: reads only k_front(t)'s lists -- complete before k_stdp(t)
@@ -668,6 +761,10 @@ k_deliver(NetDev net, StateDev st) {
     const uint32_t r_end = (uint32_t)(((uint64_t)nA * (split + 1)) / nsplit);
     const uint32_t P = net.nslices + 1;
     const float scale = net.scale;
+    const bool multi_rc = net.nrcpt > 1;
+    const uint32_t bw_a = smem_u32(s_bw), ptr_a = smem_u32(s_ptr), rc_a = smem_u32(s_rc);
+    const uint32_t acc_a = smem_u32(acc) - 4u * slo;       // accumulator of target j, receptor r: + 4 (r C + j)
+    const uint64_t dw = (uint64_t)st.w - (uint64_t)st.idx;   // w[c] at idx[c] + dw (bytes)
     uint32_t n_ev = 0, n_seg = 0;
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kDelRows) {
         // ---- tabulate (two rows per thread): descriptor + pivot pair
@@ -687,86 +784,70 @@ k_deliver(NetDev net, StateDev st) {
                 pp[q] = make_uint2(pv[0], pv[1]);
             }
         }
+        int64_t c0q[2] = {0, 0};                     // CSR offset of the segment's first synapse
+        uint32_t rcq[2] = {0, 0};
 #pragma unroll
         for (int q = 0; q < 2; q++) {
             const uint32_t r = r0 + threadIdx.x * 2 + q;
-            if (r >= r_end) continue;
-            len2[q] = pp[q].y - pp[q].x;
-            uint32_t rc = (d2[q].meta >> 8) & 3u;
-            if (rc == 3u) rc = 3u | (((d2[q].meta >> 16) & 0xfu) << 2);
-            s_rc[threadIdx.x * 2 + q] = rc;
-            s_c0[threadIdx.x * 2 + q] = d2[q].start + pp[q].x;
+            if (r < r_end) {
+                len2[q] = pp[q].y - pp[q].x;
+                c0q[q] = d2[q].start + pp[q].x;
+                rcq[q] = (d2[q].meta >> 8) & 3u;
+                if (rcq[q] == 3u) rcq[q] = 3u | (((d2[q].meta >> 16) & 0xfu) << 2);
+            }
         }
+        const uint32_t ns = (len2[0] != 0) + (len2[1] != 0);
         n_ev += len2[0] + len2[1];
-        n_seg += (len2[0] != 0) + (len2[1] != 0);
-        uint32_t T = 0;
-        const uint32_t inc = block_incl_scan<kDelThreads>(len2[0] + len2[1], wsum, T);
-        s_inc[threadIdx.x * 2] = inc - len2[1];
-        s_inc[threadIdx.x * 2 + 1] = inc;
-        s_c0[threadIdx.x * 2] -= (int64_t)(inc - len2[1] - len2[0]);   // element e at s_c0[o] + e
-        s_c0[threadIdx.x * 2 + 1] -= (int64_t)(inc - len2[1]);
-        const uint32_t nrows = min(r_end - r0, (uint32_t)kDelRows);
-        __syncthreads();
+        n_seg += ns;
+        // ---- compact the non-empty segments: flattened start and slot of each
+        unsigned long long tot = 0;
+        const unsigned long long inc =
+            block_incl_scan64(((unsigned long long)ns << 32) | (len2[0] + len2[1]), wsum64, tot);
+        const uint32_t T = (uint32_t)tot;
+        uint32_t est[2];                             // flattened start of the thread's two segments
+        est[0] = (uint32_t)inc - len2[0] - len2[1];
+        est[1] = est[0] + len2[0];
+        uint32_t g = (uint32_t)(inc >> 32) - ns;     // compacted slot of the first non-empty one
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            if (len2[q] == 0) continue;
+            s_rc[g] = (uint8_t)rcq[q];
+            s_ptr[g] = (uint64_t)(st.idx + c0q[q]) - 4ull * est[q];
+            g++;
+        }
         if (r0 == r_begin) {
             pdl_wait();    // k_stdp(t): updated weights of plastic arrivals
             pdl_launch();
         }
         trace_mark(st.trace, 2, 1);
-        // ---- warps split the T elements evenly; a lane takes 4 consecutive
-        // elements per slot (its segment's fields stay in registers)
-        const uint32_t e_begin = (uint32_t)(((uint64_t)T * warp) / kDelWarps);
-        const uint32_t e_end = (uint32_t)(((uint64_t)T * (warp + 1)) / kDelWarps);
-        uint32_t o = e_begin < e_end ? owner_search(s_inc, nrows, min(e_begin + 4 * lane, e_end - 1)) : 0u;
-        uint32_t o_end = s_inc[o], o_rc = s_rc[o];
-        int64_t o_c0 = s_c0[o];
-        for (uint32_t base = e_begin; base < e_end; base += 128 * kDelU4) {
-            uint32_t jj[kDelU4][4], rr[kDelU4][4];
-            float ww[kDelU4][4];
+        for (uint32_t w0 = 0; w0 < T; w0 += kDelWin) {
+            const uint32_t wlen = min(T - w0, (uint32_t)kDelWin);
+            s_bw[threadIdx.x].x = 0u;
+            __syncthreads();                         // also: table written, previous window done
 #pragma unroll
-            for (int u = 0; u < kDelU4; u++) {
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const uint32_t e = base + 128 * u + 4 * lane + k;
-                    rr[u][k] = 0xffffffffu;
-                    if (e < e_end) {
-                        while (e >= o_end) {
-                            o++;
-                            o_end = s_inc[o];
-                            o_rc = s_rc[o];
-                            o_c0 = s_c0[o];
-                        }
-                        const int64_t c = o_c0 + e;
-                        if (net.debug & 2u) {  // experiment: no global loads
-                            jj[u][k] = slo + (e & (C - 1));
-                            ww[u][k] = 0.001f;
-                        } else {
-                            jj[u][k] = __ldg(st.idx + c);
-                            ww[u][k] = __ldg(st.w + c);
-                        }
-                        rr[u][k] = o_rc;
-                    }
+            for (int q = 0; q < 2; q++)
+                if (len2[q] != 0 && est[q] >= w0 && est[q] - w0 < wlen)
+                    atomicOr(&s_bw[(est[q] - w0) >> 5].x, 1u << ((est[q] - w0) & 31));
+            // segments begun before the window (the sync of the bitmap, too)
+            const uint32_t before = __syncthreads_count(len2[0] != 0 && est[0] < w0) +
+                                    __syncthreads_count(len2[1] != 0 && est[1] < w0);
+            const uint32_t pc = __popc(s_bw[threadIdx.x].x);
+            uint32_t wt = 0;
+            const uint32_t winc = block_incl_scan<kDelThreads>(pc, wsum, wt);
+            s_bw[threadIdx.x].y = before + winc - pc - 1u;
+            __syncthreads();
+            // ---- elements: thread x takes w0 + x + 512 u (coalesced)
+            for (uint32_t x0 = 0; x0 < wlen; x0 += kDelThreads * kDelU) {
+                const bool full = x0 + kDelThreads * kDelU <= wlen;
+                if (multi_rc) {
+                    if (full) deliver_pass<true, false>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale);
+                    else deliver_pass<true, true>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale);
+                } else {
+                    if (full) deliver_pass<false, false>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale);
+                    else deliver_pass<false, true>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale);
                 }
             }
-            if (net.debug & 1u) {          // experiment: no shared atomics
-                uint32_t sink = 0;
-#pragma unroll
-                for (int u = 0; u < kDelU4; u++)
-#pragma unroll
-                    for (int k = 0; k < 4; k++)
-                        if (rr[u][k] != 0xffffffffu) sink += jj[u][k] + __float2int_rn(__fmul_rn(ww[u][k], scale));
-                if (sink == 0x7fffffffu) acc[0] = 1;
-                continue;
-            }
-#pragma unroll
-            for (int u = 0; u < kDelU4; u++) {
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    uint32_t r2 = rr[u][k];
-                    if (r2 == 0xffffffffu) continue;
-                    if (r2 >= 3u) r2 = (uint32_t)net.rcpt[r2 >> 2][find_pop(net, jj[u][k])];
-                    atomicAdd(&acc[r2 * C + (jj[u][k] - slo)], __float2int_rn(__fmul_rn(ww[u][k], scale)));
-                }
-            }
+            if (w0 + kDelWin < T) __syncthreads();  // bitmap reused by the next window
         }
         __syncthreads();                           // table reused next round
     }

@@ -1,5 +1,5 @@
-timeout 1200 python -m pytest tests -m gpu -q --timeout 300 -x > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
-for D in 0 3; do
-SNN_TRACE_DEBUG=$D python scripts/trace.py 3 0 > gpurun_out/trace_d$D.log 2>&1
-done
-timeout 600 python bench.py --steps 3000 --warmup 500 --no-cpu-baseline --no-e2e > gpurun_out/bench_C0.log 2>&1; echo bench=$?
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+tail -3 gpurun_out/pytest_gpu.log
+python scripts/trace.py 3 0 > gpurun_out/trace_new.log 2>&1
+python bench.py --steps 3000 --warmup 300 --no-cpu-baseline --no-e2e > gpurun_out/bench_new.json 2>&1
+tail -n 3 gpurun_out/bench_new.json

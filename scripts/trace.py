@@ -9,7 +9,8 @@ from paper_2107_04092_b200 import Snn, FLAG_TRACE
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 C = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 rc = W.config(cfg)
-g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, flags=FLAG_TRACE)
+extra = int(os.environ.get("SNN_TRACE_FLAGS", "0"))
+g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, flags=FLAG_TRACE | extra)
 rc.apply(g)
 g.step(1500)
 torch.cuda.synchronize()
