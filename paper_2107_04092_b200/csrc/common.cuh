@@ -62,6 +62,7 @@ struct NetDev {
     StdpDev stdp[4];
     // plastic source rows: concatenation of the PF_PRE_PLASTIC populations
     uint32_t n_plastic_rows;
+    uint32_t pp_lo, pp_hi;        // neurons [pp_lo, pp_hi) hold the post-synaptic STDP state (hist, x_post)
 };
 
 // Tables of the graph builder (per (src pop, dst pop) projection).
@@ -80,9 +81,11 @@ struct Counters {
     unsigned long long metric[8];
 };
 
-// One row to process in the slice kernel, written by the front kernel.
+// One row to process, written by the front kernel: forced flushes for k_stdp,
+// arrivals for k_deliver (which also runs the STDP of plastic arrivals).
 // meta: bits 0-6 age (1..64), bit 7 arrival, bits 8-9 receptor (3 = per target),
-//       bit 10 plastic row, bits 12-15 STDP projection index.
+//       bit 10 plastic row, bits 12-15 STDP projection index, bits 16+ source pop
+//       (per-target receptor).
 struct __align__(16) RowDesc {
     int64_t start;   // CSR offset of the row
     uint32_t row;    // source neuron id
@@ -99,6 +102,7 @@ struct StateDev {
     float *V, *ge, *gi, *xpost;
     int32_t *ref, *in_e, *in_i;
     uint64_t *hist;
+    uint8_t *fpos;           // post-plastic j with hist != 0: bit index of its only spike, 0xff if several
     uint32_t *nspk;
     uint32_t *ring;          // [kRingSlots][ring_stride]
     // source rows
@@ -111,9 +115,10 @@ struct StateDev {
     uint32_t *piv;           // [N][nslices+1], row-relative
     uint2 *seg;              // [N] plastic segment (lo, hi), row-relative
     // work lists (by step parity), one region of kFrontThreads entries per
-    // k_front CTA (no global atomics): plastic visits and static arrivals
+    // k_front CTA (no global atomics): plastic visits (arrivals from the front
+    // of the region, forced flushes from its back) and arrivals
     RowDesc *vdesc[2], *adesc[2];
-    uint4 *cnt[2];           // per k_front CTA: (visits, static arrivals, arrivals, flushes)
+    uint4 *cnt[2];           // per k_front CTA: (plastic arrivals, arrivals, forced flushes, 0)
     RowDesc *rdesc;          // read-out flush rows (same region layout)
     uint4 *rcnt;
     uint32_t nblk;           // k_front CTAs = list regions
@@ -122,12 +127,14 @@ struct StateDev {
     uint32_t *sendbuf;       // [wmax] this rank's spike words of the step (world > 1)
     uint32_t *gath;          // [2][world][wmax] all ranks' words (NCCL: slot 0; local group: by step parity)
     Counters *ctr;
+    const StdpDev *stdp;     // device copy of NetDev::stdp (coalesced table loads into shared memory)
     unsigned long long *trace;   // optional (SNN_FLAG_TRACE): per-CTA phase timestamps
 };
 
 // Phase trace (debug, SNN_FLAG_TRACE): thread 0 of each CTA stores %globaltimer
 // at phase boundaries: trace[(kernel * kTraceCtas + cta) * 4 + phase].
 constexpr int kTraceCtas = 4096;
+constexpr int kTraceKernels = 4;   // front, stdp (flush), deliver, stdp_arr
 __device__ __forceinline__ void trace_mark(unsigned long long *tr, int kernel, int phase) {
 #ifdef __CUDA_ARCH__
     if (tr && threadIdx.x == 0) {

@@ -338,6 +338,7 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.in_e, int32_t, N);
     ALLOC(st.in_i, int32_t, N);
     ALLOC(st.hist, uint64_t, N);
+    ALLOC(st.fpos, uint8_t, (size_t)N + 16);
     ALLOC(st.nspk, uint32_t, N);
     // exchange geometry: rank r owns words [r share_w, ...), at most share_w + 1
     // of them (the word straddling R); ring slots padded for the unpack
@@ -368,11 +369,11 @@ static snn_status finalize(snn_sim *sim) {
     }
     ALLOC(st.rdesc, RowDesc, net.nstdp ? nreg : 1);
     ALLOC(st.rcnt, uint4, st.nblk);
-    ALLOC(st.recent, uint32_t, net.nwords);
+    ALLOC(st.recent, uint32_t, net.nwords + 4);   // + the tail of its 16-byte bulk copy
     st.trace = nullptr;
     if (cfg.flags & SNN_FLAG_TRACE) {
-        ALLOC(st.trace, unsigned long long, 3ull * kTraceCtas * 4);
-        CK(cudaMemsetAsync(st.trace, 0, 8ull * 3 * kTraceCtas * 4, sim->stream));
+        ALLOC(st.trace, unsigned long long, (size_t)kTraceKernels * kTraceCtas * 4);
+        CK(cudaMemsetAsync(st.trace, 0, 8ull * kTraceKernels * kTraceCtas * 4, sim->stream));
     }
     ALLOC(st.ctr, Counters, 1);
     cudaStream_t s = sim->stream;
@@ -411,6 +412,12 @@ static snn_status finalize(snn_sim *sim) {
     CK(build_fill(net, tabs, st.piv, st.row_ptr, st.idx, st.w, s));
     CK(build_segments(net, st.row_ptr, st.idx, st.seg, s));
     CK(init_state(net, st, s));
+    {
+        StdpDev *tab = nullptr;
+        ALLOC(tab, StdpDev, 4);
+        CK(cudaMemcpyAsync(tab, net.stdp, sizeof(StdpDev) * 4, cudaMemcpyHostToDevice, s));
+        st.stdp = tab;
+    }
 
     // ---- launch shapes: k_deliver = nslices x splits CTAs (~1 wave at 2 per
     //      SM); k_stdp = 4 CTAs per SM, grid-striding over the visited rows
@@ -422,17 +429,21 @@ static snn_status finalize(snn_sim *sim) {
             sim->pp_hi = std::max(sim->pp_hi, net.pop[k].base + net.pop[k].n);
         }
     if (sim->pp_hi <= sim->pp_lo) sim->pp_lo = sim->pp_hi = 0;
+    net.pp_lo = sim->pp_lo;
+    net.pp_hi = sim->pp_hi;
     if (deliver_smem_bytes(net) > 200 * 1024)
         return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory", C, deliver_smem_bytes(net));
-    if (stdp_smem_bytes(net, sim->pp_lo, sim->pp_hi) > 200 * 1024)
+    if (sim->plastic && stdp_smem_bytes(net, sim->pp_lo, sim->pp_hi) > 227 * 1024)
         return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for the shared bitmap");
+    if (sim->plastic && net.N >= (1u << 23) - 8)   // k_stdp queue entries hold a 23-bit row offset
+        return sim->fail(SNN_E_UNSUPPORTED, "STDP rows longer than 2^23 - 8 synapses");
     CK(kernels_configure(net, sim->pp_lo, sim->pp_hi));
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg.device);
     const uint32_t ns = std::max(1u, net.nslices);
     sim->splits = std::max(1u, (uint32_t)(2 * nsm) / ns);   // <= 2 CTAs per SM, one wave
     if (const char *sp = getenv("SNN_DELIVER_SPLITS")) sim->splits = std::max(1, atoi(sp));  // tuning knob
-    sim->stdp_grid = 3 * (uint32_t)nsm;
+    sim->stdp_grid = (uint32_t)nsm;                 // k_stdp: one CTA per SM
     CK(cudaStreamSynchronize(s));
     sim->state = 1;
     return SNN_OK;
@@ -693,7 +704,7 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
     case SNN_FIELD_PHASE_TIMES: bytes = 8 * 8; break;
     case SNN_FIELD_TRACE:
         if (!st.trace) return sim->fail(SNN_E_STATE, "trace needs SNN_FLAG_TRACE");
-        src = st.trace; bytes = 8ull * 3 * kTraceCtas * 4; break;
+        src = st.trace; bytes = 8ull * kTraceKernels * kTraceCtas * 4; break;
     case SNN_FIELD_INFO:
         host_i64[0] = sim->N; host_i64[1] = sim->nsyn; host_i64[2] = net.nslices; host_i64[3] = net.C;
         host_i64[4] = net.R; host_i64[5] = net.tgt_lo; host_i64[6] = net.tgt_hi;

@@ -42,11 +42,51 @@ __device__ __forceinline__ float xpre_after(const StdpDev &sd, float xp, int age
     return arr ? __fadd_rn(x, 1.0f) : x;
 }
 
-// Block-wide compaction of up to two predicates into this CTA's list regions.
-// Returns each thread's slot for (a, b); writes the per-CTA counts to *counts.
+// Block-wide compaction of up to three predicates into this CTA's list regions.
+// Returns each thread's slot for (a, b[, c]) and the CTA totals.
 struct Compact2 {
-    uint32_t wa[kFrontThreads / 32], wb[kFrontThreads / 32];
+    uint32_t wa[kFrontThreads / 32], wb[kFrontThreads / 32], wc[kFrontThreads / 32];
 };
+__device__ __forceinline__ void compact3(Compact2 &sm, bool a, bool b, bool c, uint32_t &slot_a, uint32_t &slot_b,
+                                         uint32_t &slot_c, uint32_t &tot_a, uint32_t &tot_b, uint32_t &tot_c) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t ba = __ballot_sync(0xffffffffu, a), bb = __ballot_sync(0xffffffffu, b),
+                   bc = __ballot_sync(0xffffffffu, c);
+    if (lane == 0) {
+        sm.wa[warp] = __popc(ba);
+        sm.wb[warp] = __popc(bb);
+        sm.wc[warp] = __popc(bc);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        uint32_t va = lane < nw ? sm.wa[lane] : 0u, vb = lane < nw ? sm.wb[lane] : 0u, vc = lane < nw ? sm.wc[lane] : 0u;
+        uint32_t ia = va, ib = vb, ic = vc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t xa = __shfl_up_sync(0xffffffffu, ia, o), xb = __shfl_up_sync(0xffffffffu, ib, o),
+                           xc = __shfl_up_sync(0xffffffffu, ic, o);
+            if (lane >= o) {
+                ia += xa;
+                ib += xb;
+                ic += xc;
+            }
+        }
+        if (lane < nw) {
+            sm.wa[lane] = ia - va;
+            sm.wb[lane] = ib - vb;
+            sm.wc[lane] = ic - vc;
+        }
+    }
+    __syncthreads();
+    const uint32_t lm = (1u << lane) - 1u;
+    slot_a = sm.wa[warp] + __popc(ba & lm);
+    slot_b = sm.wb[warp] + __popc(bb & lm);
+    slot_c = sm.wc[warp] + __popc(bc & lm);
+    tot_a = __syncthreads_count(a);
+    tot_b = __syncthreads_count(b);
+    tot_c = __syncthreads_count(c);
+}
 __device__ __forceinline__ void compact2(Compact2 &sm, bool a, bool b, uint32_t &slot_a, uint32_t &slot_b,
                                          uint32_t &tot_a, uint32_t &tot_b) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -157,6 +197,8 @@ k_front(NetDev net, StateDev st) {
             const uint64_t h = (st.hist[i] << 1) | (uint64_t)fired;
             st.hist[i] = h;
             recent = h != 0ull;
+            // position of the window's only post spike (lean forced flush in k_stdp), 0xff: several
+            if (recent) st.fpos[i] = (h & (h - 1ull)) ? (uint8_t)0xffu : (uint8_t)(63 - __clzll((long long)h));
             const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
             st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
         }
@@ -213,10 +255,15 @@ k_front(NetDev net, StateDev st) {
     }
     const uint32_t vword = __ballot_sync(0xffffffffu, visit);
     if (net.nstdp && lane == 0 && valid) st.vmask[par][i >> 5] = vword;
-    uint32_t sv, sa, nv, na;
-    compact2(cs, visit, arr, sv, sa, nv, na);
+    // plastic visits -> k_stdp: the arrivals from the front of the CTA's region,
+    // the forced flushes from its back (so k_stdp can share each kind evenly);
+    // every arrival -> k_deliver
+    const bool parr = visit && arr, flush = visit && !arr;
+    uint32_t sp, sa, sf, np, na, nf;
+    compact3(cs, parr, arr, flush, sp, sa, sf, np, na, nf);
     const size_t region = (size_t)blockIdx.x * kFrontThreads;
-    if (visit) st.vdesc[par][region + sv] = d;
+    if (parr) st.vdesc[par][region + sp] = d;
+    if (flush) st.vdesc[par][region + kFrontThreads - 1 - sf] = d;
     if (arr) {                                       // every arriving row is delivered
         RowDesc a;
         a.start = st.row_ptr[i];
@@ -228,16 +275,14 @@ k_front(NetDev net, StateDev st) {
         a.pad = 0;
         st.adesc[par][region + sa] = a;
     }
-    // per-CTA counts (arrivals and flushes for the metrics)
-    const uint32_t na_all = __syncthreads_count(arr);
-    const uint32_t nflush = __syncthreads_count(visit && !arr);
-    if (threadIdx.x == 0) st.cnt[par][blockIdx.x] = make_uint4(nv, na, na_all, nflush);
+    if (threadIdx.x == 0) st.cnt[par][blockIdx.x] = make_uint4(np, na, nf, 0u);
     trace_mark(st.trace, 0, 3);
 }
 
 // ------------------------------------------------------- list region prefix
 // Per-CTA list regions (k_front) -> exclusive prefix over the regions of the
-// selected count (0 = visits, 1 = arrivals), into pre[0..nblk].
+// selected count (0 = plastic arrivals / read-out rows, 1 = arrivals, 2 = forced
+// flushes), into pre[0..nblk].
 template <int kThreads>
 __device__ __forceinline__ void region_prefix(const uint4 *cnt, uint32_t nblk, int which, uint32_t *pre,
                                               uint32_t *wsum) {
@@ -245,7 +290,7 @@ __device__ __forceinline__ void region_prefix(const uint4 *cnt, uint32_t nblk, i
     const uint32_t per = (nblk + kThreads - 1) / kThreads;
     const uint32_t b0 = threadIdx.x * per;
     uint32_t sv = 0;
-    for (uint32_t b = b0; b < min(b0 + per, nblk); b++) sv += which ? cnt[b].y : cnt[b].x;
+    for (uint32_t b = b0; b < min(b0 + per, nblk); b++) sv += which == 0 ? cnt[b].x : which == 1 ? cnt[b].y : cnt[b].z;
     uint32_t iv = sv;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -259,7 +304,7 @@ __device__ __forceinline__ void region_prefix(const uint4 *cnt, uint32_t nblk, i
     uint32_t rv = ov + iv - sv;
     for (uint32_t b = b0; b < min(b0 + per, nblk); b++) {
         pre[b] = rv;
-        rv += which ? cnt[b].y : cnt[b].x;
+        rv += which == 0 ? cnt[b].x : which == 1 ? cnt[b].y : cnt[b].z;
     }
     if (threadIdx.x == kThreads - 1) pre[nblk] = rv;
 }
@@ -272,6 +317,15 @@ __device__ __forceinline__ size_t region_index(const uint32_t *pre, uint32_t nbl
         if (pre[mid] <= r) lo = mid; else hi = mid;
     }
     return (size_t)lo * kFrontThreads + (r - pre[lo]);
+}
+// Same for a list filled from the back of each region (forced flushes).
+__device__ __forceinline__ size_t region_index_back(const uint32_t *pre, uint32_t nblk, uint32_t r) {
+    uint32_t lo = 0, hi = nblk;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (pre[mid] <= r) lo = mid; else hi = mid;
+    }
+    return (size_t)lo * kFrontThreads + (kFrontThreads - 1 - (r - pre[lo]));
 }
 
 // ---------------------------------------------------- CTA row-table helpers
@@ -333,47 +387,96 @@ __device__ __forceinline__ float ldg_f32_if(const float *p, uint32_t pred) {
                  : "=f"(v) : "l"(p), "r"(pred));
     return v;
 }
+__device__ __forceinline__ uint32_t ldg_u8_if(const uint8_t *p, uint32_t pred) {
+    uint32_t v;
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.b32 %0, 255;\n @q ld.global.nc.u8 %0, [%1];\n}\n"
+                 : "=r"(v) : "l"(p), "r"(pred));
+    return v;
+}
 __device__ __forceinline__ void stg_f32_if(float *p, float v, uint32_t pred) {
     asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}\n"
                  :: "l"(p), "f"(v), "r"(pred) : "memory");
 }
 
-// One plastic synapse (Fig. 2c, R7), written branch-free for the common cases:
-// potentiation by the post spikes in m, oldest first ("__clz") with the
-// closed-form skip-ahead w = min(w + A+ (x_pre D+[age - p]), w_max) -- the
-// first spike by selects, further ones (rare) in a loop -- then, on an
-// arrival, the depression w = max(w - A- x_post, 0).  dp = shared address of
-// the D+ table of the projection.
+// ---- TMA bulk copies and mbarriers (producer / consumer stage ring)
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+}
+// global -> shared bulk copy (16-byte aligned, size a multiple of 16), completes on mbar
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// One plastic synapse (Fig. 2c, R7): potentiation by the post spikes in m,
+// oldest first ("__clz") with the closed-form skip-ahead
+// w = min(w + A+ (x_pre D+[age - p]), w_max), then, on an arrival, the
+// depression w = max(w - A- x_post, 0).  dp = shared address of the D+ table.
 __device__ __forceinline__ float stdp_synapse(float w, uint64_t m, bool arr, float xq, float xp, int age,
                                               uint32_t dp, float a_plus, float a_minus, float w_max) {
-    const bool has = m != 0ull;
-    const int pb = 63 - __clzll((long long)m);
-    const float d = lds_f32(dp + 4u * (uint32_t)(has ? age - pb : 0));
-    const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, d)));
-    w = has ? (nw < w_max ? nw : w_max) : w;
-    m = has ? (m & ~(1ull << (pb & 63))) : 0ull;
     while (m) {
-        const int pb2 = 63 - __clzll((long long)m);
-        m &= ~(1ull << pb2);
-        const float nw2 = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, lds_f32(dp + 4u * (uint32_t)(age - pb2)))));
-        w = nw2 < w_max ? nw2 : w_max;
+        const int pb = 63 - __clzll((long long)m);
+        m &= ~(1ull << pb);
+        const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, lds_f32(dp + 4u * (uint32_t)(age - pb)))));
+        w = nw < w_max ? nw : w_max;
     }
     const float dw = __fsub_rn(w, __fmul_rn(a_minus, xq));
     return arr ? (dw > 0.0f ? dw : 0.0f) : w;
 }
 
-constexpr int kStdpThreads = 256;
+// k_stdp launch shape: one CTA per SM; 4 consumer groups of 4 warps take the
+// stages round-robin (so the gathers of one group overlap the filtering of the
+// others) + 1 TMA producer warp.
+constexpr int kStdpGroups = 4;
+constexpr int kStdpGroupWarps = 4;
+constexpr int kStdpGroupThr = kStdpGroupWarps * 32;
+constexpr int kStdpConsWarps = kStdpGroups * kStdpGroupWarps;
+constexpr int kStdpCons = kStdpConsWarps * 32;     // consumer threads
+constexpr int kStdpThreads = kStdpCons + 32;       // + the producer warp
 constexpr int kStdpWarps = kStdpThreads / 32;
-constexpr int kStdpRows = kStdpThreads;   // row table per round (one row per thread)
-constexpr int kStdpU = 2;                 // 16-byte chunks in flight per lane
+constexpr int kStdpChPerThr = 4;                   // 16-byte chunks (16 synapses) per consumer thread and stage
+constexpr int kStdpStageCh = kStdpChPerThr * kStdpGroupThr;   // 512 chunks per stage: 8 KB ids + 8 KB weights
+constexpr int kStdpStages = 2 * kStdpGroups;       // 2 per group: 128 KB in flight per SM
+constexpr int kStdpRows = 256;                     // row table per round
+constexpr int kStdpList = 32 * 4 * kStdpChPerThr;  // per-warp list of the synapses to update (one stage)
 
 struct __align__(16) StdpRow {   // one visited row of this CTA (shared memory)
-    int64_t cb;           // 16-byte aligned CSR offset of its plastic span
-    uint32_t lo, hi;      // valid elements [lo, hi) relative to cb
-    float xp;             // x_pre at tlu
+    int64_t cb;      // 16-byte aligned CSR offset of its plastic span
+    float xp;        // x_pre at tlu
     uint32_t meta;
-    uint32_t first;       // flattened index of its first 16-byte chunk
-    uint32_t pad;
+    uint32_t lo, hi; // valid elements [lo, hi) relative to cb
+    uint32_t first;  // flattened index of its first 16-byte chunk
+    uint32_t nch;    // chunks
+};
+
+struct StdpSmem {                       // static part of k_stdp's shared memory
+    uint64_t full[kStdpStages], empty[kStdpStages], bmap;
+    StdpRow rows[kStdpRows];
+    uint32_t incl[kStdpRows];
+    uint32_t wsum[kStdpWarps];
+    float dplus[4 * (kHistBits + 1)];
+    float4 par[4];                      // per projection: a_plus, a_minus, w_max
+    uint32_t list[kStdpConsWarps][kStdpList];   // (element p in stage << 9) | (rec << 8) | row slot
 };
 
 // Lazy + event-driven STDP over the visited rows (Fig. 2c).  For each plastic
@@ -381,65 +484,78 @@ struct __align__(16) StdpRow {   // one visited row of this CTA (shared memory)
 //   m = hist[j] & window(age)        post spikes in steps (tlu, t]   (R2)
 //   for set bits p, oldest first:    w = min(w + A+ (x_pre D+[age-p]), w_max)
 //   on an arrival:                   w = max(w - A- x_post[j], 0)
-// The CTA takes a contiguous share of the visited rows, tabulates them in
-// shared memory, and its warps split the flattened 16-byte chunks of all those
-// rows evenly (a lane keeps its current row's fields in registers).  hist[j] is
-// gathered only when the shared bitmap says j fired in the last 64 steps (a
-// superset of every window), x_post[j] only on arrivals; all gathers of a pass
-// are issued before any is consumed.
-__global__ void __launch_bounds__(kStdpThreads, 3)
+// One CTA per SM takes a contiguous share of the visited rows.  A producer
+// thread streams the rows' plastic spans (target ids and weights) into a ring
+// of shared-memory stages with TMA bulk copies (cp.async.bulk, mbarrier
+// complete_tx), so the bytes in flight do not depend on the consumers.  A
+// consumer group filters a stage (16 synapses per thread): forced-flush
+// synapses whose target fired in the last 64 steps (shared bitmap probe) and
+// every synapse of an arriving row go to its warp's list; the list is then
+// drained four entries per lane (history / x_post gathers, Fig. 2c, store of
+// the changed weights) and the stage released to the producer.
+__global__ void __launch_bounds__(kStdpThreads, 1)
 k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t wsum[kStdpWarps];
-    __shared__ float dplus_s[4 * (kHistBits + 1)];
-    __shared__ StdpRow rows_s[kStdpRows];
-    __shared__ uint32_t incl_s[kStdpRows];
+    StdpSmem &sm = *reinterpret_cast<StdpSmem *>(smem);
+    unsigned char *stage_base = smem + ((sizeof(StdpSmem) + 127) & ~(size_t)127);   // [stages][ids 8K | w 8K]
     const uint32_t nblk = st.nblk;
+    uint32_t *pre = reinterpret_cast<uint32_t *>(stage_base + (size_t)kStdpStages * kStdpStageCh * 32);  // [nblk+1]
+    uint32_t *preF = pre + ((nblk + 1 + 3) & ~3u);                                                      // [nblk+1]
+    uint32_t *recent_s = preF + ((nblk + 1 + 3) & ~3u);                                                 // bitmap
     const bool readout = t_fixed >= 0;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool producer = warp == kStdpConsWarps;
+    const uint32_t w_lo = (pp_lo >> 7) << 2, w_hi = (pp_hi + 31) >> 5;     // 16-byte aligned start
+    const uint32_t full_a = smem_u32(sm.full), empty_a = smem_u32(sm.empty), bmap_a = smem_u32(&sm.bmap);
+    const uint32_t stage_a = smem_u32(stage_base);
+    // ---- prologue independent of k_front(t): barriers, STDP constants
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStdpStages; s++) {
+            mbar_init(full_a + 8 * s, 1);
+            mbar_init(empty_a + 8 * s, kStdpGroupWarps);
+        }
+        mbar_init(bmap_a, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (uint32_t x = threadIdx.x; x < net.nstdp * (kHistBits + 1); x += kStdpThreads)
+        sm.dplus[x] = st.stdp[x / (kHistBits + 1)].dplus[x % (kHistBits + 1)];
+    if (threadIdx.x < net.nstdp)
+        sm.par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
+                                          st.stdp[threadIdx.x].w_max, 0.0f);
+    pdl_wait();            // k_front(t): lists, histories, bitmap
+    pdl_launch();          // k_deliver may start its tabulation (k_front is complete)
+    if (!readout) trace_mark(st.trace, 1, 0);
     const int64_t t = readout ? t_fixed : st.ctr->t;
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Vl = readout ? st.rdesc : st.vdesc[par];
     const uint4 *cnt = readout ? st.rcnt : st.cnt[par];
-    const uint32_t w_lo = (pp_lo >> 7) << 2, w_hi = (pp_hi + 31) >> 5;     // 16-byte aligned start
-    uint32_t *pre = reinterpret_cast<uint32_t *>(smem);                       // [nblk + 1]
-    uint32_t *recent_s = pre + ((nblk + 1 + 3) & ~3u);                        // [w_hi - w_lo]
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t bm_bytes = 16u * ((w_hi - w_lo + 3) >> 2);
+    region_prefix<kStdpThreads>(cnt, nblk, 0, pre, sm.wsum);
+    __syncthreads();       // also: barrier init visible
+    region_prefix<kStdpThreads>(cnt, nblk, 2, preF, sm.wsum);
+    __syncthreads();
+    // even shares of each kind: plastic arrivals (front lists; read-out rows)
+    // and forced flushes (back lists); this CTA's rows: [0, nAb) arrivals, then flushes
+    const uint32_t nA = pre[nblk], nF = preF[nblk];
+    const uint32_t a_begin = (uint32_t)(((uint64_t)nA * blockIdx.x) / gridDim.x);
+    const uint32_t a_end = (uint32_t)(((uint64_t)nA * (blockIdx.x + 1)) / gridDim.x);
+    const uint32_t f_begin = (uint32_t)(((uint64_t)nF * blockIdx.x) / gridDim.x);
+    const uint32_t f_end = (uint32_t)(((uint64_t)nF * (blockIdx.x + 1)) / gridDim.x);
+    const uint32_t nAb = a_end - a_begin;
+    const uint32_t r_begin = 0, r_end = nAb + (f_end - f_begin);
+    if (producer && lane == 0 && r_begin < r_end) {   // bitmap of recently fired post neurons (one bulk copy)
+        mbar_expect_tx(bmap_a, bm_bytes);
+        bulk_g2s(smem_u32(recent_s), st.recent + w_lo, bm_bytes, bmap_a);
+    }
+    const uint32_t rs_addr = smem_u32(recent_s) - 4u * w_lo;     // bitmap word of neuron j: + 4 (j >> 5)
+    const uint32_t dp_addr = smem_u32(sm.dplus);
+    if (!readout) trace_mark(st.trace, 1, 1);
+    uint32_t n_syn = 0, n_w = 0;
+    uint32_t g0 = 0;             // global stage index of the round's first stage (ring position)
+    bool bm_ready = false;
     const uint64_t *__restrict__ ghist = st.hist;
     const float *__restrict__ gxpost = st.xpost;
-    pdl_wait();            // k_front(t): lists, histories, bitmap
-    pdl_launch();          // k_deliver may start its prologue (k_front is complete)
-    if (!readout) trace_mark(st.trace, 1, 0);
-
-    {   // bitmap of recently fired post-synaptic neurons: 16-byte loads, all issued first
-        const uint32_t n4 = (w_hi - w_lo + 3) >> 2;
-        const uint4 *src = reinterpret_cast<const uint4 *>(st.recent + w_lo);
-        uint4 *dst = reinterpret_cast<uint4 *>(recent_s);
-        constexpr int kMaxU = 16;
-        uint4 v[kMaxU];
-#pragma unroll
-        for (int u = 0; u < kMaxU; u++) {
-            const uint32_t x = threadIdx.x + u * kStdpThreads;
-            if (x < n4) v[u] = src[x];
-        }
-#pragma unroll
-        for (int u = 0; u < kMaxU; u++) {
-            const uint32_t x = threadIdx.x + u * kStdpThreads;
-            if (x < n4) dst[x] = v[u];
-        }
-        for (uint32_t x = threadIdx.x + kMaxU * kStdpThreads; x < n4; x += kStdpThreads) dst[x] = src[x];
-    }
-    for (uint32_t x = threadIdx.x; x < net.nstdp * (kHistBits + 1); x += kStdpThreads)
-        dplus_s[x] = net.stdp[x / (kHistBits + 1)].dplus[x % (kHistBits + 1)];
-    region_prefix<kStdpThreads>(cnt, nblk, 0, pre, wsum);
-    __syncthreads();
-    const uint32_t nV = pre[nblk];
-    // 32-bit shared addresses: bitmap word of neuron j at rs_addr + 4 (j >> 5); D+ tables
-    const uint32_t rs_addr = smem_u32(recent_s) - 4u * w_lo;
-    const uint32_t dp_addr = smem_u32(dplus_s);
-    if (!readout) trace_mark(st.trace, 1, 1);
-    const uint32_t r_begin = (uint32_t)(((uint64_t)nV * blockIdx.x) / gridDim.x);
-    const uint32_t r_end = (uint32_t)(((uint64_t)nV * (blockIdx.x + 1)) / gridDim.x);
-    uint32_t n_syn = 0, n_w = 0;
+    float *__restrict__ gw = st.w;
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kStdpRows) {
         // ---- tabulate up to kStdpRows rows (one per thread), chunk prefix
         const uint32_t r = r0 + threadIdx.x;
@@ -449,8 +565,9 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
         rw.lo = rw.hi = 0;
         rw.xp = 0.0f;
         rw.meta = 0;
-        if (r < r_end) {
-            const RowDesc d = Vl[region_index(pre, nblk, r)];
+        if (threadIdx.x < kStdpRows && r < r_end) {
+            const RowDesc d = Vl[r < nAb ? region_index(pre, nblk, a_begin + r)
+                                         : region_index_back(preF, nblk, f_begin + (r - nAb))];
             const bool arr = (d.meta & kMetaArr) != 0;
             const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
             // a flush with x_pre == 0 changes no weight (potentiation adds 0)
@@ -464,151 +581,246 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 n_syn += (uint32_t)(ce - cs);
             }
         }
-        __syncthreads();                           // previous round done with the table
         uint32_t T = 0;
-        const uint32_t inc = block_incl_scan<kStdpThreads>(nch, wsum, T);
-        rw.first = inc - nch;
-        rw.pad = 0;
-        rows_s[threadIdx.x] = rw;
-        incl_s[threadIdx.x] = inc;
-        const uint32_t nrows = min(r_end - r0, (uint32_t)kStdpRows);
+        const uint32_t inc = block_incl_scan<kStdpThreads>(nch, sm.wsum, T);
+        if (threadIdx.x < kStdpRows) {
+            rw.first = inc - nch;
+            rw.nch = nch;
+            sm.rows[threadIdx.x] = rw;
+            sm.incl[threadIdx.x] = inc;
+        }
         __syncthreads();
         if (!readout) trace_mark(st.trace, 1, 2);
-        // ---- warps split the T chunks evenly; lane = one 16-byte chunk per slot
-        const uint32_t c_begin = (uint32_t)(((uint64_t)T * warp) / kStdpWarps);
-        const uint32_t c_end = (uint32_t)(((uint64_t)T * (warp + 1)) / kStdpWarps);
-        if (c_begin >= c_end) continue;
-        // current row of this lane (refreshed when its chunk passes the row end)
-        uint32_t o = owner_search(incl_s, nrows, min(c_begin + lane, c_end - 1));
-        StdpRow cur = rows_s[o];
-        uint32_t o_end = incl_s[o];
-        for (uint32_t base = c_begin; base < c_end; base += 32 * kStdpU) {
-            uint4 j4[kStdpU];
-            float4 w4[kStdpU];
-            int64_t cc[kStdpU];
-            uint32_t lo4[kStdpU], hi4[kStdpU];      // valid elements of the chunk: [lo4, hi4)
-            uint32_t meta4[kStdpU];
-            float xp4[kStdpU];
-#pragma unroll
-            for (int u = 0; u < kStdpU; u++) {
-                const uint32_t ch = base + 32 * u + lane;
-                lo4[u] = hi4[u] = 0;
-                meta4[u] = 0;
-                xp4[u] = 0.0f;
-                cc[u] = 0;
-                if (ch < c_end) {
-                    while (ch >= o_end) {
-                        o++;
-                        cur = rows_s[o];
-                        o_end = incl_s[o];
+        const uint32_t nst = (T + kStdpStageCh - 1) / kStdpStageCh;
+        if (producer) {
+            // ---- TMA producer: stage s covers flattened chunks [s C, s C + C)
+            if (lane == 0) {
+                uint32_t pr = 0;
+                for (uint32_t s = 0; s < nst; s++) {
+                    const uint32_t g = g0 + s, slot = g % kStdpStages;
+                    mbar_wait(empty_a + 8 * slot, ((g / kStdpStages) & 1u) ^ 1u);
+                    const uint32_t a = s * kStdpStageCh, b = min(a + kStdpStageCh, T);
+                    const uint32_t fb = full_a + 8 * slot;
+                    mbar_expect_tx(fb, 32u * (b - a));
+                    const uint32_t dst = stage_a + slot * (kStdpStageCh * 32);
+                    for (uint32_t c = a; c < b;) {
+                        while (c >= sm.incl[pr]) pr++;
+                        const StdpRow &rr = sm.rows[pr];
+                        const uint32_t e = min(b, sm.incl[pr]);
+                        const int64_t gc = rr.cb + 4ll * (c - rr.first);     // element offset
+                        const uint32_t bytes = 16u * (e - c);
+                        bulk_g2s(dst + 16u * (c - a), st.idx + gc, bytes, fb);
+                        bulk_g2s(dst + kStdpStageCh * 16 + 16u * (c - a), gw + gc, bytes, fb);
+                        c = e;
                     }
-                    const uint32_t x0 = 4 * (ch - cur.first);
-                    cc[u] = cur.cb + x0;
-                    lo4[u] = cur.lo > x0 ? cur.lo - x0 : 0u;
-                    hi4[u] = min(cur.hi - x0, 4u);
-                    meta4[u] = cur.meta;
-                    xp4[u] = cur.xp;
-                    j4[u] = __ldg(reinterpret_cast<const uint4 *>(st.idx + cc[u]));
-                    w4[u] = *reinterpret_cast<const float4 *>(st.w + cc[u]);
                 }
             }
-            // ---- lean path: every chunk of this pass belongs to a forced flush
-            // (R3; ~90 % of the visits): potentiation only, w updated where a
-            // probed target fired -- 4-bit probe masks, predicated gathers,
-            // the first spike branch-free, predicated stores
-            bool fl = true;
-#pragma unroll
-            for (int u = 0; u < kStdpU; u++) fl &= (meta4[u] & kMetaArr) == 0;
-            if (__all_sync(0xffffffffu, fl)) {
-                uint32_t pm[kStdpU];
-                uint64_t hh[kStdpU * 4];
-#pragma unroll
-                for (int u = 0; u < kStdpU; u++) {
-                    const uint32_t jj[4] = {j4[u].x, j4[u].y, j4[u].z, j4[u].w};
-                    pm[u] = 0;
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        const uint32_t j = (e >= (int)lo4[u] && e < (int)hi4[u]) ? jj[e] : pp_lo;
-                        const uint32_t word = lds_u32(rs_addr + ((j >> 5) << 2));
-                        pm[u] |= ((word >> (j & 31)) & 1u) << e;
-                    }
-                    const uint32_t vm = ((1u << hi4[u]) - 1u) & ~((1u << lo4[u]) - 1u);
-                    pm[u] = xp4[u] != 0.0f ? (pm[u] & vm) : 0u;
-#pragma unroll
-                    for (int e = 0; e < 4; e++) hh[4 * u + e] = ldg_u64_if(ghist + jj[e], (pm[u] >> e) & 1u);
+        } else {
+            // ---- consumer group grp takes the stages g = grp (mod 4); thread gt
+            //      of the group takes chunks gt + 128 u of the stage
+            const uint32_t grp = warp / kStdpGroupWarps, gt = threadIdx.x % kStdpGroupThr;
+            if (!bm_ready) {
+                mbar_wait(bmap_a, 0);
+                bm_ready = true;
+            }
+            uint32_t o = 0, o_end = sm.incl[0];
+            uint4 cur = lds_v4(smem_u32(&sm.rows[0]) + 16);     // lo, hi, first, nch
+            uint2 cm = make_uint2(sm.rows[0].meta, __float_as_uint(sm.rows[0].xp));
+            uint32_t *list = sm.list[warp];
+            const uint32_t list_a = smem_u32(list);
+            for (uint32_t g = g0 + ((grp + kStdpGroups - g0 % kStdpGroups) % kStdpGroups); g < g0 + nst;
+                 g += kStdpGroups) {
+                const uint32_t slot = g % kStdpStages;
+                const uint32_t a = (g - g0) * kStdpStageCh;
+                const uint32_t sa = stage_a + slot * (kStdpStageCh * 32);
+                uint32_t hm = 0, rm = 0, slots = 0;   // 16-bit masks: list the synapse / target may hold a post spike
+                uint32_t am = 0;                      // 16-bit mask: synapses of arriving rows (updated in place)
+                bool nonlean = false;                 // a listed synapse is not a plain forced flush (age 64)
+                mbar_wait(full_a + 8 * slot, (g / kStdpStages) & 1u);
+                if (net.debug & 2u) {   // experiment: stream the stages only
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty_a + 8 * slot);
+                    continue;
                 }
 #pragma unroll
-                for (int u = 0; u < kStdpU; u++) {
-                    if (pm[u] == 0u) continue;
-                    const int age = (int)(meta4[u] & 0x7fu);
-                    const uint64_t wmask = age >= 64 ? ~0ull : ((1ull << age) - 1ull);
-                    const uint32_t si = (meta4[u] >> 12) & 0xfu;
-                    const uint32_t dp = dp_addr + si * 4u * (kHistBits + 1);
-                    const float a_plus = net.stdp[si].a_plus, w_max = net.stdp[si].w_max;
-                    const float ww[4] = {w4[u].x, w4[u].y, w4[u].z, w4[u].w};
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        uint64_t m = ((pm[u] >> e) & 1u) ? (hh[4 * u + e] & wmask) : 0ull;   // R2 window
-                        const bool has = m != 0ull;
-                        const int pb = 63 - __clzll((long long)m);
-                        const float d = lds_f32(dp + 4u * (uint32_t)(has ? age - pb : 0));
-                        const float nw = __fadd_rn(ww[e], __fmul_rn(a_plus, __fmul_rn(xp4[u], d)));
-                        float w = nw < w_max ? nw : w_max;
-                        m &= ~(1ull << (pb & 63));
-                        while (has && m) {                      // further spikes (rare), oldest first
-                            const int p2 = 63 - __clzll((long long)m);
-                            m &= ~(1ull << p2);
-                            const float n2 =
-                                __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp4[u], lds_f32(dp + 4u * (uint32_t)(age - p2)))));
-                            w = n2 < w_max ? n2 : w_max;
+                for (int u = 0; u < kStdpChPerThr; u++) {
+                    const uint32_t c = a + gt + kStdpGroupThr * u;
+                    if (c < T) {
+                        if (c >= o_end) {
+                            while (c >= o_end) o_end = sm.incl[++o];
+                            cur = lds_v4(smem_u32(&sm.rows[o]) + 16);
+                            cm = make_uint2(sm.rows[o].meta, __float_as_uint(sm.rows[o].xp));
                         }
-                        const uint32_t chg = (has && __float_as_uint(w) != __float_as_uint(ww[e])) ? 1u : 0u;
-                        stg_f32_if(st.w + cc[u] + e, w, chg);
+                        const uint4 j4 = lds_v4(sa + 16u * (gt + kStdpGroupThr * u));
+                        const uint32_t x0 = 4u * (c - cur.z);
+                        const bool arr = (cm.x & kMetaArr) != 0;
+                        const bool pot = __uint_as_float(cm.y) != 0.0f;
+                        const uint32_t jj[4] = {j4.x, j4.y, j4.z, j4.w};
+                        uint32_t bits = 0, inm = 0xfu;
+                        if (x0 < cur.x || x0 + 4 > cur.y) {      // a row's first / last chunk
+                            inm = 0;
+#pragma unroll
+                            for (int e = 0; e < 4; e++) inm |= (uint32_t)(x0 + e >= cur.x && x0 + e < cur.y) << e;
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            const uint32_t j = ((inm >> e) & 1u) ? jj[e] : pp_lo;
+                            bits |= ((lds_u32(rs_addr + ((j >> 5) << 2)) >> (j & 31)) & 1u) << e;
+                        }
+                        const uint32_t rec = pot ? (bits & inm) : 0u;
+                        const uint32_t sel = arr ? 0u : rec;
+                        hm |= sel << (4 * u);
+                        am |= (arr ? inm : 0u) << (4 * u);
+                        rm |= rec << (4 * u);
+                        nonlean |= sel != 0u && (cm.x & 0x7fu) != (uint32_t)kHistBits;
+                        slots |= o << (8 * u);
+                    }
+                }
+                if (net.debug & 1u) hm = 0;   // experiment: filter only
+                // ---- arrivals (every synapse: history window + depression, Fig. 2c):
+                //      in place, two chunks (8 synapses) of gathers in flight per lane
+                if (net.debug & 128u) am = 0;   // experiment: skip the arrivals
+                if (__any_sync(0xffffffffu, am != 0u)) {
+#pragma unroll
+                    for (int hf = 0; hf < kStdpChPerThr / 2; hf++) {
+                        uint64_t hh[8];
+                        float xq[8];
+                        uint32_t jv[8];
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            const int u = 2 * hf + (q >> 2);
+                            const uint32_t bit = 4 * u + (q & 3);
+                            const uint32_t on = (am >> bit) & 1u;
+                            jv[q] = on ? lds_u32(sa + 16u * (gt + kStdpGroupThr * u) + 4u * (q & 3)) : 0u;
+                            hh[q] = ldg_u64_if(ghist + jv[q], (net.debug & 64u) ? 0u : (on & (rm >> bit)));
+                            xq[q] = ldg_f32_if(gxpost + jv[q], (net.debug & 16u) ? 0u : on);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            const int u = 2 * hf + (q >> 2);
+                            const uint32_t bit = 4 * u + (q & 3);
+                            if (!((am >> bit) & 1u)) continue;
+                            const StdpRow &rr = sm.rows[(slots >> (8 * u)) & 0xffu];
+                            const uint32_t meta = rr.meta;
+                            const int age = (int)(meta & 0x7fu);
+                            const uint32_t si = (meta >> 12) & 0x3u;
+                            const float4 pr = sm.par[si];
+                            const uint32_t ch = gt + kStdpGroupThr * u;             // chunk in the stage
+                            const float w0v = lds_f32(sa + kStdpStageCh * 16 + 16u * ch + 4u * (q & 3));
+                            const uint64_t m = hh[q] & (age >= 64 ? ~0ull : ((1ull << age) - 1ull));   // (tlu, t], R2
+                            const float w = stdp_synapse(w0v, m, true, xq[q], rr.xp, age,
+                                                         dp_addr + si * 4u * (kHistBits + 1), pr.x, pr.y, pr.z);
+                            const uint32_t chg = __float_as_uint(w) != __float_as_uint(w0v) ? 1u : 0u;
+                            const int64_t off = rr.cb + 4ll * ((int64_t)(a + ch) - (int64_t)rr.first) + (q & 3);
+                            stg_f32_if(gw + off, w, (net.debug & 32u) ? 0u : chg);
+                            n_w += chg;
+                        }
+                    }
+                }
+                // ---- list the selected synapses (warp-exclusive prefix of the counts)
+                const uint32_t k = __popc(hm);
+                uint32_t ex = k;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, ex, d);
+                    if (lane >= (uint32_t)d) ex += y;
+                }
+                uint32_t n = __shfl_sync(0xffffffffu, ex, 31);
+                ex -= k;
+                while (hm) {
+                    const uint32_t bpos = __ffs(hm) - 1u;
+                    hm &= hm - 1u;
+                    const uint32_t u = bpos >> 2;
+                    const uint32_t p = 4u * (gt + kStdpGroupThr * u) + (bpos & 3u);     // element in the stage
+                    sts_u32(list_a + 4u * ex, (p << 9) | (((rm >> bpos) & 1u) << 8) | ((slots >> (8 * u)) & 0xffu));
+                    ex++;
+                }
+                __syncwarp();
+                if (!__any_sync(0xffffffffu, nonlean)) {
+                    // ---- lean drain (forced flushes, R3): potentiation by the window's
+                    //      post spikes; the only spike's position comes from fpos[j]
+                    //      (one byte), several spikes take the history loop
+                    for (uint32_t b = 0; b < n; b += 128) {
+                        uint32_t ent[4], jv[4], pos[4];
+                        float wv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const uint32_t q = b + 32 * u + lane;
+                            const bool ok = q < n;
+                            ent[u] = ok ? lds_u32(list_a + 4u * q) : 0u;
+                            const uint32_t p = ent[u] >> 9;
+                            jv[u] = lds_u32(sa + 4u * p);
+                            wv[u] = lds_f32(sa + kStdpStageCh * 16 + 4u * p);
+                            pos[u] = ldg_u8_if(st.fpos + jv[u], ok && !(net.debug & 8u) ? 1u : 0u);
+                            if (net.debug & 8u) pos[u] = jv[u] & 31u;   // experiment: no gather
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            if (b + 32 * u + lane >= n) continue;
+                            const StdpRow &rr = sm.rows[ent[u] & 0xffu];
+                            const uint32_t si = (rr.meta >> 12) & 0x3u;
+                            const float4 pr = sm.par[si];
+                            const uint32_t dp = dp_addr + si * 4u * (kHistBits + 1);
+                            float w;
+                            if (pos[u] < 64u) {
+                                const float d = lds_f32(dp + 4u * ((uint32_t)kHistBits - pos[u]));
+                                const float nw = __fadd_rn(wv[u], __fmul_rn(pr.x, __fmul_rn(rr.xp, d)));
+                                w = nw < pr.z ? nw : pr.z;
+                            } else {
+                                w = stdp_synapse(wv[u], __ldg(ghist + jv[u]), false, 0.0f, rr.xp, kHistBits, dp,
+                                                 pr.x, pr.y, pr.z);
+                            }
+                            const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
+                            const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);
+                            stg_f32_if(gw + off, w, chg && !(net.debug & 4u));   // experiment 4: no store
+                            n_w += chg;
+                        }
+                    }
+                    n = 0;
+                }
+                // ---- drain the list, four entries per lane in flight
+                for (uint32_t b = 0; b < n; b += 128) {
+                    uint32_t ent[4];
+                    uint32_t jv[4];
+                    float wv[4];
+                    uint64_t hh[4];
+                    float xq[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint32_t q = b + 32 * u + lane;
+                        const bool ok = q < n;
+                        ent[u] = ok ? lds_u32(list_a + 4u * q) : 0u;
+                        const uint32_t p = ent[u] >> 9;
+                        jv[u] = lds_u32(sa + 4u * p);
+                        wv[u] = lds_f32(sa + kStdpStageCh * 16 + 4u * p);
+                        const bool arr = ok && (sm.rows[ent[u] & 0xffu].meta & kMetaArr) != 0;
+                        hh[u] = ldg_u64_if(ghist + jv[u], ok && ((ent[u] >> 8) & 1u) ? 1u : 0u);
+                        xq[u] = ldg_f32_if(gxpost + jv[u], arr ? 1u : 0u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (b + 32 * u + lane >= n) continue;
+                        const StdpRow &rr = sm.rows[ent[u] & 0xffu];
+                        const uint32_t meta = rr.meta;
+                        const bool arr = (meta & kMetaArr) != 0;
+                        const int age = (int)(meta & 0x7fu);
+                        const uint32_t si = (meta >> 12) & 0x3u;
+                        const float4 pr = sm.par[si];
+                        const uint64_t m = hh[u] & (age >= 64 ? ~0ull : ((1ull << age) - 1ull));   // (tlu, t], R2
+                        const float w = stdp_synapse(wv[u], m, arr, xq[u], rr.xp, age,
+                                                     dp_addr + si * 4u * (kHistBits + 1), pr.x, pr.y, pr.z);
+                        const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
+                        const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);
+                        stg_f32_if(gw + off, w, chg);
                         n_w += chg;
                     }
                 }
-                continue;
-            }
-            // ---- generic path (arrivals): gathers first, then the updates
-            // (branch-free: bitmap probe at a clamped index, predicated loads)
-            uint64_t h[kStdpU * 4];
-            float xq[kStdpU * 4];
-#pragma unroll
-            for (int u = 0; u < kStdpU; u++) {
-                const uint32_t jj[4] = {j4[u].x, j4[u].y, j4[u].z, j4[u].w};
-                const bool arr = (meta4[u] & kMetaArr) != 0;
-                const bool pot = xp4[u] != 0.0f;
-#pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const bool in = e >= (int)lo4[u] && e < (int)hi4[u];
-                    const uint32_t j = in ? jj[e] : pp_lo;
-                    const uint32_t word = lds_u32(rs_addr + ((j >> 5) << 2));
-                    const uint32_t rec = (in && pot) ? ((word >> (j & 31)) & 1u) : 0u;
-                    h[4 * u + e] = ldg_u64_if(ghist + j, rec);
-                    xq[4 * u + e] = ldg_f32_if(gxpost + j, (in && arr) ? 1u : 0u);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kStdpU; u++) {
-                const bool arr = (meta4[u] & kMetaArr) != 0;
-                const int age = (int)(meta4[u] & 0x7fu);
-                const uint64_t wmask = age >= 64 ? ~0ull : ((1ull << age) - 1ull);
-                const uint32_t si = (meta4[u] >> 12) & 0xfu;
-                const uint32_t dp = dp_addr + si * 4u * (kHistBits + 1);
-                const StdpDev &sd = net.stdp[si];
-                const float ww[4] = {w4[u].x, w4[u].y, w4[u].z, w4[u].w};
-#pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const bool in = e >= (int)lo4[u] && e < (int)hi4[u];
-                    const uint64_t m = in ? (h[4 * u + e] & wmask) : 0ull;     // post spikes in (tlu, t], R2
-                    const float w = stdp_synapse(ww[e], m, arr, xq[4 * u + e], xp4[u], age, dp, sd.a_plus,
-                                                 sd.a_minus, sd.w_max);
-                    const uint32_t chg = (in && __float_as_uint(w) != __float_as_uint(ww[e])) ? 1u : 0u;
-                    stg_f32_if(st.w + cc[u] + e, w, chg);
-                    n_w += chg;
-                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty_a + 8 * slot);   // stage and list free
             }
         }
+        g0 += nst;
+        __syncthreads();                           // row table reused next round
     }
     n_syn = __reduce_add_sync(0xffffffffu, n_syn);
     n_w = __reduce_add_sync(0xffffffffu, n_w);
@@ -616,7 +828,6 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
         if (n_syn) atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
         if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
     }
-    if (!readout && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&st.ctr->metric[2], (unsigned long long)nV);
     if (!readout) {
         __syncthreads();
         trace_mark(st.trace, 1, 3);
@@ -851,10 +1062,6 @@ k_deliver(NetDev net, StateDev st) {
         }
         __syncthreads();                           // table reused next round
     }
-    if (r_begin >= r_end) {        // no rows: still order the write-back after k_stdp(t)
-        pdl_wait();
-        pdl_launch();
-    }
     trace_mark(st.trace, 2, 2);
     // ---- write-back (one coalesced pass; several CTAs may share a slice)
     for (uint32_t rr = 0; rr < net.nrcpt; rr++) {
@@ -873,6 +1080,10 @@ k_deliver(NetDev net, StateDev st) {
         }
         if (n_seg) atomicAdd(&st.ctr->metric[6], (unsigned long long)n_seg);
     }
+    if (r_begin >= r_end) {        // no rows: still order the write-back after k_stdp(t)
+        pdl_wait();
+        pdl_launch();
+    }
     // ---- step completion: the last CTA books the list counts and advances t
     __syncthreads();
     trace_mark(st.trace, 2, 3);
@@ -881,13 +1092,15 @@ k_deliver(NetDev net, StateDev st) {
         const uint32_t nb = gridDim.x * gridDim.y;
         const uint32_t tk = atomicAdd(&st.ctr->ticket, 1u);
         if (tk == nb - 1) {
-            unsigned long long spikes = 0, flushes = 0;
+            unsigned long long spikes = 0, flushes = 0, visits = 0;
             for (uint32_t b = 0; b < nblk; b++) {
                 const uint4 c4 = cnt[b];
-                spikes += c4.z;
-                flushes += c4.w;
+                spikes += c4.y;
+                visits += c4.x + c4.z;
+                flushes += c4.z;
             }
             st.ctr->metric[1] += spikes;
+            st.ctr->metric[2] += visits;             // plastic rows visited: arrivals + forced flushes
             st.ctr->metric[5] += flushes;
             st.ctr->ticket = 0;
             __threadfence();
@@ -1013,7 +1226,8 @@ cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, 
 
 size_t stdp_smem_bytes(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
     const size_t nblk = front_blocks(net);
-    return 4 * ((nblk + 1 + 3) & ~(size_t)3) + 4ull * (((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 4);
+    return ((sizeof(StdpSmem) + 127) & ~(size_t)127) + (size_t)kStdpStages * kStdpStageCh * 32 +
+           8 * ((nblk + 1 + 3) & ~(size_t)3) + 16ull * ((((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 3) >> 2);
 }
 
 size_t deliver_smem_bytes(const NetDev &net) {

@@ -1,3 +1,2 @@
 python -c "import __graft_entry__ as g; g.build()"
-python scripts/trace.py 3 0 > gpurun_out/trace.log 2>&1
-python scripts/trace.py 3 2048 >> gpurun_out/trace.log 2>&1
+for C in 0 2048 512; do echo "== C=$C"; python scripts/trace.py 3 $C; done > gpurun_out/trace.log 2>&1

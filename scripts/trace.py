@@ -20,9 +20,9 @@ for rep in range(3):
         os.environ["SNN_DEBUG_KERNELS"] = dbg     # kernel experiment on the traced steps only
     g.step(1)
     os.environ.pop("SNN_DEBUG_KERNELS", None)
-    tr = g.read_state("TRACE").reshape(3, 4096, 4).astype(np.int64)
+    tr = g.read_state("TRACE").reshape(4, 4096, 4).astype(np.int64)
     t0 = tr[0][tr[0][:, 0] > 0][:, 0].min()
-    for k, name in enumerate(["front", "stdp", "deliver"]):
+    for k, name in [(0, "front"), (3, "stdp_arr"), (2, "deliver"), (1, "stdp")]:
         a = tr[k]
         a = a[a[:, 0] > 0]
         if len(a) == 0:
