@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--slice-width", type=int, default=0)
+    ap.add_argument("--history-bits", type=int, default=64, choices=[64, 128],
+                    help="H: 64 (the paper's default, P:192) or 128 (SURVEY 8(f3), P:399)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -173,7 +175,7 @@ def main():
     def make(flags=0):
         uid = pdist.nccl_unique_id() if world > 1 else None
         s = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream,
-                flags=flags, rank=rank, world=world, nccl_unique_id=uid)
+                flags=flags, rank=rank, world=world, nccl_unique_id=uid, history_bits=a.history_bits)
         rc.apply(s)
         return s
 
@@ -290,7 +292,7 @@ def main():
         "vs_baseline": None, "dtype": "f32 (int32 fixed-point accumulators)", "data": "synthetic",
         "config": {"workload": f"BASELINE config {a.config}: {rc.name}", "neurons": info["N"],
                    "synapses": info["S"], "plastic": rc.plastic, "dt_ms": rc.dt_ms, "delay_steps": rc.delay,
-                   "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
+                   "history_bits": a.history_bits, "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
                    "parallelism": f"target-range partition x{world}, NCCL spike-word all-gather" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2: %.1f GB of graph, each step touches the rows of that step's spikes"
                          % (info["S"] * 8 / 1e9)},

@@ -93,7 +93,8 @@ typedef struct {
     uint32_t struct_size;    /* sizeof(snn_config)                                */
     float dt_ms;             /* step length; 0.1 ms in the paper          */
     uint32_t delay_steps;    /* network-wide delay D in steps; D <= 62    */
-    uint32_t history_bits;   /* H: 64; only 64 is supported        */
+    uint32_t history_bits;   /* H: 64 or 128 ("64 to 128"):
+                                  forced flush at age H; 128 halves the flush work  */
     uint32_t slice_width;    /* C: neurons per slice; power of two
                                 in [32, 32768]; 0 = automatic                      */
     int32_t accum_frac_bits; /* F: fixed-point fraction bits of the int32 input

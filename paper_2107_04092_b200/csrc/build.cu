@@ -184,6 +184,7 @@ __global__ void k_init_state(NetDev net, StateDev st) {
     st.in_e[i] = 0;
     st.in_i[i] = 0;
     st.hist[i] = 0ull;
+    if (net.H > 64) st.hist_hi[i] = 0ull;
     st.nspk[i] = 0u;
     st.xpre[i] = 0.0f;
     st.tlu[i] = -1;

@@ -8,7 +8,8 @@
 namespace snn {
 
 constexpr int kMaxPops = 16;
-constexpr int kHistBits = 64;     // H
+constexpr int kHistBits = 64;     // bits per history word
+constexpr int kMaxHist = 128;     // H: 64 (one word) or 128 (two words)
 constexpr int kRingSlots = 64;    // bitmask ring: slot t % 64 holds step t's spikes
 constexpr uint32_t kArrBit = 0x80000000u;
 
@@ -37,7 +38,7 @@ struct PopDev {
 struct StdpDev {
     uint32_t dst_pop;
     float a_plus, a_minus, w_max;
-    float dplus[kHistBits + 1];   // fp32(exp(-n dt / tau_+)), n = 0..64 (closed-form skip-ahead)
+    float dplus[kMaxHist + 1];    // fp32(exp(-n dt / tau_+)), n = 0..H (closed-form skip-ahead)
 };
 
 struct NetDev {
@@ -52,6 +53,7 @@ struct NetDev {
     uint32_t share_w;            // words per rank share (rank r owns words [r share_w, ...))
     uint32_t wmax;               // words exchanged per rank and step
     uint32_t D;          // delay
+    uint32_t H;          // history bits: 64 or 128 (forced flush at age H, R3)
     uint32_t npop, nstdp;
     int32_t F;           // fixed-point fraction bits
     float scale, inv_scale;       // 2^F, 2^-F
@@ -83,9 +85,9 @@ struct Counters {
 
 // One row to process, written by the front kernel: forced flushes for k_stdp,
 // arrivals for k_deliver (which also runs the STDP of plastic arrivals).
-// meta: bits 0-6 age (1..64), bit 7 arrival, bits 8-9 receptor (3 = per target),
-//       bit 10 plastic row, bits 12-15 STDP projection index, bits 16+ source pop
-//       (per-target receptor).
+// meta: bits 0-7 age (1..H), bits 8-9 receptor (3 = per target), bit 10
+//       plastic row, bit 11 arrival, bits 12-15 STDP projection index, bits 16+
+//       source pop (per-target receptor).
 struct __align__(16) RowDesc {
     int64_t start;   // CSR offset of the row
     uint32_t row;    // source neuron id
@@ -94,14 +96,16 @@ struct __align__(16) RowDesc {
     uint32_t s0, s1; // plastic segment [s0, s1), row-relative
     uint32_t pad;
 };
-constexpr uint32_t kMetaArr = 1u << 7;
+constexpr uint32_t kMetaArr = 1u << 11;
+constexpr uint32_t kMetaAge = 0xffu;
 constexpr uint32_t kMetaPlastic = 1u << 10;
 
 struct StateDev {
     // neurons (indexed by global id)
     float *V, *ge, *gi, *xpost;
     int32_t *ref, *in_e, *in_i;
-    uint64_t *hist;
+    uint64_t *hist;          // bits 0..63 of the spike history (bit s: step t - s)
+    uint64_t *hist_hi;       // H = 128: bits 64..127 (else unused)
     uint8_t *fpos;           // post-plastic j with hist != 0: bit index of its only spike, 0xff if several
     uint32_t *nspk;
     uint32_t *ring;          // [kRingSlots][ring_stride]

@@ -222,6 +222,7 @@ static snn_status finalize(snn_sim *sim) {
     net.npop = (uint32_t)sim->pops.size();
     net.N = sim->N;
     net.D = cfg.delay_steps;
+    net.H = cfg.history_bits;
     net.F = cfg.accum_frac_bits;
     net.scale = std::ldexp(1.0f, net.F);
     net.inv_scale = std::ldexp(1.0f, -net.F);
@@ -271,7 +272,7 @@ static snn_status finalize(snn_sim *sim) {
             sd.a_plus = q.a_plus;
             sd.a_minus = q.a_minus;
             sd.w_max = q.w_max;
-            for (int n = 0; n <= kHistBits; n++) sd.dplus[n] = (float)std::exp(-(double)n * dt / (double)q.tau_plus_ms);
+            for (int n = 0; n <= kMaxHist; n++) sd.dplus[n] = (float)std::exp(-(double)n * dt / (double)q.tau_plus_ms);
             const float dm = (float)std::exp(-dt / (double)q.tau_minus_ms);
             if ((dp.flags & PF_POST_PLASTIC) && dp.d_minus != dm)
                 return sim->fail(SNN_E_UNSUPPORTED, "STDP projections into one population must share tau_minus");
@@ -338,6 +339,7 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.in_e, int32_t, N);
     ALLOC(st.in_i, int32_t, N);
     ALLOC(st.hist, uint64_t, N);
+    ALLOC(st.hist_hi, uint64_t, cfg.history_bits > 64 ? N : 1);
     ALLOC(st.fpos, uint8_t, (size_t)N + 16);
     ALLOC(st.nspk, uint32_t, N);
     // exchange geometry: rank r owns words [r share_w, ...), at most share_w + 1
@@ -510,10 +512,10 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         g_create_error = "snn_config: ABI version / struct size mismatch";
         return SNN_E_INVALID;
     }
-    if (!(cfg->dt_ms > 0.0f) || cfg->history_bits != 64 || cfg->delay_steps > 62 ||
+    if (!(cfg->dt_ms > 0.0f) || (cfg->history_bits != 64 && cfg->history_bits != 128) || cfg->delay_steps > 62 ||
         cfg->accum_frac_bits < 0 || cfg->accum_frac_bits > 30 || cfg->world < 1 || cfg->rank < 0 ||
         cfg->rank >= cfg->world) {
-        g_create_error = "snn_config: need dt > 0, history_bits == 64, delay <= 62, 0 <= F <= 30, 0 <= rank < world";
+        g_create_error = "snn_config: need dt > 0, history_bits 64 or 128, delay <= 62, 0 <= F <= 30, 0 <= rank < world";
         return SNN_E_INVALID;
     }
     const uint32_t C = cfg->slice_width;

@@ -194,11 +194,21 @@ k_front(NetDev net, StateDev st) {
             st.gi[i] = gi;
         }
         if (p.flags & PF_POST_PLASTIC) {
-            const uint64_t h = (st.hist[i] << 1) | (uint64_t)fired;
+            const uint64_t h0 = st.hist[i];
+            const uint64_t h = (h0 << 1) | (uint64_t)fired;
             st.hist[i] = h;
-            recent = h != 0ull;
+            uint64_t hh = 0ull;
+            if (net.H > kHistBits) {                 // H = 128: second word, bits 64..127
+                hh = (st.hist_hi[i] << 1) | (h0 >> 63);
+                st.hist_hi[i] = hh;
+            }
+            recent = (h | hh) != 0ull;
             // position of the window's only post spike (lean forced flush in k_stdp), 0xff: several
-            if (recent) st.fpos[i] = (h & (h - 1ull)) ? (uint8_t)0xffu : (uint8_t)(63 - __clzll((long long)h));
+            if (recent) {
+                const uint32_t n1 = __popcll(h) + __popcll(hh);
+                st.fpos[i] = n1 > 1 ? (uint8_t)0xffu
+                                    : (uint8_t)(h ? 63 - __clzll((long long)h) : 127 - __clzll((long long)hh));
+            }
             const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
             st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
         }
@@ -240,7 +250,7 @@ k_front(NetDev net, StateDev st) {
             st.tlu[i] = tl;
         }
         const int age = (int)(t - tl);
-        visit = arr || age >= kHistBits;    // forced flush at maximum age (R3)
+        visit = arr || age >= (int)net.H;    // forced flush at maximum age (R3)
         if (visit) {
             const uint2 sg = st.seg[i];
             d.start = st.row_ptr[i];
@@ -428,12 +438,26 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-// One plastic synapse (Fig. 2c, R7): potentiation by the post spikes in m,
-// oldest first ("__clz") with the closed-form skip-ahead
+// Window of a row of age `age`: history bits [0, age) = post spikes in steps
+// (tlu, t] (R2); bits 64..127 live in the second word (H = 128).
+__device__ __forceinline__ uint64_t window_lo(uint64_t lo, int age) { return age >= 64 ? lo : lo & ((1ull << age) - 1ull); }
+__device__ __forceinline__ uint64_t window_hi(uint64_t hi, int age) {
+    return age <= 64 ? 0ull : (age >= 128 ? hi : hi & ((1ull << (age - 64)) - 1ull));
+}
+
+// One plastic synapse (Fig. 2c, R7): potentiation by the post spikes in
+// (mhi:m), oldest first ("__clz") with the closed-form skip-ahead
 // w = min(w + A+ (x_pre D+[age - p]), w_max), then, on an arrival, the
 // depression w = max(w - A- x_post, 0).  dp = shared address of the D+ table.
 __device__ __forceinline__ float stdp_synapse(float w, uint64_t m, bool arr, float xq, float xp, int age,
-                                              uint32_t dp, float a_plus, float a_minus, float w_max) {
+                                              uint32_t dp, float a_plus, float a_minus, float w_max,
+                                              uint64_t mhi = 0ull) {
+    while (mhi) {                         // steps t-127 .. t-64 (H = 128)
+        const int pb = 127 - __clzll((long long)mhi);
+        mhi &= ~(1ull << (pb - 64));
+        const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, lds_f32(dp + 4u * (uint32_t)(age - pb)))));
+        w = nw < w_max ? nw : w_max;
+    }
     while (m) {
         const int pb = 63 - __clzll((long long)m);
         m &= ~(1ull << pb);
@@ -474,7 +498,7 @@ struct StdpSmem {                       // static part of k_stdp's shared memory
     StdpRow rows[kStdpRows];
     uint32_t incl[kStdpRows];
     uint32_t wsum[kStdpWarps];
-    float dplus[4 * (kHistBits + 1)];
+    float dplus[4 * (kMaxHist + 1)];
     float4 par[4];                      // per projection: a_plus, a_minus, w_max
     uint32_t list[kStdpConsWarps][kStdpList];   // (element p in stage << 9) | (rec << 8) | row slot
 };
@@ -517,8 +541,8 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
         mbar_init(bmap_a, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (uint32_t x = threadIdx.x; x < net.nstdp * (kHistBits + 1); x += kStdpThreads)
-        sm.dplus[x] = st.stdp[x / (kHistBits + 1)].dplus[x % (kHistBits + 1)];
+    for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kStdpThreads)
+        sm.dplus[x] = st.stdp[x / (kMaxHist + 1)].dplus[x % (kMaxHist + 1)];
     if (threadIdx.x < net.nstdp)
         sm.par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
                                           st.stdp[threadIdx.x].w_max, 0.0f);
@@ -554,6 +578,8 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     uint32_t g0 = 0;             // global stage index of the round's first stage (ring position)
     bool bm_ready = false;
     const uint64_t *__restrict__ ghist = st.hist;
+    const uint64_t *__restrict__ ghist_hi = st.hist_hi;
+    const uint32_t hi_on = net.H > kHistBits ? 1u : 0u;
     const float *__restrict__ gxpost = st.xpost;
     float *__restrict__ gw = st.w;
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kStdpRows) {
@@ -672,18 +698,18 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         hm |= sel << (4 * u);
                         am |= (arr ? inm : 0u) << (4 * u);
                         rm |= rec << (4 * u);
-                        nonlean |= sel != 0u && (cm.x & 0x7fu) != (uint32_t)kHistBits;
+                        nonlean |= sel != 0u && (cm.x & kMetaAge) != net.H;
                         slots |= o << (8 * u);
                     }
                 }
-                if (net.debug & 1u) hm = 0;   // experiment: filter only
+                if (net.debug & 1u) hm = 0;   // experiment: filter only (no list; arrivals still updated)
                 // ---- arrivals (every synapse: history window + depression, Fig. 2c):
                 //      in place, two chunks (8 synapses) of gathers in flight per lane
                 if (net.debug & 128u) am = 0;   // experiment: skip the arrivals
                 if (__any_sync(0xffffffffu, am != 0u)) {
 #pragma unroll
                     for (int hf = 0; hf < kStdpChPerThr / 2; hf++) {
-                        uint64_t hh[8];
+                        uint64_t hh[8], hh2[8];
                         float xq[8];
                         uint32_t jv[8];
 #pragma unroll
@@ -693,6 +719,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             const uint32_t on = (am >> bit) & 1u;
                             jv[q] = on ? lds_u32(sa + 16u * (gt + kStdpGroupThr * u) + 4u * (q & 3)) : 0u;
                             hh[q] = ldg_u64_if(ghist + jv[q], (net.debug & 64u) ? 0u : (on & (rm >> bit)));
+                            hh2[q] = ldg_u64_if(ghist_hi + jv[q], on & (rm >> bit) & hi_on);
                             xq[q] = ldg_f32_if(gxpost + jv[q], (net.debug & 16u) ? 0u : on);
                         }
 #pragma unroll
@@ -702,14 +729,14 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             if (!((am >> bit) & 1u)) continue;
                             const StdpRow &rr = sm.rows[(slots >> (8 * u)) & 0xffu];
                             const uint32_t meta = rr.meta;
-                            const int age = (int)(meta & 0x7fu);
+                            const int age = (int)(meta & kMetaAge);
                             const uint32_t si = (meta >> 12) & 0x3u;
                             const float4 pr = sm.par[si];
                             const uint32_t ch = gt + kStdpGroupThr * u;             // chunk in the stage
                             const float w0v = lds_f32(sa + kStdpStageCh * 16 + 16u * ch + 4u * (q & 3));
-                            const uint64_t m = hh[q] & (age >= 64 ? ~0ull : ((1ull << age) - 1ull));   // (tlu, t], R2
-                            const float w = stdp_synapse(w0v, m, true, xq[q], rr.xp, age,
-                                                         dp_addr + si * 4u * (kHistBits + 1), pr.x, pr.y, pr.z);
+                            const float w = stdp_synapse(w0v, window_lo(hh[q], age), true, xq[q], rr.xp, age,
+                                                         dp_addr + si * 4u * (kMaxHist + 1), pr.x, pr.y, pr.z,
+                                                         window_hi(hh2[q], age));   // (tlu, t], R2
                             const uint32_t chg = __float_as_uint(w) != __float_as_uint(w0v) ? 1u : 0u;
                             const int64_t off = rr.cb + 4ll * ((int64_t)(a + ch) - (int64_t)rr.first) + (q & 3);
                             stg_f32_if(gw + off, w, (net.debug & 32u) ? 0u : chg);
@@ -760,15 +787,15 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             const StdpRow &rr = sm.rows[ent[u] & 0xffu];
                             const uint32_t si = (rr.meta >> 12) & 0x3u;
                             const float4 pr = sm.par[si];
-                            const uint32_t dp = dp_addr + si * 4u * (kHistBits + 1);
+                            const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
                             float w;
-                            if (pos[u] < 64u) {
-                                const float d = lds_f32(dp + 4u * ((uint32_t)kHistBits - pos[u]));
+                            if (pos[u] < (uint32_t)kMaxHist) {
+                                const float d = lds_f32(dp + 4u * (net.H - pos[u]));
                                 const float nw = __fadd_rn(wv[u], __fmul_rn(pr.x, __fmul_rn(rr.xp, d)));
                                 w = nw < pr.z ? nw : pr.z;
                             } else {
-                                w = stdp_synapse(wv[u], __ldg(ghist + jv[u]), false, 0.0f, rr.xp, kHistBits, dp,
-                                                 pr.x, pr.y, pr.z);
+                                w = stdp_synapse(wv[u], __ldg(ghist + jv[u]), false, 0.0f, rr.xp, (int)net.H, dp,
+                                                 pr.x, pr.y, pr.z, hi_on ? __ldg(ghist_hi + jv[u]) : 0ull);
                             }
                             const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
                             const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);
@@ -783,7 +810,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                     uint32_t ent[4];
                     uint32_t jv[4];
                     float wv[4];
-                    uint64_t hh[4];
+                    uint64_t hh[4], hh2[4];
                     float xq[4];
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
@@ -795,6 +822,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         wv[u] = lds_f32(sa + kStdpStageCh * 16 + 4u * p);
                         const bool arr = ok && (sm.rows[ent[u] & 0xffu].meta & kMetaArr) != 0;
                         hh[u] = ldg_u64_if(ghist + jv[u], ok && ((ent[u] >> 8) & 1u) ? 1u : 0u);
+                        hh2[u] = ldg_u64_if(ghist_hi + jv[u], ok && ((ent[u] >> 8) & 1u) ? hi_on : 0u);
                         xq[u] = ldg_f32_if(gxpost + jv[u], arr ? 1u : 0u);
                     }
 #pragma unroll
@@ -803,12 +831,12 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         const StdpRow &rr = sm.rows[ent[u] & 0xffu];
                         const uint32_t meta = rr.meta;
                         const bool arr = (meta & kMetaArr) != 0;
-                        const int age = (int)(meta & 0x7fu);
+                        const int age = (int)(meta & kMetaAge);
                         const uint32_t si = (meta >> 12) & 0x3u;
                         const float4 pr = sm.par[si];
-                        const uint64_t m = hh[u] & (age >= 64 ? ~0ull : ((1ull << age) - 1ull));   // (tlu, t], R2
-                        const float w = stdp_synapse(wv[u], m, arr, xq[u], rr.xp, age,
-                                                     dp_addr + si * 4u * (kHistBits + 1), pr.x, pr.y, pr.z);
+                        const float w = stdp_synapse(wv[u], window_lo(hh[u], age), arr, xq[u], rr.xp, age,
+                                                     dp_addr + si * 4u * (kMaxHist + 1), pr.x, pr.y, pr.z,
+                                                     window_hi(hh2[u], age));   // (tlu, t], R2
                         const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
                         const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);
                         stg_f32_if(gw + off, w, chg);
@@ -1159,7 +1187,7 @@ k_readout_finish(NetDev net, StateDev st, int64_t t_last) {
     if (threadIdx.x >= st.rcnt[blockIdx.x].x) return;
     const RowDesc d = st.rdesc[(size_t)blockIdx.x * kFrontThreads + threadIdx.x];
     const StdpDev &sd = net.stdp[(d.meta >> 12) & 0xfu];
-    st.xpre[d.row] = xpre_after(sd, d.xp, (int)(d.meta & 0x7fu), false);
+    st.xpre[d.row] = xpre_after(sd, d.xp, (int)(d.meta & kMetaAge), false);
     st.tlu[d.row] = (int32_t)t_last;
 }
 

@@ -163,7 +163,7 @@ class Snn:
     def __init__(self, seed: int, dt_ms: float = 0.1, delay: int = 0, frac_bits: int = 20,
                  slice_width: int = 0, device: int = 0, stream=None, flags: int = 0, rank: int = 0,
                  world: int = 1, nccl_unique_id: bytes | None = None, group_key: int = 0,
-                 torch_allocator: bool = True):
+                 torch_allocator: bool = True, history_bits: int = 64):
         import torch  # plumbing: device memory and streams
         self._torch = torch
         self.device = device
@@ -175,7 +175,7 @@ class Snn:
         cfg.struct_size = ctypes.sizeof(snn_config)
         cfg.dt_ms = dt_ms
         cfg.delay_steps = delay
-        cfg.history_bits = 64
+        cfg.history_bits = history_bits   # H: 64 or 128
         cfg.slice_width = slice_width
         cfg.accum_frac_bits = frac_bits
         cfg.flags = flags

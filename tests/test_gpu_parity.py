@@ -11,9 +11,10 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _pair(rc, slice_width=0, flags=0):
+def _pair(rc, slice_width=0, flags=0, history_bits=64):
     from paper_2107_04092_b200 import Snn
-    g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=slice_width, flags=flags)
+    g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=slice_width, flags=flags,
+            history_bits=history_bits)
     rc.apply(g)
     g.finalize()
     o = O.Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, threads=8)
@@ -98,12 +99,14 @@ def _compare_weights(g, o, rc):
     return err.max()
 
 
-@pytest.mark.parametrize("delay", [0, 15])
-def test_brunel_plus_stdp_parity(delay):
+@pytest.mark.parametrize("delay,H", [(0, 64), (15, 64), (0, 128), (15, 128)])
+def test_brunel_plus_stdp_parity(delay, H):
     """Lazy+event STDP (GPU) vs naive STDP (oracle), 400 steps: forced flushes
-    at t = 63, 127, ... and arrivals both exercised; rasters bit-exact."""
+    at t = H-1, 2H-1, ... and arrivals both exercised; rasters bit-exact.  The
+    naive oracle has no history length: H = 128 must give
+    the same result as H = 64."""
     rc = W.brunel(10000, p=0.05, plastic=True, delay=delay, seed=7)
-    g, o = _pair(rc, slice_width=512)
+    g, o = _pair(rc, slice_width=512, history_bits=H)
     _run_compare(g, o, 400, exact_v=False, every=20)
     _compare_weights(g, o, rc)
     xp = g.read_state("XPRE_ROW")
@@ -120,14 +123,15 @@ def test_brunel_plus_stdp_parity(delay):
     assert m["FLUSH_ROWS"] > 0 and m["STDP_WTOUCH"] > 0
 
 
-def test_readout_flush_does_not_change_future():
+@pytest.mark.parametrize("H", [64, 128])
+def test_readout_flush_does_not_change_future(H):
     """Reading weights mid-run (read-out flush, R11) does not change later
     results: rasters identical, weights equal up to the rounding of splitting a
     closed-form decay D+[a+b] into D+[a] D+[b] (relative 1e-5)."""
     rc = W.brunel(6000, p=0.05, plastic=True, delay=3, seed=8)
-    g1, o = _pair(rc, slice_width=256)
+    g1, o = _pair(rc, slice_width=256, history_bits=H)
     from paper_2107_04092_b200 import Snn
-    g2 = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=256)
+    g2 = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=256, history_bits=H)
     rc.apply(g2)
     for t in range(200):
         g1.step(1)
@@ -154,11 +158,12 @@ def test_graph_replay_equals_direct_launches():
     assert a.t == b.t == 100
 
 
-def test_from_shared_state_100_steps():
+@pytest.mark.parametrize("H", [64, 128])
+def test_from_shared_state_100_steps(H):
     """North-star parity: GPU snapshot (after read-out flush) loaded into the
     oracle, then 100 steps on both: rasters bit-exact, V / w within 1e-4."""
     rc = W.brunel(10000, p=0.05, plastic=True, delay=15, seed=11)
-    g, o = _pair(rc, slice_width=1024)
+    g, o = _pair(rc, slice_width=1024, history_bits=H)
     g.step(250)
     # snapshot -> oracle
     for f, name in [("V", "V"), ("REFRACTORY", "ref"), ("G_EXC", "ge"), ("G_INH", "gi"),
@@ -208,6 +213,8 @@ def test_invalid_arguments_rejected():
         Snn(1, 0.1, 64, 20)                  # D >= H
     with pytest.raises(SnnError):
         Snn(1, 0.1, 0, 20, slice_width=1000)  # not a power of two
+    with pytest.raises(SnnError):
+        Snn(1, 0.1, 0, 20, history_bits=96)   # H is 64 or 128
     g = Snn(1, 0.1, 0, 20)
     with pytest.raises(SnnError) as e:
         g.add_population(W.LIF_DELTA, 0)
