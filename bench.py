@@ -38,6 +38,10 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--slice-width", type=int, default=0)
+    ap.add_argument("--plasticity", default="event", choices=["event", "lazy", "naive"],
+                    help="STDP schedule: Fig. 2c (default) / 2b / 2a (ablation, SURVEY 8(f2))")
+    ap.add_argument("--delivery", default="sliced", choices=["sliced", "rowwise"],
+                    help="delivery: Fig. 3b (default) / 3a (ablation)")
     ap.add_argument("--history-bits", type=int, default=64, choices=[64, 128],
                     help="H: 64 (the paper's default, P:192) or 128 (SURVEY 8(f3), P:399)")
     ap.add_argument("--seed", type=int, default=1)
@@ -175,7 +179,9 @@ def main():
     def make(flags=0):
         uid = pdist.nccl_unique_id() if world > 1 else None
         s = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream,
-                flags=flags, rank=rank, world=world, nccl_unique_id=uid, history_bits=a.history_bits)
+                flags=flags, rank=rank, world=world, nccl_unique_id=uid, history_bits=a.history_bits,
+                plasticity=["event", "lazy", "naive"].index(a.plasticity),
+                delivery=["sliced", "rowwise"].index(a.delivery))
         rc.apply(s)
         return s
 
@@ -292,7 +298,8 @@ def main():
         "vs_baseline": None, "dtype": "f32 (int32 fixed-point accumulators)", "data": "synthetic",
         "config": {"workload": f"BASELINE config {a.config}: {rc.name}", "neurons": info["N"],
                    "synapses": info["S"], "plastic": rc.plastic, "dt_ms": rc.dt_ms, "delay_steps": rc.delay,
-                   "history_bits": a.history_bits, "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
+                   "history_bits": a.history_bits, "plasticity": a.plasticity,
+                   "delivery": a.delivery, "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
                    "parallelism": f"target-range partition x{world}, NCCL spike-word all-gather" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2: %.1f GB of graph, each step touches the rows of that step's spikes"
                          % (info["S"] * 8 / 1e9)},
@@ -301,7 +308,8 @@ def main():
         "rates_hz": rates,
         "per_step": {k.lower(): v / a.steps for k, v in dm.items()},
         "gpu_launches": a.steps * (3 if rc.plastic else 2),
-        "roofline": {"bound": "hbm", "kernel": {"STDP": "k_stdp", "DELIVERY": "k_deliver"}[dom],
+        "roofline": {"bound": "hbm", "kernel": {"STDP": "k_stdp", "DELIVERY": "k_deliver_rowwise" if a.delivery == "rowwise"
+                                                 else "k_deliver"}[dom],
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                      "peak_source": peak_src, "kernels": kern,
                      "stdp_plus_delivery": {"achieved_gbs": sd_bytes / (sd_ms * 1e-3) / 1e9 if sd_ms else 0.0,

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 1u
+#define SNN_ABI_VERSION 2u
 
 typedef struct snn_sim snn_sim; /* opaque; owned by the library */
 typedef int32_t snn_status;
@@ -73,6 +73,22 @@ enum {
 enum { SNN_SYN_STATIC = 0, SNN_SYN_STDP = 1 };
 /* receptors: */
 enum { SNN_RCPT_EXC = 0, SNN_RCPT_INH = 1 };
+
+/* plasticity schedules (the paper's ablation, Fig. 2 / P:362,
+   P:399); all three compute the same weights (the naive sweep of Fig. 2a): */
+enum {
+    SNN_PLAST_EVENT = 0,    /* Fig. 2c: lazy + event-driven (default)            */
+    SNN_PLAST_LAZY = 1,     /* Fig. 2b: lazy, every synapse of a visited row is
+                               replayed step by step over its window (no bitmap
+                               filter, no skipping of empty steps)             */
+    SNN_PLAST_NAIVE = 2     /* Fig. 2a schedule: every plastic row is visited
+                               (streamed and updated) every step               */
+};
+/* delivery kernels (Fig. 3): */
+enum {
+    SNN_DELIV_SLICED = 0,   /* Fig. 3b: neuron-domain slices, shared atomics     */
+    SNN_DELIV_ROWWISE = 1   /* Fig. 3a: a warp per arriving row, global atomics  */
+};
 
 /* config flags */
 enum {
@@ -119,6 +135,8 @@ typedef struct {
        test transport: partitions of one network on one GPU, stepped in
        lockstep by the caller).                                                 */
     uint64_t group_key;
+    uint32_t plasticity;     /* SNN_PLAST_* (ablation; results identical)        */
+    uint32_t delivery;       /* SNN_DELIV_* (ablation; results identical)        */
 } snn_config;
 
 typedef struct {

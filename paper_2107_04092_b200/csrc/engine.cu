@@ -31,6 +31,7 @@ size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
 size_t deliver_smem_bytes(const NetDev &);
 cudaError_t kernels_configure(const NetDev &, uint32_t, uint32_t);
 cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
+cudaError_t launch_deliver_rowwise(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
@@ -223,6 +224,8 @@ static snn_status finalize(snn_sim *sim) {
     net.N = sim->N;
     net.D = cfg.delay_steps;
     net.H = cfg.history_bits;
+    net.plast_mode = cfg.plasticity;
+    net.deliv_mode = cfg.delivery;
     net.F = cfg.accum_frac_bits;
     net.scale = std::ldexp(1.0f, net.F);
     net.inv_scale = std::ldexp(1.0f, -net.F);
@@ -474,7 +477,8 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     if (sim->plastic)                                               // (2) P:37-39
         CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
     if (ev) CK(cudaEventRecord(ev[2], s));
-    CK(launch_deliver(net, st, sim->splits, s, pdl));               // (3) P:41
+    if (net.deliv_mode == SNN_DELIV_ROWWISE) CK(launch_deliver_rowwise(net, st, sim->stdp_grid, s, pdl));   // Fig. 3a
+    else CK(launch_deliver(net, st, sim->splits, s, pdl));          // (3) P:41, Fig. 3b
     if (ev) CK(cudaEventRecord(ev[3], s));
     return SNN_OK;
 }
@@ -516,6 +520,10 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         cfg->accum_frac_bits < 0 || cfg->accum_frac_bits > 30 || cfg->world < 1 || cfg->rank < 0 ||
         cfg->rank >= cfg->world) {
         g_create_error = "snn_config: need dt > 0, history_bits 64 or 128, delay <= 62, 0 <= F <= 30, 0 <= rank < world";
+        return SNN_E_INVALID;
+    }
+    if (cfg->plasticity > SNN_PLAST_NAIVE || cfg->delivery > SNN_DELIV_ROWWISE) {
+        g_create_error = "snn_config: plasticity must be SNN_PLAST_*, delivery SNN_DELIV_*";
         return SNN_E_INVALID;
     }
     const uint32_t C = cfg->slice_width;

@@ -251,6 +251,7 @@ k_front(NetDev net, StateDev st) {
         }
         const int age = (int)(t - tl);
         visit = arr || age >= (int)net.H;    // forced flush at maximum age (R3)
+        if (net.plast_mode == 2u) visit = true;   // SNN_PLAST_NAIVE: every row every step (Fig. 2a schedule)
         if (visit) {
             const uint2 sg = st.seg[i];
             d.start = st.row_ptr[i];
@@ -438,6 +439,22 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// Fig. 2b (SNN_PLAST_LAZY, ablation): the same updates as stdp_synapse, found
+// by replaying every step of the window instead of jumping between set bits.
+__device__ __noinline__ float stdp_synapse_lazy(float w, uint64_t m, bool arr, float xq, float xp, int age,
+                                                uint32_t dp, float a_plus, float a_minus, float w_max,
+                                                uint64_t mhi) {
+    for (int s = age - 1; s >= 0; s--) {             // steps t - s, oldest first
+        const uint64_t bit = s >= 64 ? (mhi >> (s - 64)) & 1ull : (m >> s) & 1ull;
+        if (bit) {
+            const float nw = __fadd_rn(w, __fmul_rn(a_plus, __fmul_rn(xp, lds_f32(dp + 4u * (uint32_t)(age - s)))));
+            w = nw < w_max ? nw : w_max;
+        }
+    }
+    const float dw = __fsub_rn(w, __fmul_rn(a_minus, xq));
+    return arr ? (dw > 0.0f ? dw : 0.0f) : w;
+}
+
 // Window of a row of age `age`: history bits [0, age) = post spikes in steps
 // (tlu, t] (R2); bits 64..127 live in the second word (H = 128).
 __device__ __forceinline__ uint64_t window_lo(uint64_t lo, int age) { return age >= 64 ? lo : lo & ((1ull << age) - 1ull); }
@@ -580,6 +597,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     const uint64_t *__restrict__ ghist = st.hist;
     const uint64_t *__restrict__ ghist_hi = st.hist_hi;
     const uint32_t hi_on = net.H > kHistBits ? 1u : 0u;
+    const bool lazy = net.plast_mode == 1u;          // SNN_PLAST_LAZY (ablation, Fig. 2b)
     const float *__restrict__ gxpost = st.xpost;
     float *__restrict__ gw = st.w;
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kStdpRows) {
@@ -597,7 +615,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
             const bool arr = (d.meta & kMetaArr) != 0;
             const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
             // a flush with x_pre == 0 changes no weight (potentiation adds 0)
-            if (cs < ce && (arr || d.xp != 0.0f)) {
+            if (cs < ce && (arr || d.xp != 0.0f || lazy)) {
                 rw.cb = cs & ~3ll;
                 rw.lo = (uint32_t)(cs - rw.cb);
                 rw.hi = (uint32_t)(ce - rw.cb);
@@ -693,12 +711,14 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             const uint32_t j = ((inm >> e) & 1u) ? jj[e] : pp_lo;
                             bits |= ((lds_u32(rs_addr + ((j >> 5) << 2)) >> (j & 31)) & 1u) << e;
                         }
-                        const uint32_t rec = pot ? (bits & inm) : 0u;
+                        // event (Fig. 2c): only targets that fired in the window; lazy
+                        // (Fig. 2b): every synapse, its history always read
+                        const uint32_t rec = lazy ? inm : (pot ? (bits & inm) : 0u);
                         const uint32_t sel = arr ? 0u : rec;
                         hm |= sel << (4 * u);
                         am |= (arr ? inm : 0u) << (4 * u);
                         rm |= rec << (4 * u);
-                        nonlean |= sel != 0u && (cm.x & kMetaAge) != net.H;
+                        nonlean |= sel != 0u && ((cm.x & kMetaAge) != net.H || lazy);
                         slots |= o << (8 * u);
                     }
                 }
@@ -734,9 +754,11 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             const float4 pr = sm.par[si];
                             const uint32_t ch = gt + kStdpGroupThr * u;             // chunk in the stage
                             const float w0v = lds_f32(sa + kStdpStageCh * 16 + 16u * ch + 4u * (q & 3));
-                            const float w = stdp_synapse(w0v, window_lo(hh[q], age), true, xq[q], rr.xp, age,
-                                                         dp_addr + si * 4u * (kMaxHist + 1), pr.x, pr.y, pr.z,
-                                                         window_hi(hh2[q], age));   // (tlu, t], R2
+                            const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+                            const float w = lazy ? stdp_synapse_lazy(w0v, window_lo(hh[q], age), true, xq[q], rr.xp, age,
+                                                                     dp, pr.x, pr.y, pr.z, window_hi(hh2[q], age))
+                                                 : stdp_synapse(w0v, window_lo(hh[q], age), true, xq[q], rr.xp, age,
+                                                                dp, pr.x, pr.y, pr.z, window_hi(hh2[q], age));   // (tlu, t], R2
                             const uint32_t chg = __float_as_uint(w) != __float_as_uint(w0v) ? 1u : 0u;
                             const int64_t off = rr.cb + 4ll * ((int64_t)(a + ch) - (int64_t)rr.first) + (q & 3);
                             stg_f32_if(gw + off, w, (net.debug & 32u) ? 0u : chg);
@@ -834,9 +856,11 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         const int age = (int)(meta & kMetaAge);
                         const uint32_t si = (meta >> 12) & 0x3u;
                         const float4 pr = sm.par[si];
-                        const float w = stdp_synapse(wv[u], window_lo(hh[u], age), arr, xq[u], rr.xp, age,
-                                                     dp_addr + si * 4u * (kMaxHist + 1), pr.x, pr.y, pr.z,
-                                                     window_hi(hh2[u], age));   // (tlu, t], R2
+                        const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+                        const float w = lazy ? stdp_synapse_lazy(wv[u], window_lo(hh[u], age), arr, xq[u], rr.xp, age,
+                                                                 dp, pr.x, pr.y, pr.z, window_hi(hh2[u], age))
+                                             : stdp_synapse(wv[u], window_lo(hh[u], age), arr, xq[u], rr.xp, age,
+                                                            dp, pr.x, pr.y, pr.z, window_hi(hh2[u], age));   // (tlu, t], R2
                         const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
                         const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);
                         stg_f32_if(gw + off, w, chg);
@@ -1137,6 +1161,74 @@ k_deliver(NetDev net, StateDev st) {
     }
 }
 
+// ------------------------------------------------------ k_deliver_rowwise
+// Fig. 3a (SNN_DELIV_ROWWISE, the ablation baseline): a warp per
+// arriving row, lanes over its columns, each delivery an int32 global atomic
+// (RED.ADD) into the target's accumulator -- no slicing, no shared memory.
+constexpr int kRowThreads = 512;
+
+__global__ void __launch_bounds__(kRowThreads)
+k_deliver_rowwise(NetDev net, StateDev st) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t wsum[kRowThreads / 32];
+    uint32_t *pre = reinterpret_cast<uint32_t *>(smem);                         // [nblk + 1]
+    const uint32_t nblk = st.nblk;
+    const uint32_t lane = threadIdx.x & 31;
+    if (net.nstdp == 0) pdl_wait();
+    const int64_t t = st.ctr->t;
+    const uint32_t par = (uint32_t)(t & 1);
+    const RowDesc *Al = st.adesc[par];
+    const uint4 *cnt = st.cnt[par];
+    region_prefix<kRowThreads>(cnt, nblk, 1, pre, wsum);
+    __syncthreads();
+    pdl_wait();            // k_stdp(t): updated weights of plastic arrivals
+    pdl_launch();
+    const uint32_t nA = pre[nblk];
+    const float scale = net.scale;
+    uint32_t n_ev = 0;
+    const uint32_t gw = (blockIdx.x * kRowThreads + threadIdx.x) >> 5, nw = (gridDim.x * kRowThreads) >> 5;
+    for (uint32_t r = gw; r < nA; r += nw) {
+        const RowDesc d = Al[region_index(pre, nblk, r)];
+        const int64_t c0 = d.start, c1 = st.row_ptr[d.row + 1];
+        uint32_t rc = (d.meta >> 8) & 3u;
+        const int src_pop = (int)((d.meta >> 16) & 0xfu);
+        n_ev += (uint32_t)(c1 - c0);
+        for (int64_t c = c0 + lane; c < c1; c += 32) {
+            const uint32_t j = __ldg(st.idx + c);
+            const float w = __ldg(st.w + c);
+            uint32_t r2 = rc;
+            if (r2 == 3u) r2 = (uint32_t)net.rcpt[src_pop][find_pop(net, j)];
+            atomicAdd((r2 == 0 ? st.in_e : st.in_i) + j, __float2int_rn(__fmul_rn(w, scale)));
+        }
+    }
+    n_ev = __reduce_add_sync(0xffffffffu, lane == 0 ? n_ev : 0u);
+    if (lane == 0 && n_ev) {
+        atomicAdd(&st.ctr->metric[0], (unsigned long long)n_ev);
+        atomicAdd(&st.ctr->metric[7], (unsigned long long)n_ev);
+    }
+    // ---- step completion: the last CTA books the list counts and advances t
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t tk = atomicAdd(&st.ctr->ticket, 1u);
+        if (tk == gridDim.x - 1) {
+            unsigned long long spikes = 0, flushes = 0, visits = 0;
+            for (uint32_t b = 0; b < nblk; b++) {
+                const uint4 c4 = cnt[b];
+                spikes += c4.y;
+                visits += c4.x + c4.z;
+                flushes += c4.z;
+            }
+            st.ctr->metric[1] += spikes;
+            st.ctr->metric[2] += visits;
+            st.ctr->metric[5] += flushes;
+            st.ctr->ticket = 0;
+            __threadfence();
+            st.ctr->t = t + 1;
+        }
+    }
+}
+
 // ----------------------------------------------------------- read-out (R11)
 // (1) finalise the visits of step t_last (pending x_pre / tlu updates) and
 //     clear their mask; (2) list every plastic row with tlu < t_last.
@@ -1275,6 +1367,11 @@ cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, 
                         uint32_t pp_hi, cudaStream_t s, bool pdl) {
     return launch_pdl(k_stdp, dim3(grid), dim3(kStdpThreads), stdp_smem_bytes(net, pp_lo, pp_hi), s, pdl, net, st,
                       t_fixed, pp_lo, pp_hi);
+}
+
+cudaError_t launch_deliver_rowwise(const NetDev &net, const StateDev &st, uint32_t grid, cudaStream_t s, bool pdl) {
+    return launch_pdl(k_deliver_rowwise, dim3(grid), dim3(kRowThreads), 4 * ((front_blocks(net) + 1 + 3) & ~(size_t)3),
+                      s, pdl, net, st);
 }
 
 cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s, bool pdl) {

@@ -22,12 +22,14 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- constants
-SNN_ABI_VERSION = 1
+SNN_ABI_VERSION = 2
 SNN_OK, SNN_E_INVALID, SNN_E_STATE, SNN_E_OOM, SNN_E_CUDA, SNN_E_NCCL, SNN_E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 POISSON, LIF_DELTA, LIF_CUBA = 0, 1, 2
 STATIC, STDP = 0, 1
 EXC, INH = 0, 1
 FLAG_NO_GRAPH, FLAG_PHASE_TIMING, FLAG_TRACE, FLAG_NO_PDL = 1, 2, 4, 8
+PLAST_EVENT, PLAST_LAZY, PLAST_NAIVE = 0, 1, 2        # Fig. 2c / 2b / 2a schedules
+DELIV_SLICED, DELIV_ROWWISE = 0, 1                    # Fig. 3b / 3a delivery
 ALL = 0xFFFFFFFF
 
 FIELD = dict(V=0, REFRACTORY=1, G_EXC=2, G_INH=3, INPUT_EXC=4, INPUT_INH=5, HIST=6, SPIKE_COUNT=7,
@@ -54,7 +56,8 @@ class snn_config(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("device", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
-                ("nccl_unique_id", ctypes.c_void_p), ("group_key", ctypes.c_uint64)]
+                ("nccl_unique_id", ctypes.c_void_p), ("group_key", ctypes.c_uint64),
+                ("plasticity", ctypes.c_uint32), ("delivery", ctypes.c_uint32)]
 
 
 class snn_pop_params(ctypes.Structure):
@@ -163,7 +166,7 @@ class Snn:
     def __init__(self, seed: int, dt_ms: float = 0.1, delay: int = 0, frac_bits: int = 20,
                  slice_width: int = 0, device: int = 0, stream=None, flags: int = 0, rank: int = 0,
                  world: int = 1, nccl_unique_id: bytes | None = None, group_key: int = 0,
-                 torch_allocator: bool = True, history_bits: int = 64):
+                 torch_allocator: bool = True, history_bits: int = 64, plasticity: int = 0, delivery: int = 0):
         import torch  # plumbing: device memory and streams
         self._torch = torch
         self.device = device
@@ -176,6 +179,8 @@ class Snn:
         cfg.dt_ms = dt_ms
         cfg.delay_steps = delay
         cfg.history_bits = history_bits   # H: 64 or 128
+        cfg.plasticity = plasticity       # PLAST_EVENT / PLAST_LAZY / PLAST_NAIVE (ablation, f2)
+        cfg.delivery = delivery           # DELIV_SLICED / DELIV_ROWWISE (ablation, f2)
         cfg.slice_width = slice_width
         cfg.accum_frac_bits = frac_bits
         cfg.flags = flags

@@ -38,9 +38,9 @@ def test_library_exports_every_declared_symbol(libpath):
 def test_library_loads_and_reports_abi_without_gpu(libpath):
     lib = ctypes.CDLL(libpath)
     lib.snn_abi_version.restype = ctypes.c_uint32
-    assert lib.snn_abi_version() == 1
     import paper_2107_04092_b200 as P
-    assert P.snn_abi_version() == 1
+    assert lib.snn_abi_version() == P.SNN_ABI_VERSION == 2
+    assert P.snn_abi_version() == 2
     for s in P.EXPORTS:
         assert hasattr(P, s)
 

@@ -11,10 +11,10 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _pair(rc, slice_width=0, flags=0, history_bits=64):
+def _pair(rc, slice_width=0, flags=0, history_bits=64, plasticity=0, delivery=0):
     from paper_2107_04092_b200 import Snn
     g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=slice_width, flags=flags,
-            history_bits=history_bits)
+            history_bits=history_bits, plasticity=plasticity, delivery=delivery)
     rc.apply(g)
     g.finalize()
     o = O.Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, threads=8)
@@ -123,6 +123,28 @@ def test_brunel_plus_stdp_parity(delay, H):
     assert m["FLUSH_ROWS"] > 0 and m["STDP_WTOUCH"] > 0
 
 
+@pytest.mark.parametrize("plasticity,delivery", [(1, 0), (2, 0), (0, 1), (2, 1)])
+def test_ablation_schedules_same_result(plasticity, delivery):
+    """the paper's ablation kernels -- lazy (Fig. 2b) and naive
+    (Fig. 2a schedule) plasticity, row-wise global-atomic delivery (Fig. 3a) --
+    compute the same network as the default (lazy + event-driven, sliced):
+    rasters bit-exact against the naive oracle, weights within 1e-4."""
+    rc = W.brunel(8000, p=0.05, plastic=True, delay=15, seed=17)
+    g, o = _pair(rc, slice_width=256, plasticity=plasticity, delivery=delivery)
+    _run_compare(g, o, 200, exact_v=False, every=25)
+    _compare_weights(g, o, rc)
+    if plasticity == 2:                         # naive: every plastic row every step
+        m = g.metrics()
+        assert m["STDP_ROWS"] >= 200 * 8000 // 2 * 0.99
+
+
+def test_rowwise_delivery_static_bit_exact():
+    rc = W.brunel(12000, p=0.02, plastic=False, seed=4)
+    g, o = _pair(rc, slice_width=64, delivery=1)
+    _run_compare(g, o, 120, every=10)
+    assert g.metrics()["EVENTS"] == o.events
+
+
 @pytest.mark.parametrize("H", [64, 128])
 def test_readout_flush_does_not_change_future(H):
     """Reading weights mid-run (read-out flush, R11) does not change later
@@ -215,6 +237,8 @@ def test_invalid_arguments_rejected():
         Snn(1, 0.1, 0, 20, slice_width=1000)  # not a power of two
     with pytest.raises(SnnError):
         Snn(1, 0.1, 0, 20, history_bits=96)   # H is 64 or 128
+    with pytest.raises(SnnError):
+        Snn(1, 0.1, 0, 20, plasticity=3)      # no such schedule
     g = Snn(1, 0.1, 0, 20)
     with pytest.raises(SnnError) as e:
         g.add_population(W.LIF_DELTA, 0)
