@@ -51,6 +51,22 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
+    summary (profiles/<round>/ncu_<tag>.json, written by scripts/summarize_ncu.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_v*.json")),
+                   key=lambda p: (os.path.basename(os.path.dirname(p)), int(os.path.basename(p)[5:-5])))
+    for p in reversed(files):
+        try:
+            d = json.load(open(p))
+        except Exception:
+            continue
+        if kernel in d and "dram_bytes" in d[kernel]:
+            return d[kernel]["dram_bytes"], os.path.relpath(p, ROOT)
+    return None, None
+
+
 def peaks():
     try:
         d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -287,6 +303,8 @@ def main():
                     "achieved_gbs": by / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0}
     dom = max(kern, key=lambda k2: kern[k2]["ms_per_step"])
     achieved = kern[dom]["achieved_gbs"]
+    dom_kernel = {"STDP": "k_stdp", "DELIVERY": "k_deliver_rowwise" if a.delivery == "rowwise" else "k_deliver"}[dom]
+    traffic, traffic_src = ncu_traffic(dom_kernel)
     shares = {k: ph[k] / ph["TOTAL"] for k in ("FRONT", "STDP", "DELIVERY")} if ph["TOTAL"] else {}
     sd_bytes, sd_ms = kb["STDP"] + kb["DELIVERY"], ph["STDP"] + ph["DELIVERY"]
     split_group = info["pivot_bytes"]
@@ -308,9 +326,10 @@ def main():
         "rates_hz": rates,
         "per_step": {k.lower(): v / a.steps for k, v in dm.items()},
         "gpu_launches": a.steps * (3 if rc.plastic else 2),
-        "roofline": {"bound": "hbm", "kernel": {"STDP": "k_stdp", "DELIVERY": "k_deliver_rowwise" if a.delivery == "rowwise"
-                                                 else "k_deliver"}[dom],
-                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+        "roofline": {"bound": "hbm", "kernel": dom_kernel,
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read + write)",
+                     "traffic_source": traffic_src, "algorithmic_bytes_per_launch": kern[dom]["bytes_per_step"],
                      "peak_source": peak_src, "kernels": kern,
                      "stdp_plus_delivery": {"achieved_gbs": sd_bytes / (sd_ms * 1e-3) / 1e9 if sd_ms else 0.0,
                                             "frac": sd_bytes / (sd_ms * 1e-3) / 1e9 / hbm if sd_ms else 0.0},

@@ -1,3 +1,3 @@
-# A/B: the committed (HEAD) build in _ab_head vs the working tree, same box
-echo "=== HEAD"; (cd _ab_head && timeout 300 python scripts/trace.py 3 0 2>&1 | tail -4 && timeout 300 python bench.py --steps 3000 --warmup 300 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('HEAD ms/step', d['ms_per_step'], d['roofline']['phase_ms_per_step'])")
-echo "=== WORK"; python -c "import __graft_entry__ as g; g.build()"; timeout 300 python scripts/trace.py 3 0 2>&1 | tail -4 && timeout 300 python bench.py --steps 3000 --warmup 300 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('WORK ms/step', d['ms_per_step'], d['roofline']['phase_ms_per_step'])"
+for cv in 25 -1 100 50; do
+SNN_DELIVER_CARVEOUT=$cv timeout 300 python bench.py --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('carveout $cv ms/step', d['ms_per_step'], d['roofline']['phase_ms_per_step'])"
+done
