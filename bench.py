@@ -42,6 +42,8 @@ def parse():
                     help="STDP schedule: Fig. 2c (default) / 2b / 2a (ablation, SURVEY 8(f2))")
     ap.add_argument("--delivery", default="sliced", choices=["sliced", "rowwise"],
                     help="delivery: Fig. 3b (default) / 3a (ablation)")
+    ap.add_argument("--idx16", action="store_true",
+                    help="delivery reads 16-bit slice-local target offsets (SURVEY 8(f1), P:405)")
     ap.add_argument("--history-bits", type=int, default=64, choices=[64, 128],
                     help="H: 64 (the paper's default, P:192) or 128 (SURVEY 8(f3), P:399)")
     ap.add_argument("--seed", type=int, default=1)
@@ -180,7 +182,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2107_04092_b200 import Snn, FLAG_PHASE_TIMING
+    from paper_2107_04092_b200 import Snn, FLAG_PHASE_TIMING, FLAG_IDX16
     from paper_2107_04092_b200 import dist as pdist
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
@@ -193,6 +195,8 @@ def main():
     stream = torch.cuda.Stream(dev)
 
     def make(flags=0):
+        if a.idx16:
+            flags |= FLAG_IDX16
         uid = pdist.nccl_unique_id() if world > 1 else None
         s = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream,
                 flags=flags, rank=rank, world=world, nccl_unique_id=uid, history_bits=a.history_bits,
@@ -289,11 +293,12 @@ def main():
     # algorithmic HBM bytes per kernel:
     #   k_stdp:    4 B target id per visited plastic synapse, 8 B where the weight
     #              is read and written, 16 B per visited row (x_pre, tlu, row_ptr, seg)
-    #   k_deliver: 8 B per delivered event (id + weight), 8 B per (arriving row,
+    #   k_deliver: 8 B per delivered event (id + weight; 6 B with --idx16), 8 B per (arriving row,
     #              slice) pivot pair, 4 B per slice neuron and receptor written back
     kb = {
         "STDP": 4 * d["STDP_SYN"] + 8 * d["STDP_WTOUCH"] + 16 * d["STDP_ROWS"],
-        "DELIVERY": 8 * d["EVENTS"] + 8 * d["SPIKES"] * info["nslices"] + 4 * nrcpt * info["R"] * psteps,
+        "DELIVERY": (6 if a.idx16 else 8) * d["EVENTS"] + 8 * d["SPIKES"] * info["nslices"]
+                    + 4 * nrcpt * info["R"] * psteps,
     }
     hbm, peak_src = peaks()
     kern = {}
@@ -317,7 +322,7 @@ def main():
         "config": {"workload": f"BASELINE config {a.config}: {rc.name}", "neurons": info["N"],
                    "synapses": info["S"], "plastic": rc.plastic, "dt_ms": rc.dt_ms, "delay_steps": rc.delay,
                    "history_bits": a.history_bits, "plasticity": a.plasticity,
-                   "delivery": a.delivery, "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
+                   "delivery": a.delivery, "index_bits": 16 if a.idx16 else 32, "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
                    "parallelism": f"target-range partition x{world}, NCCL spike-word all-gather" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2: %.1f GB of graph, each step touches the rows of that step's spikes"
                          % (info["S"] * 8 / 1e9)},

@@ -100,8 +100,13 @@ enum {
     SNN_FLAG_TRACE = 1u << 2,        /* debug: per-CTA %globaltimer phase marks of
                                         the last step (implies NO_GRAPH); read with
                                         SNN_FIELD_TRACE                             */
-    SNN_FLAG_NO_PDL = 1u << 3        /* no programmatic dependent launch between
+    SNN_FLAG_NO_PDL = 1u << 3,       /* no programmatic dependent launch between
                                         the kernels of a step                       */
+    SNN_FLAG_IDX16 = 1u << 4         /* compressed indices:
+                                        delivery reads 16-bit slice-local target
+                                        offsets (j - slice base) instead of 32-bit
+                                        ids -- 6 instead of 8 B per event; the
+                                        32-bit ids stay for STDP and read-out      */
 };
 
 typedef struct {
@@ -191,10 +196,12 @@ enum {
                                    over steps run with SNN_FLAG_PHASE_TIMING     */
     SNN_FIELD_INFO = 19,        /* [i64 / 8]  N, S, nslices, C, R, tgt_lo, tgt_hi,
                                    (delivery splits << 32) | STDP grid          */
-    SNN_FIELD_TRACE = 20,       /* [u64 / 3*4096*4] debug phase marks (ns) of the
+    SNN_FIELD_TRACE = 20,       /* [u64 / 4*4096*4] debug phase marks (ns) of the
                                    last step: [kernel][cta][phase], kernels
                                    front / stdp / deliver                        */
-    SNN_FIELD_COUNT = 21
+    SNN_FIELD_IDX16 = 21,       /* [u16 / S]   slice-local target offsets
+                                   (j - tgt_lo) mod C (SNN_FLAG_IDX16 only)      */
+    SNN_FIELD_COUNT = 22
 };
 
 /* SNN_FIELD_METRICS layout (device counters, cumulative over steps) */

@@ -218,6 +218,18 @@ cudaError_t build_fill(const NetDev &net, const BuildTabs &tabs, const uint32_t 
     return cudaGetLastError();
 }
 
+// Compressed indices: a target's offset in its slice,
+// (j - tgt_lo) mod C -- every (row, slice) segment indexes only C neurons.
+__global__ void k_idx16(NetDev net, const uint32_t *idx, uint16_t *idx16, int64_t S) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < S; c += (int64_t)gridDim.x * blockDim.x)
+        idx16[c] = (uint16_t)((idx[c] - net.tgt_lo) & (net.C - 1u));
+}
+
+cudaError_t build_idx16(const NetDev &net, const uint32_t *idx, uint16_t *idx16, int64_t S, cudaStream_t s) {
+    if (S > 0) k_idx16<<<1184, 256, 0, s>>>(net, idx, idx16, S);
+    return cudaGetLastError();
+}
+
 cudaError_t build_segments(const NetDev &net, const int64_t *row_ptr, const uint32_t *idx,
                            uint2 *seg, cudaStream_t s) {
     k_segments<<<(net.N + 255) / 256, 256, 0, s>>>(net, row_ptr, idx, seg);

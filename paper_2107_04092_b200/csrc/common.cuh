@@ -117,6 +117,7 @@ struct StateDev {
     // graph (this rank's target range)
     int64_t *row_ptr;        // [N+1]
     uint32_t *idx;           // [S + pad]
+    uint16_t *idx16;         // [S + pad] slice-local target offsets (SNN_FLAG_IDX16), else null
     float *w;                // [S + pad]
     uint32_t *piv;           // [N][nslices+1], row-relative
     uint2 *seg;              // [N] plastic segment (lo, hi), row-relative

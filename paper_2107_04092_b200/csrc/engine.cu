@@ -25,6 +25,7 @@ cudaError_t build_fill(const NetDev &, const BuildTabs &, const uint32_t *, cons
                        float *, cudaStream_t);
 cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, uint2 *, cudaStream_t);
 cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
+cudaError_t build_idx16(const NetDev &, const uint32_t *, uint16_t *, int64_t, cudaStream_t);
 uint32_t front_blocks(const NetDev &);
 cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool);
 size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
@@ -416,6 +417,11 @@ static snn_status finalize(snn_sim *sim) {
     CK(cudaMemsetAsync(st.w + sim->nsyn, 0, 8 * sizeof(float), s));
     CK(build_fill(net, tabs, st.piv, st.row_ptr, st.idx, st.w, s));
     CK(build_segments(net, st.row_ptr, st.idx, st.seg, s));
+    st.idx16 = nullptr;
+    if (cfg.flags & SNN_FLAG_IDX16) {
+        ALLOC(st.idx16, uint16_t, (size_t)sim->nsyn + 16);
+        CK(build_idx16(net, st.idx, st.idx16, sim->nsyn, s));
+    }
     CK(init_state(net, st, s));
     {
         StdpDev *tab = nullptr;
@@ -706,6 +712,9 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
     case SNN_FIELD_HIST: bytes = 8ull * n; break;
     case SNN_FIELD_ROW_PTR: src = st.row_ptr; bytes = 8ull * (sim->N + 1); break;
     case SNN_FIELD_IDX: src = st.idx; bytes = 4ull * sim->nsyn; break;
+    case SNN_FIELD_IDX16:
+        if (!st.idx16) return sim->fail(SNN_E_STATE, "IDX16 needs SNN_FLAG_IDX16");
+        src = st.idx16; bytes = 2ull * sim->nsyn; break;
     case SNN_FIELD_WEIGHTS: src = st.w; bytes = 4ull * sim->nsyn; break;
     case SNN_FIELD_PIVOTS: src = st.piv; bytes = 4ull * sim->N * (net.nslices + 1); break;
     case SNN_FIELD_SPIKE_RING: src = st.ring; bytes = 4ull * kRingSlots * net.nwords; break;

@@ -950,10 +950,19 @@ __device__ __forceinline__ float ldg_nc_f32(uint64_t a) {
 // Owner-window pass (k_deliver): thread x takes elements w0 + x + 512 u of the
 // window.  Segment of element x: bw.y + popc(start bits <= x) (s_bw word).
 // s_ptr holds per segment the byte address of idx[c] for flattened element 0.
-template <bool kMulti, bool kCheck>
+__device__ __forceinline__ uint32_t ldg_nc_u16(uint64_t a) {
+    uint16_t v;
+    asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(a));
+    return v;
+}
+
+// kIdx16 (SNN_FLAG_IDX16): s_ptr addresses the 16-bit
+// slice-local offsets (2 B per element, the weight at 2 a + dw) and the target
+// is already local to the slice; else the 32-bit ids (4 B, weight at a + dw).
+template <bool kMulti, bool kCheck, bool kIdx16>
 __device__ __forceinline__ void deliver_pass(const NetDev &net, uint32_t x0, uint32_t wlen, uint32_t w0,
                                              uint32_t bw_a, uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a,
-                                             uint64_t dw, float scale) {
+                                             uint64_t dw, float scale, uint32_t slo) {
     uint32_t jj[kDelU], rr[kDelU];
     float ww[kDelU];
 #pragma unroll
@@ -965,9 +974,15 @@ __device__ __forceinline__ void deliver_pass(const NetDev &net, uint32_t x0, uin
                                   : x0 + u * kDelThreads + threadIdx.x;
         const uint2 bw = lds_u2(bw_a + ((x >> 5) << 3));
         const uint32_t gi = bw.y + __popc(bw.x & (0xffffffffu >> (31u - (x & 31u))));
-        const uint64_t a = lds_u64(ptr_a + (gi << 3)) + 4ull * (w0 + x);
-        jj[u] = ldg_nc_u32(a);
-        ww[u] = ldg_nc_f32(a + dw);
+        if (kIdx16) {
+            const uint64_t a = lds_u64(ptr_a + (gi << 3)) + 2ull * (w0 + x);
+            jj[u] = ldg_nc_u16(a);
+            ww[u] = ldg_nc_f32(2ull * a + dw);
+        } else {
+            const uint64_t a = lds_u64(ptr_a + (gi << 3)) + 4ull * (w0 + x);
+            jj[u] = ldg_nc_u32(a);
+            ww[u] = ldg_nc_f32(a + dw);
+        }
         rr[u] = kMulti ? lds_u8(rc_a + gi) : 0u;
     }
 #pragma unroll
@@ -975,8 +990,25 @@ __device__ __forceinline__ void deliver_pass(const NetDev &net, uint32_t x0, uin
         const uint32_t x = x0 + u * kDelThreads + threadIdx.x;
         if (!kCheck || x < wlen) {
             uint32_t r2 = rr[u];
-            if (kMulti && r2 >= 3u) r2 = (uint32_t)net.rcpt[r2 >> 2][find_pop(net, jj[u])];
+            if (kMulti && r2 >= 3u) r2 = (uint32_t)net.rcpt[r2 >> 2][find_pop(net, kIdx16 ? slo + jj[u] : jj[u])];
             red_shared_add(acc_a + ((r2 * net.C + jj[u]) << 2), __float2int_rn(__fmul_rn(ww[u], scale)));
+        }
+    }
+}
+
+template <bool kIdx16>
+__device__ __forceinline__ void deliver_window(const NetDev &net, uint32_t wlen, uint32_t w0, uint32_t bw_a,
+                                               uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a, uint64_t dw,
+                                               float scale, uint32_t slo) {
+    const bool multi_rc = net.nrcpt > 1;
+    for (uint32_t x0 = 0; x0 < wlen; x0 += kDelThreads * kDelU) {
+        const bool full = x0 + kDelThreads * kDelU <= wlen;
+        if (multi_rc) {
+            if (full) deliver_pass<true, false, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+            else deliver_pass<true, true, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+        } else {
+            if (full) deliver_pass<false, false, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+            else deliver_pass<false, true, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
         }
     }
 }
@@ -1024,10 +1056,12 @@ k_deliver(NetDev net, StateDev st) {
     const uint32_t r_end = (uint32_t)(((uint64_t)nA * (split + 1)) / nsplit);
     const uint32_t P = net.nslices + 1;
     const float scale = net.scale;
-    const bool multi_rc = net.nrcpt > 1;
     const uint32_t bw_a = smem_u32(s_bw), ptr_a = smem_u32(s_ptr), rc_a = smem_u32(s_rc);
-    const uint32_t acc_a = smem_u32(acc) - 4u * slo;       // accumulator of target j, receptor r: + 4 (r C + j)
-    const uint64_t dw = (uint64_t)st.w - (uint64_t)st.idx;   // w[c] at idx[c] + dw (bytes)
+    const bool idx16 = st.idx16 != nullptr;
+    // accumulator of target j (32-bit ids) / slice offset j - slo (16-bit), receptor r: + 4 (r C + j)
+    const uint32_t acc_a = idx16 ? smem_u32(acc) : smem_u32(acc) - 4u * slo;
+    // w[c] at idx[c] + dw, or at 2 idx16[c] + dw (bytes)
+    const uint64_t dw = idx16 ? (uint64_t)st.w - 2ull * (uint64_t)st.idx16 : (uint64_t)st.w - (uint64_t)st.idx;
     uint32_t n_ev = 0, n_seg = 0;
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kDelRows) {
         // ---- tabulate (two rows per thread): descriptor + pivot pair
@@ -1075,7 +1109,8 @@ k_deliver(NetDev net, StateDev st) {
         for (int q = 0; q < 2; q++) {
             if (len2[q] == 0) continue;
             s_rc[g] = (uint8_t)rcq[q];
-            s_ptr[g] = (uint64_t)(st.idx + c0q[q]) - 4ull * est[q];
+            s_ptr[g] = idx16 ? (uint64_t)(st.idx16 + c0q[q]) - 2ull * est[q]
+                             : (uint64_t)(st.idx + c0q[q]) - 4ull * est[q];
             g++;
         }
         if (r0 == r_begin) {
@@ -1100,16 +1135,8 @@ k_deliver(NetDev net, StateDev st) {
             s_bw[threadIdx.x].y = before + winc - pc - 1u;
             __syncthreads();
             // ---- elements: thread x takes w0 + x + 512 u (coalesced)
-            for (uint32_t x0 = 0; x0 < wlen; x0 += kDelThreads * kDelU) {
-                const bool full = x0 + kDelThreads * kDelU <= wlen;
-                if (multi_rc) {
-                    if (full) deliver_pass<true, false>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale);
-                    else deliver_pass<true, true>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale);
-                } else {
-                    if (full) deliver_pass<false, false>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale);
-                    else deliver_pass<false, true>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale);
-                }
-            }
+            if (idx16) deliver_window<true>(net, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+            else deliver_window<false>(net, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
             if (w0 + kDelWin < T) __syncthreads();  // bitmap reused by the next window
         }
         __syncthreads();                           // table reused next round

@@ -27,20 +27,20 @@ SNN_OK, SNN_E_INVALID, SNN_E_STATE, SNN_E_OOM, SNN_E_CUDA, SNN_E_NCCL, SNN_E_UNS
 POISSON, LIF_DELTA, LIF_CUBA = 0, 1, 2
 STATIC, STDP = 0, 1
 EXC, INH = 0, 1
-FLAG_NO_GRAPH, FLAG_PHASE_TIMING, FLAG_TRACE, FLAG_NO_PDL = 1, 2, 4, 8
+FLAG_NO_GRAPH, FLAG_PHASE_TIMING, FLAG_TRACE, FLAG_NO_PDL, FLAG_IDX16 = 1, 2, 4, 8, 16
 PLAST_EVENT, PLAST_LAZY, PLAST_NAIVE = 0, 1, 2        # Fig. 2c / 2b / 2a schedules
 DELIV_SLICED, DELIV_ROWWISE = 0, 1                    # Fig. 3b / 3a delivery
 ALL = 0xFFFFFFFF
 
 FIELD = dict(V=0, REFRACTORY=1, G_EXC=2, G_INH=3, INPUT_EXC=4, INPUT_INH=5, HIST=6, SPIKE_COUNT=7,
              XPOST=8, XPRE_ROW=9, TLU=10, ROW_PTR=11, IDX=12, WEIGHTS=13, PIVOTS=14, STEP=15,
-             METRICS=16, SPIKE_RING=17, PHASE_TIMES=18, INFO=19, TRACE=20)
+             METRICS=16, SPIKE_RING=17, PHASE_TIMES=18, INFO=19, TRACE=20, IDX16=21)
 FIELD_DTYPE = dict(V=np.float32, REFRACTORY=np.int32, G_EXC=np.float32, G_INH=np.float32,
                    INPUT_EXC=np.int32, INPUT_INH=np.int32, HIST=np.uint64, SPIKE_COUNT=np.uint32,
                    XPOST=np.float32, XPRE_ROW=np.float32, TLU=np.int32, ROW_PTR=np.int64,
                    IDX=np.uint32, WEIGHTS=np.float32, PIVOTS=np.uint32, STEP=np.int64,
                    METRICS=np.uint64, SPIKE_RING=np.uint32, PHASE_TIMES=np.float64, INFO=np.int64,
-                   TRACE=np.uint64)
+                   TRACE=np.uint64, IDX16=np.uint16)
 METRIC = dict(EVENTS=0, SPIKES=1, STDP_ROWS=2, STDP_SYN=3, STDP_WTOUCH=4, FLUSH_ROWS=5, SEGMENTS=6, ELEMS=7)
 PHASE = dict(FRONT=0, STDP=1, DELIVERY=2, EXCHANGE=3, TOTAL=4)
 

@@ -138,6 +138,28 @@ def test_ablation_schedules_same_result(plasticity, delivery):
         assert m["STDP_ROWS"] >= 200 * 8000 // 2 * 0.99
 
 
+@pytest.mark.parametrize("C", [64, 1024])
+def test_idx16_offsets_and_delivery_bit_exact(C):
+    """SURVEY 8(f1) compressed indices: the 16-bit slice-local offsets equal
+    (j - tgt_lo) mod C of the oracle's ids, and delivery through them
+    reproduces Vogels config 1 (two receptors) bit-exactly."""
+    from paper_2107_04092_b200 import FLAG_IDX16
+    rc = W.config(1)
+    g, o = _pair(rc, slice_width=C, flags=FLAG_IDX16)
+    lo = g.info()["tgt_lo"]
+    assert np.array_equal(g.read_state("IDX16").astype(np.int64), (o.array("idx").astype(np.int64) - lo) % C)
+    _run_compare(g, o, 200, every=20)
+    assert g.metrics()["EVENTS"] == o.events
+
+
+def test_idx16_brunel_plus_parity():
+    from paper_2107_04092_b200 import FLAG_IDX16
+    rc = W.brunel(10000, p=0.05, plastic=True, delay=15, seed=7)
+    g, o = _pair(rc, slice_width=512, flags=FLAG_IDX16)
+    _run_compare(g, o, 200, exact_v=False, every=25)
+    _compare_weights(g, o, rc)
+
+
 def test_rowwise_delivery_static_bit_exact():
     rc = W.brunel(12000, p=0.02, plastic=False, seed=4)
     g, o = _pair(rc, slice_width=64, delivery=1)
