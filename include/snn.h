@@ -222,7 +222,10 @@ enum {
     SNN_PHASE_STDP = 1,     /* lazy + event-driven STDP                       */
     SNN_PHASE_DELIVERY = 2, /* sliced shared-atomic delivery                  */
     SNN_PHASE_EXCHANGE = 3, /* spike-bitmask all-gather (world > 1)           */
-    SNN_PHASE_TOTAL = 4
+    SNN_PHASE_TOTAL = 4,
+    SNN_PHASE_BUILD = 5     /* graph construction on the GPU (count, scan, fill,
+                               segments), device time of the last finalize; not
+                               part of a step            */
 };
 
 /* Creates a simulation handle bound to cfg->device / cfg->stream.

@@ -403,20 +403,34 @@ static snn_status finalize(snn_sim *sim) {
     int64_t *len = nullptr;
     ALLOC(len, int64_t, (size_t)N + 1);
     CK(cudaMemsetAsync(len + N, 0, sizeof(int64_t), s));
+    cudaEvent_t bev[4];
+    for (auto &e : bev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(bev[0], s));
     CK(build_count(net, tabs, st.piv, s));
     size_t tmp_bytes = 0;
     CK(build_scan(net, st.piv, len, st.row_ptr, nullptr, &tmp_bytes, s));
     void *tmp = sim->dalloc(tmp_bytes);
     if (!tmp) return sim->fail(SNN_E_OOM, "scan scratch");
     CK(build_scan(net, st.piv, len, st.row_ptr, tmp, &tmp_bytes, s));
+    CK(cudaEventRecord(bev[1], s));
     CK(cudaMemcpyAsync(&sim->nsyn, st.row_ptr + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     ALLOC(st.idx, uint32_t, (size_t)sim->nsyn + 8);
     ALLOC(st.w, float, (size_t)sim->nsyn + 8);
     CK(cudaMemsetAsync(st.idx + sim->nsyn, 0, 8 * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(st.w + sim->nsyn, 0, 8 * sizeof(float), s));
+    CK(cudaEventRecord(bev[2], s));
     CK(build_fill(net, tabs, st.piv, st.row_ptr, st.idx, st.w, s));
     CK(build_segments(net, st.row_ptr, st.idx, st.seg, s));
+    CK(cudaEventRecord(bev[3], s));
+    {   // device time of the construction (SNN_PHASE_BUILD), allocation excluded
+        CK(cudaEventSynchronize(bev[3]));
+        float m0 = 0.0f, m1 = 0.0f;
+        CK(cudaEventElapsedTime(&m0, bev[0], bev[1]));
+        CK(cudaEventElapsedTime(&m1, bev[2], bev[3]));
+        sim->phase_ms[SNN_PHASE_BUILD] = (double)m0 + (double)m1;
+        for (auto &e : bev) cudaEventDestroy(e);
+    }
     st.idx16 = nullptr;
     if (cfg.flags & SNN_FLAG_IDX16) {
         ALLOC(st.idx16, uint16_t, (size_t)sim->nsyn + 16);

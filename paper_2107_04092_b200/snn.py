@@ -42,7 +42,7 @@ FIELD_DTYPE = dict(V=np.float32, REFRACTORY=np.int32, G_EXC=np.float32, G_INH=np
                    METRICS=np.uint64, SPIKE_RING=np.uint32, PHASE_TIMES=np.float64, INFO=np.int64,
                    TRACE=np.uint64, IDX16=np.uint16)
 METRIC = dict(EVENTS=0, SPIKES=1, STDP_ROWS=2, STDP_SYN=3, STDP_WTOUCH=4, FLUSH_ROWS=5, SEGMENTS=6, ELEMS=7)
-PHASE = dict(FRONT=0, STDP=1, DELIVERY=2, EXCHANGE=3, TOTAL=4)
+PHASE = dict(FRONT=0, STDP=1, DELIVERY=2, EXCHANGE=3, TOTAL=4, BUILD=5)
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
