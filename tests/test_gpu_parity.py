@@ -279,3 +279,35 @@ def test_invalid_arguments_rejected():
     with pytest.raises(SnnError) as e:
         g.finalize()
     assert e.value.code == SNN_E_INVALID
+
+
+# ------------------------------------------------------------- long run
+def test_long_run_rates_and_weight_histogram_within_1pct():
+    """BASELINE north star: "Long-run firing rates and weight histograms must
+    agree within 1%".  Brunel+ scaled to N = 31,623 (1e7 synapses, 40 %
+    plastic, D = 15), 10,000 steps = 1 s of biological time on both sides; the
+    trajectories may part once a weight rounding difference (<= 2e-6 relative)
+    flips a spike, so the statistics are compared: per-population rates and the
+    64-bin histogram of the plastic weights on [0, w_max]."""
+    rc = W.brunel(31_623, p=0.02, plastic=True, delay=15, seed=3)
+    g, o = _pair(rc)
+    g.step(10_000)
+    o.step(10_000)
+    sg = g.read_state("SPIKE_COUNT").astype(np.float64)
+    so = o.array("nspk").astype(np.float64)
+    b = 0
+    for p in rc.pops:
+        rg, ro = sg[b:b + p.n].sum(), so[b:b + p.n].sum()
+        assert ro > 0 and abs(rg - ro) <= 0.01 * ro, f"{p.name}: {rg} vs {ro} spikes"
+        b += p.n
+    wmax = rc.projs[4].stdp["w_max"]
+    rp, idx = o.array("row_ptr"), o.array("idx")
+    src = np.repeat(np.arange(o.n), np.diff(rp))
+    base_p, ne = rc.pops[0].n + rc.pops[1].n, rc.pops[0].n
+    plastic = (src >= base_p) & (idx < ne)                     # P -> E (R8)
+    hg, _ = np.histogram(g.read_state("WEIGHTS")[plastic], bins=64, range=(0.0, wmax))
+    ho, _ = np.histogram(o.array("w")[plastic], bins=64, range=(0.0, wmax))
+    n = plastic.sum()
+    assert np.abs(hg - ho).sum() <= 0.01 * n, f"histograms differ by {np.abs(hg - ho).sum() / n:.4f} of the mass"
+    big = ho >= 0.01 * n
+    assert np.all(np.abs(hg[big] - ho[big]) <= 0.01 * ho[big])
