@@ -80,6 +80,8 @@ def lib():
         L.oracle_field.argtypes = [vp, ctypes.c_int]
         L.oracle_destroy.argtypes = [vp]
         L.oracle_philox.argtypes = [P(u32), P(u32), P(u32)]
+        L.oracle_synapse_replay.restype = ctypes.c_float
+        L.oracle_synapse_replay.argtypes = [vp, ctypes.c_int, ctypes.c_int, P(ctypes.c_uint8), P(ctypes.c_uint8), i64]
         _lib = L
     return _lib
 
@@ -149,6 +151,17 @@ class Oracle:
         out = np.zeros(max(length, 1), dtype=np.uint32)
         L.oracle_build_row(self._s, i, lo, hi, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), length)
         return out[:length]
+
+    def synapse_replay(self, src_pop: int, dst_pop: int, pre, post) -> float:
+        """Naive STDP (Fig. 2a, R7) of one synapse of the projection src_pop ->
+        dst_pop from its initial state, given its pre events (pre[t]: the source
+        fired at t - D) and post events (post[t]: the target fired at t)."""
+        pre = np.ascontiguousarray(pre, dtype=np.uint8)
+        post = np.ascontiguousarray(post, dtype=np.uint8)
+        assert pre.shape == post.shape
+        P8 = ctypes.POINTER(ctypes.c_uint8)
+        return float(lib().oracle_synapse_replay(self._s, src_pop, dst_pop, pre.ctypes.data_as(P8),
+                                                  post.ctypes.data_as(P8), len(pre)))
 
     def finalize(self):
         if lib().oracle_finalize(self._s) != 0:

@@ -368,6 +368,28 @@ static int neuron_update(osim *s, uint32_t i, const opop *p)
  *   x_pre *= d+;  x_post *= d-;
  *   if post: w = min(w + A+ x_pre, w_max); x_post += 1
  *   if pre:  w = max(w - A- x_post, 0);    x_pre  += 1                         */
+static void naive_stdp_synapse(const oproj *q, int pre, int post, float *w_, float *xp_, float *xq_)
+{
+    float xp = *xp_ * q->d_plus;
+    float xq = *xq_ * q->d_minus;
+    float w = *w_;
+    if (post) {
+        float dw = q->a_plus * xp;
+        float nw = w + dw;
+        w = nw < q->w_max ? nw : q->w_max;
+        xq = xq + 1.0f;
+    }
+    if (pre) {
+        float dw = q->a_minus * xq;
+        float nw = w - dw;
+        w = nw > 0.0f ? nw : 0.0f;
+        xp = xp + 1.0f;
+    }
+    *w_ = w;
+    *xp_ = xp;
+    *xq_ = xq;
+}
+
 static void naive_stdp_row(osim *s, uint32_t i, int sp)
 {
     int pre = (int)((s->hist[i] >> s->D) & 1u);
@@ -378,25 +400,25 @@ static void naive_stdp_row(osim *s, uint32_t i, int sp)
         const oproj *q = &s->proj[pj];
         if (q->kind != O_STDP) continue;
         int post = (int)(s->hist[j] & 1u);
-        float xp = s->xpre[c] * q->d_plus;
-        float xq = s->xpost[c] * q->d_minus;
-        float w = s->w[c];
-        if (post) {
-            float dw = q->a_plus * xp;
-            float nw = w + dw;
-            w = nw < q->w_max ? nw : q->w_max;
-            xq = xq + 1.0f;
-        }
-        if (pre) {
-            float dw = q->a_minus * xq;
-            float nw = w - dw;
-            w = nw > 0.0f ? nw : 0.0f;
-            xp = xp + 1.0f;
-        }
-        s->w[c] = w;
-        s->xpre[c] = xp;
-        s->xpost[c] = xq;
+        naive_stdp_synapse(q, pre, post, &s->w[c], &s->xpre[c], &s->xpost[c]);
     }
+}
+
+/* The same per-synapse update, replayed for one synapse of the STDP projection
+ * src_pop -> dst_pop over T steps from the initial state (w0, traces 0), with
+ * its pre events (pre[t]: the source fired at t - D) and post events (post[t]:
+ * the target fired at t) given -- the naive oracle on a sampled synapse of a
+ * network too large to run here in full.  Returns the weight, NAN if the
+ * projection is not plastic. */
+float oracle_synapse_replay(const osim *s, int src_pop, int dst_pop, const uint8_t *pre, const uint8_t *post,
+                            int64_t T)
+{
+    int pj = s->proj_of[src_pop][dst_pop];
+    if (pj < 0 || s->proj[pj].kind != O_STDP) return NAN;
+    const oproj *q = &s->proj[pj];
+    float w = q->w, xp = 0.0f, xq = 0.0f;
+    for (int64_t t = 0; t < T; t++) naive_stdp_synapse(q, pre[t] != 0, post[t] != 0, &w, &xp, &xq);
+    return w;
 }
 
 /* Quantisation of a weight to the int32 fixed-point accumulator, R18:

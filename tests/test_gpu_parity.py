@@ -311,3 +311,75 @@ def test_long_run_rates_and_weight_histogram_within_1pct():
     assert np.abs(hg - ho).sum() <= 0.01 * n, f"histograms differ by {np.abs(hg - ho).sum() / n:.4f} of the mass"
     big = ho >= 0.01 * n
     assert np.all(np.abs(hg[big] - ho[big]) <= 0.01 * ho[big])
+
+
+# ------------------------------------------------------------- full size
+def test_full_size_cfg3_sampled_against_oracle():
+    """BASELINE config 3 at full size (316,228 neurons, 1.0e9 synapses, 40 %
+    plastic, D = 15), in the launch configuration bench.py times (captured-graph
+    replay, PDL, C = 1024, H = 64): sampled outputs the oracle computes one by
+    one -- 48 rows and their pivots bit-exact; after 130 steps (forced flushes
+    at t = 63 and 127) the pending input of 64 sampled targets bit-exact
+    against the row-wise sum of the step's arrivals (Fig. 3a), 300 sampled
+    plastic synapses within 1e-4 of the naive oracle replayed on their own
+    spike trains, and the event count equal to the out-degrees of all
+    arrivals."""
+    from paper_2107_04092_b200 import Snn
+    rc = W.config(3)
+    g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits)
+    rc.apply(g)
+    g.finalize()
+    o = O.Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits)     # rows on demand, never finalized
+    rc.apply(o)
+    info = g.info()
+    N, C, ns, R = info["N"], info["C"], info["nslices"], info["R"]
+    assert info["S"] > 0.99e9
+    rp = g.read_state("ROW_PTR")
+    idx = g.read_state("IDX")
+    piv = g.read_state("PIVOTS").reshape(N, ns + 1)
+    rng = np.random.default_rng(0)
+    for i in rng.choice(N, 48, replace=False):
+        ref = o.build_row(int(i))
+        assert np.array_equal(idx[rp[i]:rp[i + 1]], ref), f"row {i}"
+        assert np.array_equal(piv[i].astype(np.int64), O.pivots(ref, 0, C, ns)), f"pivots of row {i}"
+    T, D = 130, rc.delay
+    raster = np.zeros((T, N), dtype=np.uint8)
+    done = 0
+    while done < T:
+        n = min(50, T - done)
+        g.step(n)
+        ring = g.read_state("SPIKE_RING").reshape(64, -1)
+        for tt in range(done, done + n):
+            raster[tt] = np.unpackbits(ring[tt % 64].view(np.uint8), bitorder="little")[:N]
+        done += n
+    pending = g.read_state("INPUT_EXC")
+    w = g.read_state("WEIGHTS")          # read-out flush (R11): the naive state
+    # events: every arrival (spike of t - D) delivers its whole row (R24)
+    outdeg = np.diff(rp)
+    ev = sum(int(outdeg[np.flatnonzero(raster[t - D])].sum()) for t in range(D, T))
+    assert g.metrics()["EVENTS"] == ev
+    # pending input of step T - 1 = sum over its arrivals of q(w) (fixed point, R18)
+    arrivals = np.flatnonzero(raster[T - 1 - D])
+    for j in rng.choice(R, 64, replace=False):
+        tot = 0
+        for a in arrivals:
+            row = idx[rp[a]:rp[a + 1]]
+            k = np.searchsorted(row, j)
+            if k < len(row) and row[k] == j:
+                tot += int(np.rint(np.float64(w[rp[a] + k]) * 2.0 ** rc.frac_bits))
+        assert pending[j] == tot, f"target {j}: {pending[j]} vs {tot}"
+    # plastic synapses P -> E against the naive oracle on their own spike trains
+    ne, base_p = rc.pops[0].n, rc.pops[0].n + rc.pops[1].n
+    wmax = rc.projs[4].stdp["w_max"]
+    pre = np.zeros_like(raster)
+    pre[D:] = raster[:T - D]
+    checked = 0
+    for i in rng.choice(np.arange(base_p, N), 60, replace=False):
+        b = rp[i]
+        plen = int(np.searchsorted(idx[b:rp[i + 1]], ne))     # the plastic (E) prefix of the row
+        for c in rng.choice(plen, 5, replace=False):
+            j = idx[b + c]
+            ref = o.synapse_replay(2, 0, pre[:, i], raster[:, j])
+            assert abs(float(w[b + c]) - ref) <= 1e-4 * max(abs(ref), 1e-2 * wmax), (i, j, w[b + c], ref)
+            checked += 1
+    assert checked == 300

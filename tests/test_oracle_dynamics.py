@@ -227,3 +227,38 @@ def test_quantisation_rounds_half_to_even():
         o.array("in_e")[0] = q(100.0)
         o.step(1)
         assert o.array("in_e")[1] == expect
+
+
+def test_synapse_replay_equals_the_network_oracle():
+    """oracle.synapse_replay (used to check sampled synapses of networks too
+    large for the full oracle) reproduces, for every plastic synapse of a small
+    Brunel+ network, the weight the network oracle computes over 150 steps
+    (same per-synapse update, pre = source fired at t - D, post = target fired
+    at t)."""
+    import workloads as W
+    rc = W.brunel(1500, p=0.1, plastic=True, delay=3, seed=5)
+    o = O.Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits)
+    rc.apply(o)
+    o.finalize()
+    T = 150
+    fired = np.zeros((T, o.n), dtype=np.uint8)
+    for t in range(T):
+        o.step(1)
+        fired[t] = (o.array("hist") & 1).astype(np.uint8)
+    rp, idx, w = o.array("row_ptr"), o.array("idx"), o.array("w")
+    ne, ni = rc.pops[0].n, rc.pops[1].n
+    base_p = ne + ni
+    pre_shift = np.zeros_like(fired)
+    pre_shift[rc.delay:] = fired[:T - rc.delay]
+    checked = 0
+    rng = np.random.default_rng(1)
+    for i in rng.choice(np.arange(base_p, o.n), 40, replace=False):
+        for c in range(rp[i], rp[i + 1]):
+            j = idx[c]
+            if j >= ne:
+                continue
+            ww = o.synapse_replay(2, 0, pre_shift[:, i], fired[:, j])
+            assert ww == w[c], (i, j, ww, w[c])
+            checked += 1
+    assert checked > 200
+    assert np.isnan(o.synapse_replay(0, 0, pre_shift[:, 0], fired[:, 0]))   # E -> E is static
