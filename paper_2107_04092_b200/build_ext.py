@@ -14,6 +14,7 @@ LIB = os.path.join(HERE, "libsnn.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--fmad=false", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+FLAGS += os.environ.get("SNN_NVCC_EXTRA", "").split()      # tuning experiments (-D...) only
 
 
 def nccl_include() -> str:

@@ -891,7 +891,13 @@ constexpr int kDelThreads = 512;
 constexpr int kDelWarps = kDelThreads / 32;
 constexpr int kDelRows = 1024;     // row table per round (two rows per thread)
 constexpr int kDelWin = 32 * kDelThreads;   // flattened elements per owner window (one bitmap word per thread)
-constexpr int kDelU = 8;           // elements in flight per thread
+#ifndef SNN_DEL_U
+#define SNN_DEL_U 8
+#endif
+#ifndef SNN_DEL_MINB
+#define SNN_DEL_MINB 2
+#endif
+constexpr int kDelU = SNN_DEL_U;   // elements in flight per thread
 
 // Block-wide inclusive scan of a packed pair (low 32 bits: elements, high 32:
 // segments) per thread.
@@ -1021,7 +1027,7 @@ __device__ __forceinline__ void deliver_window(const NetDev &net, uint32_t wlen,
 // the threads then stride the range 512 wide -- consecutive threads read
 // consecutive synapses -- and each element adds q(w) = RNE(w 2^F) to the slice
 // accumulator with a shared atomic.
-__global__ void __launch_bounds__(kDelThreads, 2)
+__global__ void __launch_bounds__(kDelThreads, SNN_DEL_MINB)
 k_deliver(NetDev net, StateDev st) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t wsum[kDelWarps];
