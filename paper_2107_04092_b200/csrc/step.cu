@@ -534,6 +534,7 @@ struct StdpSmem {                       // static part of k_stdp's shared memory
 // every synapse of an arriving row go to its warp's list; the list is then
 // drained four entries per lane (history / x_post gathers, Fig. 2c, store of
 // the changed weights) and the stage released to the producer.
+template <bool kLazy, bool kH128>
 __global__ void __launch_bounds__(kStdpThreads, 1)
 k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -596,8 +597,9 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     bool bm_ready = false;
     const uint64_t *__restrict__ ghist = st.hist;
     const uint64_t *__restrict__ ghist_hi = st.hist_hi;
-    const uint32_t hi_on = net.H > kHistBits ? 1u : 0u;
-    const bool lazy = net.plast_mode == 1u;          // SNN_PLAST_LAZY (ablation, Fig. 2b)
+    // compile-time variants: H = 128 (second history word), SNN_PLAST_LAZY (Fig. 2b)
+    constexpr uint32_t hi_on = kH128 ? 1u : 0u;
+    constexpr bool lazy = kLazy;
     const float *__restrict__ gxpost = st.xpost;
     float *__restrict__ gw = st.w;
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kStdpRows) {
@@ -681,11 +683,6 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 uint32_t am = 0;                      // 16-bit mask: synapses of arriving rows (updated in place)
                 bool nonlean = false;                 // a listed synapse is not a plain forced flush (age 64)
                 mbar_wait(full_a + 8 * slot, (g / kStdpStages) & 1u);
-                if (net.debug & 2u) {   // experiment: stream the stages only
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(empty_a + 8 * slot);
-                    continue;
-                }
 #pragma unroll
                 for (int u = 0; u < kStdpChPerThr; u++) {
                     const uint32_t c = a + gt + kStdpGroupThr * u;
@@ -722,10 +719,8 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         slots |= o << (8 * u);
                     }
                 }
-                if (net.debug & 1u) hm = 0;   // experiment: filter only (no list; arrivals still updated)
                 // ---- arrivals (every synapse: history window + depression, Fig. 2c):
                 //      in place, two chunks (8 synapses) of gathers in flight per lane
-                if (net.debug & 128u) am = 0;   // experiment: skip the arrivals
                 if (__any_sync(0xffffffffu, am != 0u)) {
 #pragma unroll
                     for (int hf = 0; hf < kStdpChPerThr / 2; hf++) {
@@ -738,9 +733,9 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             const uint32_t bit = 4 * u + (q & 3);
                             const uint32_t on = (am >> bit) & 1u;
                             jv[q] = on ? lds_u32(sa + 16u * (gt + kStdpGroupThr * u) + 4u * (q & 3)) : 0u;
-                            hh[q] = ldg_u64_if(ghist + jv[q], (net.debug & 64u) ? 0u : (on & (rm >> bit)));
+                            hh[q] = ldg_u64_if(ghist + jv[q], on & (rm >> bit));
                             hh2[q] = ldg_u64_if(ghist_hi + jv[q], on & (rm >> bit) & hi_on);
-                            xq[q] = ldg_f32_if(gxpost + jv[q], (net.debug & 16u) ? 0u : on);
+                            xq[q] = ldg_f32_if(gxpost + jv[q], on);
                         }
 #pragma unroll
                         for (int q = 0; q < 8; q++) {
@@ -761,7 +756,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                                                                 dp, pr.x, pr.y, pr.z, window_hi(hh2[q], age));   // (tlu, t], R2
                             const uint32_t chg = __float_as_uint(w) != __float_as_uint(w0v) ? 1u : 0u;
                             const int64_t off = rr.cb + 4ll * ((int64_t)(a + ch) - (int64_t)rr.first) + (q & 3);
-                            stg_f32_if(gw + off, w, (net.debug & 32u) ? 0u : chg);
+                            stg_f32_if(gw + off, w, chg);
                             n_w += chg;
                         }
                     }
@@ -800,8 +795,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             const uint32_t p = ent[u] >> 9;
                             jv[u] = lds_u32(sa + 4u * p);
                             wv[u] = lds_f32(sa + kStdpStageCh * 16 + 4u * p);
-                            pos[u] = ldg_u8_if(st.fpos + jv[u], ok && !(net.debug & 8u) ? 1u : 0u);
-                            if (net.debug & 8u) pos[u] = jv[u] & 31u;   // experiment: no gather
+                            pos[u] = ldg_u8_if(st.fpos + jv[u], ok ? 1u : 0u);
                         }
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
@@ -817,11 +811,11 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                                 w = nw < pr.z ? nw : pr.z;
                             } else {
                                 w = stdp_synapse(wv[u], __ldg(ghist + jv[u]), false, 0.0f, rr.xp, (int)net.H, dp,
-                                                 pr.x, pr.y, pr.z, hi_on ? __ldg(ghist_hi + jv[u]) : 0ull);
+                                                 pr.x, pr.y, pr.z, kH128 ? __ldg(ghist_hi + jv[u]) : 0ull);
                             }
                             const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
                             const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);
-                            stg_f32_if(gw + off, w, chg && !(net.debug & 4u));   // experiment 4: no store
+                            stg_f32_if(gw + off, w, chg);
                             n_w += chg;
                         }
                     }
@@ -1392,13 +1386,22 @@ cudaError_t kernels_configure(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi)
     cudaError_t e = cudaFuncSetAttribute(k_deliver, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)deliver_smem_bytes(net));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_stdp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)stdp_smem_bytes(net, pp_lo, pp_hi));
+    const int sm = (int)stdp_smem_bytes(net, pp_lo, pp_hi);
+    if ((e = cudaFuncSetAttribute(k_stdp<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(k_stdp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(k_stdp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) != cudaSuccess)
+        return e;
+    return cudaFuncSetAttribute(k_stdp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 
 cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, uint32_t grid, uint32_t pp_lo,
                         uint32_t pp_hi, cudaStream_t s, bool pdl) {
-    return launch_pdl(k_stdp, dim3(grid), dim3(kStdpThreads), stdp_smem_bytes(net, pp_lo, pp_hi), s, pdl, net, st,
+    const bool lazy = net.plast_mode == 1u, h128 = net.H > kHistBits;
+    void (*k)(NetDev, StateDev, int64_t, uint32_t, uint32_t) =
+        lazy ? (h128 ? k_stdp<true, true> : k_stdp<true, false>) : (h128 ? k_stdp<false, true> : k_stdp<false, false>);
+    return launch_pdl(k, dim3(grid), dim3(kStdpThreads), stdp_smem_bytes(net, pp_lo, pp_hi), s, pdl, net, st,
                       t_fixed, pp_lo, pp_hi);
 }
 
