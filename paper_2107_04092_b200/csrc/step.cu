@@ -534,7 +534,9 @@ struct StdpSmem {                       // static part of k_stdp's shared memory
 // every synapse of an arriving row go to its warp's list; the list is then
 // drained four entries per lane (history / x_post gathers, Fig. 2c, store of
 // the changed weights) and the stage released to the producer.
-template <bool kLazy, bool kH128>
+// kGeneric: lists of other rows than forced flushes at age H (read-out flush,
+// naive and lazy schedules) -- the default step kernel does not carry it.
+template <bool kLazy, bool kH128, bool kGeneric>
 __global__ void __launch_bounds__(kStdpThreads, 1)
 k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -822,6 +824,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                     n = 0;
                 }
                 // ---- drain the list, four entries per lane in flight
+                if (!kGeneric) n = 0;       // (a step of the event schedule lists only age-H flushes)
                 for (uint32_t b = 0; b < n; b += 128) {
                     uint32_t ent[4];
                     uint32_t jv[4];
@@ -1387,20 +1390,22 @@ cudaError_t kernels_configure(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi)
                                          (int)deliver_smem_bytes(net));
     if (e != cudaSuccess) return e;
     const int sm = (int)stdp_smem_bytes(net, pp_lo, pp_hi);
-    if ((e = cudaFuncSetAttribute(k_stdp<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) != cudaSuccess)
-        return e;
-    if ((e = cudaFuncSetAttribute(k_stdp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) != cudaSuccess)
-        return e;
-    if ((e = cudaFuncSetAttribute(k_stdp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) != cudaSuccess)
-        return e;
-    return cudaFuncSetAttribute(k_stdp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    void (*ks[6])(NetDev, StateDev, int64_t, uint32_t, uint32_t) = {
+        k_stdp<false, false, false>, k_stdp<false, true, false>, k_stdp<false, false, true>,
+        k_stdp<false, true, true>, k_stdp<true, false, true>, k_stdp<true, true, true>};
+    for (auto k : ks)
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) != cudaSuccess) return e;
+    return cudaSuccess;
 }
 
 cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, uint32_t grid, uint32_t pp_lo,
                         uint32_t pp_hi, cudaStream_t s, bool pdl) {
     const bool lazy = net.plast_mode == 1u, h128 = net.H > kHistBits;
+    const bool generic = t_fixed >= 0 || net.plast_mode != 0u;   // read-out flush, lazy, naive
     void (*k)(NetDev, StateDev, int64_t, uint32_t, uint32_t) =
-        lazy ? (h128 ? k_stdp<true, true> : k_stdp<true, false>) : (h128 ? k_stdp<false, true> : k_stdp<false, false>);
+        lazy ? (h128 ? k_stdp<true, true, true> : k_stdp<true, false, true>)
+             : generic ? (h128 ? k_stdp<false, true, true> : k_stdp<false, false, true>)
+                       : (h128 ? k_stdp<false, true, false> : k_stdp<false, false, false>);
     return launch_pdl(k, dim3(grid), dim3(kStdpThreads), stdp_smem_bytes(net, pp_lo, pp_hi), s, pdl, net, st,
                       t_fixed, pp_lo, pp_hi);
 }
