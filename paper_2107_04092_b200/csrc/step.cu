@@ -999,20 +999,15 @@ __device__ __forceinline__ void deliver_pass(const NetDev &net, uint32_t x0, uin
     }
 }
 
-template <bool kIdx16>
+template <bool kMulti, bool kIdx16>
 __device__ __forceinline__ void deliver_window(const NetDev &net, uint32_t wlen, uint32_t w0, uint32_t bw_a,
                                                uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a, uint64_t dw,
                                                float scale, uint32_t slo) {
-    const bool multi_rc = net.nrcpt > 1;
     for (uint32_t x0 = 0; x0 < wlen; x0 += kDelThreads * kDelU) {
-        const bool full = x0 + kDelThreads * kDelU <= wlen;
-        if (multi_rc) {
-            if (full) deliver_pass<true, false, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
-            else deliver_pass<true, true, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
-        } else {
-            if (full) deliver_pass<false, false, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
-            else deliver_pass<false, true, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
-        }
+        if (x0 + kDelThreads * kDelU <= wlen)
+            deliver_pass<kMulti, false, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+        else
+            deliver_pass<kMulti, true, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
     }
 }
 
@@ -1024,6 +1019,9 @@ __device__ __forceinline__ void deliver_window(const NetDev &net, uint32_t wlen,
 // the threads then stride the range 512 wide -- consecutive threads read
 // consecutive synapses -- and each element adds q(w) = RNE(w 2^F) to the slice
 // accumulator with a shared atomic.
+// kMulti: two receptor accumulators (a receptor code per segment); kIdx16:
+// SNN_FLAG_IDX16 -- compile-time variants, so a kernel carries only its path.
+template <bool kMulti, bool kIdx16>
 __global__ void __launch_bounds__(kDelThreads, SNN_DEL_MINB)
 k_deliver(NetDev net, StateDev st) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1060,7 +1058,7 @@ k_deliver(NetDev net, StateDev st) {
     const uint32_t P = net.nslices + 1;
     const float scale = net.scale;
     const uint32_t bw_a = smem_u32(s_bw), ptr_a = smem_u32(s_ptr), rc_a = smem_u32(s_rc);
-    const bool idx16 = st.idx16 != nullptr;
+    constexpr bool idx16 = kIdx16;
     // accumulator of target j (32-bit ids) / slice offset j - slo (16-bit), receptor r: + 4 (r C + j)
     const uint32_t acc_a = idx16 ? smem_u32(acc) : smem_u32(acc) - 4u * slo;
     // w[c] at idx[c] + dw, or at 2 idx16[c] + dw (bytes)
@@ -1138,8 +1136,7 @@ k_deliver(NetDev net, StateDev st) {
             s_bw[threadIdx.x].y = before + winc - pc - 1u;
             __syncthreads();
             // ---- elements: thread x takes w0 + x + 512 u (coalesced)
-            if (idx16) deliver_window<true>(net, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
-            else deliver_window<false>(net, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+            deliver_window<kMulti, kIdx16>(net, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
             if (w0 + kDelWin < T) __syncthreads();  // bitmap reused by the next window
         }
         __syncthreads();                           // table reused next round
@@ -1386,9 +1383,13 @@ size_t deliver_smem_bytes(const NetDev &net) {
 }
 
 cudaError_t kernels_configure(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
-    cudaError_t e = cudaFuncSetAttribute(k_deliver, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)deliver_smem_bytes(net));
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    void (*kd[4])(NetDev, StateDev) = {k_deliver<false, false>, k_deliver<false, true>, k_deliver<true, false>,
+                                       k_deliver<true, true>};
+    for (auto k : kd)
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)deliver_smem_bytes(net))) !=
+            cudaSuccess)
+            return e;
     const int sm = (int)stdp_smem_bytes(net, pp_lo, pp_hi);
     void (*ks[6])(NetDev, StateDev, int64_t, uint32_t, uint32_t) = {
         k_stdp<false, false, false>, k_stdp<false, true, false>, k_stdp<false, false, true>,
@@ -1417,7 +1418,10 @@ cudaError_t launch_deliver_rowwise(const NetDev &net, const StateDev &st, uint32
 
 cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s, bool pdl) {
     dim3 grid(net.nslices > 0 ? net.nslices : 1, splits);
-    return launch_pdl(k_deliver, grid, dim3(kDelThreads), deliver_smem_bytes(net), s, pdl, net, st);
+    const bool multi = net.nrcpt > 1, idx16 = st.idx16 != nullptr;
+    void (*k)(NetDev, StateDev) = multi ? (idx16 ? k_deliver<true, true> : k_deliver<true, false>)
+                                        : (idx16 ? k_deliver<false, true> : k_deliver<false, false>);
+    return launch_pdl(k, grid, dim3(kDelThreads), deliver_smem_bytes(net), s, pdl, net, st);
 }
 
 cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last, uint32_t grid, uint32_t pp_lo,
