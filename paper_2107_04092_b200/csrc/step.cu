@@ -724,7 +724,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 // ---- arrivals (every synapse: history window + depression, Fig. 2c):
                 //      in place, two chunks (8 synapses) of gathers in flight per lane
                 if (__any_sync(0xffffffffu, am != 0u)) {
-#pragma unroll
+#pragma unroll 1
                     for (int hf = 0; hf < kStdpChPerThr / 2; hf++) {
                         uint64_t hh[8], hh2[8];
                         float xq[8];
