@@ -46,36 +46,31 @@ __device__ __forceinline__ uint32_t decide4(const NetDev &net, const uint64_t *t
     return mask;
 }
 
-// Pass 1: per (row, slice) counts -> piv[i][k+1]; piv[i][0] = 0.
+// Pass 1: per (row, slice) counts -> piv[i][k+1]; piv[i][0] = 0.  The CTA of
+// row i walks the row's candidates 1024 at a time (4 per thread, one Philox
+// draw); a thread adds its kept count to its slice's shared counter, so there
+// is no barrier per slice.
 __global__ void __launch_bounds__(kBuildThreads)
 k_count(NetDev net, BuildTabs tabs, uint32_t *piv, uint32_t row0, uint32_t nrows) {
+    extern __shared__ uint32_t cnt_s[];           // [nslices]
     const uint32_t i = row0 + blockIdx.x;
     if (i >= row0 + nrows) return;
     const int sp = find_pop(net, i);
     const uint32_t P = net.nslices + 1;
     uint32_t *prow = piv + (size_t)i * P;
-    __shared__ uint32_t red[kBuildThreads / 32];
     bool any = false;
     for (int d = 0; d < (int)net.npop; d++) any |= tabs.thr[sp * kMaxPops + d] != 0;
-    if (threadIdx.x == 0) prow[0] = 0;
-    for (uint32_t k = 0; k < net.nslices; k++) {
-        const uint32_t lo = net.tgt_lo + (k << net.log2C);
-        const uint32_t hi = min(lo + net.C, net.tgt_hi);
-        uint32_t cnt = 0;
-        if (any) {
-            for (uint32_t j0 = lo + 4 * threadIdx.x; j0 < hi; j0 += 4 * kBuildThreads)
-                cnt += __popc(decide4(net, tabs.thr, tabs.autapse, sp, i, j0, hi));
+    for (uint32_t k = threadIdx.x; k < net.nslices; k += kBuildThreads) cnt_s[k] = 0;
+    __syncthreads();
+    if (any) {
+        for (uint32_t j0 = net.tgt_lo + 4 * threadIdx.x; j0 < net.tgt_hi; j0 += 4 * kBuildThreads) {
+            const uint32_t m = decide4(net, tabs.thr, tabs.autapse, sp, i, j0, net.tgt_hi);
+            if (m) atomicAdd(&cnt_s[(j0 - net.tgt_lo) >> net.log2C], (uint32_t)__popc(m));   // C >= 32: one slice
         }
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t s = 0;
-            for (int w = 0; w < kBuildThreads / 32; w++) s += red[w];
-            prow[k + 1] = s;
-        }
-        __syncthreads();
     }
+    __syncthreads();
+    if (threadIdx.x == 0) prow[0] = 0;
+    for (uint32_t k = threadIdx.x; k < net.nslices; k += kBuildThreads) prow[k + 1] = cnt_s[k];
 }
 
 // Pass 2: per row, counts -> exclusive prefix (the pivots); row length out.
@@ -100,7 +95,10 @@ __global__ void k_pivot_scan(NetDev net, uint32_t *piv, int64_t *len, uint32_t n
     if (lane == 0) len[warp] = carry;
 }
 
-// Pass 3: fill targets (sorted by construction) and initial weights.
+// Pass 3: fill targets (sorted by construction) and initial weights.  The CTA
+// of row i walks the row's candidates 4096 at a time (16 per thread, four
+// Philox draws); one block scan of the kept counts orders the writes.
+constexpr int kFillPer = 16;                      // candidates per thread and pass
 __global__ void __launch_bounds__(kBuildThreads)
 k_fill(NetDev net, BuildTabs tabs, const uint32_t *piv, const int64_t *row_ptr, uint32_t *idx,
        float *w) {
@@ -111,30 +109,27 @@ k_fill(NetDev net, BuildTabs tabs, const uint32_t *piv, const int64_t *row_ptr, 
     const uint32_t P = net.nslices + 1;
     const uint32_t *prow = piv + (size_t)i * P;
     if (prow[net.nslices] == 0) return;
-    const int64_t rbase = row_ptr[i];
-    for (uint32_t k = 0; k < net.nslices; k++) {
-        if (prow[k + 1] == prow[k]) continue;
-        const uint32_t lo = net.tgt_lo + (k << net.log2C);
-        const uint32_t hi = min(lo + net.C, net.tgt_hi);
-        int64_t pos = rbase + prow[k];
-        for (uint32_t jb = lo; jb < hi; jb += 4 * kBuildThreads) {
-            const uint32_t j0 = jb + 4 * threadIdx.x;
-            const uint32_t m = j0 < hi ? decide4(net, tabs.thr, tabs.autapse, sp, i, j0, hi) : 0u;
-            uint32_t off, tot;
-            Scan(tmp).ExclusiveSum((uint32_t)__popc(m), off, tot);
-            uint32_t mm = m;
-            while (mm) {
-                const int e = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const uint32_t j = j0 + e;
-                const int dp = find_pop(net, j);
-                idx[pos + off] = j;
-                w[pos + off] = tabs.weight[sp * kMaxPops + dp];
-                off++;
-            }
-            pos += tot;
-            __syncthreads();
+    int64_t pos = row_ptr[i];
+    for (uint32_t jb = net.tgt_lo; jb < net.tgt_hi; jb += kFillPer * kBuildThreads) {
+        const uint32_t j0 = jb + kFillPer * threadIdx.x;
+        uint32_t m = 0;                           // bit e: candidate j0 + e kept
+#pragma unroll
+        for (int q = 0; q < kFillPer / 4; q++)
+            if (j0 + 4 * q < net.tgt_hi)
+                m |= decide4(net, tabs.thr, tabs.autapse, sp, i, j0 + 4 * q, net.tgt_hi) << (4 * q);
+        uint32_t off, tot;
+        Scan(tmp).ExclusiveSum((uint32_t)__popc(m), off, tot);
+        while (m) {
+            const int e = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t j = j0 + e;
+            const int dp = find_pop(net, j);
+            idx[pos + off] = j;
+            w[pos + off] = tabs.weight[sp * kMaxPops + dp];
+            off++;
         }
+        pos += tot;
+        __syncthreads();
     }
 }
 
@@ -192,10 +187,16 @@ __global__ void k_init_state(NetDev net, StateDev st) {
 
 // ---------------------------------------------------------------- launchers
 cudaError_t build_count(const NetDev &net, const BuildTabs &tabs, uint32_t *piv, cudaStream_t s) {
+    const size_t smem = 4ull * (net.nslices > 0 ? net.nslices : 1);
+    if (smem > 48 * 1024) {
+        if (smem > 227 * 1024) return cudaErrorInvalidValue;       // > 58K slices per rank
+        const cudaError_t e = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
     const uint32_t chunk = 1u << 20;
     for (uint32_t r0 = 0; r0 < net.N; r0 += chunk) {
         const uint32_t nr = min(chunk, net.N - r0);
-        k_count<<<nr, kBuildThreads, 0, s>>>(net, tabs, piv, r0, nr);
+        k_count<<<nr, kBuildThreads, smem, s>>>(net, tabs, piv, r0, nr);
     }
     return cudaGetLastError();
 }

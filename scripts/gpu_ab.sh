@@ -1,5 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()" >/dev/null
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
-for r in 1 2; do
-timeout 300 python bench.py --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('ms/step', d['ms_per_step'], d['roofline']['phase_ms_per_step'], d['roofline']['frac'])"
-done
+timeout 300 python bench.py --steps 1000 --warmup 100 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('ms/step', d['ms_per_step'], d['setup'])"
