@@ -93,7 +93,13 @@ typedef struct {
     float d_plus, d_minus;  /* fp32(exp(-dt/tau_+)), fp32(exp(-dt/tau_-)) */
 } oproj;
 
+/* Geometric gap table of a projection (R32): gap_tab[k-1] = floor((1-p)^k 2^32),
+ * k = 1..OGAP; the gap g >= 1 between kept candidates has P(g > k) =
+ * gap_tab[k-1] / 2^32. */
+#define OGAP 4096
+
 typedef struct osim {
+    uint32_t *gap_tab[OMAX_PROJ];   /* R32: per projection, OGAP entries */
     uint64_t seed;
     uint32_t key[2];
     float dt;
@@ -192,6 +198,12 @@ int oracle_connect(osim *s, uint32_t src, uint32_t dst, int kind, int receptor, 
     memset(q, 0, sizeof(*q));
     q->src = src; q->dst = dst; q->kind = kind; q->receptor = receptor;
     q->autapses = autapses; q->p = p; q->thr = bern_threshold(p);
+    /* R32: gap table floor((1-p)^k 2^32), k = 1..OGAP, in double */
+    s->gap_tab[s->nproj] = (uint32_t *)malloc(OGAP * sizeof(uint32_t));
+    for (int k = 1; k <= OGAP; k++) {
+        double v = floor(pow(1.0 - p, (double)k) * 4294967296.0);
+        s->gap_tab[s->nproj][k - 1] = v >= 4294967295.0 ? 4294967295u : (uint32_t)v;
+    }
     q->w = f[0]; q->tau_plus = f[1]; q->tau_minus = f[2];
     q->a_plus = f[3]; q->a_minus = f[4]; q->w_max = f[5];
     if (kind == O_STDP) {
@@ -203,10 +215,15 @@ int oracle_connect(osim *s, uint32_t src, uint32_t dst, int kind, int receptor, 
 }
 
 /* Row i of the graph (grouped by source, sorted): for each destination
- * population in ascending id order, each candidate j ascending is kept iff the
- * Philox draw (i, jl>>2, 1, d)[jl & 3] < floor(p 2^32)  (R22, R23), no autapses
- * unless allowed (R21).  Only targets in [lo, hi) are produced (a rank's column
- * range).  Returns the row length; writes at most cap ids. */
+ * population d in ascending id order, the kept candidates are found by exact
+ * geometric skipping (R32, R23): the candidates are d's neurons ascending,
+ * without i itself unless autapses are allowed (R21); starting before the
+ * first, each draw x_n = Philox(i, n>>2, 4, d)[n & 3] (n = 0, 1, ...) advances
+ * by the gap g(x) = 1 + #{k in 1..OGAP : gap_tab[k-1] > x} and keeps the
+ * candidate reached; a draw below gap_tab[OGAP-1] advances OGAP and keeps
+ * nothing (the geometric law is memoryless).  p = 1 keeps every candidate,
+ * p = 0 none.  Only targets in [lo, hi) are produced (a rank's column range,
+ * DESIGN.md section 7).  Returns the row length; writes at most cap ids. */
 int64_t oracle_build_row(const osim *s, uint32_t i, uint32_t lo, uint32_t hi,
                          uint32_t *out, int64_t cap)
 {
@@ -217,15 +234,33 @@ int64_t oracle_build_row(const osim *s, uint32_t i, uint32_t lo, uint32_t hi,
         int pj = s->proj_of[sp][d];
         if (pj < 0) continue;
         const oproj *q = &s->proj[pj];
+        if (q->p <= 0.0) continue;
+        const uint32_t *tab = s->gap_tab[pj];
         const opop *dp = &s->pop[d];
-        for (uint32_t jl = 0; jl < dp->n; jl++) {
-            uint32_t j = dp->base + jl;
-            if (j < lo || j >= hi) continue;
-            if (!q->autapses && j == i) continue;
-            uint32_t ctr[4] = { i, jl >> 2, 1u, (uint32_t)d };
+        /* candidate list: d's local indices, i's own left out (no autapse) */
+        int excl = !q->autapses && i >= dp->base && i < dp->base + dp->n;
+        uint32_t il = i - dp->base;
+        int64_t M = (int64_t)dp->n - (excl ? 1 : 0);
+        int64_t c = -1;
+        for (uint64_t n = 0;; n++) {
+            uint32_t ctr[4] = { i, (uint32_t)(n >> 2), 4u, (uint32_t)d };
             uint32_t r[4];
             philox4x32_10(ctr, s->key, r);
-            if ((uint64_t)r[jl & 3] < q->thr) {
+            uint32_t x = r[n & 3];
+            /* g = 1 + number of k with tab[k-1] > x (tab is non-increasing) */
+            int64_t g = 1;
+            while (g <= OGAP && tab[g - 1] > x) g++;
+            if (g > OGAP) {            /* beyond the table: advance, keep nothing */
+                c += OGAP;
+                if (c >= M) break;
+                continue;
+            }
+            c += g;
+            if (c >= M) break;
+            uint32_t jl = (uint32_t)c + ((excl && (uint32_t)c >= il) ? 1u : 0u);
+            uint32_t j = dp->base + jl;
+            if (j >= hi) break;
+            if (j >= lo) {
                 if (len < cap) out[len] = j;
                 len++;
             }
@@ -510,5 +545,6 @@ void oracle_destroy(osim *s)
     free(s->row_ptr); free(s->idx); free(s->w); free(s->xpre); free(s->xpost);
     free(s->V); free(s->ge); free(s->gi); free(s->ref); free(s->in_e); free(s->in_i);
     free(s->hist); free(s->nspk);
+    for (int k = 0; k < s->nproj; k++) free(s->gap_tab[k]);
     free(s);
 }

@@ -15,62 +15,75 @@
 namespace snn {
 
 constexpr int kBuildThreads = 256;
+constexpr int kGeoThreads = 128;
 
-// Decision for 4 consecutive candidates j0..j0+3 of source row i.
-// Returns a 4-bit mask (bit e = candidate j0+e kept).
-__device__ __forceinline__ uint32_t decide4(const NetDev &net, const uint64_t *thr_tab,
-                                            const uint8_t *autapse_tab, int sp, uint32_t i,
-                                            uint32_t j0, uint32_t jend) {
-    uint32_t mask = 0;
-    int cached_dp = -1;
-    uint32_t cached_q = 0xffffffffu;
-    u32x4 r{0, 0, 0, 0};
-    int dp = find_pop(net, j0 < net.N ? j0 : net.N - 1);
-#pragma unroll
-    for (int e = 0; e < 4; e++) {
-        const uint32_t j = j0 + e;
-        if (j >= jend) break;
-        while (dp + 1 < (int)net.npop && j >= net.pop[dp + 1].base) dp++;
-        const uint64_t thr = thr_tab[sp * kMaxPops + dp];
-        if (thr == 0) continue;                       // no projection sp -> dp (or p == 0)
-        if (j == i && !autapse_tab[sp * kMaxPops + dp]) continue;
-        const uint32_t jl = j - net.pop[dp].base;
-        const uint32_t qd = jl >> 2;
-        if (dp != cached_dp || qd != cached_q) {
-            r = philox4x32_10(i, qd, 1u, (uint32_t)dp, net.key0, net.key1);
-            cached_dp = dp;
-            cached_q = qd;
+// Exact geometric skipping (R32): the kept candidates of row i
+// in destination population d are reached by gaps g >= 1 with P(g > k) =
+// gap[k-1] / 2^32 = floor((1-p)^k 2^32) / 2^32, drawn from the counter-based
+// stream Philox(i, n >> 2, 4, d)[n & 3] -- the law of independent Bernoulli(p)
+// trials with one draw per synapse instead of one per candidate pair.  The
+// candidates are d's neurons ascending without i itself (no autapse, R21).
+// A draw beyond the table advances kGapTab and keeps nothing (memoryless).
+// Calls f(j) for every kept target j < hi, ascending; stops at hi.
+template <typename F>
+__device__ __forceinline__ void geo_row(const NetDev &net, const BuildTabs &tabs, uint32_t i, int sp,
+                                        uint32_t hi, F &&f) {
+    for (int d = 0; d < (int)net.npop; d++) {
+        const int slot = tabs.gap_slot[sp * kMaxPops + d];
+        if (slot < 0) continue;
+        const PopDev &dp = net.pop[d];
+        if (dp.base >= hi) break;
+        const uint32_t *tab = tabs.gap + (size_t)slot * kGapTab;
+        const bool excl = !tabs.autapse[sp * kMaxPops + d] && i >= dp.base && i < dp.base + dp.n;
+        const uint32_t il = i - dp.base;
+        const int64_t M = (int64_t)dp.n - (excl ? 1 : 0);
+        int64_t c = -1;
+        u32x4 r = {0, 0, 0, 0};
+        for (uint32_t n = 0;; n++) {
+            if ((n & 3u) == 0) r = philox4x32_10(i, n >> 2, 4u, (uint32_t)d, net.key0, net.key1);
+            const uint32_t x = lane_of(r, n & 3u);
+            uint32_t lo = 0, up = kGapTab;        // entries > x (the table is non-increasing)
+            while (lo < up) {
+                const uint32_t mid = (lo + up) >> 1;
+                if (__ldg(tab + mid) > x) lo = mid + 1; else up = mid;
+            }
+            // g = 1 + #{k : gap[k-1] > x}; lo == kGapTab: beyond the table -> advance kGapTab, keep nothing
+            const bool beyond = lo == (uint32_t)kGapTab;
+            c += beyond ? (int64_t)kGapTab : (int64_t)lo + 1;
+            if (c >= M) break;
+            if (beyond) continue;
+            const uint32_t jl = (uint32_t)c + ((excl && (uint32_t)c >= il) ? 1u : 0u);
+            const uint32_t j = dp.base + jl;
+            if (j >= hi) return;
+            f(j, d);
         }
-        if ((uint64_t)lane_of(r, jl & 3u) < thr) mask |= 1u << e;
     }
-    return mask;
 }
 
-// Pass 1: per (row, slice) counts -> piv[i][k+1]; piv[i][0] = 0.  The CTA of
-// row i walks the row's candidates 1024 at a time (4 per thread, one Philox
-// draw); a thread adds its kept count to its slice's shared counter, so there
-// is no barrier per slice.
-__global__ void __launch_bounds__(kBuildThreads)
-k_count(NetDev net, BuildTabs tabs, uint32_t *piv, uint32_t row0, uint32_t nrows) {
-    extern __shared__ uint32_t cnt_s[];           // [nslices]
-    const uint32_t i = row0 + blockIdx.x;
-    if (i >= row0 + nrows) return;
+// Pass 1: per (row, slice) counts -> piv[i][k+1]; piv[i][0] = 0 (thread per row;
+// the targets come ascending, so the slices are written in order).
+__global__ void __launch_bounds__(kGeoThreads)
+k_count(NetDev net, BuildTabs tabs, uint32_t *piv) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= net.N) return;
     const int sp = find_pop(net, i);
-    const uint32_t P = net.nslices + 1;
-    uint32_t *prow = piv + (size_t)i * P;
-    bool any = false;
-    for (int d = 0; d < (int)net.npop; d++) any |= tabs.thr[sp * kMaxPops + d] != 0;
-    for (uint32_t k = threadIdx.x; k < net.nslices; k += kBuildThreads) cnt_s[k] = 0;
-    __syncthreads();
-    if (any) {
-        for (uint32_t j0 = net.tgt_lo + 4 * threadIdx.x; j0 < net.tgt_hi; j0 += 4 * kBuildThreads) {
-            const uint32_t m = decide4(net, tabs.thr, tabs.autapse, sp, i, j0, net.tgt_hi);
-            if (m) atomicAdd(&cnt_s[(j0 - net.tgt_lo) >> net.log2C], (uint32_t)__popc(m));   // C >= 32: one slice
+    uint32_t *prow = piv + (size_t)i * (net.nslices + 1);
+    prow[0] = 0;
+    uint32_t k = 0, cnt = 0;                      // current slice and its count
+    geo_row(net, tabs, i, sp, net.tgt_hi, [&](uint32_t j, int) {
+        if (j < net.tgt_lo) return;
+        const uint32_t kj = (j - net.tgt_lo) >> net.log2C;
+        while (k < kj) {
+            prow[k + 1] = cnt;
+            cnt = 0;
+            k++;
         }
+        cnt++;
+    });
+    for (; k < net.nslices; k++) {
+        prow[k + 1] = cnt;
+        cnt = 0;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) prow[0] = 0;
-    for (uint32_t k = threadIdx.x; k < net.nslices; k += kBuildThreads) prow[k + 1] = cnt_s[k];
 }
 
 // Pass 2: per row, counts -> exclusive prefix (the pivots); row length out.
@@ -95,42 +108,19 @@ __global__ void k_pivot_scan(NetDev net, uint32_t *piv, int64_t *len, uint32_t n
     if (lane == 0) len[warp] = carry;
 }
 
-// Pass 3: fill targets (sorted by construction) and initial weights.  The CTA
-// of row i walks the row's candidates 4096 at a time (16 per thread, four
-// Philox draws); one block scan of the kept counts orders the writes.
-constexpr int kFillPer = 16;                      // candidates per thread and pass
-__global__ void __launch_bounds__(kBuildThreads)
-k_fill(NetDev net, BuildTabs tabs, const uint32_t *piv, const int64_t *row_ptr, uint32_t *idx,
-       float *w) {
-    typedef cub::BlockScan<uint32_t, kBuildThreads> Scan;
-    __shared__ typename Scan::TempStorage tmp;
-    const uint32_t i = blockIdx.x;
+// Pass 3: fill targets (sorted by construction) and initial weights.
+__global__ void __launch_bounds__(kGeoThreads)
+k_fill(NetDev net, BuildTabs tabs, const int64_t *row_ptr, uint32_t *idx, float *w) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= net.N) return;
     const int sp = find_pop(net, i);
-    const uint32_t P = net.nslices + 1;
-    const uint32_t *prow = piv + (size_t)i * P;
-    if (prow[net.nslices] == 0) return;
     int64_t pos = row_ptr[i];
-    for (uint32_t jb = net.tgt_lo; jb < net.tgt_hi; jb += kFillPer * kBuildThreads) {
-        const uint32_t j0 = jb + kFillPer * threadIdx.x;
-        uint32_t m = 0;                           // bit e: candidate j0 + e kept
-#pragma unroll
-        for (int q = 0; q < kFillPer / 4; q++)
-            if (j0 + 4 * q < net.tgt_hi)
-                m |= decide4(net, tabs.thr, tabs.autapse, sp, i, j0 + 4 * q, net.tgt_hi) << (4 * q);
-        uint32_t off, tot;
-        Scan(tmp).ExclusiveSum((uint32_t)__popc(m), off, tot);
-        while (m) {
-            const int e = __ffs(m) - 1;
-            m &= m - 1;
-            const uint32_t j = j0 + e;
-            const int dp = find_pop(net, j);
-            idx[pos + off] = j;
-            w[pos + off] = tabs.weight[sp * kMaxPops + dp];
-            off++;
-        }
-        pos += tot;
-        __syncthreads();
-    }
+    geo_row(net, tabs, i, sp, net.tgt_hi, [&](uint32_t j, int d) {
+        if (j < net.tgt_lo) return;
+        idx[pos] = j;
+        w[pos] = tabs.weight[sp * kMaxPops + d];
+        pos++;
+    });
 }
 
 // Plastic segment [lo, hi) of each PF_PRE_PLASTIC row: the targets inside the
@@ -187,17 +177,7 @@ __global__ void k_init_state(NetDev net, StateDev st) {
 
 // ---------------------------------------------------------------- launchers
 cudaError_t build_count(const NetDev &net, const BuildTabs &tabs, uint32_t *piv, cudaStream_t s) {
-    const size_t smem = 4ull * (net.nslices > 0 ? net.nslices : 1);
-    if (smem > 48 * 1024) {
-        if (smem > 227 * 1024) return cudaErrorInvalidValue;       // > 58K slices per rank
-        const cudaError_t e = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    const uint32_t chunk = 1u << 20;
-    for (uint32_t r0 = 0; r0 < net.N; r0 += chunk) {
-        const uint32_t nr = min(chunk, net.N - r0);
-        k_count<<<nr, kBuildThreads, smem, s>>>(net, tabs, piv, r0, nr);
-    }
+    k_count<<<(net.N + kGeoThreads - 1) / kGeoThreads, kGeoThreads, 0, s>>>(net, tabs, piv);
     return cudaGetLastError();
 }
 
@@ -215,7 +195,8 @@ cudaError_t build_scan(const NetDev &net, uint32_t *piv, int64_t *len, int64_t *
 
 cudaError_t build_fill(const NetDev &net, const BuildTabs &tabs, const uint32_t *piv,
                        const int64_t *row_ptr, uint32_t *idx, float *w, cudaStream_t s) {
-    k_fill<<<net.N, kBuildThreads, 0, s>>>(net, tabs, piv, row_ptr, idx, w);
+    (void)piv;
+    k_fill<<<(net.N + kGeoThreads - 1) / kGeoThreads, kGeoThreads, 0, s>>>(net, tabs, row_ptr, idx, w);
     return cudaGetLastError();
 }
 

@@ -70,10 +70,13 @@ struct NetDev {
 };
 
 // Tables of the graph builder (per (src pop, dst pop) projection).
+constexpr int kGapTab = 4096;          // geometric gap table length (R32)
 struct BuildTabs {
     uint64_t thr[kMaxPops * kMaxPops];     // Bernoulli thresholds floor(p 2^32), 0 = none
     uint8_t autapse[kMaxPops * kMaxPops];
     float weight[kMaxPops * kMaxPops];     // initial (final, caller-scaled) weight
+    int16_t gap_slot[kMaxPops * kMaxPops]; // projection (src, dst) -> its gap table, -1 = none
+    const uint32_t *gap;                   // [projections][kGapTab]: floor((1-p)^k 2^32), k = 1..kGapTab
 };
 
 constexpr int kFrontThreads = 1024;   // k_front CTA = one list region

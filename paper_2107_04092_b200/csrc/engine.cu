@@ -236,6 +236,8 @@ static snn_status finalize(snn_sim *sim) {
         for (int b = 0; b < kMaxPops; b++) net.rcpt[a][b] = -1;
     BuildTabs tabs;
     memset(&tabs, 0, sizeof tabs);
+    for (int k = 0; k < kMaxPops * kMaxPops; k++) tabs.gap_slot[k] = -1;
+    std::vector<uint32_t> gap_host;               // R32: floor((1-p)^k 2^32), k = 1..kGapTab, per projection
     uint32_t R = 0;
     for (uint32_t k = 0; k < net.npop; k++) {
         const HostPop &hp = sim->pops[k];
@@ -268,6 +270,13 @@ static snn_status finalize(snn_sim *sim) {
         tabs.thr[hj.src * kMaxPops + hj.dst] = bernoulli_thr(q.p);
         tabs.autapse[hj.src * kMaxPops + hj.dst] = q.allow_autapses ? 1 : 0;
         tabs.weight[hj.src * kMaxPops + hj.dst] = q.weight;
+        if (q.p > 0.0) {
+            tabs.gap_slot[hj.src * kMaxPops + hj.dst] = (int16_t)(gap_host.size() / kGapTab);
+            for (int k = 1; k <= kGapTab; k++) {
+                const double v = std::floor(std::pow(1.0 - q.p, (double)k) * 4294967296.0);
+                gap_host.push_back(v >= 4294967295.0 ? 4294967295u : (uint32_t)v);
+            }
+        }
         double wabs = std::fabs((double)q.weight);
         if (q.kind == SNN_SYN_STDP) {
             if (net.nstdp >= 4) return sim->fail(SNN_E_UNSUPPORTED, "at most 4 STDP projections");
@@ -400,6 +409,13 @@ static snn_status finalize(snn_sim *sim) {
     CK(cudaMemsetAsync(st.ctr, 0, sizeof(Counters), s));
 
     // ---- graph (count -> pivots/row_ptr -> fill)
+    {
+        uint32_t *gap = nullptr;
+        ALLOC(gap, uint32_t, gap_host.empty() ? 1 : gap_host.size());
+        if (!gap_host.empty())
+            CK(cudaMemcpyAsync(gap, gap_host.data(), 4 * gap_host.size(), cudaMemcpyHostToDevice, s));
+        tabs.gap = gap;
+    }
     int64_t *len = nullptr;
     ALLOC(len, int64_t, (size_t)N + 1);
     CK(cudaMemsetAsync(len + N, 0, sizeof(int64_t), s));

@@ -118,3 +118,32 @@ def test_pair_acceptance_frequency_is_p():
     o = _net(1000, 0.02, autapses=True, seed=11)
     n = 1000 * 1000
     assert abs(o.nsyn / n - 0.02) < 5 * np.sqrt(0.02 * 0.98 / n)
+
+
+@pytest.mark.parametrize("N,p,rows,ks", [(40_000, 0.02, 50, (1, 5, 20, 50, 100, 200)),
+                                        (4_000_000, 0.0002, 50, (100, 2000, 4096, 5000, 9000))])
+def test_geometric_gaps_follow_the_bernoulli_law(N, p, rows, ks):
+    """R32: the gaps between kept candidates of a row are geometric -- the law
+    of independent Bernoulli(p) trials (P(gap > k) = (1-p)^k) -- checked at
+    several k within 5 sigma, including gaps beyond the 4096-entry table (the
+    memoryless continuation), and each target position is kept with frequency
+    p across rows (no positional bias).  Rows are long against the mean gap
+    (the gap cut by a row's end is not observed)."""
+    o = O.Oracle(7, 0.1, 0, 20)
+    a = o.add_population(O.LIF_DELTA, N, tau_m=20.0, v_reset=10.0, v_th=20.0)
+    o.connect(a, a, O.STATIC, 0, p, 0.1, autapses=True)
+    gaps = []
+    hits = np.zeros(N, dtype=np.int64)
+    for i in range(rows):
+        r = o.build_row(i).astype(np.int64)
+        hits[r] += 1
+        gaps.append(np.diff(np.concatenate([[-1], r])))
+    g = np.concatenate(gaps)
+    n = len(g)
+    assert n > 20_000
+    for k in ks:
+        q = (1 - p) ** k
+        assert abs((g > k).mean() - q) < 5 * np.sqrt(q * (1 - q) / n), k
+    B = N // 40                                                  # 40 blocks of positions
+    f = hits.reshape(40, B).sum(axis=1) / (rows * B)
+    assert np.all(np.abs(f - p) < 5 * np.sqrt(p * (1 - p) / (rows * B)))
