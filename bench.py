@@ -42,6 +42,8 @@ def parse():
                     help="STDP schedule: Fig. 2c (default) / 2b / 2a (ablation, SURVEY 8(f2))")
     ap.add_argument("--delivery", default="sliced", choices=["sliced", "rowwise"],
                     help="delivery: Fig. 3b (default) / 3a (ablation)")
+    ap.add_argument("--flush-period", type=int, default=0,
+                    help="forced flushes batched every K steps at ages >= H - K (DESIGN.md R33); 0 = at age H")
     ap.add_argument("--idx16", action="store_true",
                     help="delivery reads 16-bit slice-local target offsets (SURVEY 8(f1), P:405)")
     ap.add_argument("--history-bits", type=int, default=64, choices=[64, 128],
@@ -201,7 +203,7 @@ def main():
         s = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream,
                 flags=flags, rank=rank, world=world, nccl_unique_id=uid, history_bits=a.history_bits,
                 plasticity=["event", "lazy", "naive"].index(a.plasticity),
-                delivery=["sliced", "rowwise"].index(a.delivery))
+                delivery=["sliced", "rowwise"].index(a.delivery), flush_period=a.flush_period)
         rc.apply(s)
         return s
 
@@ -322,7 +324,7 @@ def main():
         "vs_baseline": None, "dtype": "f32 (int32 fixed-point accumulators)", "data": "synthetic",
         "config": {"workload": f"BASELINE config {a.config}: {rc.name}", "neurons": info["N"],
                    "synapses": info["S"], "plastic": rc.plastic, "dt_ms": rc.dt_ms, "delay_steps": rc.delay,
-                   "history_bits": a.history_bits, "plasticity": a.plasticity,
+                   "history_bits": a.history_bits, "flush_period": a.flush_period, "plasticity": a.plasticity,
                    "delivery": a.delivery, "index_bits": 16 if a.idx16 else 32, "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
                    "parallelism": f"target-range partition x{world}, NCCL spike-word all-gather" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2: %.1f GB of graph, each step touches the rows of that step's spikes"

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 2u
+#define SNN_ABI_VERSION 3u
 
 typedef struct snn_sim snn_sim; /* opaque; owned by the library */
 typedef int32_t snn_status;
@@ -142,6 +142,12 @@ typedef struct {
     uint64_t group_key;
     uint32_t plasticity;     /* SNN_PLAST_* (ablation; results identical)        */
     uint32_t delivery;       /* SNN_DELIV_* (ablation; results identical)        */
+    uint32_t flush_period;   /* forced-flush schedule (R3, R33): 0 = a
+                                row is flushed when its age reaches H (the
+                                paper's); K in [1, H/2] = every K steps, all rows
+                                of age >= H - K at once (same results: any
+                                schedule with age <= H is exact, R4), so the
+                                flushes stream as one bulk pass               */
 } snn_config;
 
 typedef struct {

@@ -54,6 +54,7 @@ struct NetDev {
     uint32_t wmax;               // words exchanged per rank and step
     uint32_t D;          // delay
     uint32_t H;          // history bits: 64 or 128 (forced flush at age H, R3)
+    uint32_t flush_period; // 0: flush at age H; K: every K steps the rows of age >= H - K (R33)
     uint32_t plast_mode; // SNN_PLAST_EVENT / LAZY / NAIVE (ablation)
     uint32_t deliv_mode; // SNN_DELIV_SLICED / ROWWISE (ablation)
     uint32_t npop, nstdp;

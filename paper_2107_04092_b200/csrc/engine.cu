@@ -225,6 +225,7 @@ static snn_status finalize(snn_sim *sim) {
     net.N = sim->N;
     net.D = cfg.delay_steps;
     net.H = cfg.history_bits;
+    net.flush_period = cfg.flush_period;
     net.plast_mode = cfg.plasticity;
     net.deliv_mode = cfg.delivery;
     net.F = cfg.accum_frac_bits;
@@ -556,6 +557,10 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         cfg->accum_frac_bits < 0 || cfg->accum_frac_bits > 30 || cfg->world < 1 || cfg->rank < 0 ||
         cfg->rank >= cfg->world) {
         g_create_error = "snn_config: need dt > 0, history_bits 64 or 128, delay <= 62, 0 <= F <= 30, 0 <= rank < world";
+        return SNN_E_INVALID;
+    }
+    if (cfg->flush_period > cfg->history_bits / 2) {
+        g_create_error = "snn_config: flush_period must be 0 or at most history_bits / 2";
         return SNN_E_INVALID;
     }
     if (cfg->plasticity > SNN_PLAST_NAIVE || cfg->delivery > SNN_DELIV_ROWWISE) {

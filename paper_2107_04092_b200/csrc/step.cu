@@ -250,7 +250,10 @@ k_front(NetDev net, StateDev st) {
             st.tlu[i] = tl;
         }
         const int age = (int)(t - tl);
-        visit = arr || age >= (int)net.H;    // forced flush at maximum age (R3)
+        // forced flush (R3): at age H, or -- batched schedule (R33) -- every
+        // flush_period steps for the rows of age >= H - flush_period
+        const uint32_t K = net.flush_period;
+        visit = arr || (K == 0 ? age >= (int)net.H : ((uint32_t)(t % K) == K - 1 && age >= (int)(net.H - K)));
         if (net.plast_mode == 2u) visit = true;   // SNN_PLAST_NAIVE: every row every step (Fig. 2a schedule)
         if (visit) {
             const uint2 sg = st.seg[i];
@@ -534,8 +537,8 @@ struct StdpSmem {                       // static part of k_stdp's shared memory
 // every synapse of an arriving row go to its warp's list; the list is then
 // drained four entries per lane (history / x_post gathers, Fig. 2c, store of
 // the changed weights) and the stage released to the producer.
-// kGeneric: lists of other rows than forced flushes at age H (read-out flush,
-// naive and lazy schedules) -- the default step kernel does not carry it.
+// kGeneric: the step-by-step list drain of the lazy schedule (and the read-out
+// flush) -- the default step kernel does not carry it.
 template <bool kLazy, bool kH128, bool kGeneric>
 __global__ void __launch_bounds__(kStdpThreads, 1)
 k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi) {
@@ -683,7 +686,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 const uint32_t sa = stage_a + slot * (kStdpStageCh * 32);
                 uint32_t hm = 0, rm = 0, slots = 0;   // 16-bit masks: list the synapse / target may hold a post spike
                 uint32_t am = 0;                      // 16-bit mask: synapses of arriving rows (updated in place)
-                bool nonlean = false;                 // a listed synapse is not a plain forced flush (age 64)
+                bool nonlean = false;                 // lazy schedule: the generic drain replays step by step
                 mbar_wait(full_a + 8 * slot, (g / kStdpStages) & 1u);
 #pragma unroll
                 for (int u = 0; u < kStdpChPerThr; u++) {
@@ -717,7 +720,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         hm |= sel << (4 * u);
                         am |= (arr ? inm : 0u) << (4 * u);
                         rm |= rec << (4 * u);
-                        nonlean |= sel != 0u && ((cm.x & kMetaAge) != net.H || lazy);
+                        nonlean |= sel != 0u && lazy;
                         slots |= o << (8 * u);
                     }
                 }
@@ -806,14 +809,18 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             const uint32_t si = (rr.meta >> 12) & 0x3u;
                             const float4 pr = sm.par[si];
                             const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
-                            float w;
-                            if (pos[u] < (uint32_t)kMaxHist) {
-                                const float d = lds_f32(dp + 4u * (net.H - pos[u]));
-                                const float nw = __fadd_rn(wv[u], __fmul_rn(pr.x, __fmul_rn(rr.xp, d)));
-                                w = nw < pr.z ? nw : pr.z;
-                            } else {
-                                w = stdp_synapse(wv[u], __ldg(ghist + jv[u]), false, 0.0f, rr.xp, (int)net.H, dp,
-                                                 pr.x, pr.y, pr.z, kH128 ? __ldg(ghist_hi + jv[u]) : 0ull);
+                            const int age = (int)(rr.meta & kMetaAge);
+                            float w = wv[u];
+                            if (pos[u] < (uint32_t)kMaxHist) {      // the history's only spike: in the window?
+                                if (pos[u] < (uint32_t)age) {
+                                    const float d = lds_f32(dp + 4u * ((uint32_t)age - pos[u]));
+                                    const float nw = __fadd_rn(wv[u], __fmul_rn(pr.x, __fmul_rn(rr.xp, d)));
+                                    w = nw < pr.z ? nw : pr.z;
+                                }
+                            } else {                                // several: replay the window
+                                w = stdp_synapse(wv[u], window_lo(__ldg(ghist + jv[u]), age), false, 0.0f, rr.xp, age,
+                                                 dp, pr.x, pr.y, pr.z,
+                                                 kH128 ? window_hi(__ldg(ghist_hi + jv[u]), age) : 0ull);
                             }
                             const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
                             const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);

@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- constants
-SNN_ABI_VERSION = 2
+SNN_ABI_VERSION = 3
 SNN_OK, SNN_E_INVALID, SNN_E_STATE, SNN_E_OOM, SNN_E_CUDA, SNN_E_NCCL, SNN_E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 POISSON, LIF_DELTA, LIF_CUBA = 0, 1, 2
 STATIC, STDP = 0, 1
@@ -57,7 +57,7 @@ class snn_config(ctypes.Structure):
                 ("world", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
                 ("nccl_unique_id", ctypes.c_void_p), ("group_key", ctypes.c_uint64),
-                ("plasticity", ctypes.c_uint32), ("delivery", ctypes.c_uint32)]
+                ("plasticity", ctypes.c_uint32), ("delivery", ctypes.c_uint32), ("flush_period", ctypes.c_uint32)]
 
 
 class snn_pop_params(ctypes.Structure):
@@ -166,7 +166,8 @@ class Snn:
     def __init__(self, seed: int, dt_ms: float = 0.1, delay: int = 0, frac_bits: int = 20,
                  slice_width: int = 0, device: int = 0, stream=None, flags: int = 0, rank: int = 0,
                  world: int = 1, nccl_unique_id: bytes | None = None, group_key: int = 0,
-                 torch_allocator: bool = True, history_bits: int = 64, plasticity: int = 0, delivery: int = 0):
+                 torch_allocator: bool = True, history_bits: int = 64, plasticity: int = 0, delivery: int = 0,
+                 flush_period: int = 0):
         import torch  # plumbing: device memory and streams
         self._torch = torch
         self.device = device
@@ -181,6 +182,7 @@ class Snn:
         cfg.history_bits = history_bits   # H: 64 or 128
         cfg.plasticity = plasticity       # PLAST_EVENT / PLAST_LAZY / PLAST_NAIVE (ablation, f2)
         cfg.delivery = delivery           # DELIV_SLICED / DELIV_ROWWISE (ablation, f2)
+        cfg.flush_period = flush_period   # 0: flush at age H; K: batched every K steps (R33)
         cfg.slice_width = slice_width
         cfg.accum_frac_bits = frac_bits
         cfg.flags = flags

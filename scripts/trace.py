@@ -10,9 +10,11 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 C = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 rc = W.config(cfg)
 extra = int(os.environ.get("SNN_TRACE_FLAGS", "0"))
-g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, flags=FLAG_TRACE | extra)
+import json as _json
+kw = _json.loads(os.environ.get("SNN_TRACE_KW", "{}"))      # e.g. {"flush_period": 16}
+g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, flags=FLAG_TRACE | extra, **kw)
 rc.apply(g)
-g.step(1500)
+g.step(int(os.environ.get("SNN_TRACE_T0", "1500")))
 torch.cuda.synchronize()
 dbg = os.environ.pop("SNN_TRACE_DEBUG", None)
 for rep in range(3):

@@ -11,10 +11,10 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _pair(rc, slice_width=0, flags=0, history_bits=64, plasticity=0, delivery=0):
+def _pair(rc, slice_width=0, flags=0, history_bits=64, plasticity=0, delivery=0, flush_period=0):
     from paper_2107_04092_b200 import Snn
     g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=slice_width, flags=flags,
-            history_bits=history_bits, plasticity=plasticity, delivery=delivery)
+            history_bits=history_bits, plasticity=plasticity, delivery=delivery, flush_period=flush_period)
     rc.apply(g)
     g.finalize()
     o = O.Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, threads=8)
@@ -129,6 +129,18 @@ def test_brunel_plus_stdp_parity(delay, H):
     assert checked > 100
     m = g.metrics()
     assert m["FLUSH_ROWS"] > 0 and m["STDP_WTOUCH"] > 0
+
+
+@pytest.mark.parametrize("H,K,delay", [(64, 16, 15), (64, 32, 0), (128, 32, 15), (64, 1, 3)])
+def test_batched_flush_schedule_same_result(H, K, delay):
+    """R33: forced flushes batched every K steps (rows of age >= H - K) give the
+    naive oracle's rasters bit-exactly and its weights within 1e-4 -- any
+    schedule that visits a row before its age exceeds H is exact (R4)."""
+    rc = W.brunel(10000, p=0.05, plastic=True, delay=delay, seed=23)
+    g, o = _pair(rc, slice_width=512, history_bits=H, flush_period=K)
+    _run_compare(g, o, 400, exact_v=False, every=25)
+    _compare_weights(g, o, rc)
+    assert g.metrics()["FLUSH_ROWS"] > 0
 
 
 @pytest.mark.parametrize("plasticity,delivery", [(1, 0), (2, 0), (0, 1), (2, 1)])
@@ -269,6 +281,8 @@ def test_invalid_arguments_rejected():
         Snn(1, 0.1, 0, 20, history_bits=96)   # H is 64 or 128
     with pytest.raises(SnnError):
         Snn(1, 0.1, 0, 20, plasticity=3)      # no such schedule
+    with pytest.raises(SnnError):
+        Snn(1, 0.1, 0, 20, flush_period=33)   # K <= H / 2
     g = Snn(1, 0.1, 0, 20)
     with pytest.raises(SnnError) as e:
         g.add_population(W.LIF_DELTA, 0)
