@@ -52,7 +52,7 @@ typedef int32_t snn_status;
 enum {
     SNN_OK = 0,
     SNN_E_INVALID = -1,     /* bad argument: p outside [0,1], n == 0, D > 62,
-                               slice width not a power of two in [32, 32768],
+                               slice width not a multiple of 32 in [32, 32768],
                                fixed-point overflow bound violated, ...      */
     SNN_E_STATE = -2,       /* call not allowed in the handle's lifecycle state */
     SNN_E_OOM = -3,         /* device allocation failed                        */
@@ -116,7 +116,7 @@ typedef struct {
     uint32_t delay_steps;    /* network-wide delay D in steps; D <= 62    */
     uint32_t history_bits;   /* H: 64 or 128 ("64 to 128"):
                                   forced flush at age H; 128 halves the flush work  */
-    uint32_t slice_width;    /* C: neurons per slice; power of two
+    uint32_t slice_width;    /* C: neurons per slice; multiple of 32
                                 in [32, 32768]; 0 = automatic                      */
     int32_t accum_frac_bits; /* F: fixed-point fraction bits of the int32 input
                                 accumulators (R18); 0..30, default 20   */
@@ -286,7 +286,7 @@ uint32_t snn_abi_version(void);
  * among `world` ranks for n_targets neurons with inputs and slice width C --
  * C-aligned equal shares, the last one truncated (the
  * partition of the neuron domain of P:48 / P:348).  Errors: SNN_E_INVALID
- * (world == 0, rank >= world, C not a power of two, NULL outputs). */
+ * (world == 0, rank >= world, C not a multiple of 32, NULL outputs). */
 snn_status snn_partition(uint32_t n_targets, uint32_t slice_width, uint32_t world, uint32_t rank, uint32_t *lo,
                          uint32_t *hi);
 

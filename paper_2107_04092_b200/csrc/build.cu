@@ -72,7 +72,7 @@ k_count(NetDev net, BuildTabs tabs, uint32_t *piv) {
     uint32_t k = 0, cnt = 0;                      // current slice and its count
     geo_row(net, tabs, i, sp, net.tgt_hi, [&](uint32_t j, int) {
         if (j < net.tgt_lo) return;
-        const uint32_t kj = (j - net.tgt_lo) >> net.log2C;
+        const uint32_t kj = (j - net.tgt_lo) / net.C;
         while (k < kj) {
             prow[k + 1] = cnt;
             cnt = 0;
@@ -204,7 +204,7 @@ cudaError_t build_fill(const NetDev &net, const BuildTabs &tabs, const uint32_t 
 // (j - tgt_lo) mod C -- every (row, slice) segment indexes only C neurons.
 __global__ void k_idx16(NetDev net, const uint32_t *idx, uint16_t *idx16, int64_t S) {
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < S; c += (int64_t)gridDim.x * blockDim.x)
-        idx16[c] = (uint16_t)((idx[c] - net.tgt_lo) & (net.C - 1u));
+        idx16[c] = (uint16_t)((idx[c] - net.tgt_lo) % net.C);
 }
 
 cudaError_t build_idx16(const NetDev &net, const uint32_t *idx, uint16_t *idx16, int64_t S, cudaStream_t s) {

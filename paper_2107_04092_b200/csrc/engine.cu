@@ -315,15 +315,22 @@ static snn_status finalize(snn_sim *sim) {
         if (hj.prm.receptor == SNN_RCPT_INH) net.nrcpt = 2;
     // slice width C of the delivery ("delicate, tunable"): the
     // paper's 1024 by default, shrunk so that each rank keeps >= ~64 slices
-    // when its target range is small
+    // when its target range is small, and widened to a multiple of 32 when
+    // 1024 would give just over one slice per SM (one CTA per slice: a few SMs
+    // would deliver two slices and set the step's tail)
     uint32_t C = cfg.slice_width;
     if (C == 0) {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg.device);
+        const uint32_t Rr = (R + (uint32_t)cfg.world - 1) / (uint32_t)cfg.world;
         C = 1024;
-        while (C > 128 && (R / (uint32_t)cfg.world + C - 1) / C < 64) C >>= 1;
+        while (C > 128 && (Rr + C - 1) / C < 64) C >>= 1;
+        const uint32_t ns = (Rr + C - 1) / C;
+        if (ns > (uint32_t)nsm && ns < 2u * (uint32_t)nsm)
+            C = 32u * ((Rr + 32u * (uint32_t)nsm - 1) / (32u * (uint32_t)nsm));
     }
     net.C = C;
-    net.log2C = 0;
-    while ((1u << net.log2C) < C) net.log2C++;
+    net.log2C = 0;   // (unused: C need not be a power of two)
     // this rank's target range: C-aligned equal shares of [0, R)
     uint32_t lo = 0, hi = R;
     snn_partition(R, C, (uint32_t)cfg.world, (uint32_t)cfg.rank, &lo, &hi);
@@ -568,8 +575,8 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         return SNN_E_INVALID;
     }
     const uint32_t C = cfg->slice_width;
-    if (C != 0 && (C < 32 || C > 32768 || (C & (C - 1)) != 0)) {
-        g_create_error = "snn_config: slice_width must be 0 or a power of two in [32, 32768]";
+    if (C != 0 && (C < 32 || C > 32768 || (C & 31u) != 0)) {
+        g_create_error = "snn_config: slice_width must be 0 or a multiple of 32 in [32, 32768]";
         return SNN_E_INVALID;
     }
     if ((cfg->dev_alloc == nullptr) != (cfg->dev_free == nullptr)) {
@@ -817,7 +824,7 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
 
 snn_status snn_partition(uint32_t n_targets, uint32_t slice_width, uint32_t world, uint32_t rank, uint32_t *lo,
                          uint32_t *hi) {
-    if (world == 0 || rank >= world || !lo || !hi || slice_width == 0 || (slice_width & (slice_width - 1)))
+    if (world == 0 || rank >= world || !lo || !hi || slice_width == 0 || (slice_width & 31u))
         return SNN_E_INVALID;
     const uint64_t share = ((uint64_t)(n_targets + world - 1) / world + slice_width - 1) / slice_width * slice_width;
     *lo = (uint32_t)std::min<uint64_t>((uint64_t)rank * share, n_targets);

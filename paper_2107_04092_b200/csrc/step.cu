@@ -1047,7 +1047,7 @@ k_deliver(NetDev net, StateDev st) {
     int32_t *acc = reinterpret_cast<int32_t *>(pre + ((nblk + 1 + 3) & ~3u));  // [nrcpt][C]
     const uint32_t k = blockIdx.x;
     const uint32_t nsplit = gridDim.y, split = blockIdx.y;
-    const uint32_t slo = net.tgt_lo + (k << net.log2C);
+    const uint32_t slo = net.tgt_lo + k * C;
     const uint32_t shi = min(slo + C, net.tgt_hi);
     const uint32_t width = shi > slo ? shi - slo : 0u;
     const uint32_t lane = threadIdx.x & 31;

@@ -39,7 +39,7 @@ def _check_graph(g, o):
 
 
 # ------------------------------------------------------------------ graph
-@pytest.mark.parametrize("C", [32, 256, 1024])
+@pytest.mark.parametrize("C", [32, 96, 256, 1024, 1088])
 def test_connectivity_and_pivots_bit_exact(C):
     rc = W.brunel(6000, p=0.05, plastic=True, seed=2)
     g, o = _pair(rc, slice_width=C)
@@ -90,7 +90,7 @@ def test_vogels_cfg1_raster_and_state_bit_exact_300_steps():
     assert g.read_state("SPIKE_COUNT").sum() > 0
 
 
-@pytest.mark.parametrize("C", [64, 1024])
+@pytest.mark.parametrize("C", [64, 160, 1024])
 def test_brunel_static_bit_exact(C):
     rc = W.brunel(12000, p=0.02, plastic=False, seed=4)
     g, o = _pair(rc, slice_width=C)
@@ -158,7 +158,7 @@ def test_ablation_schedules_same_result(plasticity, delivery):
         assert m["STDP_ROWS"] >= 200 * 8000 // 2 * 0.99
 
 
-@pytest.mark.parametrize("C", [64, 1024])
+@pytest.mark.parametrize("C", [64, 96, 1024])
 def test_idx16_offsets_and_delivery_bit_exact(C):
     """SURVEY 8(f1) compressed indices: the 16-bit slice-local offsets equal
     (j - tgt_lo) mod C of the oracle's ids, and delivery through them
