@@ -66,8 +66,9 @@ def ncu_traffic(kernel):
             d = json.load(open(p))
         except Exception:
             continue
-        if kernel in d and "dram_bytes" in d[kernel]:
-            return d[kernel]["dram_bytes"], os.path.relpath(p, ROOT)
+        for name, v in d.items():              # template instances: "k_stdp<false, ...>"
+            if name.split("<")[0].split()[-1] == kernel and "dram_bytes" in v:
+                return v["dram_bytes"], os.path.relpath(p, ROOT)
     return None, None
 
 
