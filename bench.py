@@ -257,7 +257,8 @@ def main():
     e2e = None
     if not a.no_e2e:
         chunk = 64
-        ring = np.empty(64 * ((info["N"] + 31) // 32), dtype=np.uint32)
+        # the step rasters land in a pinned host buffer (the caller owns host_dst)
+        ring = torch.empty(64 * ((info["N"] + 31) // 32), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
         m0e = sim.metrics()
         barrier()
         t0 = time.perf_counter()
@@ -274,8 +275,8 @@ def main():
         e2e = {"value": evs / wall, "unit": "events/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(ring.nbytes / chunk),
                "wall_s_per_bio_s": wall / (a.steps * rc.dt_ms * 1e-3),
-               "note": "snn_step(64) + snn_read_state(SPIKE_RING) per 64 steps; an SNN step has no host input "
-                       "(Poisson drive is counter-based on device), so h2d = 0"}
+               "note": "snn_step(64) + snn_read_state(SPIKE_RING) into a pinned host buffer per 64 steps; an SNN "
+                       "step has no host input (Poisson drive is counter-based on device), so h2d = 0"}
     sim.close()
     del sim
     torch.cuda.synchronize()
