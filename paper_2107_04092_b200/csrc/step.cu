@@ -569,10 +569,12 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     if (threadIdx.x < net.nstdp)
         sm.par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
                                           st.stdp[threadIdx.x].w_max, 0.0f);
+    // the step counter was advanced by k_deliver(t-1), which completed before
+    // k_front(t) triggered this launch: read it before waiting for k_front(t)
+    const int64_t t = readout ? t_fixed : *(volatile const int64_t *)&st.ctr->t;
     pdl_wait();            // k_front(t): lists, histories, bitmap
     pdl_launch();          // k_deliver may start its tabulation (k_front is complete)
     if (!readout) trace_mark(st.trace, 1, 0);
-    const int64_t t = readout ? t_fixed : st.ctr->t;
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Vl = readout ? st.rdesc : st.vdesc[par];
     const uint4 *cnt = readout ? st.rcnt : st.cnt[par];
