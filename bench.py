@@ -317,6 +317,12 @@ def main():
     traffic, traffic_src = ncu_traffic(dom_kernel)
     shares = {k: ph[k] / ph["TOTAL"] for k in ("FRONT", "STDP", "DELIVERY")} if ph["TOTAL"] else {}
     sd_bytes, sd_ms = kb["STDP"] + kb["DELIVERY"], ph["STDP"] + ph["DELIVERY"]
+    # level (i) of SURVEY 8(d): the whole step -- STDP + delivery bytes plus the
+    # neuron update (~32 B per LIF neuron, 16 B per Poisson neuron, 8(a1)) over
+    # the graph-replayed step time
+    n_pois = sum(p.n for p in rc.pops if p.kind == W.POISSON)
+    front_bytes_step = 32.0 * (info["N"] - n_pois) + 16.0 * n_pois
+    step_bytes = sd_bytes / psteps + front_bytes_step
     split_group = info["pivot_bytes"]
 
     out = {
@@ -347,6 +353,8 @@ def main():
                      "peak_source": peak_src, "kernels": kern,
                      "stdp_plus_delivery": {"achieved_gbs": sd_bytes / (sd_ms * 1e-3) / 1e9 if sd_ms else 0.0,
                                             "frac": sd_bytes / (sd_ms * 1e-3) / 1e9 / hbm if sd_ms else 0.0},
+                     "step": {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9,
+                              "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm},
                      "phase_ms_per_step": {k: ph[k] / psteps for k in ph}, "phase_share": shares,
                      "deliver_splits": split_group >> 32, "stdp_grid": split_group & 0xffffffff},
         "e2e": e2e,
