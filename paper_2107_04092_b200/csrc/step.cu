@@ -289,7 +289,14 @@ k_front(NetDev net, StateDev st) {
         a.pad = 0;
         st.adesc[par][region + sa] = a;
     }
-    if (threadIdx.x == 0) st.cnt[par][blockIdx.x] = make_uint4(np, na, nf, 0u);
+    if (threadIdx.x == 0) {
+        st.cnt[par][blockIdx.x] = make_uint4(np, na, nf, 0u);
+        // metrics (fire-and-forget reductions): spikes arriving, plastic rows
+        // visited (arrivals + forced flushes), forced flushes
+        if (na) atomicAdd(&st.ctr->metric[1], (unsigned long long)na);
+        if (np + nf) atomicAdd(&st.ctr->metric[2], (unsigned long long)(np + nf));
+        if (nf) atomicAdd(&st.ctr->metric[5], (unsigned long long)nf);
+    }
     trace_mark(st.trace, 0, 3);
 }
 
@@ -1175,23 +1182,12 @@ k_deliver(NetDev net, StateDev st) {
     // ---- step completion: the last CTA books the list counts and advances t
     __syncthreads();
     trace_mark(st.trace, 2, 3);
+    // (no fence: nothing the last CTA does depends on the other CTAs' writes,
+    // and k_front(t+1) reads them after this grid completes)
     if (threadIdx.x == 0) {
-        __threadfence();
         const uint32_t nb = gridDim.x * gridDim.y;
-        const uint32_t tk = atomicAdd(&st.ctr->ticket, 1u);
-        if (tk == nb - 1) {
-            unsigned long long spikes = 0, flushes = 0, visits = 0;
-            for (uint32_t b = 0; b < nblk; b++) {
-                const uint4 c4 = cnt[b];
-                spikes += c4.y;
-                visits += c4.x + c4.z;
-                flushes += c4.z;
-            }
-            st.ctr->metric[1] += spikes;
-            st.ctr->metric[2] += visits;             // plastic rows visited: arrivals + forced flushes
-            st.ctr->metric[5] += flushes;
+        if (atomicAdd(&st.ctr->ticket, 1u) == nb - 1) {
             st.ctr->ticket = 0;
-            __threadfence();
             st.ctr->t = t + 1;
         }
     }
@@ -1245,21 +1241,8 @@ k_deliver_rowwise(NetDev net, StateDev st) {
     // ---- step completion: the last CTA books the list counts and advances t
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t tk = atomicAdd(&st.ctr->ticket, 1u);
-        if (tk == gridDim.x - 1) {
-            unsigned long long spikes = 0, flushes = 0, visits = 0;
-            for (uint32_t b = 0; b < nblk; b++) {
-                const uint4 c4 = cnt[b];
-                spikes += c4.y;
-                visits += c4.x + c4.z;
-                flushes += c4.z;
-            }
-            st.ctr->metric[1] += spikes;
-            st.ctr->metric[2] += visits;
-            st.ctr->metric[5] += flushes;
+        if (atomicAdd(&st.ctr->ticket, 1u) == gridDim.x - 1) {
             st.ctr->ticket = 0;
-            __threadfence();
             st.ctr->t = t + 1;
         }
     }
