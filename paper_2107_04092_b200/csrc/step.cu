@@ -46,6 +46,7 @@ __device__ __forceinline__ float xpre_after(const StdpDev &sd, float xp, int age
 // Returns each thread's slot for (a, b[, c]) and the CTA totals.
 struct Compact2 {
     uint32_t wa[kFrontThreads / 32], wb[kFrontThreads / 32], wc[kFrontThreads / 32];
+    uint32_t tot[3];
 };
 __device__ __forceinline__ void compact3(Compact2 &sm, bool a, bool b, bool c, uint32_t &slot_a, uint32_t &slot_b,
                                          uint32_t &slot_c, uint32_t &tot_a, uint32_t &tot_b, uint32_t &tot_c) {
@@ -77,15 +78,20 @@ __device__ __forceinline__ void compact3(Compact2 &sm, bool a, bool b, bool c, u
             sm.wb[lane] = ib - vb;
             sm.wc[lane] = ic - vc;
         }
+        if (lane == 31) {                     // lanes >= nw add 0: lane 31 holds the totals
+            sm.tot[0] = ia;
+            sm.tot[1] = ib;
+            sm.tot[2] = ic;
+        }
     }
     __syncthreads();
     const uint32_t lm = (1u << lane) - 1u;
     slot_a = sm.wa[warp] + __popc(ba & lm);
     slot_b = sm.wb[warp] + __popc(bb & lm);
     slot_c = sm.wc[warp] + __popc(bc & lm);
-    tot_a = __syncthreads_count(a);
-    tot_b = __syncthreads_count(b);
-    tot_c = __syncthreads_count(c);
+    tot_a = sm.tot[0];
+    tot_b = sm.tot[1];
+    tot_c = sm.tot[2];
 }
 __device__ __forceinline__ void compact2(Compact2 &sm, bool a, bool b, uint32_t &slot_a, uint32_t &slot_b,
                                          uint32_t &tot_a, uint32_t &tot_b) {
@@ -586,6 +592,10 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     const RowDesc *Vl = readout ? st.rdesc : st.vdesc[par];
     const uint4 *cnt = readout ? st.rcnt : st.cnt[par];
     const uint32_t bm_bytes = 16u * ((w_hi - w_lo + 3) >> 2);
+    if (threadIdx.x == 0) {   // bitmap of recently fired post neurons (one bulk copy; the barrier's initialiser)
+        mbar_expect_tx(bmap_a, bm_bytes);
+        bulk_g2s(smem_u32(recent_s), st.recent + w_lo, bm_bytes, bmap_a);
+    }
     region_prefix<kStdpThreads>(cnt, nblk, 0, pre, sm.wsum);
     __syncthreads();       // also: barrier init visible
     region_prefix<kStdpThreads>(cnt, nblk, 2, preF, sm.wsum);
@@ -599,10 +609,6 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     const uint32_t f_end = (uint32_t)(((uint64_t)nF * (blockIdx.x + 1)) / gridDim.x);
     const uint32_t nAb = a_end - a_begin;
     const uint32_t r_begin = 0, r_end = nAb + (f_end - f_begin);
-    if (producer && lane == 0 && r_begin < r_end) {   // bitmap of recently fired post neurons (one bulk copy)
-        mbar_expect_tx(bmap_a, bm_bytes);
-        bulk_g2s(smem_u32(recent_s), st.recent + w_lo, bm_bytes, bmap_a);
-    }
     const uint32_t rs_addr = smem_u32(recent_s) - 4u * w_lo;     // bitmap word of neuron j: + 4 (j >> 5)
     const uint32_t dp_addr = smem_u32(sm.dplus);
     if (!readout) trace_mark(st.trace, 1, 1);
@@ -887,6 +893,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
         g0 += nst;
         __syncthreads();                           // row table reused next round
     }
+    if (threadIdx.x == 0 && !bm_ready) mbar_wait(bmap_a, 0);   // (no rows) the bitmap copy has landed
     n_syn = __reduce_add_sync(0xffffffffu, n_syn);
     n_w = __reduce_add_sync(0xffffffffu, n_w);
     if (lane == 0) {
