@@ -43,7 +43,7 @@ using namespace snn;
 
 namespace {
 
-constexpr uint32_t kGraphSteps = 16;
+constexpr uint32_t kGraphSteps = 64;
 std::string g_create_error;
 
 // NCCL, loaded at run time (only world > 1 with an ncclUniqueId needs it)
