@@ -1137,10 +1137,6 @@ k_deliver(NetDev net, StateDev st) {
                              : (uint64_t)(st.idx + c0q[q]) - 4ull * est[q];
             g++;
         }
-        if (r0 == r_begin) {
-            pdl_wait();    // k_stdp(t): updated weights of plastic arrivals
-            pdl_launch();
-        }
         trace_mark(st.trace, 2, 1);
         for (uint32_t w0 = 0; w0 < T; w0 += kDelWin) {
             const uint32_t wlen = min(T - w0, (uint32_t)kDelWin);
@@ -1158,6 +1154,10 @@ k_deliver(NetDev net, StateDev st) {
             const uint32_t winc = block_incl_scan<kDelThreads>(pc, wsum, wt);
             s_bw[threadIdx.x].y = before + winc - pc - 1u;
             __syncthreads();
+            if (r0 == r_begin && w0 == 0) {   // (the segment tables and the bitmap are ready)
+                pdl_wait();    // k_stdp(t): updated weights of plastic arrivals
+                pdl_launch();
+            }
             // ---- elements: thread x takes w0 + x + 512 u (coalesced)
             deliver_window<kMulti, kIdx16>(net, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
             if (w0 + kDelWin < T) __syncthreads();  // bitmap reused by the next window
@@ -1182,11 +1182,9 @@ k_deliver(NetDev net, StateDev st) {
         }
         if (n_seg) atomicAdd(&st.ctr->metric[6], (unsigned long long)n_seg);
     }
-    if (r_begin >= r_end) {        // no rows: still order the write-back after k_stdp(t)
-        pdl_wait();
-        pdl_launch();
-    }
-    // ---- step completion: the last CTA books the list counts and advances t
+    pdl_wait();            // (no segments) this grid still completes after k_stdp(t)
+    pdl_launch();
+    // ---- step completion: the last CTA advances t
     __syncthreads();
     trace_mark(st.trace, 2, 3);
     // (no fence: nothing the last CTA does depends on the other CTAs' writes,
