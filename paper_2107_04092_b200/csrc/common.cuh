@@ -87,6 +87,8 @@ struct Counters {
     uint32_t ticket;         // CTA-completion ticket of the slice kernel
     uint32_t pad;
     unsigned long long metric[8];
+    uint32_t lst[2][4];      // by step parity: list lengths (plastic arrivals, arrivals, forced flushes, 0)
+    uint32_t rlst[4];        // read-out flush list length
 };
 
 // One row to process, written by the front kernel: forced flushes for k_stdp,
@@ -125,14 +127,12 @@ struct StateDev {
     float *w;                // [S + pad]
     uint32_t *piv;           // [N][nslices+1], row-relative
     uint2 *seg;              // [N] plastic segment (lo, hi), row-relative
-    // work lists (by step parity), one region of kFrontThreads entries per
-    // k_front CTA (no global atomics): plastic visits (arrivals from the front
-    // of the region, forced flushes from its back) and arrivals
+    // work lists (by step parity), appended by k_front CTAs (one atomic per
+    // CTA and list, lengths in Counters::lst): plastic visits (arrivals from
+    // the front, forced flushes from the back: entry cap - 1 - r) and arrivals
     RowDesc *vdesc[2], *adesc[2];
-    uint4 *cnt[2];           // per k_front CTA: (plastic arrivals, arrivals, forced flushes, 0)
-    RowDesc *rdesc;          // read-out flush rows (same region layout)
-    uint4 *rcnt;
-    uint32_t nblk;           // k_front CTAs = list regions
+    RowDesc *rdesc;          // read-out flush rows (length Counters::rlst[0])
+    uint32_t nblk;           // k_front CTAs (list capacity nblk * kFrontThreads)
     uint32_t *vmask[2];      // [nwords] rows visited at the step of that parity
     uint32_t *recent;        // [nwords] bit i: post-plastic neuron i fired in the last 64 steps
     uint32_t *sendbuf;       // [wmax] this rank's spike words of the step (world > 1)

@@ -387,11 +387,9 @@ static snn_status finalize(snn_sim *sim) {
     for (int b = 0; b < 2; b++) {
         ALLOC(st.vdesc[b], RowDesc, net.nstdp ? nreg : 1);
         ALLOC(st.adesc[b], RowDesc, nreg);
-        ALLOC(st.cnt[b], uint4, st.nblk);
         ALLOC(st.vmask[b], uint32_t, net.nwords);
     }
     ALLOC(st.rdesc, RowDesc, net.nstdp ? nreg : 1);
-    ALLOC(st.rcnt, uint4, st.nblk);
     ALLOC(st.recent, uint32_t, net.nwords + 4);   // + the tail of its 16-byte bulk copy
     st.trace = nullptr;
     if (cfg.flags & SNN_FLAG_TRACE) {
@@ -412,7 +410,6 @@ static snn_status finalize(snn_sim *sim) {
     CK(cudaMemsetAsync(st.recent, 0, sizeof(uint32_t) * net.nwords, s));
     for (int b = 0; b < 2; b++) {
         CK(cudaMemsetAsync(st.vmask[b], 0, sizeof(uint32_t) * net.nwords, s));
-        CK(cudaMemsetAsync(st.cnt[b], 0, sizeof(uint4) * st.nblk, s));
     }
     CK(cudaMemsetAsync(st.ctr, 0, sizeof(Counters), s));
 

@@ -5,7 +5,9 @@
 //                         steps" bitmap of post-synaptic neurons, and the work
 //                         lists: plastic row visits A(t) u F(t) (arrivals +
 //                         forced flushes, R3) and arrivals A(t), compacted per
-//                         CTA into that CTA's list region (no global atomics);
+//                         CTA and appended to global lists (one atomic per CTA
+//                         and list: the lists' order is irrelevant, every row
+//                         is processed independently and sums are integer);
 //                         also finalises the per-row STDP state (x_pre, tlu) of
 //                         rows visited at t-1.
 //   k_stdp     (a3)       lazy + event-driven STDP (Fig. 2c) over the
@@ -42,14 +44,16 @@ __device__ __forceinline__ float xpre_after(const StdpDev &sd, float xp, int age
     return arr ? __fadd_rn(x, 1.0f) : x;
 }
 
-// Block-wide compaction of up to three predicates into this CTA's list regions.
-// Returns each thread's slot for (a, b[, c]) and the CTA totals.
+// Block-wide compaction of up to three predicates into global lists: the CTA
+// books its totals with one atomic per list on lens[0..2] (the lists' lengths)
+// and returns each thread's slot for (a, b[, c]) and the CTA totals.
 struct Compact2 {
     uint32_t wa[kFrontThreads / 32], wb[kFrontThreads / 32], wc[kFrontThreads / 32];
-    uint32_t tot[3];
+    uint32_t tot[3], base[3];
 };
-__device__ __forceinline__ void compact3(Compact2 &sm, bool a, bool b, bool c, uint32_t &slot_a, uint32_t &slot_b,
-                                         uint32_t &slot_c, uint32_t &tot_a, uint32_t &tot_b, uint32_t &tot_c) {
+__device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *lens, bool a, bool b, bool c, uint32_t &slot_a,
+                                         uint32_t &slot_b, uint32_t &slot_c, uint32_t &tot_a, uint32_t &tot_b,
+                                         uint32_t &tot_c) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ba = __ballot_sync(0xffffffffu, a), bb = __ballot_sync(0xffffffffu, b),
                    bc = __ballot_sync(0xffffffffu, c);
@@ -82,49 +86,19 @@ __device__ __forceinline__ void compact3(Compact2 &sm, bool a, bool b, bool c, u
             sm.tot[0] = ia;
             sm.tot[1] = ib;
             sm.tot[2] = ic;
+            sm.base[0] = ia ? atomicAdd(lens + 0, ia) : 0u;
+            sm.base[1] = ib ? atomicAdd(lens + 1, ib) : 0u;
+            sm.base[2] = ic ? atomicAdd(lens + 2, ic) : 0u;
         }
     }
     __syncthreads();
     const uint32_t lm = (1u << lane) - 1u;
-    slot_a = sm.wa[warp] + __popc(ba & lm);
-    slot_b = sm.wb[warp] + __popc(bb & lm);
-    slot_c = sm.wc[warp] + __popc(bc & lm);
+    slot_a = sm.base[0] + sm.wa[warp] + __popc(ba & lm);
+    slot_b = sm.base[1] + sm.wb[warp] + __popc(bb & lm);
+    slot_c = sm.base[2] + sm.wc[warp] + __popc(bc & lm);
     tot_a = sm.tot[0];
     tot_b = sm.tot[1];
     tot_c = sm.tot[2];
-}
-__device__ __forceinline__ void compact2(Compact2 &sm, bool a, bool b, uint32_t &slot_a, uint32_t &slot_b,
-                                         uint32_t &tot_a, uint32_t &tot_b) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t ba = __ballot_sync(0xffffffffu, a), bb = __ballot_sync(0xffffffffu, b);
-    if (lane == 0) {
-        sm.wa[warp] = __popc(ba);
-        sm.wb[warp] = __popc(bb);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t nw = blockDim.x >> 5;
-        uint32_t va = lane < nw ? sm.wa[lane] : 0u, vb = lane < nw ? sm.wb[lane] : 0u;
-        uint32_t ia = va, ib = vb;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t xa = __shfl_up_sync(0xffffffffu, ia, o), xb = __shfl_up_sync(0xffffffffu, ib, o);
-            if (lane >= o) {
-                ia += xa;
-                ib += xb;
-            }
-        }
-        if (lane < nw) {
-            sm.wa[lane] = ia - va;
-            sm.wb[lane] = ib - vb;
-        }
-        tot_a = __shfl_sync(0xffffffffu, ia, 31);
-        tot_b = __shfl_sync(0xffffffffu, ib, 31);
-    }
-    __syncthreads();
-    const uint32_t lm = (1u << lane) - 1u;
-    slot_a = sm.wa[warp] + __popc(ba & lm);
-    slot_b = sm.wb[warp] + __popc(bb & lm);
 }
 
 // ------------------------------------------------------------------ k_front
@@ -275,15 +249,14 @@ k_front(NetDev net, StateDev st) {
     }
     const uint32_t vword = __ballot_sync(0xffffffffu, visit);
     if (net.nstdp && lane == 0 && valid) st.vmask[par][i >> 5] = vword;
-    // plastic visits -> k_stdp: the arrivals from the front of the CTA's region,
-    // the forced flushes from its back (so k_stdp can share each kind evenly);
+    // plastic visits -> k_stdp: the arrivals from the front of the list, the
+    // forced flushes from its back (so k_stdp can share each kind evenly);
     // every arrival -> k_deliver
     const bool parr = visit && arr, flush = visit && !arr;
     uint32_t sp, sa, sf, np, na, nf;
-    compact3(cs, parr, arr, flush, sp, sa, sf, np, na, nf);
-    const size_t region = (size_t)blockIdx.x * kFrontThreads;
-    if (parr) st.vdesc[par][region + sp] = d;
-    if (flush) st.vdesc[par][region + kFrontThreads - 1 - sf] = d;
+    compact3(cs, st.ctr->lst[par], parr, arr, flush, sp, sa, sf, np, na, nf);
+    if (parr) st.vdesc[par][sp] = d;
+    if (flush) st.vdesc[par][(size_t)st.nblk * kFrontThreads - 1 - sf] = d;
     if (arr) {                                       // every arriving row is delivered
         RowDesc a;
         a.start = st.row_ptr[i];
@@ -293,10 +266,11 @@ k_front(NetDev net, StateDev st) {
         a.xp = 0.0f;
         a.s0 = a.s1 = 0;
         a.pad = 0;
-        st.adesc[par][region + sa] = a;
+        st.adesc[par][sa] = a;
     }
     if (threadIdx.x == 0) {
-        st.cnt[par][blockIdx.x] = make_uint4(np, na, nf, 0u);
+        // the lists of step t-1 are consumed (k_deliver(t-1) completed): reset for t+1
+        if (blockIdx.x == 0) *reinterpret_cast<uint4 *>(st.ctr->lst[par ^ 1u]) = make_uint4(0u, 0u, 0u, 0u);
         // metrics (fire-and-forget reductions): spikes arriving, plastic rows
         // visited (arrivals + forced flushes), forced flushes
         if (na) atomicAdd(&st.ctr->metric[1], (unsigned long long)na);
@@ -304,55 +278,6 @@ k_front(NetDev net, StateDev st) {
         if (nf) atomicAdd(&st.ctr->metric[5], (unsigned long long)nf);
     }
     trace_mark(st.trace, 0, 3);
-}
-
-// ------------------------------------------------------- list region prefix
-// Per-CTA list regions (k_front) -> exclusive prefix over the regions of the
-// selected count (0 = plastic arrivals / read-out rows, 1 = arrivals, 2 = forced
-// flushes), into pre[0..nblk].
-template <int kThreads>
-__device__ __forceinline__ void region_prefix(const uint4 *cnt, uint32_t nblk, int which, uint32_t *pre,
-                                              uint32_t *wsum) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t per = (nblk + kThreads - 1) / kThreads;
-    const uint32_t b0 = threadIdx.x * per;
-    uint32_t sv = 0;
-    for (uint32_t b = b0; b < min(b0 + per, nblk); b++) sv += which == 0 ? cnt[b].x : which == 1 ? cnt[b].y : cnt[b].z;
-    uint32_t iv = sv;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t x = __shfl_up_sync(0xffffffffu, iv, o);
-        if (lane >= o) iv += x;
-    }
-    if (lane == 31) wsum[warp] = iv;
-    __syncthreads();
-    uint32_t ov = 0;
-    for (uint32_t w2 = 0; w2 < warp; w2++) ov += wsum[w2];
-    uint32_t rv = ov + iv - sv;
-    for (uint32_t b = b0; b < min(b0 + per, nblk); b++) {
-        pre[b] = rv;
-        rv += which == 0 ? cnt[b].x : which == 1 ? cnt[b].y : cnt[b].z;
-    }
-    if (threadIdx.x == kThreads - 1) pre[nblk] = rv;
-}
-
-// Row index r over the per-CTA regions -> position in the region array.
-__device__ __forceinline__ size_t region_index(const uint32_t *pre, uint32_t nblk, uint32_t r) {
-    uint32_t lo = 0, hi = nblk;          // largest b with pre[b] <= r
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (pre[mid] <= r) lo = mid; else hi = mid;
-    }
-    return (size_t)lo * kFrontThreads + (r - pre[lo]);
-}
-// Same for a list filled from the back of each region (forced flushes).
-__device__ __forceinline__ size_t region_index_back(const uint32_t *pre, uint32_t nblk, uint32_t r) {
-    uint32_t lo = 0, hi = nblk;
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (pre[mid] <= r) lo = mid; else hi = mid;
-    }
-    return (size_t)lo * kFrontThreads + (kFrontThreads - 1 - (r - pre[lo]));
 }
 
 // ---------------------------------------------------- CTA row-table helpers
@@ -558,10 +483,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     extern __shared__ __align__(16) unsigned char smem[];
     StdpSmem &sm = *reinterpret_cast<StdpSmem *>(smem);
     unsigned char *stage_base = smem + ((sizeof(StdpSmem) + 127) & ~(size_t)127);   // [stages][ids 8K | w 8K]
-    const uint32_t nblk = st.nblk;
-    uint32_t *pre = reinterpret_cast<uint32_t *>(stage_base + (size_t)kStdpStages * kStdpStageCh * 32);  // [nblk+1]
-    uint32_t *preF = pre + ((nblk + 1 + 3) & ~3u);                                                      // [nblk+1]
-    uint32_t *recent_s = preF + ((nblk + 1 + 3) & ~3u);                                                 // bitmap
+    uint32_t *recent_s = reinterpret_cast<uint32_t *>(stage_base + (size_t)kStdpStages * kStdpStageCh * 32);  // bitmap
     const bool readout = t_fixed >= 0;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool producer = warp == kStdpConsWarps;
@@ -590,19 +512,17 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     if (!readout) trace_mark(st.trace, 1, 0);
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Vl = readout ? st.rdesc : st.vdesc[par];
-    const uint4 *cnt = readout ? st.rcnt : st.cnt[par];
+    const uint32_t *lens = readout ? st.ctr->rlst : st.ctr->lst[par];
+    const uint32_t nA = lens[0], nF = readout ? 0u : lens[2];     // (k_front(t) complete)
+    const size_t cap_back = (size_t)st.nblk * kFrontThreads - 1;   // forced flushes: from the back
     const uint32_t bm_bytes = 16u * ((w_hi - w_lo + 3) >> 2);
     if (threadIdx.x == 0) {   // bitmap of recently fired post neurons (one bulk copy; the barrier's initialiser)
         mbar_expect_tx(bmap_a, bm_bytes);
         bulk_g2s(smem_u32(recent_s), st.recent + w_lo, bm_bytes, bmap_a);
     }
-    region_prefix<kStdpThreads>(cnt, nblk, 0, pre, sm.wsum);
-    __syncthreads();       // also: barrier init visible
-    region_prefix<kStdpThreads>(cnt, nblk, 2, preF, sm.wsum);
-    __syncthreads();
-    // even shares of each kind: plastic arrivals (front lists; read-out rows)
-    // and forced flushes (back lists); this CTA's rows: [0, nAb) arrivals, then flushes
-    const uint32_t nA = pre[nblk], nF = preF[nblk];
+    __syncthreads();       // barrier init visible
+    // even shares of each kind: plastic arrivals (front of the list; read-out
+    // rows) and forced flushes (back); this CTA's rows: [0, nAb) arrivals, then flushes
     const uint32_t a_begin = (uint32_t)(((uint64_t)nA * blockIdx.x) / gridDim.x);
     const uint32_t a_end = (uint32_t)(((uint64_t)nA * (blockIdx.x + 1)) / gridDim.x);
     const uint32_t f_begin = (uint32_t)(((uint64_t)nF * blockIdx.x) / gridDim.x);
@@ -632,8 +552,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
         rw.xp = 0.0f;
         rw.meta = 0;
         if (threadIdx.x < kStdpRows && r < r_end) {
-            const RowDesc d = Vl[r < nAb ? region_index(pre, nblk, a_begin + r)
-                                         : region_index_back(preF, nblk, f_begin + (r - nAb))];
+            const RowDesc d = Vl[r < nAb ? (size_t)(a_begin + r) : cap_back - (f_begin + (r - nAb))];
             const bool arr = (d.meta & kMetaArr) != 0;
             const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
             // a flush with x_pre == 0 changes no weight (potentiation adds 0)
@@ -1054,13 +973,10 @@ k_deliver(NetDev net, StateDev st) {
     __shared__ uint8_t s_rc[kDelRows];       // segment g: receptor code
     __shared__ uint2 s_bw[kDelWin / 32];     // window word: (segment-start bits, segments begun before it - 1)
     const uint32_t C = net.C;
-    const uint32_t nblk = st.nblk;
     const int64_t t = st.ctr->t;
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Al = st.adesc[par];
-    const uint4 *cnt = st.cnt[par];
-    uint32_t *pre = reinterpret_cast<uint32_t *>(smem);                         // [nblk + 1]
-    int32_t *acc = reinterpret_cast<int32_t *>(pre + ((nblk + 1 + 3) & ~3u));  // [nrcpt][C]
+    int32_t *acc = reinterpret_cast<int32_t *>(smem);                           // [nrcpt][C]
     const uint32_t k = blockIdx.x;
     const uint32_t nsplit = gridDim.y, split = blockIdx.y;
     const uint32_t slo = net.tgt_lo + k * C;
@@ -1072,10 +988,9 @@ k_deliver(NetDev net, StateDev st) {
     // prologue: reads only k_front(t)'s lists -- complete before k_stdp(t)
     // triggered this launch; without STDP the primary IS k_front(t), so wait
     if (net.nstdp == 0) pdl_wait();
-    region_prefix<kDelThreads>(cnt, nblk, 1, pre, wsum);
+    const uint32_t nA = k < net.nslices ? st.ctr->lst[par][1] : 0u;
     for (uint32_t x = threadIdx.x; x < net.nrcpt * C; x += kDelThreads) acc[x] = 0;
     __syncthreads();
-    const uint32_t nA = k < net.nslices ? pre[nblk] : 0u;
     const uint32_t r_begin = (uint32_t)(((uint64_t)nA * split) / nsplit);
     const uint32_t r_end = (uint32_t)(((uint64_t)nA * (split + 1)) / nsplit);
     const uint32_t P = net.nslices + 1;
@@ -1095,7 +1010,7 @@ k_deliver(NetDev net, StateDev st) {
 #pragma unroll
         for (int q = 0; q < 2; q++) {                 // both rows' loads in flight together
             const uint32_t r = r0 + threadIdx.x * 2 + q;
-            if (r < r_end) d2[q] = Al[region_index(pre, nblk, r)];
+            if (r < r_end) d2[q] = Al[r];
         }
 #pragma unroll
         for (int q = 0; q < 2; q++) {
@@ -1206,26 +1121,19 @@ constexpr int kRowThreads = 512;
 
 __global__ void __launch_bounds__(kRowThreads)
 k_deliver_rowwise(NetDev net, StateDev st) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t wsum[kRowThreads / 32];
-    uint32_t *pre = reinterpret_cast<uint32_t *>(smem);                         // [nblk + 1]
-    const uint32_t nblk = st.nblk;
     const uint32_t lane = threadIdx.x & 31;
     if (net.nstdp == 0) pdl_wait();
     const int64_t t = st.ctr->t;
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Al = st.adesc[par];
-    const uint4 *cnt = st.cnt[par];
-    region_prefix<kRowThreads>(cnt, nblk, 1, pre, wsum);
-    __syncthreads();
+    const uint32_t nA = st.ctr->lst[par][1];
     pdl_wait();            // k_stdp(t): updated weights of plastic arrivals
     pdl_launch();
-    const uint32_t nA = pre[nblk];
     const float scale = net.scale;
     uint32_t n_ev = 0;
     const uint32_t gw = (blockIdx.x * kRowThreads + threadIdx.x) >> 5, nw = (gridDim.x * kRowThreads) >> 5;
     for (uint32_t r = gw; r < nA; r += nw) {
-        const RowDesc d = Al[region_index(pre, nblk, r)];
+        const RowDesc d = Al[r];
         const int64_t c0 = d.start, c1 = st.row_ptr[d.row + 1];
         uint32_t rc = (d.meta >> 8) & 3u;
         const int src_pop = (int)((d.meta >> 16) & 0xfu);
@@ -1291,20 +1199,21 @@ k_readout_prepare(NetDev net, StateDev st, int64_t t_last) {
     }
     __syncwarp();
     if (valid && lane == 0 && net.nstdp) st.vmask[par][i >> 5] = 0u;
-    uint32_t s0, s1, n0, n1;
-    compact2(cs, stale, false, s0, s1, n0, n1);
-    if (stale) st.rdesc[(size_t)blockIdx.x * kFrontThreads + s0] = d;
-    if (threadIdx.x == 0) st.rcnt[blockIdx.x] = make_uint4(n0, 0u, 0u, 0u);
+    uint32_t s0, s1, s2, n0, n1, n2;
+    compact3(cs, st.ctr->rlst, stale, false, false, s0, s1, s2, n0, n1, n2);   // (rlst zeroed by the launcher)
+    if (stale) st.rdesc[s0] = d;
 }
 
 // (3) after k_stdp ran the flush on the listed rows: their x_pre / tlu.
 __global__ void __launch_bounds__(kFrontThreads)
 k_readout_finish(NetDev net, StateDev st, int64_t t_last) {
-    if (threadIdx.x >= st.rcnt[blockIdx.x].x) return;
-    const RowDesc d = st.rdesc[(size_t)blockIdx.x * kFrontThreads + threadIdx.x];
-    const StdpDev &sd = net.stdp[(d.meta >> 12) & 0xfu];
-    st.xpre[d.row] = xpre_after(sd, d.xp, (int)(d.meta & kMetaAge), false);
-    st.tlu[d.row] = (int32_t)t_last;
+    const uint32_t n = st.ctr->rlst[0];
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const RowDesc d = st.rdesc[r];
+        const StdpDev &sd = net.stdp[(d.meta >> 12) & 0xfu];
+        st.xpre[d.row] = xpre_after(sd, d.xp, (int)(d.meta & kMetaAge), false);
+        st.tlu[d.row] = (int32_t)t_last;
+    }
 }
 
 // Exchange (world > 1): the other ranks' spike words of step tp, gathered in
@@ -1369,14 +1278,12 @@ cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, 
 }
 
 size_t stdp_smem_bytes(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
-    const size_t nblk = front_blocks(net);
-    return ((sizeof(StdpSmem) + 127) & ~(size_t)127) + (size_t)kStdpStages * kStdpStageCh * 32 +
-           8 * ((nblk + 1 + 3) & ~(size_t)3) + 16ull * ((((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 3) >> 2);
+    (void)net;
+    return ((sizeof(StdpSmem) + 127) & ~(size_t)127) + (size_t)kStdpStages * kStdpStageCh * 32 + 16ull * ((((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 3) >> 2);
 }
 
 size_t deliver_smem_bytes(const NetDev &net) {
-    const size_t nblk = front_blocks(net);
-    return 4 * ((nblk + 1 + 3) & ~(size_t)3) + 4ull * net.nrcpt * net.C;
+    return 4ull * net.nrcpt * net.C;
 }
 
 cudaError_t kernels_configure(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
@@ -1409,8 +1316,7 @@ cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, 
 }
 
 cudaError_t launch_deliver_rowwise(const NetDev &net, const StateDev &st, uint32_t grid, cudaStream_t s, bool pdl) {
-    return launch_pdl(k_deliver_rowwise, dim3(grid), dim3(kRowThreads), 4 * ((front_blocks(net) + 1 + 3) & ~(size_t)3),
-                      s, pdl, net, st);
+    return launch_pdl(k_deliver_rowwise, dim3(grid), dim3(kRowThreads), 0, s, pdl, net, st);
 }
 
 cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s, bool pdl) {
@@ -1423,8 +1329,10 @@ cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t split
 
 cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last, uint32_t grid, uint32_t pp_lo,
                            uint32_t pp_hi, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(st.ctr->rlst, 0, sizeof(st.ctr->rlst), s);
+    if (e != cudaSuccess) return e;
     k_readout_prepare<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if ((e = launch_stdp(net, st, t_last, grid, pp_lo, pp_hi, s, false)) != cudaSuccess) return e;
     k_readout_finish<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
