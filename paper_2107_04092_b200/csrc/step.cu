@@ -363,8 +363,9 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
     uint32_t ok = 0;
     while (!ok)
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                     : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+                     " selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(a), "r"(parity), "r"(0x989680u) : "memory");   // suspend-time hint (ns)
 }
 // global -> shared bulk copy (16-byte aligned, size a multiple of 16), completes on mbar
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
@@ -429,14 +430,20 @@ __device__ __forceinline__ float stdp_synapse(float w, uint64_t m, bool arr, flo
 // k_stdp launch shape: one CTA per SM; 4 consumer groups of 4 warps take the
 // stages round-robin (so the gathers of one group overlap the filtering of the
 // others) + 1 TMA producer warp.
-constexpr int kStdpGroups = 4;
+#ifndef SNN_STDP_GROUPS
+#define SNN_STDP_GROUPS 4
+#endif
+#ifndef SNN_STDP_CH
+#define SNN_STDP_CH 4
+#endif
+constexpr int kStdpGroups = SNN_STDP_GROUPS;
 constexpr int kStdpGroupWarps = 4;
 constexpr int kStdpGroupThr = kStdpGroupWarps * 32;
 constexpr int kStdpConsWarps = kStdpGroups * kStdpGroupWarps;
 constexpr int kStdpCons = kStdpConsWarps * 32;     // consumer threads
 constexpr int kStdpThreads = kStdpCons + 32;       // + the producer warp
 constexpr int kStdpWarps = kStdpThreads / 32;
-constexpr int kStdpChPerThr = 4;                   // 16-byte chunks (16 synapses) per consumer thread and stage
+constexpr int kStdpChPerThr = SNN_STDP_CH;         // 16-byte chunks (16 synapses) per consumer thread and stage
 constexpr int kStdpStageCh = kStdpChPerThr * kStdpGroupThr;   // 512 chunks per stage: 8 KB ids + 8 KB weights
 constexpr int kStdpStages = 2 * kStdpGroups;       // 2 per group: 128 KB in flight per SM
 constexpr int kStdpRows = 256;                     // row table per round
@@ -1052,7 +1059,6 @@ k_deliver(NetDev net, StateDev st) {
                              : (uint64_t)(st.idx + c0q[q]) - 4ull * est[q];
             g++;
         }
-        trace_mark(st.trace, 2, 1);
         for (uint32_t w0 = 0; w0 < T; w0 += kDelWin) {
             const uint32_t wlen = min(T - w0, (uint32_t)kDelWin);
             s_bw[threadIdx.x].x = 0u;
@@ -1072,6 +1078,7 @@ k_deliver(NetDev net, StateDev st) {
             if (r0 == r_begin && w0 == 0) {   // (the segment tables and the bitmap are ready)
                 pdl_wait();    // k_stdp(t): updated weights of plastic arrivals
                 pdl_launch();
+                trace_mark(st.trace, 2, 1);
             }
             // ---- elements: thread x takes w0 + x + 512 u (coalesced)
             deliver_window<kMulti, kIdx16>(net, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
