@@ -405,3 +405,42 @@ def test_full_size_cfg3_sampled_against_oracle():
             assert abs(float(w[b + c]) - ref) <= 1e-4 * max(abs(ref), 1e-2 * wmax), (i, j, w[b + c], ref)
             checked += 1
     assert checked == 300
+
+
+def _dense_recipe(n_p, n_e, p, delay, seed):
+    """Poisson sources firing every step (rate * dt = 1) onto one LIF
+    population through STDP: every source row arrives (or is visited) each
+    step -- the multi-round / multi-window paths of k_stdp and k_deliver."""
+    wmax = 0.02
+    stdp = dict(tau_plus=20.0, tau_minus=20.0, a_plus=0.01 * wmax, a_minus=0.0105 * wmax, w_max=wmax)
+    pops = [W.Pop("E", W.LIF_DELTA, n_e, dict(W.BRUNEL_LIF)), W.Pop("P", W.POISSON, n_p, dict(rate_hz=10000.0))]
+    projs = [W.Proj(1, 0, W.STDP, W.EXC, p, 0.5 * wmax, stdp), W.Proj(0, 0, W.STATIC, W.EXC, 0.05, -0.3)]
+    return W.Recipe("dense", seed, 0.1, delay, 20, pops, projs, plastic=True), wmax
+
+
+def _compare_weights_wmax(g, o, wmax):
+    wg, wo = g.read_state("WEIGHTS"), o.array("w")
+    err = np.abs(wg.astype(np.float64) - wo)
+    bad = err > 1e-4 * np.maximum(np.abs(wo), 1e-2 * wmax)
+    assert not bad.any(), f"{bad.sum()} weights off, max err {err.max():.3g}"
+
+
+@pytest.mark.parametrize("plasticity", [0, 2])
+def test_dense_rows_several_stdp_rounds(plasticity):
+    """40,000 plastic rows visited every step: > 256 rows per k_stdp CTA
+    (several row-table rounds), > 1024 arrivals per k_deliver CTA."""
+    rc, wmax = _dense_recipe(40000, 2048, 0.01, 1, 21)
+    g, o = _pair(rc, slice_width=32, plasticity=plasticity)
+    _run_compare(g, o, 12, exact_v=False, every=3)
+    _compare_weights_wmax(g, o, wmax)
+    assert g.metrics()["EVENTS"] == o.events
+
+
+def test_dense_slices_several_windows():
+    """One slice per 32 targets (296 slices: one CTA each) and ~19 events per
+    (row, slice): several 16k-element windows per row round, several rounds."""
+    rc, wmax = _dense_recipe(3000, 296 * 32, 0.6, 2, 22)
+    g, o = _pair(rc, slice_width=32)
+    _run_compare(g, o, 8, exact_v=False, every=2)
+    _compare_weights_wmax(g, o, wmax)
+    assert g.metrics()["EVENTS"] == o.events
