@@ -980,9 +980,6 @@ k_deliver(NetDev net, StateDev st) {
     __shared__ uint8_t s_rc[kDelRows];       // segment g: receptor code
     __shared__ uint2 s_bw[kDelWin / 32];     // window word: (segment-start bits, segments begun before it - 1)
     const uint32_t C = net.C;
-    const int64_t t = st.ctr->t;
-    const uint32_t par = (uint32_t)(t & 1);
-    const RowDesc *Al = st.adesc[par];
     int32_t *acc = reinterpret_cast<int32_t *>(smem);                           // [nrcpt][C]
     const uint32_t k = blockIdx.x;
     const uint32_t nsplit = gridDim.y, split = blockIdx.y;
@@ -995,7 +992,12 @@ k_deliver(NetDev net, StateDev st) {
     // prologue: reads only k_front(t)'s lists -- complete before k_stdp(t)
     // triggered this launch; without STDP the primary IS k_front(t), so wait
     if (net.nstdp == 0) pdl_wait();
-    const uint32_t nA = k < net.nslices ? st.ctr->lst[par][1] : 0u;
+    // the step and both parities' arrival counts in one round trip
+    const int64_t t = st.ctr->t;
+    const uint32_t nA0 = st.ctr->lst[0][1], nA1 = st.ctr->lst[1][1];
+    const uint32_t par = (uint32_t)(t & 1);
+    const RowDesc *Al = st.adesc[par];
+    const uint32_t nA = k < net.nslices ? (par ? nA1 : nA0) : 0u;
     for (uint32_t x = threadIdx.x; x < net.nrcpt * C; x += kDelThreads) acc[x] = 0;
     __syncthreads();
     const uint32_t r_begin = (uint32_t)(((uint64_t)nA * split) / nsplit);
