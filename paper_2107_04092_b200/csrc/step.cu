@@ -429,7 +429,7 @@ __device__ __forceinline__ float stdp_synapse(float w, uint64_t m, bool arr, flo
 
 // k_stdp launch shape: one CTA per SM; 4 consumer groups of 4 warps take the
 // stages round-robin (so the gathers of one group overlap the filtering of the
-// others) + 1 TMA producer warp.
+// others) + 1 TMA producer warp; 6 stages in the ring.
 #ifndef SNN_STDP_GROUPS
 #define SNN_STDP_GROUPS 4
 #endif
@@ -445,7 +445,12 @@ constexpr int kStdpThreads = kStdpCons + 32;       // + the producer warp
 constexpr int kStdpWarps = kStdpThreads / 32;
 constexpr int kStdpChPerThr = SNN_STDP_CH;         // 16-byte chunks (16 synapses) per consumer thread and stage
 constexpr int kStdpStageCh = kStdpChPerThr * kStdpGroupThr;   // 512 chunks per stage: 8 KB ids + 8 KB weights
-constexpr int kStdpStages = 2 * kStdpGroups;       // 2 per group: 128 KB in flight per SM
+#ifndef SNN_STDP_STAGES
+#define SNN_STDP_STAGES 6
+#endif
+// 96 KB in flight per SM: measured on cfg3 (us/step) 4: 50.3, 5: 47.5, 6: 46.0,
+// 7: 46.3, 8: 46.3, 10: 50.8 -- the rest of the 256 KB stays L1 for the gathers
+constexpr int kStdpStages = SNN_STDP_STAGES;
 constexpr int kStdpRows = 256;                     // row table per round
 constexpr int kStdpList = 32 * 4 * kStdpChPerThr;  // per-warp list of the synapses to update (one stage)
 
