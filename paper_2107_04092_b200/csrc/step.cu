@@ -451,8 +451,15 @@ constexpr int kStdpStageCh = kStdpChPerThr * kStdpGroupThr;   // 512 chunks per 
 // 96 KB in flight per SM: measured on cfg3 (us/step) 4: 50.3, 5: 47.5, 6: 46.0,
 // 7: 46.3, 8: 46.3, 10: 50.8 -- the rest of the 256 KB stays L1 for the gathers
 constexpr int kStdpStages = SNN_STDP_STAGES;
-constexpr int kStdpRows = 256;                     // row table per round
-constexpr int kStdpList = 32 * 4 * kStdpChPerThr;  // per-warp list of the synapses to update (one stage)
+#ifndef SNN_STDP_ROWS
+#define SNN_STDP_ROWS 128
+#endif
+#ifndef SNN_STDP_LIST
+#define SNN_STDP_LIST 128
+#endif
+constexpr int kStdpRows = SNN_STDP_ROWS;            // row table per round
+constexpr uint32_t kStdpList = SNN_STDP_LIST;       // per-warp list of the synapses to update (a stage
+                                                    // lists more in several passes)
 
 struct __align__(16) StdpRow {   // one visited row of this CTA (shared memory)
     int64_t cb;      // 16-byte aligned CSR offset of its plastic span
@@ -720,15 +727,22 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                     const uint32_t y = __shfl_up_sync(0xffffffffu, ex, d);
                     if (lane >= (uint32_t)d) ex += y;
                 }
-                uint32_t n = __shfl_sync(0xffffffffu, ex, 31);
+                const uint32_t ntot = __shfl_sync(0xffffffffu, ex, 31);
                 ex -= k;
-                while (hm) {
-                    const uint32_t bpos = __ffs(hm) - 1u;
-                    hm &= hm - 1u;
-                    const uint32_t u = bpos >> 2;
-                    const uint32_t p = 4u * (gt + kStdpGroupThr * u) + (bpos & 3u);     // element in the stage
-                    sts_u32(list_a + 4u * ex, (p << 9) | (((rm >> bpos) & 1u) << 8) | ((slots >> (8 * u)) & 0xffu));
-                    ex++;
+                for (uint32_t base = 0; base < ntot; base += kStdpList) {
+                uint32_t n = ntot - base < kStdpList ? ntot - base : kStdpList;
+                {
+                    uint32_t m = hm, e = ex;
+                    while (m) {
+                        const uint32_t bpos = __ffs(m) - 1u;
+                        m &= m - 1u;
+                        const uint32_t u = bpos >> 2;
+                        const uint32_t p = 4u * (gt + kStdpGroupThr * u) + (bpos & 3u);     // element in the stage
+                        if (e - base < kStdpList)
+                            sts_u32(list_a + 4u * (e - base),
+                                    (p << 9) | (((rm >> bpos) & 1u) << 8) | ((slots >> (8 * u)) & 0xffu));
+                        e++;
+                    }
                 }
                 __syncwarp();
                 if (!__any_sync(0xffffffffu, nonlean)) {
@@ -817,7 +831,8 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         n_w += chg;
                     }
                 }
-                __syncwarp();
+                __syncwarp();                              // list reused by the next pass
+                }
                 if (lane == 0) mbar_arrive(empty_a + 8 * slot);   // stage and list free
             }
         }
