@@ -14,7 +14,6 @@
 
 namespace snn {
 
-constexpr int kBuildThreads = 256;
 constexpr int kGeoThreads = 128;
 
 // Exact geometric skipping (R32): the kept candidates of row i

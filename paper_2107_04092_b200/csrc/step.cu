@@ -303,16 +303,6 @@ __device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t *wsum, 
     return off + inc;
 }
 
-// Index of the row whose [incl - len, incl) range holds e (incl ascending).
-__device__ __forceinline__ uint32_t owner_search(const uint32_t *incl, uint32_t n, uint32_t e) {
-    uint32_t lo = 0, hi = n;            // first r with incl[r] > e
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (incl[mid] <= e) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
 // ------------------------------------------------------------------ k_stdp
 // Shared / predicated global loads written out in PTX so that the compiler
 // neither re-derives the shared window per access nor branches around a load.
