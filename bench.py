@@ -174,7 +174,8 @@ def main():
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "events/s",
             "n_gpus": a.gpus, "steps": r["steps"], "warmup": a.warmup,
-            "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
+            "scaling": "strong" if a.config in (2, 3, 4) else "weak",      # (as the GPU arm's line)
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"BASELINE config {a.config} (oracle sample: {r['sample']})"},
             "wall_s_per_bio_s": r["wall_s_per_bio_s"],
