@@ -2,17 +2,32 @@
 wall-s per bio-second & synaptic events/s; % HBM roofline) on synthetic
 Brunel+ / Brunel / Vogels-Abbott networks.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--settle S] [--config 3] [--impl ours|reference]
 
 A "step" is one simulation step (dt = 0.1 ms) of the whole hot path: neuron
 update, lazy+event-driven STDP, sliced shared-atomic delivery.
 Default workload: BASELINE config 3 (Brunel+, 316,228 neurons, ~1e9 synapses,
 40 % plastic) -- the only single-GPU config that exercises every 8(a) row.
+
+The timed window is the network's steady state: every run first simulates S
+"settle" steps (default 3,000 = 0.3 s of biological time: past the
+synchronous first forced flush at t = 63 and the rate transient), then W
+warm-up steps, then times exactly K steps (the paper's measure is wall time
+over long biological time).  `value` = wall-seconds per biological
+second over the K steps (lower is better); synaptic events/s is reported
+beside it.  Three handles of the same seed simulate the identical trajectory
+(the simulation is deterministic) over the same window:
+  A  the device-timed K steps (CUDA events on the simulation stream),
+  B  the same K steps with in-graph kernel spans (SNN_FLAG_KTIME): per-kernel
+     durations for the roofline, measured inside the graph-replayed step,
+  C  the same K steps through the public API with host buffers (e2e).
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
+import glob
+import hashlib
 import json
 import os
 import subprocess
@@ -28,13 +43,16 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 METRIC = "wall-s per bio-second & synaptic events/s at 1/2/4/8 B200; % HBM roofline"
+KERNEL_OF = {"front": "k_front", "stdp": "k_stdp", "deliver": "k_deliver"}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10000)
     ap.add_argument("--warmup", type=int, default=1000)
+    ap.add_argument("--settle", type=int, default=3000,
+                    help="steps simulated before the warm-up (steady state; not timed)")
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--slice-width", type=int, default=0)
@@ -48,26 +66,40 @@ def parse():
                     help="delivery reads 16-bit slice-local target offsets (SURVEY 8(f1), P:405)")
     ap.add_argument("--history-bits", type=int, default=64, choices=[64, 128],
                     help="H: 64 (the paper's default, P:192) or 128 (SURVEY 8(f3), P:399)")
+    ap.add_argument("--exchange-window", type=int, default=0, help="world > 1: steps per spike exchange (0 = auto)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--phase-steps", type=int, default=0, help="steps of the per-phase timing pass (0 = --steps)")
-    return ap.parse_args()
+    ap.add_argument("--no-ktime", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0 = all host cores)")
+    ap.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of timed oracle steps (cpu_baseline)")
+    return ap.parse_args(argv)
 
 
-def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
-    summary (profiles/<round>/ncu_<tag>.json, written by scripts/summarize_ncu.py)."""
-    import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_v*.json")),
-                   key=lambda p: (os.path.basename(os.path.dirname(p)), int(os.path.basename(p)[5:-5])))
-    for p in reversed(files):
+def source_sha() -> str:
+    """Hash of the CUDA sources: an ncu capture counts for this run only if it
+    was taken on the same kernels."""
+    h = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(ROOT, "paper_2107_04092_b200", "csrc", "*.cu*"))):
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
+def ncu_traffic(kernel: str, cfg: int, flags: str):
+    """DRAM bytes per launch of `kernel` from a committed `ncu --set full`
+    summary (profiles/<round>/ncu_<tag>.json, scripts/summarize_ncu.py) taken
+    on the same source revision, config and flags -- else None."""
+    sha = source_sha()
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_*.json")), reverse=True):
         try:
             d = json.load(open(p))
         except Exception:
             continue
-        for name, v in d.items():              # template instances: "k_stdp<false, ...>"
-            if name.split("<")[0].split()[-1] == kernel and "dram_bytes" in v:
+        meta = d.get("_meta", {})
+        if meta.get("source_sha") != sha or meta.get("config") != cfg or meta.get("flags", "") != flags:
+            continue
+        for name, v in d.items():              # template instances: "void k_stdp<0, 0, 0>"
+            if name != "_meta" and name.split("<")[0].split()[-1] == kernel and "dram_bytes" in v:
                 return v["dram_bytes"], os.path.relpath(p, ROOT)
     return None, None
 
@@ -75,7 +107,7 @@ def ncu_traffic(kernel):
 def peaks():
     try:
         d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
@@ -99,6 +131,7 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)                    # first sample before the timed region
         except Exception:
             self.proc = None
         return self
@@ -127,25 +160,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_sample_recipe(cfg: int, seed: int):
-    """Bounded oracle sample of the same workload family."""
-    if cfg in (3, 4):
-        return W.brunel(31_623, plastic=True, seed=seed), "Brunel+ scaled to N=31,623 (same composition, p=0.02, ~1e7 synapses, 40% plastic)"
-    if cfg == 2:
-        return W.brunel(31_623, plastic=False, seed=seed), "Brunel scaled to N=31,623 (same composition, p=0.02, ~1e7 synapses)"
-    if cfg == 5:
-        return W.vogels(31_623, seed=seed), "Vogels CUBA scaled to N=31,623 (p=0.02, ~2e7 synapses)"
-    return W.config(1, seed=seed), "Vogels CUBA 4,000 (the full config 1)"
-
-
-def run_oracle(cfg: int, seed: int, steps: int, warmup: int, budget_s: float = 20.0):
-    """Time the oracle as it stands (test infrastructure; only this leg of bench.py runs it)."""
+# ------------------------------------------------------------------ oracle
+def run_oracle(cfg: int, seed: int, steps: int, warmup: int, budget_s: float, threads: int = 0):
+    """Time the oracle as it stands (test infrastructure; only this leg of
+    bench.py runs it) on the FULL network of the BASELINE config: build the
+    graph (untimed), `warmup` untimed steps, then up to `steps` timed steps or
+    until `budget_s` seconds -- a bounded sample of the workload.  Per-step
+    time x 10,000 = wall-s per bio-second, extrapolated."""
     from oracle.oracle import Oracle
-    rc, sample = cpu_sample_recipe(cfg, seed)
-    cores = os.cpu_count() or 1
+    rc = W.config(cfg, seed=seed)
+    cores = threads or os.cpu_count() or 1
     o = Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, threads=cores)
     rc.apply(o)
+    t0 = time.perf_counter()
     o.finalize()
+    build_s = time.perf_counter() - t0
     o.step(warmup)
     e0 = o.events
     t0 = time.perf_counter()
@@ -157,36 +186,44 @@ def run_oracle(cfg: int, seed: int, steps: int, warmup: int, budget_s: float = 2
             break
     dt = time.perf_counter() - t0
     ev = o.events - e0
-    return dict(value=ev / dt, unit="events/s", cores=cores, kind="oracle",
-                sample=f"{sample}; {done} timed steps after {warmup} warm-up steps",
-                wall_s_per_bio_s=(dt / done) / (rc.dt_ms * 1e-3), steps=done, seconds=dt,
-                synapses=int(o.nsyn))
+    per_step = dt / done
+    return dict(value=per_step / (rc.dt_ms * 1e-3), unit="wall-s per bio-second (extrapolated)", cores=cores,
+                kind="oracle",
+                sample=(f"BASELINE config {cfg} at full size ({rc.name}, {o.nsyn:,} synapses; graph build "
+                        f"{build_s:.1f} s untimed): {done} timed steps after {warmup} untimed steps from t = 0 "
+                        f"on {cores} host threads, per-step time x 10,000 = 1 bio-second (extrapolated).  The "
+                        f"naive STDP sweep (Fig. 2a, every plastic synapse every step) dominates the oracle's "
+                        f"step and does not depend on activity; delivery runs at the cold network's rates"),
+                events_per_s=ev / dt, steps=done, seconds=dt, synapses=int(o.nsyn), ms_per_step=1e3 * per_step)
 
 
-def main():
-    a = parse()
+# ------------------------------------------------------------------ GPU arm
+def main(argv=None):
+    a = parse(argv)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    scaling = "strong" if a.config in (2, 3, 4) else "weak"
     if a.impl == "reference":
         if rank != 0:
             return
-        r = run_oracle(a.config, a.seed, a.steps, max(a.warmup, 0), budget_s=60.0)
+        r = run_oracle(a.config, a.seed, a.steps, max(a.warmup, 0), budget_s=60.0, threads=a.cpu_threads)
         print(json.dumps({
-            "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "events/s",
-            "n_gpus": a.gpus, "steps": r["steps"], "warmup": a.warmup,
-            "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
-            "scaling": "strong" if a.config in (2, 3, 4) else "weak",      # (as the GPU arm's line)
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"BASELINE config {a.config} (oracle sample: {r['sample']})"},
-            "wall_s_per_bio_s": r["wall_s_per_bio_s"],
-            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": r["value"], "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "wall-s per bio-second",
+            "n_gpus": a.gpus, "steps": r["steps"], "warmup": a.warmup, "ms_per_step": r["ms_per_step"],
+            "higher_is_better": False, "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"BASELINE config {a.config}: {W.config(a.config).name} (oracle, full size)",
+                       "settle_steps": 0},
+            "events_per_s": r["events_per_s"],
+            "cpu_baseline": {"value": r["value"], "unit": r["unit"], "cores": r["cores"], "kind": "oracle",
+                             "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "wall-s per bio-second", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
         }))
         return
 
     import torch
     import torch.distributed as dist
-    from paper_2107_04092_b200 import Snn, FLAG_PHASE_TIMING, FLAG_IDX16
+    from paper_2107_04092_b200 import Snn, FLAG_IDX16, FLAG_KTIME
     from paper_2107_04092_b200 import dist as pdist
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
@@ -197,6 +234,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     rc = W.config(a.config, seed=a.seed, gpus=world)
     stream = torch.cuda.Stream(dev)
+    pre_steps = a.settle + a.warmup
 
     def make(flags=0):
         if a.idx16:
@@ -205,7 +243,8 @@ def main():
         s = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=a.slice_width, device=dev, stream=stream,
                 flags=flags, rank=rank, world=world, nccl_unique_id=uid, history_bits=a.history_bits,
                 plasticity=["event", "lazy", "naive"].index(a.plasticity),
-                delivery=["sliced", "rowwise"].index(a.delivery), flush_period=a.flush_period)
+                delivery=["sliced", "rowwise"].index(a.delivery), flush_period=a.flush_period,
+                exchange_window=a.exchange_window)
         rc.apply(s)
         return s
 
@@ -224,7 +263,7 @@ def main():
     MAX = dist.ReduceOp.MAX if world > 1 else None
     SUM = dist.ReduceOp.SUM if world > 1 else None
 
-    # ---------------------------------------------------------- device-timed
+    # ------------------------------------------- A: device-timed K steps
     sim = make()
     t0 = time.perf_counter()
     sim.finalize()
@@ -232,11 +271,12 @@ def main():
     setup_s = time.perf_counter() - t0
     info = sim.info()
     build_ms = sim.phase_times()["BUILD"]      # device time of count + scan + fill + segments (f4)
+    sim.step(pre_steps)                        # settle + warm-up (untimed)
+    barrier()
+    m0 = sim.metrics()
+    spk0 = sim.read_state("SPIKE_COUNT").astype(np.int64)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
-        sim.step(a.warmup)
-        barrier()
-        m0 = sim.metrics()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         ev0.record(stream)
         sim.step(a.steps)
@@ -244,127 +284,173 @@ def main():
         barrier()
     ms = reduce(ev0.elapsed_time(ev1), MAX)                   # max over ranks
     m1 = sim.metrics()
-    dm = {k: int(reduce(m1[k] - m0[k], SUM)) for k in m1}     # work of all ranks
-    spikes = sim.read_state("SPIKE_COUNT")
-    t_total = (a.warmup + a.steps) * rc.dt_ms * 1e-3
-    rates = {p.name: float(spikes[b:b + p.n].sum()) / p.n / t_total
+    spk = sim.read_state("SPIKE_COUNT").astype(np.int64) - spk0
+    dm = {k: int(reduce(m1[k] - m0[k], SUM)) for k in m1}     # work of all ranks in the window
+    dm_local = {k: m1[k] - m0[k] for k in m1}
+    sim.close()
+    del sim
+    t_win = a.steps * rc.dt_ms * 1e-3
+    rates = {p.name: float(spk[b:b + p.n].sum()) / p.n / t_win
              for p, b in zip(rc.pops, np.cumsum([0] + [p.n for p in rc.pops])[:-1])}
     sec = ms * 1e-3
     events_per_s = dm["EVENTS"] / sec
     ms_per_step = ms / a.steps
     wall_per_bio = (ms_per_step * 1e-3) / (rc.dt_ms * 1e-3)
 
-    # --------------------------------------------------- e2e through the C ABI
+    # ------------------------------ B: kernel spans inside the replayed graph
+    spans = None
+    if not a.no_ktime:
+        sk = make(FLAG_KTIME)
+        sk.step(pre_steps)
+        k0 = sk.ktime()                         # folds (and discards) the settle / warm-up steps
+        mk0 = sk.metrics()
+        barrier()
+        ek0, ek1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ek0.record(stream)
+        sk.step(a.steps)
+        ek1.record(stream)
+        barrier()
+        k1 = sk.ktime()
+        mk1 = sk.metrics()
+        ms_k = reduce(ek0.elapsed_time(ek1), MAX)
+        same = all(mk1[k] - mk0[k] == dm_local[k] for k in dm_local)
+        sk.close()
+        del sk
+        spans = {"same_window": bool(reduce(0.0 if same else 1.0, MAX) == 0.0),
+                 "ms_per_step_instrumented": ms_k / a.steps}
+        for k in ("front", "stdp", "deliver"):
+            st = k1[k]["steps"] - k0[k]["steps"]
+            if st <= 0:
+                continue
+            spans[k] = {"us_from_entry": reduce((k1[k]["entry_ns"] - k0[k]["entry_ns"]) / st * 1e-3, MAX),
+                        "us_from_wait": reduce((k1[k]["wait_ns"] - k0[k]["wait_ns"]) / st * 1e-3, MAX),
+                        "steps": st, "ctas_per_launch": (k1[k]["ctas"] - k0[k]["ctas"]) / st}
+
+    # --------------------------------- C: end to end through the public API
     e2e = None
     if not a.no_e2e:
+        se = make()
+        se.step(pre_steps)
+        nw = (info["N"] + 31) // 32
         chunk = 64
-        # the step rasters land in a pinned host buffer (the caller owns host_dst)
-        ring = torch.empty(64 * ((info["N"] + 31) // 32), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-        m0e = sim.metrics()
+        # the steps' rasters land in a pinned host buffer the caller owns
+        host = torch.empty(chunk * nw, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        me0 = se.metrics()
         barrier()
         t0 = time.perf_counter()
         done = 0
+        d2h = 0
         while done < a.steps:
             n = min(chunk, a.steps - done)
-            sim.step(n)
-            sim.read_state("SPIKE_RING", out=ring)     # D2H of the step rasters into a host buffer
+            t_first = pre_steps + done
+            se.step(n)
+            s0 = t_first % 64                       # ring slots of the chunk's steps (slot t % 64)
+            k1n = min(n, 64 - s0)
+            se.read_range("SPIKE_RING", s0 * nw, k1n * nw, out=host[:k1n * nw])
+            if k1n < n:                              # the chunk wraps around the ring
+                se.read_range("SPIKE_RING", 0, (n - k1n) * nw, out=host[k1n * nw:n * nw])
+            d2h += 4 * n * nw
             done += n
         t1 = time.perf_counter()
-        m1e = sim.metrics()
+        me1 = se.metrics()
         wall = reduce(t1 - t0, MAX)
-        evs = reduce(m1e["EVENTS"] - m0e["EVENTS"], SUM)
-        e2e = {"value": evs / wall, "unit": "events/s",
-               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(ring.nbytes / chunk),
-               "wall_s_per_bio_s": wall / (a.steps * rc.dt_ms * 1e-3),
-               "note": "snn_step(64) + snn_read_state(SPIKE_RING) into a pinned host buffer per 64 steps; an SNN "
-                       "step has no host input (Poisson drive is counter-based on device), so h2d = 0"}
-    sim.close()
-    del sim
-    torch.cuda.synchronize()
+        same_e = all(me1[k] - me0[k] == dm_local[k] for k in dm_local)
+        se.close()
+        del se
+        e2e = {"value": wall / (a.steps * rc.dt_ms * 1e-3), "unit": "wall-s per bio-second",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(d2h / a.steps),
+               "events_per_s": dm["EVENTS"] / wall, "same_window": bool(reduce(0.0 if same_e else 1.0, MAX) == 0.0),
+               "note": "snn_step(n) + snn_read_state_range(SPIKE_RING) of the n steps' rasters into a pinned host "
+                       "buffer, n = 64 (host wall clock, max over ranks); an SNN step has no host input (the "
+                       "Poisson drive is counter-based on the device), so h2d = 0"}
 
-    # ------------------------------------------- per-phase timing (roofline)
-    psteps = a.phase_steps or a.steps
-    sp = make(FLAG_PHASE_TIMING)
-    sp.step(a.warmup)
-    sp.phase_times()   # drain warm-up events
-    base = sp.phase_times()
-    mp0 = sp.metrics()
-    sp.step(psteps)
-    ph = sp.phase_times()
-    mp1 = sp.metrics()
-    ph = {k: reduce(ph[k] - base[k], MAX) for k in ph}
-    d = {k: int(reduce(mp1[k] - mp0[k], SUM)) for k in mp1}
-    sp.close()
+    # ------------------------------------------------------------ roofline
     nrcpt = 2 if any(pr.receptor == W.INH for pr in rc.projs) else 1
-    # algorithmic HBM bytes per kernel:
-    #   k_stdp:    4 B target id per visited plastic synapse, 8 B where the weight
-    #              is read and written, 16 B per visited row (x_pre, tlu, row_ptr, seg)
-    #   k_deliver: 8 B per delivered event (id + weight; 6 B with --idx16), 8 B per (arriving row,
-    #              slice) pivot pair, 4 B per slice neuron and receptor written back
+    K = a.steps
+    # algorithmic HBM bytes per launch:
+    #   k_stdp:    4 B target id per visited plastic synapse + 8 B (weight read
+    #              and written) per synapse of an arriving row or whose target
+    #              fired in the window + 16 B per visited row
+    #   k_deliver: 8 B per delivered event (id + weight; 6 B with --idx16) +
+    #              8 B per (arriving row, slice) pivot pair + 4 B per slice
+    #              neuron and receptor written back
+    #   k_front:   32 B per LIF neuron, 16 B per Poisson neuron (8(a1))
+    n_pois = sum(p.n for p in rc.pops if p.kind == W.POISSON)
     kb = {
-        "STDP": 4 * d["STDP_SYN"] + 8 * d["STDP_WTOUCH"] + 16 * d["STDP_ROWS"],
-        "DELIVERY": (6 if a.idx16 else 8) * d["EVENTS"] + 8 * d["SPIKES"] * info["nslices"]
-                    + 4 * nrcpt * info["R"] * psteps,
+        "stdp": (4 * dm_local["STDP_SYN"] + 8 * dm_local["STDP_WRW"] + 16 * dm_local["STDP_ROWS"]) / K,
+        "deliver": ((6 if a.idx16 else 8) * dm_local["EVENTS"] + 8 * dm_local["SPIKES"] * info["nslices"]) / K
+                   + 4 * nrcpt * (info["tgt_hi"] - info["tgt_lo"]),
+        "front": 32.0 * (info["N"] - n_pois) + 16.0 * n_pois,
     }
     hbm, peak_src = peaks()
     kern = {}
-    for k2, by in kb.items():
-        ms_k = ph[k2]
-        kern[k2] = {"bytes_per_step": by / psteps, "ms_per_step": ms_k / psteps,
-                    "achieved_gbs": by / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0}
-    dom = max(kern, key=lambda k2: kern[k2]["ms_per_step"])
-    achieved = kern[dom]["achieved_gbs"]
-    dom_kernel = {"STDP": "k_stdp", "DELIVERY": "k_deliver_rowwise" if a.delivery == "rowwise" else "k_deliver"}[dom]
-    traffic, traffic_src = ncu_traffic(dom_kernel)
-    shares = {k: ph[k] / ph["TOTAL"] for k in ("FRONT", "STDP", "DELIVERY")} if ph["TOTAL"] else {}
-    sd_bytes, sd_ms = kb["STDP"] + kb["DELIVERY"], ph["STDP"] + ph["DELIVERY"]
-    # level (i) of SURVEY 8(d): the whole step -- STDP + delivery bytes plus the
-    # neuron update (~32 B per LIF neuron, 16 B per Poisson neuron, 8(a1)) over
-    # the graph-replayed step time
-    n_pois = sum(p.n for p in rc.pops if p.kind == W.POISSON)
-    front_bytes_step = 32.0 * (info["N"] - n_pois) + 16.0 * n_pois
-    step_bytes = sd_bytes / psteps + front_bytes_step
-    split_group = info["pivot_bytes"]
+    for k, by in kb.items():
+        if by <= 0 or not spans or k not in spans:
+            continue
+        us = spans[k]["us_from_wait"]
+        kern[k] = {"bytes_per_launch": by, "us_per_launch": us, "us_per_launch_from_entry": spans[k]["us_from_entry"],
+                   "achieved_gbs": by / (us * 1e-6) / 1e9 if us > 0 else 0.0}
+        kern[k]["frac"] = kern[k]["achieved_gbs"] / hbm
+        kern[k]["share_of_step"] = us * 1e-3 / ms_per_step
+    dom = max(kern, key=lambda k: kern[k]["us_per_launch"]) if kern else None
+    flags_s = ",".join(x for x, on in [("idx16", a.idx16), (f"H{a.history_bits}", a.history_bits != 64),
+                                       (a.plasticity, a.plasticity != "event"), (a.delivery, a.delivery != "sliced")]
+                       if on)
+    roof = None
+    if dom:
+        dk = KERNEL_OF[dom] if not (dom == "deliver" and a.delivery == "rowwise") else "k_deliver_rowwise"
+        traffic, traffic_src = ncu_traffic(dk, a.config, flags_s)
+        sd = [k for k in ("stdp", "deliver") if k in kern]
+        sd_b = sum(kern[k]["bytes_per_launch"] for k in sd)
+        sd_us = sum(kern[k]["us_per_launch"] for k in sd)
+        step_b = sum(kb.values())
+        roof = {"bound": "hbm", "kernel": dk, "achieved": kern[dom]["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": kern[dom]["achieved_gbs"] / hbm, "traffic": traffic,
+                "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+                "traffic_source": traffic_src or "no ncu --set full capture of this source revision / config",
+                "algorithmic_bytes_per_launch": kern[dom]["bytes_per_launch"], "peak_source": peak_src,
+                "duration": "per launch, from the kernel's first return from its dependency wait (PDL) to its "
+                            "last CTA's end, %globaltimer marks inside the graph-replayed timed steps "
+                            "(SNN_FLAG_KTIME, run B on the identical window); CUDA events bracket the window",
+                "kernels": kern,
+                "stdp_plus_delivery": {"bytes_per_step": sd_b, "us_per_step": sd_us,
+                                       "achieved_gbs": sd_b / (sd_us * 1e-6) / 1e9 if sd_us else 0.0,
+                                       "frac": sd_b / (sd_us * 1e-6) / 1e9 / hbm if sd_us else 0.0},
+                "step": {"bytes": step_b, "achieved_gbs": step_b / (ms_per_step * 1e-3) / 1e9,
+                         "frac": step_b / (ms_per_step * 1e-3) / 1e9 / hbm}}
 
     out = {
-        "metric": METRIC, "value": events_per_s, "unit": "events/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if a.config in (2, 3, 4) else "weak",
-        "vs_baseline": None, "dtype": "f32 (int32 fixed-point accumulators)", "data": "synthetic",
+        "metric": METRIC, "value": wall_per_bio, "unit": "wall-s per bio-second", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f32 (int32 fixed-point accumulators)",
+        "data": "synthetic",
         "config": {"workload": f"BASELINE config {a.config}: {rc.name}", "neurons": info["N"],
-                   "synapses": info["S"], "plastic": rc.plastic, "dt_ms": rc.dt_ms, "delay_steps": rc.delay,
+                   "synapses": int(reduce(info["S"], SUM)), "plastic": rc.plastic, "dt_ms": rc.dt_ms,
+                   "delay_steps": rc.delay, "settle_steps": a.settle, "timed_steps_from": pre_steps,
                    "history_bits": a.history_bits, "flush_period": a.flush_period, "plasticity": a.plasticity,
-                   "delivery": a.delivery, "index_bits": 16 if a.idx16 else 32, "slice_width": info["C"], "slices": info["nslices"], "seed": a.seed,
-                   "parallelism": f"target-range partition x{world}, NCCL spike-word all-gather" if world > 1 else "1 GPU",
+                   "delivery": a.delivery, "index_bits": 16 if a.idx16 else 32, "slice_width": info["C"],
+                   "slices": info["nslices"], "seed": a.seed,
+                   "parallelism": f"target-range partition x{world}, NCCL spike-word all-gather" if world > 1
+                   else "1 GPU",
                    "l2": "inputs larger than L2: %.1f GB of graph, each step touches the rows of that step's spikes"
                          % (info["S"] * 8 / 1e9)},
-        "wall_s_per_bio_s": wall_per_bio,
-        "setup_s": setup_s,
+        "events_per_s": events_per_s,
         "setup": {"wall_s": setup_s, "build_ms": build_ms,
                   "synapses_per_ms": info["S"] / build_ms if build_ms > 0 else None,
-                  "note": "GPU construction (Philox-Bernoulli count, scan, fill, plastic spans), device-timed, "
+                  "note": "GPU construction (geometric-skip count, scan, fill, plastic spans), device-timed, "
                           "allocation excluded; the paper quotes ~200M synapses/ms on its GPU (P:391, context)"},
         "rates_hz": rates,
         "per_step": {k.lower(): v / a.steps for k, v in dm.items()},
-        "gpu_launches": a.steps * (3 if rc.plastic else 2),
-        "roofline": {"bound": "hbm", "kernel": dom_kernel,
-                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read + write)",
-                     "traffic_source": traffic_src, "algorithmic_bytes_per_launch": kern[dom]["bytes_per_step"],
-                     "peak_source": peak_src, "kernels": kern,
-                     "stdp_plus_delivery": {"achieved_gbs": sd_bytes / (sd_ms * 1e-3) / 1e9 if sd_ms else 0.0,
-                                            "frac": sd_bytes / (sd_ms * 1e-3) / 1e9 / hbm if sd_ms else 0.0},
-                     "step": {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9,
-                              "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm},
-                     "phase_ms_per_step": {k: ph[k] / psteps for k in ph}, "phase_share": shares,
-                     "deliver_splits": split_group >> 32, "stdp_grid": split_group & 0xffffffff},
+        "gpu_launches": a.steps * (3 if rc.plastic else 2) + (a.steps if world > 1 else 0),
+        "roofline": roof,
+        "kernel_spans": spans,
         "e2e": e2e,
         "clocks": clk.summary(),
     }
     if not a.no_cpu_baseline and rank == 0 and world == 1:
-        r = run_oracle(a.config, a.seed, 2000, 50, budget_s=15.0)
+        r = run_oracle(a.config, a.seed, 1000, 1, budget_s=a.cpu_budget, threads=a.cpu_threads)
         out["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        out["cpu_baseline"]["wall_s_per_bio_s"] = r["wall_s_per_bio_s"]
+        out["cpu_baseline"]["ms_per_step"] = r["ms_per_step"]
     if rank == 0:
         print(json.dumps(out))
     if world > 1:

@@ -32,7 +32,7 @@
  *     NULL = the legacy default stream).
  *   - world > 1: every rank makes the identical call sequence (collective
  *     semantics, like NCCL).  Rank r owns the target-neuron range given by
- *     snn_read_state(SNN_FIELD_PARTITION); see DESIGN.md section 7.
+ *     snn_read_state(SNN_FIELD_INFO) (tgt_lo, tgt_hi); see DESIGN.md section 7.
  */
 #ifndef SNN_H
 #define SNN_H
@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 3u
+#define SNN_ABI_VERSION 4u
 
 typedef struct snn_sim snn_sim; /* opaque; owned by the library */
 typedef int32_t snn_status;
@@ -102,6 +102,10 @@ enum {
                                         SNN_FIELD_TRACE                             */
     SNN_FLAG_NO_PDL = 1u << 3,       /* no programmatic dependent launch between
                                         the kernels of a step                       */
+    SNN_FLAG_KTIME = 1u << 5,        /* kernel spans inside the graph-replayed step:
+                                        every CTA folds %globaltimer marks into its
+                                        step's slot (entry, end of the dependency
+                                        wait, end); read with SNN_FIELD_KTIME      */
     SNN_FLAG_IDX16 = 1u << 4         /* compressed indices:
                                         delivery reads 16-bit slice-local target
                                         offsets (j - slice base) instead of 32-bit
@@ -148,6 +152,11 @@ typedef struct {
                                 of age >= H - K at once (same results: any
                                 schedule with age <= H is exact, R4), so the
                                 flushes stream as one bulk pass               */
+    uint32_t exchange_window;/* world > 1: steps of spike words gathered per
+                                exchange (W; 0 = automatic).  W = 1 when D <= 1;
+                                else 1 <= W <= D - 1, and the exchange of a window
+                                overlaps the next steps' compute (DESIGN.md
+                                section 7)                                      */
 } snn_config;
 
 typedef struct {
@@ -167,8 +176,10 @@ typedef struct {
     uint32_t kind;           /* SNN_SYN_STATIC | SNN_SYN_STDP                     */
     uint32_t receptor;       /* SNN_RCPT_*; LIF_DELTA targets accept only EXC     */
     uint32_t allow_autapses; /* 0: no i -> i synapse (R21)                        */
-    double p;                /* connection probability in [0, 1] (Bernoulli per
-                                ordered pair, Philox, R22/R23)                    */
+    double p;                /* connection probability in [0, 1]: each ordered
+                                pair is a synapse independently with probability
+                                p, realised by exact geometric skipping over
+                                Philox draws (R32)                      */
     float weight;            /* initial weight, FINAL value (caller scales, R10)  */
     float tau_plus_ms, tau_minus_ms; /* STDP trace time constants (R7)            */
     float a_plus, a_minus;   /* STDP amplitudes (additive rule, R7)               */
@@ -185,7 +196,8 @@ enum {
     SNN_FIELD_G_INH = 3,        /* [f32 / n]   CUBA inh current                 */
     SNN_FIELD_INPUT_EXC = 4,    /* [i32 / n]   pending fixed-point input, exc   */
     SNN_FIELD_INPUT_INH = 5,    /* [i32 / n]   pending fixed-point input, inh   */
-    SNN_FIELD_HIST = 6,         /* [u64 / n]   64-bit firing history    */
+    SNN_FIELD_HIST = 6,         /* [u64 / n]   64-bit firing history of
+                                   every neuron, rebuilt from the bitmask ring   */
     SNN_FIELD_SPIKE_COUNT = 7,  /* [u32 / n]   spikes since start               */
     SNN_FIELD_XPOST = 8,        /* [f32 / n]   post-synaptic trace per neuron   */
     SNN_FIELD_XPRE_ROW = 9,     /* [f32 / n]   pre-synaptic trace per source row (after flush) */
@@ -195,7 +207,7 @@ enum {
     SNN_FIELD_WEIGHTS = 13,     /* [f32 / S]   weights, after the read-out flush (R11) */
     SNN_FIELD_PIVOTS = 14,      /* [u32 / N*(nslices+1)] row-relative pivots    */
     SNN_FIELD_STEP = 15,        /* [i64 / 1]   number of steps simulated        */
-    SNN_FIELD_METRICS = 16,     /* [u64 / 8]   see SNN_METRIC_*                 */
+    SNN_FIELD_METRICS = 16,     /* [u64 / 16]  see SNN_METRIC_*                 */
     SNN_FIELD_SPIKE_RING = 17,  /* [u32 / 64*ceil(N/32)] bitmask ring; slot t%64
                                    holds the spikes of step t                    */
     SNN_FIELD_PHASE_TIMES = 18, /* [f64 / 8]  ms per phase (SNN_PHASE_*), summed
@@ -207,7 +219,24 @@ enum {
                                    front / stdp / deliver                        */
     SNN_FIELD_IDX16 = 21,       /* [u16 / S]   slice-local target offsets
                                    (j - tgt_lo) mod C (SNN_FLAG_IDX16 only)      */
-    SNN_FIELD_COUNT = 22
+    SNN_FIELD_HIST_DEV = 22,    /* [u64 / n]   the device history word, bits 0-63
+                                   (bit s: spike at step t - s), that k_stdp
+                                   reads; maintained for neurons post-synaptic
+                                   to STDP (0 elsewhere)                         */
+    SNN_FIELD_HIST_DEV_HI = 23, /* [u64 / n]   bits 64-127 (history_bits = 128)  */
+    SNN_FIELD_FPOS = 24,        /* [u8 / n]    post-plastic neuron whose H-bit
+                                   window is non-empty: bit index of its only
+                                   spike, 0xff if several (stale elsewhere)      */
+    SNN_FIELD_RECENT = 25,      /* [u32 / ceil(N/32)] bit j: post-plastic neuron
+                                   j fired in the last H steps                   */
+    SNN_FIELD_KTIME = 26,       /* [u64 / 16] per kernel k (front, stdp, deliver,
+                                   lists): [4k] sum over steps of (last CTA end -
+                                   first CTA entry) ns, [4k+1] sum of (last end -
+                                   first return from the dependency wait) ns,
+                                   [4k+2] steps, [4k+3] CTAs; cumulative
+                                   (SNN_FLAG_KTIME; read at least every 65,536
+                                   steps)                                       */
+    SNN_FIELD_COUNT = 27
 };
 
 /* SNN_FIELD_METRICS layout (device counters, cumulative over steps) */
@@ -216,10 +245,14 @@ enum {
     SNN_METRIC_SPIKES = 1,       /* arriving spikes (rows delivered)               */
     SNN_METRIC_STDP_ROWS = 2,    /* plastic rows visited (arrivals + flushes)      */
     SNN_METRIC_STDP_SYN = 3,     /* plastic synapses visited                       */
-    SNN_METRIC_STDP_WTOUCH = 4,  /* plastic synapses whose weight was read+written */
+    SNN_METRIC_STDP_WSTORE = 4,  /* plastic synapses whose weight changed (stored) */
     SNN_METRIC_FLUSH_ROWS = 5,   /* rows visited by a forced flush (R3)            */
     SNN_METRIC_SEGMENTS = 6,     /* non-empty (row, slice) segments processed      */
-    SNN_METRIC_ELEMS = 7         /* synapse entries read by the delivery kernel    */
+    SNN_METRIC_ELEMS = 7,        /* synapse entries read by the delivery kernel    */
+    SNN_METRIC_STDP_WRW = 8      /* visited plastic synapses whose weight the method
+                                    must read and write: every
+                                    synapse of an arriving row, and forced-flush
+                                    synapses whose target fired in the window     */
 };
 
 /* SNN_FIELD_PHASE_TIMES layout: the kernels of a step */
@@ -247,10 +280,12 @@ snn_status snn_add_population(snn_sim *sim, uint32_t n, const snn_pop_params *pa
                               uint32_t *pop_id);
 
 /* Declares the projection src_pop -> dst_pop: every ordered pair (i, j) is a
- * synapse with probability p (Philox Bernoulli, R22), one projection per pair
- * of populations.  Errors: SNN_E_INVALID (p outside [0,1], POISSON target,
- * bad receptor, duplicate projection), SNN_E_UNSUPPORTED (second STDP
- * projection from one source population), SNN_E_STATE. */
+ * synapse with probability p (geometric skipping over the counter-based Philox
+ * stream (i, n >> 2, 4, dst_pop), R32), one projection per pair of
+ * populations.  Errors: SNN_E_INVALID (p outside [0,1], POISSON target, bad
+ * receptor, duplicate projection, STDP weight outside [0, w_max]),
+ * SNN_E_UNSUPPORTED (second STDP projection from one source population),
+ * SNN_E_STATE. */
 snn_status snn_connect(snn_sim *sim, uint32_t src_pop, uint32_t dst_pop,
                        const snn_syn_params *params);
 
@@ -271,6 +306,15 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps);
  * SNN_E_STATE (before finalize), SNN_E_CUDA. */
 snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *host_dst,
                           size_t dst_bytes, size_t *needed);
+
+/* Like snn_read_state, for elements [first, first + count) of the field (pop
+ * fields: relative to the population's first neuron; SPIKE_RING: slot-major,
+ * ceil(N/32) words per slot).  Sampled checks of networks with 2^32+ synapses
+ * read a few rows instead of the whole array.  Errors: SNN_E_INVALID (range
+ * outside the field, dst_bytes < count * element size, NULL host_dst), and
+ * those of snn_read_state. */
+snn_status snn_read_state_range(snn_sim *sim, uint32_t field, uint32_t pop_id, uint64_t first, uint64_t count,
+                                void *host_dst, size_t dst_bytes);
 
 /* Releases every device buffer, graph, event and communicator of the handle. */
 void snn_destroy(snn_sim *sim);

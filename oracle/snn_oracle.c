@@ -314,9 +314,13 @@ int oracle_finalize(osim *s)
     if (s->finalized) return -1;
     uint32_t N = s->N;
     s->row_ptr = (int64_t *)calloc((size_t)N + 1, sizeof(int64_t));
-    /* pass 1: row lengths */
+    /* pass 1: row lengths (rows are independent: the threads only share the
+     * read-only tables), then their running sum */
+    #pragma omp parallel for num_threads(s->nthreads) schedule(dynamic, 256)
+    for (int64_t i = 0; i < (int64_t)N; i++)
+        s->row_ptr[i + 1] = oracle_build_row(s, (uint32_t)i, 0, N, NULL, 0);
     for (uint32_t i = 0; i < N; i++)
-        s->row_ptr[i + 1] = s->row_ptr[i] + oracle_build_row(s, i, 0, N, NULL, 0);
+        s->row_ptr[i + 1] += s->row_ptr[i];
     s->nsyn = s->row_ptr[N];
     size_t ns = (size_t)(s->nsyn > 0 ? s->nsyn : 1);
     s->idx = (uint32_t *)malloc(ns * sizeof(uint32_t));
@@ -324,7 +328,9 @@ int oracle_finalize(osim *s)
     s->xpre = (float *)calloc(ns, sizeof(float));
     s->xpost = (float *)calloc(ns, sizeof(float));
     /* pass 2: fill */
-    for (uint32_t i = 0; i < N; i++) {
+    #pragma omp parallel for num_threads(s->nthreads) schedule(dynamic, 256)
+    for (int64_t ii = 0; ii < (int64_t)N; ii++) {
+        uint32_t i = (uint32_t)ii;
         int64_t b = s->row_ptr[i], len = s->row_ptr[i + 1] - b;
         oracle_build_row(s, i, 0, N, s->idx + b, len);
         int sp = pop_of(s, i);

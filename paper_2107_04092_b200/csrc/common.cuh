@@ -86,7 +86,7 @@ struct Counters {
     int64_t t;               // next step to simulate
     uint32_t ticket;         // CTA-completion ticket of the slice kernel
     uint32_t pad;
-    unsigned long long metric[8];
+    unsigned long long metric[16];
     uint32_t lst[2][4];      // by step parity: list lengths (plastic arrivals, arrivals, forced flushes, 0)
     uint32_t rlst[4];        // read-out flush list length
 };
@@ -107,6 +107,8 @@ struct __align__(16) RowDesc {
 constexpr uint32_t kMetaArr = 1u << 11;
 constexpr uint32_t kMetaAge = 0xffu;
 constexpr uint32_t kMetaPlastic = 1u << 10;
+
+struct KSpan;
 
 struct StateDev {
     // neurons (indexed by global id)
@@ -140,7 +142,47 @@ struct StateDev {
     Counters *ctr;
     const StdpDev *stdp;     // device copy of NetDev::stdp (coalesced table loads into shared memory)
     unsigned long long *trace;   // optional (SNN_FLAG_TRACE): per-CTA phase timestamps
+    struct KSpan *kspan;         // optional (SNN_FLAG_KTIME): per-step kernel spans, [slot][kernel]
 };
+
+// Kernel spans of the graph-replayed step (SNN_FLAG_KTIME): thread 0 of every
+// CTA folds its %globaltimer marks into the slot of its step t and kernel k --
+// earliest CTA entry, earliest return from the kernel's dependency wait (PDL
+// griddepcontrol.wait: the start of its exposed part), latest CTA end.  The
+// host folds the slots into per-kernel averages (snn_read_state(KTIME)).
+struct KSpan {
+    unsigned long long entry, wait, end, ctas;
+};
+constexpr uint32_t kKSpanSlots = 65536;   // steps between two read-outs
+constexpr int kKSpanKernels = 4;          // front, stdp, deliver, lists (world > 1, D = 0)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long g = 0;
+#ifdef __CUDA_ARCH__
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+#endif
+    return g;
+}
+__device__ __forceinline__ void kspan_begin(KSpan *ks, int64_t t, int k, unsigned long long t_entry,
+                                            unsigned long long t_wait) {
+#ifdef __CUDA_ARCH__
+    if (ks && threadIdx.x == 0) {
+        KSpan &s = ks[(size_t)(t & (kKSpanSlots - 1)) * kKSpanKernels + k];
+        atomicMin(&s.entry, t_entry);
+        atomicMin(&s.wait, t_wait);
+        atomicAdd(&s.ctas, 1ull);
+    }
+#endif
+}
+// (uniform in the launch: every thread calls it; the barrier makes thread 0's
+// mark the CTA's end)
+__device__ __forceinline__ void kspan_end(KSpan *ks, int64_t t, int k) {
+#ifdef __CUDA_ARCH__
+    if (ks) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(&ks[(size_t)(t & (kKSpanSlots - 1)) * kKSpanKernels + k].end, gtimer());
+    }
+#endif
+}
 
 // Phase trace (debug, SNN_FLAG_TRACE): thread 0 of each CTA stores %globaltimer
 // at phase boundaries: trace[(kernel * kTraceCtas + cta) * 4 + phase].

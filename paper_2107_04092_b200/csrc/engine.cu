@@ -30,7 +30,8 @@ uint32_t front_blocks(const NetDev &);
 cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool);
 size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
 size_t deliver_smem_bytes(const NetDev &);
-cudaError_t kernels_configure(const NetDev &, uint32_t, uint32_t);
+cudaError_t kernels_configure(int);
+cudaError_t launch_kspan_reset(KSpan *, cudaStream_t);
 cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
 cudaError_t launch_deliver_rowwise(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
@@ -112,6 +113,10 @@ struct snn_sim {
     uint32_t pp_lo = 0, pp_hi = 0;       // post-plastic neuron range (bitmap span)
     bool plastic = false;
     uint64_t *d_hist_tmp = nullptr;
+    // kernel spans (SNN_FLAG_KTIME): device slots, host totals per kernel:
+    // [sum(end - entry) ns, sum(end - wait) ns, steps, CTAs]
+    KSpan *kspan = nullptr;
+    unsigned long long ks_tot[kKSpanKernels][4] = {{0}};
     // exchange (world > 1)
     uint32_t wmax = 0;
     ncclComm_t comm = nullptr;
@@ -160,6 +165,25 @@ struct snn_sim {
         if (!ptr) return sim->fail(SNN_E_OOM, "device allocation of %zu bytes failed",     \
                                    sizeof(type) * (size_t)(count));                        \
     } while (0)
+
+// Every entry point runs on the handle's device and restores the caller's
+// current device on return.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != dev) {
+            err = cudaSetDevice(dev);
+            if (err == cudaSuccess) prev = cur;
+        } else {
+            cudaGetLastError();
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 static uint64_t bernoulli_thr(double p) {
     if (!(p > 0.0)) return 0;
@@ -397,6 +421,12 @@ static snn_status finalize(snn_sim *sim) {
         CK(cudaMemsetAsync(st.trace, 0, 8ull * kTraceKernels * kTraceCtas * 4, sim->stream));
     }
     ALLOC(st.ctr, Counters, 1);
+    st.kspan = nullptr;
+    if (cfg.flags & SNN_FLAG_KTIME) {
+        ALLOC(st.kspan, KSpan, (size_t)kKSpanSlots * kKSpanKernels);
+        CK(launch_kspan_reset(st.kspan, sim->stream));
+        sim->kspan = st.kspan;
+    }
     cudaStream_t s = sim->stream;
     CK(cudaMemsetAsync(st.ring, 0, sizeof(uint32_t) * (size_t)kRingSlots * net.ring_stride, s));
     if (cfg.world > 1) {
@@ -481,9 +511,12 @@ static snn_status finalize(snn_sim *sim) {
         return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory", C, deliver_smem_bytes(net));
     if (sim->plastic && stdp_smem_bytes(net, sim->pp_lo, sim->pp_hi) > 227 * 1024)
         return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for the shared bitmap");
-    if (sim->plastic && net.N >= (1u << 23) - 8)   // k_stdp queue entries hold a 23-bit row offset
-        return sim->fail(SNN_E_UNSUPPORTED, "STDP rows longer than 2^23 - 8 synapses");
-    CK(kernels_configure(net, sim->pp_lo, sim->pp_hi));
+    // k_stdp flattens up to 128 rows' plastic spans (16-byte chunks) per round
+    // into one uint32 chunk index
+    if (sim->plastic && 128ull * ((uint64_t)net.N / 4 + 2) >= (1ull << 32))
+        return sim->fail(SNN_E_UNSUPPORTED, "STDP with N = %u: a round of 128 plastic spans may exceed 2^32 chunks",
+                         net.N);
+    CK(kernels_configure(cfg.device));
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg.device);
     const uint32_t ns = std::max(1u, net.nslices);
@@ -584,11 +617,12 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         g_create_error = "world > 1 needs an nccl_unique_id or a local group_key";
         return SNN_E_INVALID;
     }
-    cudaError_t e = cudaSetDevice(cfg->device);
-    if (e != cudaSuccess) {
-        g_create_error = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+    DeviceGuard dg(cfg->device);
+    if (dg.err != cudaSuccess) {
+        g_create_error = std::string("cudaSetDevice: ") + cudaGetErrorString(dg.err);
         return SNN_E_CUDA;
     }
+    cudaError_t e = cudaSuccess;
     snn_sim *sim = new snn_sim();
     sim->cfg = *cfg;
     sim->stream = (cudaStream_t)cfg->stream;
@@ -659,8 +693,9 @@ snn_status snn_connect(snn_sim *sim, uint32_t src, uint32_t dst, const snn_syn_p
             return sim->fail(SNN_E_UNSUPPORTED, "one STDP projection per source population");
     }
     if (q->kind == SNN_SYN_STDP &&
-        !(q->tau_plus_ms > 0.0f && q->tau_minus_ms > 0.0f && q->w_max >= 0.0f && q->weight >= 0.0f))
-        return sim->fail(SNN_E_INVALID, "STDP needs tau_+, tau_- > 0 and 0 <= weight, w_max");
+        !(q->tau_plus_ms > 0.0f && q->tau_minus_ms > 0.0f && q->w_max >= 0.0f && q->weight >= 0.0f &&
+          q->weight <= q->w_max))
+        return sim->fail(SNN_E_INVALID, "STDP needs tau_+, tau_- > 0 and 0 <= weight <= w_max");
     HostProj hj;
     hj.src = src;
     hj.dst = dst;
@@ -672,6 +707,8 @@ snn_status snn_connect(snn_sim *sim, uint32_t src, uint32_t dst, const snn_syn_p
 snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
     if (!sim) return SNN_E_INVALID;
     sim->err.clear();
+    DeviceGuard dg(sim->cfg.device);
+    if (dg.err != cudaSuccess) return sim->fail(SNN_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(dg.err));
     if (sim->state == 0) {
         snn_status r = finalize(sim);
         if (r != SNN_OK) return r;
@@ -717,10 +754,40 @@ static snn_status readout_flush(snn_sim *sim) {
     return SNN_OK;
 }
 
-snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *host_dst, size_t dst_bytes,
-                          size_t *needed) {
-    if (!sim) return SNN_E_INVALID;
-    sim->err.clear();
+// A read-out source: a device or host array of `bytes` bytes, `elem` bytes per
+// element.  prepare = the copy is about to happen: run the field's side effects
+// (read-out flush R11, remote words of the last step, history reconstruction,
+// folding of timing records).
+struct FieldRef {
+    const void *dev = nullptr;
+    const void *host = nullptr;
+    size_t bytes = 0, elem = 1;
+    bool ring = false;   // SPIKE_RING: rows of nwords words, device stride ring_stride
+    int64_t host_i64[8];
+    unsigned long long host_u64[16];
+    double host_f64[8];
+};
+
+static snn_status fold_ktime(snn_sim *sim) {
+    if (!sim->kspan) return SNN_OK;
+    const size_t n = (size_t)kKSpanSlots * kKSpanKernels;
+    std::vector<KSpan> h(n);
+    CK(cudaMemcpyAsync(h.data(), sim->kspan, n * sizeof(KSpan), cudaMemcpyDeviceToHost, sim->stream));
+    CK(cudaStreamSynchronize(sim->stream));
+    for (size_t x = 0; x < n; x++) {
+        const KSpan &k = h[x];
+        if (k.ctas == 0 || k.end == 0 || k.entry == ~0ull || k.wait == ~0ull) continue;
+        unsigned long long *tot = sim->ks_tot[x % kKSpanKernels];
+        tot[0] += k.end > k.entry ? k.end - k.entry : 0ull;
+        tot[1] += k.end > k.wait ? k.end - k.wait : 0ull;
+        tot[2] += 1ull;
+        tot[3] += k.ctas;
+    }
+    CK(launch_kspan_reset(sim->kspan, sim->stream));
+    return SNN_OK;
+}
+
+static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool prepare, FieldRef &f) {
     if (field >= SNN_FIELD_COUNT) return sim->fail(SNN_E_INVALID, "unknown field %u", field);
     if (sim->state == 0 && field != SNN_FIELD_STEP) return sim->fail(SNN_E_STATE, "read_state before finalize");
     const NetDev &net = sim->net;
@@ -731,49 +798,57 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
         base = sim->pops[pop_id].base;
         n = sim->pops[pop_id].n;
     }
-    const void *src = nullptr;
-    size_t bytes = 0;
-    int64_t host_i64[8];
-    unsigned long long host_u64[8];
-    double host_f64[8];
-    const void *host_src = nullptr;
-    switch (field) {
-    case SNN_FIELD_V: src = st.V + base; bytes = 4ull * n; break;
-    case SNN_FIELD_REFRACTORY: src = st.ref + base; bytes = 4ull * n; break;
-    case SNN_FIELD_G_EXC: src = st.ge + base; bytes = 4ull * n; break;
-    case SNN_FIELD_G_INH: src = st.gi + base; bytes = 4ull * n; break;
-    case SNN_FIELD_INPUT_EXC: src = st.in_e + base; bytes = 4ull * n; break;
-    case SNN_FIELD_INPUT_INH: src = st.in_i + base; bytes = 4ull * n; break;
-    case SNN_FIELD_SPIKE_COUNT: src = st.nspk + base; bytes = 4ull * n; break;
-    case SNN_FIELD_XPOST: src = st.xpost + base; bytes = 4ull * n; break;
-    case SNN_FIELD_XPRE_ROW: src = st.xpre + base; bytes = 4ull * n; break;
-    case SNN_FIELD_TLU: src = st.tlu + base; bytes = 4ull * n; break;
-    case SNN_FIELD_HIST: bytes = 8ull * n; break;
-    case SNN_FIELD_ROW_PTR: src = st.row_ptr; bytes = 8ull * (sim->N + 1); break;
-    case SNN_FIELD_IDX: src = st.idx; bytes = 4ull * sim->nsyn; break;
-    case SNN_FIELD_IDX16:
-        if (!st.idx16) return sim->fail(SNN_E_STATE, "IDX16 needs SNN_FLAG_IDX16");
-        src = st.idx16; bytes = 2ull * sim->nsyn; break;
-    case SNN_FIELD_WEIGHTS: src = st.w; bytes = 4ull * sim->nsyn; break;
-    case SNN_FIELD_PIVOTS: src = st.piv; bytes = 4ull * sim->N * (net.nslices + 1); break;
-    case SNN_FIELD_SPIKE_RING: src = st.ring; bytes = 4ull * kRingSlots * net.nwords; break;
-    case SNN_FIELD_STEP: host_i64[0] = sim->t; host_src = host_i64; bytes = 8; break;
-    case SNN_FIELD_METRICS: src = st.ctr->metric; bytes = 8 * 8; break;
-    case SNN_FIELD_PHASE_TIMES: bytes = 8 * 8; break;
-    case SNN_FIELD_TRACE:
-        if (!st.trace) return sim->fail(SNN_E_STATE, "trace needs SNN_FLAG_TRACE");
-        src = st.trace; bytes = 8ull * kTraceKernels * kTraceCtas * 4; break;
-    case SNN_FIELD_INFO:
-        host_i64[0] = sim->N; host_i64[1] = sim->nsyn; host_i64[2] = net.nslices; host_i64[3] = net.C;
-        host_i64[4] = net.R; host_i64[5] = net.tgt_lo; host_i64[6] = net.tgt_hi;
-        host_i64[7] = ((int64_t)sim->splits << 32) | sim->stdp_grid;
-        host_src = host_i64; bytes = 64; break;
-    default: return sim->fail(SNN_E_INVALID, "unknown field %u", field);
-    }
-    if (needed) *needed = bytes;
-    if (!host_dst) return SNN_OK;
-    if (dst_bytes < bytes) return sim->fail(SNN_E_INVALID, "buffer of %zu bytes < %zu needed", dst_bytes, bytes);
     cudaStream_t s = sim->stream;
+    switch (field) {
+    case SNN_FIELD_V: f.dev = st.V + base; f.elem = 4; break;
+    case SNN_FIELD_REFRACTORY: f.dev = st.ref + base; f.elem = 4; break;
+    case SNN_FIELD_G_EXC: f.dev = st.ge + base; f.elem = 4; break;
+    case SNN_FIELD_G_INH: f.dev = st.gi + base; f.elem = 4; break;
+    case SNN_FIELD_INPUT_EXC: f.dev = st.in_e + base; f.elem = 4; break;
+    case SNN_FIELD_INPUT_INH: f.dev = st.in_i + base; f.elem = 4; break;
+    case SNN_FIELD_SPIKE_COUNT: f.dev = st.nspk + base; f.elem = 4; break;
+    case SNN_FIELD_XPOST: f.dev = st.xpost + base; f.elem = 4; break;
+    case SNN_FIELD_XPRE_ROW: f.dev = st.xpre + base; f.elem = 4; break;
+    case SNN_FIELD_TLU: f.dev = st.tlu + base; f.elem = 4; break;
+    case SNN_FIELD_HIST: f.elem = 8; break;
+    case SNN_FIELD_HIST_DEV: f.dev = st.hist + base; f.elem = 8; break;
+    case SNN_FIELD_HIST_DEV_HI:
+        if (net.H <= 64) return sim->fail(SNN_E_STATE, "HIST_DEV_HI needs history_bits = 128");
+        f.dev = st.hist_hi + base; f.elem = 8; break;
+    case SNN_FIELD_FPOS: f.dev = st.fpos + base; f.elem = 1; break;
+    default: break;
+    }
+    if (f.elem > 1 || field == SNN_FIELD_FPOS) {
+        f.bytes = f.elem * n;
+    } else {
+        switch (field) {
+        case SNN_FIELD_ROW_PTR: f.dev = st.row_ptr; f.elem = 8; f.bytes = 8ull * (sim->N + 1); break;
+        case SNN_FIELD_IDX: f.dev = st.idx; f.elem = 4; f.bytes = 4ull * sim->nsyn; break;
+        case SNN_FIELD_IDX16:
+            if (!st.idx16) return sim->fail(SNN_E_STATE, "IDX16 needs SNN_FLAG_IDX16");
+            f.dev = st.idx16; f.elem = 2; f.bytes = 2ull * sim->nsyn; break;
+        case SNN_FIELD_WEIGHTS: f.dev = st.w; f.elem = 4; f.bytes = 4ull * sim->nsyn; break;
+        case SNN_FIELD_PIVOTS: f.dev = st.piv; f.elem = 4; f.bytes = 4ull * sim->N * (net.nslices + 1); break;
+        case SNN_FIELD_SPIKE_RING: f.dev = st.ring; f.elem = 4; f.bytes = 4ull * kRingSlots * net.nwords; f.ring = true; break;
+        case SNN_FIELD_RECENT: f.dev = st.recent; f.elem = 4; f.bytes = 4ull * net.nwords; break;
+        case SNN_FIELD_STEP: f.host_i64[0] = sim->t; f.host = f.host_i64; f.elem = 8; f.bytes = 8; break;
+        case SNN_FIELD_METRICS: f.dev = st.ctr->metric; f.elem = 8; f.bytes = 8 * 16; break;
+        case SNN_FIELD_PHASE_TIMES: f.host = f.host_f64; f.elem = 8; f.bytes = 8 * 8; break;
+        case SNN_FIELD_KTIME:
+            if (!sim->kspan) return sim->fail(SNN_E_STATE, "KTIME needs SNN_FLAG_KTIME");
+            f.host = f.host_u64; f.elem = 8; f.bytes = 8 * 16; break;
+        case SNN_FIELD_TRACE:
+            if (!st.trace) return sim->fail(SNN_E_STATE, "trace needs SNN_FLAG_TRACE");
+            f.dev = st.trace; f.elem = 8; f.bytes = 8ull * kTraceKernels * kTraceCtas * 4; break;
+        case SNN_FIELD_INFO:
+            f.host_i64[0] = sim->N; f.host_i64[1] = sim->nsyn; f.host_i64[2] = net.nslices; f.host_i64[3] = net.C;
+            f.host_i64[4] = net.R; f.host_i64[5] = net.tgt_lo; f.host_i64[6] = net.tgt_hi;
+            f.host_i64[7] = ((int64_t)sim->splits << 32) | sim->stdp_grid;
+            f.host = f.host_i64; f.elem = 8; f.bytes = 64; break;
+        default: return sim->fail(SNN_E_INVALID, "unknown field %u", field);
+        }
+    }
+    if (!prepare) return SNN_OK;
     if (field == SNN_FIELD_WEIGHTS || field == SNN_FIELD_XPRE_ROW || field == SNN_FIELD_TLU) {
         snn_status r = readout_flush(sim);
         if (r != SNN_OK) return r;
@@ -781,19 +856,19 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
     if (sim->local_group && sim->t > 0 && (field == SNN_FIELD_HIST || field == SNN_FIELD_SPIKE_RING))
         CK(launch_unpack(net, st, st.gath + (size_t)((sim->t - 1) & 1) * sim->cfg.world * sim->wmax, sim->t - 1,
                          s));                                      // the last step's remote words
-    if (field == SNN_FIELD_SPIKE_RING && net.ring_stride != net.nwords) {
-        CK(cudaMemcpy2DAsync(host_dst, 4ull * net.nwords, st.ring, 4ull * net.ring_stride, 4ull * net.nwords,
-                             kRingSlots, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        return SNN_OK;
-    }
     if (field == SNN_FIELD_HIST) {
         if (!sim->d_hist_tmp) {
             sim->d_hist_tmp = (uint64_t *)sim->dalloc(8ull * sim->N);
             if (!sim->d_hist_tmp) return sim->fail(SNN_E_OOM, "hist scratch");
         }
         CK(launch_hist_from_ring(net, st.ring, sim->t - 1, sim->d_hist_tmp, s));
-        src = sim->d_hist_tmp + base;
+        f.dev = sim->d_hist_tmp + base;
+    }
+    if (field == SNN_FIELD_KTIME) {
+        snn_status r = fold_ktime(sim);
+        if (r != SNN_OK) return r;
+        for (int k = 0; k < kKSpanKernels; k++)
+            for (int q = 0; q < 4; q++) f.host_u64[4 * k + q] = sim->ks_tot[k][q];
     }
     if (field == SNN_FIELD_PHASE_TIMES) {
         CK(cudaStreamSynchronize(s));
@@ -806,17 +881,70 @@ snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *h
             sim->phase_ms[SNN_PHASE_TOTAL] += ms[0] + ms[1] + ms[2];
         }
         sim->ev_used = 0;
-        for (int k = 0; k < 8; k++) host_f64[k] = sim->phase_ms[k];
-        host_src = host_f64;
+        for (int k = 0; k < 8; k++) f.host_f64[k] = sim->phase_ms[k];
     }
-    (void)host_u64;
-    if (host_src) {
-        memcpy(host_dst, host_src, bytes);
+    return SNN_OK;
+}
+
+// Copies elements [first, first + count) of f into host_dst.
+static snn_status copy_out(snn_sim *sim, const FieldRef &f, size_t first, size_t count, void *host_dst) {
+    const size_t off = first * f.elem, bytes = count * f.elem;
+    if (bytes == 0) return SNN_OK;
+    if (f.host) {
+        memcpy(host_dst, (const char *)f.host + off, bytes);
         return SNN_OK;
     }
-    if (bytes) CK(cudaMemcpyAsync(host_dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    cudaStream_t s = sim->stream;
+    const NetDev &net = sim->net;
+    if (f.ring && net.ring_stride != net.nwords) {     // slots padded for the exchange: row by row
+        size_t e = first, done = 0;
+        while (done < count) {
+            const size_t slot = e / net.nwords, w = e % net.nwords;
+            const size_t take = std::min(count - done, (size_t)net.nwords - w);
+            CK(cudaMemcpyAsync((char *)host_dst + 4 * done, sim->st.ring + slot * net.ring_stride + w, 4 * take,
+                               cudaMemcpyDeviceToHost, s));
+            done += take;
+            e += take;
+        }
+    } else {
+        CK(cudaMemcpyAsync(host_dst, (const char *)f.dev + off, bytes, cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaStreamSynchronize(s));
     return SNN_OK;
+}
+
+snn_status snn_read_state(snn_sim *sim, uint32_t field, uint32_t pop_id, void *host_dst, size_t dst_bytes,
+                          size_t *needed) {
+    if (!sim) return SNN_E_INVALID;
+    sim->err.clear();
+    DeviceGuard dg(sim->cfg.device);
+    FieldRef f;
+    snn_status r = field_ref(sim, field, pop_id, false, f);
+    if (r != SNN_OK) return r;
+    if (needed) *needed = f.bytes;
+    if (!host_dst) return SNN_OK;
+    if (dst_bytes < f.bytes) return sim->fail(SNN_E_INVALID, "buffer of %zu bytes < %zu needed", dst_bytes, f.bytes);
+    if ((r = field_ref(sim, field, pop_id, true, f)) != SNN_OK) return r;
+    return copy_out(sim, f, 0, f.bytes / f.elem, host_dst);
+}
+
+snn_status snn_read_state_range(snn_sim *sim, uint32_t field, uint32_t pop_id, uint64_t first, uint64_t count,
+                                void *host_dst, size_t dst_bytes) {
+    if (!sim) return SNN_E_INVALID;
+    sim->err.clear();
+    DeviceGuard dg(sim->cfg.device);
+    FieldRef f;
+    snn_status r = field_ref(sim, field, pop_id, false, f);
+    if (r != SNN_OK) return r;
+    const uint64_t nel = f.bytes / f.elem;
+    if (first > nel || count > nel - first)
+        return sim->fail(SNN_E_INVALID, "range [%llu, +%llu) outside the field's %llu elements",
+                         (unsigned long long)first, (unsigned long long)count, (unsigned long long)nel);
+    if (!host_dst || dst_bytes < count * f.elem)
+        return sim->fail(SNN_E_INVALID, "buffer of %zu bytes < %llu needed", dst_bytes,
+                         (unsigned long long)(count * f.elem));
+    if ((r = field_ref(sim, field, pop_id, true, f)) != SNN_OK) return r;
+    return copy_out(sim, f, first, count, host_dst);
 }
 
 snn_status snn_partition(uint32_t n_targets, uint32_t slice_width, uint32_t world, uint32_t rank, uint32_t *lo,
@@ -831,6 +959,7 @@ snn_status snn_partition(uint32_t n_targets, uint32_t slice_width, uint32_t worl
 
 void snn_destroy(snn_sim *sim) {
     if (!sim) return;
+    DeviceGuard dg(sim->cfg.device);
     if (sim->cfg.world > 1 && !sim->cfg.nccl_unique_id) {
         std::lock_guard<std::mutex> lk(g_mu);
         std::vector<snn_sim *> &g = g_groups[sim->cfg.group_key];

@@ -1,6 +1,6 @@
 // philox.cuh -- Philox4x32-10 (Salmon et al., SC'11), device side.
 // The counter-based generator named by BASELINE.json north_star; counter layout
-// of DESIGN.md R22 (connectivity (i, jl>>2, 1, dst_pop); Poisson (i, t, 2, 0);
+// of DESIGN.md R22 / R32 (connectivity gaps (i, n>>2, 4, dst_pop); Poisson (i, t, 2, 0);
 // initial V (i, 0, 3, 0)).  Written independently of oracle/ (no shared code).
 #pragma once
 #include <cstdint>

@@ -23,6 +23,9 @@
 //
 // Floating point: every fp32 op is an explicit __f*_rn intrinsic, so there is no
 // FMA contraction (R19); accumulators are int32 fixed point (R18).
+#include <mutex>
+#include <set>
+
 #include "common.cuh"
 #include "philox.cuh"
 
@@ -107,10 +110,12 @@ __device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *lens, bool a, b
 __global__ void __launch_bounds__(kFrontThreads)
 k_front(NetDev net, StateDev st) {
     __shared__ Compact2 cs;
+    const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
     pdl_wait();            // k_deliver(t-1): inputs, step counter
     pdl_launch();
     trace_mark(st.trace, 0, 0);
     const int64_t t = st.ctr->t;
+    if (st.kspan) kspan_begin(st.kspan, t, 0, t_entry, gtimer());
     const uint32_t par = (uint32_t)(t & 1);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t lane = threadIdx.x & 31;
@@ -278,6 +283,7 @@ k_front(NetDev net, StateDev st) {
         if (nf) atomicAdd(&st.ctr->metric[5], (unsigned long long)nf);
     }
     trace_mark(st.trace, 0, 3);
+    kspan_end(st.kspan, t, 0);
 }
 
 // ---------------------------------------------------- CTA row-table helpers
@@ -490,6 +496,7 @@ template <bool kLazy, bool kH128, bool kGeneric>
 __global__ void __launch_bounds__(kStdpThreads, 1)
 k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
     StdpSmem &sm = *reinterpret_cast<StdpSmem *>(smem);
     unsigned char *stage_base = smem + ((sizeof(StdpSmem) + 127) & ~(size_t)127);   // [stages][ids 8K | w 8K]
     uint32_t *recent_s = reinterpret_cast<uint32_t *>(stage_base + (size_t)kStdpStages * kStdpStageCh * 32);  // bitmap
@@ -519,6 +526,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     pdl_wait();            // k_front(t): lists, histories, bitmap
     pdl_launch();          // k_deliver may start its tabulation (k_front is complete)
     if (!readout) trace_mark(st.trace, 1, 0);
+    if (!readout && st.kspan) kspan_begin(st.kspan, t, 1, t_entry, gtimer());
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Vl = readout ? st.rdesc : st.vdesc[par];
     const uint32_t *lens = readout ? st.ctr->rlst : st.ctr->lst[par];
@@ -541,7 +549,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     const uint32_t rs_addr = smem_u32(recent_s) - 4u * w_lo;     // bitmap word of neuron j: + 4 (j >> 5)
     const uint32_t dp_addr = smem_u32(sm.dplus);
     if (!readout) trace_mark(st.trace, 1, 1);
-    uint32_t n_syn = 0, n_w = 0;
+    uint32_t n_syn = 0, n_w = 0, n_rw = 0;
     uint32_t g0 = 0;             // global stage index of the round's first stage (ring position)
     bool bm_ready = false;
     const uint64_t *__restrict__ ghist = st.hist;
@@ -667,6 +675,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         slots |= o << (8 * u);
                     }
                 }
+                n_rw += __popc(am) + __popc(hm);     // 8(d): weights read + written (arrival / window hit)
                 // ---- arrivals (every synapse: history window + depression, Fig. 2c):
                 //      in place, two chunks (8 synapses) of gathers in flight per lane
                 if (__any_sync(0xffffffffu, am != 0u)) {
@@ -832,13 +841,16 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     if (threadIdx.x == 0 && !bm_ready) mbar_wait(bmap_a, 0);   // (no rows) the bitmap copy has landed
     n_syn = __reduce_add_sync(0xffffffffu, n_syn);
     n_w = __reduce_add_sync(0xffffffffu, n_w);
+    n_rw = __reduce_add_sync(0xffffffffu, n_rw);
     if (lane == 0) {
         if (n_syn) atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
         if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
+        if (n_rw) atomicAdd(&st.ctr->metric[8], (unsigned long long)n_rw);
     }
     if (!readout) {
         __syncthreads();
         trace_mark(st.trace, 1, 3);
+        kspan_end(st.kspan, t, 1);
     }
 }
 
@@ -997,6 +1009,8 @@ k_deliver(NetDev net, StateDev st) {
     const uint32_t shi = min(slo + C, net.tgt_hi);
     const uint32_t width = shi > slo ? shi - slo : 0u;
     const uint32_t lane = threadIdx.x & 31;
+    const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
+    unsigned long long t_wait = 0ull;
     trace_mark(st.trace, 2, 0);
 
     // prologue: reads only k_front(t)'s lists -- complete before k_stdp(t)
@@ -1090,6 +1104,7 @@ k_deliver(NetDev net, StateDev st) {
             if (r0 == r_begin && w0 == 0) {   // (the segment tables and the bitmap are ready)
                 pdl_wait();    // k_stdp(t): updated weights of plastic arrivals
                 pdl_launch();
+                if (st.kspan) t_wait = gtimer();
                 trace_mark(st.trace, 2, 1);
             }
             // ---- elements: thread x takes w0 + x + 512 u (coalesced)
@@ -1118,9 +1133,11 @@ k_deliver(NetDev net, StateDev st) {
     }
     pdl_wait();            // (no segments) this grid still completes after k_stdp(t)
     pdl_launch();
+    if (st.kspan) kspan_begin(st.kspan, t, 2, t_entry, t_wait ? t_wait : gtimer());
     // ---- step completion: the last CTA advances t
     __syncthreads();
     trace_mark(st.trace, 2, 3);
+    kspan_end(st.kspan, t, 2);
     // (no fence: nothing the last CTA does depends on the other CTAs' writes,
     // and k_front(t+1) reads them after this grid completes)
     if (threadIdx.x == 0) {
@@ -1305,20 +1322,33 @@ size_t deliver_smem_bytes(const NetDev &net) {
     return 4ull * net.nrcpt * net.C;
 }
 
-cudaError_t kernels_configure(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
-    cudaError_t e = cudaSuccess;
+// The dynamic shared-memory limit is an attribute of the kernel function, not
+// of a handle: set it once per device to the opt-in maximum (minus the
+// kernel's static shared memory), so no handle can lower it under another.
+cudaError_t kernels_configure(int device) {
+    static std::mutex mu;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(device)) return cudaSuccess;
+    int optin = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (e != cudaSuccess) return e;
+    auto set_max = [&](const void *k) -> cudaError_t {
+        cudaFuncAttributes a;
+        cudaError_t r = cudaFuncGetAttributes(&a, k);
+        if (r != cudaSuccess) return r;
+        return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+    };
     void (*kd[4])(NetDev, StateDev) = {k_deliver<false, false>, k_deliver<false, true>, k_deliver<true, false>,
                                        k_deliver<true, true>};
     for (auto k : kd)
-        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)deliver_smem_bytes(net))) !=
-            cudaSuccess)
-            return e;
-    const int sm = (int)stdp_smem_bytes(net, pp_lo, pp_hi);
+        if ((e = set_max((const void *)k)) != cudaSuccess) return e;
     void (*ks[6])(NetDev, StateDev, int64_t, uint32_t, uint32_t) = {
         k_stdp<false, false, false>, k_stdp<false, true, false>, k_stdp<false, false, true>,
         k_stdp<false, true, true>, k_stdp<true, false, true>, k_stdp<true, true, true>};
     for (auto k : ks)
-        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) != cudaSuccess) return e;
+        if ((e = set_max((const void *)k)) != cudaSuccess) return e;
+    done.insert(device);
     return cudaSuccess;
 }
 
@@ -1355,6 +1385,18 @@ cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last
     if (e != cudaSuccess) return e;
     if ((e = launch_stdp(net, st, t_last, grid, pp_lo, pp_hi, s, false)) != cudaSuccess) return e;
     k_readout_finish<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
+    return cudaGetLastError();
+}
+
+// SNN_FLAG_KTIME: every slot back to (entry, wait) = +inf, (end, ctas) = 0.
+__global__ void k_kspan_reset(KSpan *ks, uint32_t n) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+        ks[x] = KSpan{~0ull, ~0ull, 0ull, 0ull};
+}
+
+cudaError_t launch_kspan_reset(KSpan *ks, cudaStream_t s) {
+    const uint32_t n = kKSpanSlots * kKSpanKernels;
+    k_kspan_reset<<<256, 256, 0, s>>>(ks, n);
     return cudaGetLastError();
 }
 

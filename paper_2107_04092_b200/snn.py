@@ -22,26 +22,30 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- constants
-SNN_ABI_VERSION = 3
+SNN_ABI_VERSION = 4
 SNN_OK, SNN_E_INVALID, SNN_E_STATE, SNN_E_OOM, SNN_E_CUDA, SNN_E_NCCL, SNN_E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 POISSON, LIF_DELTA, LIF_CUBA = 0, 1, 2
 STATIC, STDP = 0, 1
 EXC, INH = 0, 1
-FLAG_NO_GRAPH, FLAG_PHASE_TIMING, FLAG_TRACE, FLAG_NO_PDL, FLAG_IDX16 = 1, 2, 4, 8, 16
+FLAG_NO_GRAPH, FLAG_PHASE_TIMING, FLAG_TRACE, FLAG_NO_PDL, FLAG_IDX16, FLAG_KTIME = 1, 2, 4, 8, 16, 32
 PLAST_EVENT, PLAST_LAZY, PLAST_NAIVE = 0, 1, 2        # Fig. 2c / 2b / 2a schedules
 DELIV_SLICED, DELIV_ROWWISE = 0, 1                    # Fig. 3b / 3a delivery
 ALL = 0xFFFFFFFF
 
 FIELD = dict(V=0, REFRACTORY=1, G_EXC=2, G_INH=3, INPUT_EXC=4, INPUT_INH=5, HIST=6, SPIKE_COUNT=7,
              XPOST=8, XPRE_ROW=9, TLU=10, ROW_PTR=11, IDX=12, WEIGHTS=13, PIVOTS=14, STEP=15,
-             METRICS=16, SPIKE_RING=17, PHASE_TIMES=18, INFO=19, TRACE=20, IDX16=21)
+             METRICS=16, SPIKE_RING=17, PHASE_TIMES=18, INFO=19, TRACE=20, IDX16=21, HIST_DEV=22,
+             HIST_DEV_HI=23, FPOS=24, RECENT=25, KTIME=26)
 FIELD_DTYPE = dict(V=np.float32, REFRACTORY=np.int32, G_EXC=np.float32, G_INH=np.float32,
                    INPUT_EXC=np.int32, INPUT_INH=np.int32, HIST=np.uint64, SPIKE_COUNT=np.uint32,
                    XPOST=np.float32, XPRE_ROW=np.float32, TLU=np.int32, ROW_PTR=np.int64,
                    IDX=np.uint32, WEIGHTS=np.float32, PIVOTS=np.uint32, STEP=np.int64,
                    METRICS=np.uint64, SPIKE_RING=np.uint32, PHASE_TIMES=np.float64, INFO=np.int64,
-                   TRACE=np.uint64, IDX16=np.uint16)
-METRIC = dict(EVENTS=0, SPIKES=1, STDP_ROWS=2, STDP_SYN=3, STDP_WTOUCH=4, FLUSH_ROWS=5, SEGMENTS=6, ELEMS=7)
+                   TRACE=np.uint64, IDX16=np.uint16, HIST_DEV=np.uint64, HIST_DEV_HI=np.uint64,
+                   FPOS=np.uint8, RECENT=np.uint32, KTIME=np.uint64)
+METRIC = dict(EVENTS=0, SPIKES=1, STDP_ROWS=2, STDP_SYN=3, STDP_WSTORE=4, FLUSH_ROWS=5, SEGMENTS=6, ELEMS=7,
+              STDP_WRW=8)
+KTIME_KERNELS = ("front", "stdp", "deliver", "lists")
 PHASE = dict(FRONT=0, STDP=1, DELIVERY=2, EXCHANGE=3, TOTAL=4, BUILD=5)
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -57,7 +61,8 @@ class snn_config(ctypes.Structure):
                 ("world", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
                 ("nccl_unique_id", ctypes.c_void_p), ("group_key", ctypes.c_uint64),
-                ("plasticity", ctypes.c_uint32), ("delivery", ctypes.c_uint32), ("flush_period", ctypes.c_uint32)]
+                ("plasticity", ctypes.c_uint32), ("delivery", ctypes.c_uint32), ("flush_period", ctypes.c_uint32),
+                ("exchange_window", ctypes.c_uint32)]
 
 
 class snn_pop_params(ctypes.Structure):
@@ -86,6 +91,9 @@ _lib.snn_step.argtypes = [ctypes.c_void_p, ctypes.c_uint32]
 _lib.snn_read_state.restype = ctypes.c_int32
 _lib.snn_read_state.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
                                 ctypes.c_size_t, _P(ctypes.c_size_t)]
+_lib.snn_read_state_range.restype = ctypes.c_int32
+_lib.snn_read_state_range.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
+                                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t]
 _lib.snn_destroy.restype = None
 _lib.snn_destroy.argtypes = [ctypes.c_void_p]
 _lib.snn_last_error.restype = ctypes.c_char_p
@@ -97,7 +105,7 @@ _lib.snn_partition.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32
                                _P(ctypes.c_uint32), _P(ctypes.c_uint32)]
 
 EXPORTS = ["snn_create", "snn_add_population", "snn_connect", "snn_step", "snn_read_state",
-           "snn_destroy", "snn_last_error", "snn_abi_version", "snn_partition"]
+           "snn_read_state_range", "snn_destroy", "snn_last_error", "snn_abi_version", "snn_partition"]
 
 
 class SnnError(RuntimeError):
@@ -153,6 +161,10 @@ def snn_read_state(sim, field: int, pop_id: int, host_dst, dst_bytes: int) -> in
     return need.value
 
 
+def snn_read_state_range(sim, field: int, pop_id: int, first: int, count: int, host_dst, dst_bytes: int):
+    _check(_lib.snn_read_state_range(sim, field, pop_id, first, count, host_dst, dst_bytes), sim)
+
+
 def snn_destroy(sim):
     _lib.snn_destroy(sim)
 
@@ -167,7 +179,7 @@ class Snn:
                  slice_width: int = 0, device: int = 0, stream=None, flags: int = 0, rank: int = 0,
                  world: int = 1, nccl_unique_id: bytes | None = None, group_key: int = 0,
                  torch_allocator: bool = True, history_bits: int = 64, plasticity: int = 0, delivery: int = 0,
-                 flush_period: int = 0):
+                 flush_period: int = 0, exchange_window: int = 0):
         import torch  # plumbing: device memory and streams
         self._torch = torch
         self.device = device
@@ -183,6 +195,7 @@ class Snn:
         cfg.plasticity = plasticity       # PLAST_EVENT / PLAST_LAZY / PLAST_NAIVE (ablation, f2)
         cfg.delivery = delivery           # DELIV_SLICED / DELIV_ROWWISE (ablation, f2)
         cfg.flush_period = flush_period   # 0: flush at age H; K: batched every K steps (R33)
+        cfg.exchange_window = exchange_window   # world > 1: steps per spike-word exchange (0 = auto)
         cfg.slice_width = slice_width
         cfg.accum_frac_bits = frac_bits
         cfg.flags = flags
@@ -257,9 +270,28 @@ class Snn:
         snn_read_state(self.h, fid, pop, out.ctypes.data_as(ctypes.c_void_p), out.nbytes)
         return out
 
+    def read_range(self, field: str, first: int, count: int, pop: int = ALL,
+                   out: np.ndarray | None = None) -> np.ndarray:
+        """Elements [first, first + count) of a field (snn_read_state_range)
+        into `out` (a caller-owned host buffer, e.g. pinned) or a new array."""
+        if out is None:
+            out = np.empty(count, dtype=np.dtype(FIELD_DTYPE[field]))
+        assert out.dtype == np.dtype(FIELD_DTYPE[field]) and out.size == count and out.flags.c_contiguous
+        snn_read_state_range(self.h, FIELD[field], pop, first, count, out.ctypes.data_as(ctypes.c_void_p),
+                             out.nbytes)
+        return out
+
     def metrics(self) -> dict:
         m = self.read_state("METRICS")
         return {k: int(m[v]) for k, v in METRIC.items()}
+
+    def ktime(self) -> dict:
+        """Cumulative kernel spans of the graph-replayed steps (SNN_FLAG_KTIME):
+        per kernel, ns summed over steps from the first CTA entry / the first
+        return from the dependency wait to the last CTA end, steps, CTAs."""
+        v = self.read_state("KTIME")
+        return {k: dict(entry_ns=int(v[4 * i]), wait_ns=int(v[4 * i + 1]), steps=int(v[4 * i + 2]),
+                        ctas=int(v[4 * i + 3])) for i, k in enumerate(KTIME_KERNELS)}
 
     def info(self) -> dict:
         v = self.read_state("INFO")

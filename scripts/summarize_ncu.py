@@ -1,6 +1,6 @@
 """Summarise a round's ncu evidence into profiles/<round>/ (run here, not on the box).
 
-    python scripts/summarize_ncu.py gpurun_out/full_cur.ncu-rep gpurun_out/launches.csv profiles/r01 v9
+    python scripts/summarize_ncu.py gpurun_out/full_cur.ncu-rep gpurun_out/launches.csv profiles/r02 v1 [config] [flags]
 
 Writes ncu_<tag>.json (per kernel: one --set full launch: duration, DRAM bytes,
 instructions, issue/warps active, top stall reasons) + ncu_<tag>_summary.txt,
@@ -12,7 +12,14 @@ import json
 import subprocess
 import sys
 
+import os
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import source_sha  # noqa: E402
+
 rep, launches, outdir, tag = sys.argv[1:5]
+CONFIG = int(sys.argv[5]) if len(sys.argv) > 5 else 3
+FLAGS = sys.argv[6] if len(sys.argv) > 6 else ""
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "usecond": 1.0,
         "nsecond": 1e-3, "msecond": 1e3}
 raw = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True)
@@ -56,6 +63,12 @@ for d in rows[2:]:
         if key in k:
             txt.append(f"   {key:60s} {k[key]:.6g}")
     txt.append("   stall samples: " + ", ".join(f"{h}={v:g}" for h, v in k["top_stalls"].items()))
+# the capture counts as bench.py's roofline.traffic only for these kernels
+# (source hash), this BASELINE config and these flags
+# (the hash written beside the report on the GPU box at capture time, else now)
+shaf = os.path.splitext(rep)[0] + ".sha"
+sha = open(shaf).read().strip() if os.path.exists(shaf) else source_sha()
+out["_meta"] = {"source_sha": sha, "config": CONFIG, "flags": FLAGS, "report": os.path.basename(rep)}
 json.dump(out, open(f"{outdir}/ncu_{tag}.json", "w"), indent=1)
 open(f"{outdir}/ncu_{tag}_summary.txt", "w").write(
     "ncu --set full --clock-control none --import-source on, BASELINE config 3, one launch per kernel "

@@ -39,8 +39,8 @@ def test_library_loads_and_reports_abi_without_gpu(libpath):
     lib = ctypes.CDLL(libpath)
     lib.snn_abi_version.restype = ctypes.c_uint32
     import paper_2107_04092_b200 as P
-    assert lib.snn_abi_version() == P.SNN_ABI_VERSION == 3
-    assert P.snn_abi_version() == 3
+    assert lib.snn_abi_version() == P.SNN_ABI_VERSION == 4
+    assert P.snn_abi_version() == 4
     for s in P.EXPORTS:
         assert hasattr(P, s)
 

@@ -128,7 +128,7 @@ def test_brunel_plus_stdp_parity(delay, H):
             checked += 1
     assert checked > 100
     m = g.metrics()
-    assert m["FLUSH_ROWS"] > 0 and m["STDP_WTOUCH"] > 0
+    assert m["FLUSH_ROWS"] > 0 and m["STDP_WSTORE"] > 0
 
 
 @pytest.mark.parametrize("H,K,delay", [(64, 16, 15), (64, 32, 0), (128, 32, 15), (64, 1, 3)])
@@ -444,3 +444,66 @@ def test_dense_slices_several_windows():
     _run_compare(g, o, 8, exact_v=False, every=2)
     _compare_weights_wmax(g, o, wmax)
     assert g.metrics()["EVENTS"] == o.events
+
+
+# ------------------------------------------------- device bitfields
+def _expected_fpos(lo, hi):
+    """Index of the only set bit of the 128-bit window (hi:lo), 0xff if several."""
+    out = np.full(lo.shape, 0xFF, dtype=np.uint8)
+    n1 = np.array([bin(int(a)).count("1") + bin(int(b)).count("1") for a, b in zip(lo, hi)])
+    one = n1 == 1
+    for k in np.flatnonzero(one):
+        a, b = int(lo[k]), int(hi[k])
+        out[k] = a.bit_length() - 1 if a else 64 + b.bit_length() - 1
+    return out, n1 > 0
+
+
+@pytest.mark.parametrize("H,delay", [(64, 15), (128, 15), (64, 0), (128, 3)])
+def test_device_history_bitfields_bit_exact_every_step(H, delay):
+    """The bitfields k_stdp actually reads -- the per-neuron history words
+    (Fig. 2 header: bit s = spike at step t - s), the second word at
+    H = 128, the one-byte position of a window's only spike and the
+    'fired in the last H steps' bitmap -- read out of device memory after every
+    step and compared bit-exactly with the oracle's history (bits 64..127 are
+    the oracle's words shifted out, kept by the test)."""
+    rc = W.brunel(10000, p=0.05, plastic=True, delay=delay, seed=31)
+    g, o = _pair(rc, slice_width=512, history_bits=H)
+    ne = rc.pops[0].n                       # E = the post-synaptic population of P -> E STDP (R8)
+    N = o.n
+    hi = np.zeros(ne, dtype=np.uint64)
+    for t in range(300):
+        lo_prev = o.array("hist")[:ne].copy()
+        g.step(1)
+        o.step(1)
+        hi = (hi << np.uint64(1)) | (lo_prev >> np.uint64(63))
+        lo = o.array("hist")[:ne]
+        assert np.array_equal(g.read_state("HIST_DEV", pop=0), lo), f"history words differ at step {t}"
+        if H == 128:
+            assert np.array_equal(g.read_state("HIST_DEV_HI", pop=0), hi), f"upper history words differ at {t}"
+            whi = hi
+        else:
+            whi = np.zeros_like(hi)
+        fpos_exp, nonempty = _expected_fpos(lo, whi)
+        fpos = g.read_state("FPOS", pop=0)
+        assert np.array_equal(fpos[nonempty], fpos_exp[nonempty]), f"fpos differs at step {t}"
+        bits = np.zeros(((N + 31) // 32) * 32, dtype=np.uint8)
+        bits[:ne] = nonempty
+        rec = np.packbits(bits, bitorder="little").view(np.uint32)
+        assert np.array_equal(g.read_state("RECENT"), rec), f"recent-spike bitmap differs at step {t}"
+    assert hi.any() or H == 64
+    assert g.read_state("HIST_DEV", pop=1).sum() == 0      # I is not post-synaptic to STDP: no word kept
+
+
+def test_read_state_range_matches_full_read():
+    rc = W.brunel(6000, p=0.05, plastic=True, delay=3, seed=8)
+    g, o = _pair(rc, slice_width=256)
+    g.step(70)
+    for f in ("IDX", "WEIGHTS", "ROW_PTR", "SPIKE_RING", "V", "PIVOTS"):
+        full = g.read_state(f)
+        for a, n in [(0, 1), (17, 1000), (len(full) - 5, 5)]:
+            assert np.array_equal(g.read_range(f, a, n), full[a:a + n]), f
+    v1 = g.read_state("V", pop=1)
+    assert np.array_equal(g.read_range("V", 3, 10, pop=1), v1[3:13])
+    from paper_2107_04092_b200 import SnnError
+    with pytest.raises(SnnError):
+        g.read_range("IDX", len(g.read_state("IDX")) - 1, 2)
