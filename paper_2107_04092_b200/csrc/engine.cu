@@ -788,6 +788,7 @@ static snn_status fold_ktime(snn_sim *sim) {
 }
 
 static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool prepare, FieldRef &f) {
+    f = FieldRef();
     if (field >= SNN_FIELD_COUNT) return sim->fail(SNN_E_INVALID, "unknown field %u", field);
     if (sim->state == 0 && field != SNN_FIELD_STEP) return sim->fail(SNN_E_STATE, "read_state before finalize");
     const NetDev &net = sim->net;

@@ -21,11 +21,13 @@ def _run(*args):
 
 
 def test_bench_line_contract():
-    d = _run("--config", "1", "--steps", "200", "--warmup", "20", "--phase-steps", "50")
+    d = _run("--config", "1", "--steps", "200", "--warmup", "20", "--settle", "100", "--cpu-budget", "3")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "cpu_baseline", "clocks"):
         assert k in d, k
-    assert d["n_gpus"] == 1 and d["steps"] == 200 and d["warmup"] == 20 and d["higher_is_better"] is True
+    assert d["n_gpus"] == 1 and d["steps"] == 200 and d["warmup"] == 20 and d["higher_is_better"] is False
+    assert d["unit"] == "wall-s per bio-second" and d["config"]["settle_steps"] == 100
+    assert d["kernel_spans"]["same_window"] and d["e2e"]["same_window"]
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] == 200 * 2
     assert "workload" in d["config"]
     r = d["roofline"]
@@ -40,6 +42,6 @@ def test_bench_line_contract():
 
 def test_reference_arm_contract():
     d = _run("--impl", "reference", "--config", "1", "--steps", "20", "--warmup", "3")
-    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is False
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0

@@ -262,3 +262,108 @@ def test_synapse_replay_equals_the_network_oracle():
             checked += 1
     assert checked > 200
     assert np.isnan(o.synapse_replay(0, 0, pre_shift[:, 0], fired[:, 0]))   # E -> E is static
+
+
+# --------------------------------------------- STDP over several spikes (R7)
+def _d(n):
+    return math.exp(-n * DT / TAU)
+
+
+@pytest.mark.parametrize("delay", [0, 4])
+def test_stdp_two_pre_then_post_traces_accumulate(delay):
+    """All-to-all pair STDP (R7): the pre trace sums every earlier pre spike,
+    x_pre(v) = d^(v-u1) + d^(v-u2), so a post at v after pre arrivals at u1 < u2
+    gives dw = A+ (d^(v-u1) + d^(v-u2)).  A nearest-neighbour trace (reset to 1
+    at a spike) would give A+ d^(v-u2) only."""
+    o = _pair(delay)
+    u1, u2, v = 10 + delay, 17 + delay, 29 + delay
+    _run(o, {u1 - delay: [0], u2 - delay: [0], v: [1]}, v + 1)
+    dw = float(o.array("w")[0]) - 0.5
+    exp = A_PLUS * (_d(v - u1) + _d(v - u2))
+    assert abs(dw - exp) <= 1e-5 * exp
+    assert abs(dw - A_PLUS * _d(v - u2)) > 0.1 * A_PLUS * _d(v - u1)     # not nearest-neighbour
+
+
+def test_stdp_pre_post_pre_triplet():
+    """pre at u1, post at v, pre at u2 > v: potentiation at v by x_pre(v) =
+    d^(v-u1), depression at u2 by x_post(u2) = d^(u2-v):
+    dw = A+ d^(v-u1) - A- d^(u2-v)."""
+    o = _pair(0)
+    u1, v, u2 = 10, 16, 25
+    _run(o, {u1: [0], v: [1], u2: [0]}, u2 + 1)
+    dw = float(o.array("w")[0]) - 0.5
+    exp = A_PLUS * _d(v - u1) - A_MINUS * _d(u2 - v)
+    assert abs(dw - exp) <= 1e-5 * (A_PLUS + A_MINUS)
+
+
+def test_stdp_post_post_pre_depression_sums_post_trace():
+    """posts at v1 < v2, then a pre at u: the potentiations see x_pre = 0 and
+    the depression sees x_post(u) = d^(u-v1) + d^(u-v2):
+    dw = -A- (d^(u-v1) + d^(u-v2))."""
+    o = _pair(0)
+    v1, v2, u = 10, 13, 30
+    _run(o, {v1: [1], v2: [1], u: [0]}, u + 1)
+    dw = float(o.array("w")[0]) - 0.5
+    exp = -A_MINUS * (_d(u - v1) + _d(u - v2))
+    assert abs(dw - exp) <= 1e-5 * abs(exp)
+
+
+def test_stdp_pre_pre_post_post_four_pairs():
+    """Two pre then two post spikes: every (pre, post) pair contributes,
+    dw = A+ sum_{a,b} d^(v_b - u_a) (four terms)."""
+    o = _pair(0)
+    u1, u2, v1, v2 = 10, 12, 20, 33
+    _run(o, {u1: [0], u2: [0], v1: [1], v2: [1]}, v2 + 1)
+    dw = float(o.array("w")[0]) - 0.5
+    exp = A_PLUS * sum(_d(v - u) for u in (u1, u2) for v in (v1, v2))
+    assert abs(dw - exp) <= 1e-5 * exp
+
+
+def test_stdp_sequential_upper_bound_per_post_spike():
+    """The hard bound applies at every post spike (min(w + A+ x_pre, w_max)),
+    not once at the end: from w0 = w_max - A+/2, a pre then two posts saturate
+    at w_max and stay there."""
+    o = _pair(0, w0=W_MAX - A_PLUS / 2)
+    _run(o, {10: [0], 11: [1], 12: [1]}, 13)
+    assert o.array("w")[0] == np.float32(W_MAX)
+
+
+# ------------------------------------------------- CUBA refractory (R20)
+def test_cuba_refractory_holds_v_while_currents_integrate():
+    """R20 (CUBA): for n_ref = round(tau_ref / dt) = 50 steps after a spike V
+    is held at V_reset, while the exponential currents keep decaying and keep
+    taking input: g_n = sum_k in_k d^(n-k).  The first step after the
+    refractory period integrates with the accumulated currents:
+    V = V_reset + a (E_l - V_reset + g_e + g_i)."""
+    o = O.Oracle(9, DT, 0, F)
+    o.add_population(O.LIF_CUBA, 1, tau_m=20.0, v_rest=-49.0, v_reset=-60.0, v_th=-50.0,
+                     tau_ref=5.0, tau_e=5.0, tau_i=10.0)
+    o.finalize()
+    V, ge, gi, ine, ini, ref = (o.array(k) for k in ("V", "ge", "gi", "in_e", "in_i", "ref"))
+    de, di, a = math.exp(-DT / 5.0), math.exp(-DT / 10.0), DT / 20.0
+    inputs_e = {0: 2000.0, 12: 3.0, 40: 1.5}        # step -> exc input (the first one forces the spike)
+    inputs_i = {20: -4.0, 50: -2.0}
+    T = 52
+    for n in range(T):
+        if n in inputs_e:
+            ine[0] = q(inputs_e[n])
+        if n in inputs_i:
+            ini[0] = q(inputs_i[n])
+        o.step(1)
+        fired = int(o.array("hist")[0] & 1)
+        ge_exp = sum(q(x) / Q * de ** (n - k + 1) for k, x in inputs_e.items() if k <= n)
+        gi_exp = sum(q(x) / Q * di ** (n - k + 1) for k, x in inputs_i.items() if k <= n)
+        assert abs(ge[0] - ge_exp) <= 1e-5 * abs(ge_exp)
+        if gi_exp:
+            assert abs(gi[0] - gi_exp) <= 1e-5 * abs(gi_exp)
+        if n == 0:
+            assert fired and ref[0] == 50 and V[0] == np.float32(-60.0)
+        elif n <= 50:
+            assert not fired and V[0] == np.float32(-60.0), n     # held for exactly 50 steps
+            assert ref[0] == 50 - n
+        else:
+            # first free step: the currents of this step before their decay
+            g_e = sum(q(x) / Q * de ** (n - k) for k, x in inputs_e.items() if k <= n)
+            g_i = sum(q(x) / Q * di ** (n - k) for k, x in inputs_i.items() if k <= n)
+            exp = -60.0 + a * (-49.0 + 60.0 + g_e + g_i)
+            assert abs(V[0] - exp) <= 1e-5 * abs(exp)

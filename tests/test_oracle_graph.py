@@ -1,5 +1,6 @@
 """Pins of the oracle's Philox, connectivity and pivots against things the
 paper / mathematics fix (not against the oracle itself)."""
+import math
 import os
 
 import numpy as np
@@ -147,3 +148,26 @@ def test_geometric_gaps_follow_the_bernoulli_law(N, p, rows, ks):
     B = N // 40                                                  # 40 blocks of positions
     f = hits.reshape(40, B).sum(axis=1) / (rows * B)
     assert np.all(np.abs(f - p) < 5 * np.sqrt(p * (1 - p) / (rows * B)))
+
+
+def test_pair_inclusion_independent_at_every_lag():
+    """Independent Bernoulli(p) per pair (R23, realised by R32): for two
+    candidates k apart in one row, P(both kept) = p^2 at every lag k -- in
+    particular at k = 1, which a gap law off by one (gaps >= 2, or g = 0
+    allowed) would empty or double."""
+    import workloads as W
+    from oracle.oracle import Oracle
+    p, n = 0.05, 4000
+    rc = W.Recipe("lag", 3, 0.1, 0, 20,
+                  [W.Pop("A", W.LIF_DELTA, n, dict(W.BRUNEL_LIF)), W.Pop("B", W.LIF_DELTA, 600, dict(W.BRUNEL_LIF))],
+                  [W.Proj(1, 0, W.STATIC, W.EXC, p, 0.1)])
+    o = Oracle(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits)
+    rc.apply(o)
+    X = np.zeros((600, n), dtype=bool)
+    for r in range(600):
+        X[r, o.build_row(n + r)] = True
+    for k in (1, 2, 3, 7, 50, 333):
+        both = (X[:, :-k] & X[:, k:]).mean()
+        m = X[:, :-k].size
+        assert abs(both - p * p) < 5 * math.sqrt(p * p * (1 - p * p) / m), (k, both)
+    assert abs(X.mean() - p) < 5 * math.sqrt(p * (1 - p) / X.size)
