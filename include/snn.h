@@ -224,9 +224,11 @@ enum {
                                    reads; maintained for neurons post-synaptic
                                    to STDP (0 elsewhere)                         */
     SNN_FIELD_HIST_DEV_HI = 23, /* [u64 / n]   bits 64-127 (history_bits = 128)  */
-    SNN_FIELD_FPOS = 24,        /* [u8 / n]    post-plastic neuron whose H-bit
-                                   window is non-empty: bit index of its only
-                                   spike, 0xff if several (stale elsewhere)      */
+    SNN_FIELD_FPOT = 24,        /* [f32 / n]   post-plastic neuron with spikes in
+                                   its H-bit window: the forced-flush factor, the
+                                   sum over those spikes s (oldest first) of
+                                   D+[H - s] = fp32(exp(-(H - s) dt / tau_+))
+                                   (stale elsewhere)                             */
     SNN_FIELD_RECENT = 25,      /* [u32 / ceil(N/32)] bit j: post-plastic neuron
                                    j fired in the last H steps                   */
     SNN_FIELD_KTIME = 26,       /* [u64 / 16] per kernel k (front, stdp, deliver,

@@ -33,6 +33,7 @@ struct PopDev {
     float d_minus;       // PF_POST_PLASTIC: fp32(exp(-dt/tau_-)) of the x_post trace
     int32_t stdp;        // PF_PRE_PLASTIC: index into NetDev::stdp, else -1
     int32_t rcpt_uniform;// receptor used by every projection out of this pop (-1: mixed)
+    int32_t post_stdp;   // PF_POST_PLASTIC: the StdpDev whose D+ table its forced-flush factor uses, else -1
 };
 
 struct StdpDev {
@@ -116,7 +117,7 @@ struct StateDev {
     int32_t *ref, *in_e, *in_i;
     uint64_t *hist;          // bits 0..63 of the spike history (bit s: step t - s)
     uint64_t *hist_hi;       // H = 128: bits 64..127 (else unused)
-    uint8_t *fpos;           // post-plastic j with hist != 0: bit index of its only spike, 0xff if several
+    float *fpot;             // post-plastic j with spikes in its H-bit window: sum of D+[H - s] over them
     uint32_t *nspk;
     uint32_t *ring;          // [kRingSlots][ring_stride]
     // source rows

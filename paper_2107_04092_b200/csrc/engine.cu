@@ -271,6 +271,7 @@ static snn_status finalize(snn_sim *sim) {
         p.n = hp.n;
         p.kind = hp.prm.kind;
         p.stdp = -1;
+        p.post_stdp = -1;
         p.rcpt_uniform = -2;  // unset
         p.thr = bernoulli_thr((double)hp.prm.rate_hz * 1e-3 * dt);
         p.k_m = (float)(1.0 - dt / (double)hp.prm.tau_m_ms);
@@ -314,6 +315,11 @@ static snn_status finalize(snn_sim *sim) {
             const float dm = (float)std::exp(-dt / (double)q.tau_minus_ms);
             if ((dp.flags & PF_POST_PLASTIC) && dp.d_minus != dm)
                 return sim->fail(SNN_E_UNSUPPORTED, "STDP projections into one population must share tau_minus");
+            // the forced-flush factor of a target (k_front) uses one D+ table per population
+            if ((dp.flags & PF_POST_PLASTIC) &&
+                memcmp(net.stdp[dp.post_stdp].dplus, sd.dplus, sizeof sd.dplus) != 0)
+                return sim->fail(SNN_E_UNSUPPORTED, "STDP projections into one population must share tau_plus");
+            if (!(dp.flags & PF_POST_PLASTIC)) dp.post_stdp = (int32_t)net.nstdp;
             dp.flags |= PF_POST_PLASTIC;
             dp.d_minus = dm;
             sp.flags |= PF_PRE_PLASTIC;
@@ -385,7 +391,7 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.in_i, int32_t, N);
     ALLOC(st.hist, uint64_t, N);
     ALLOC(st.hist_hi, uint64_t, cfg.history_bits > 64 ? N : 1);
-    ALLOC(st.fpos, uint8_t, (size_t)N + 16);
+    ALLOC(st.fpot, float, N);
     ALLOC(st.nspk, uint32_t, N);
     // exchange geometry: rank r owns words [r share_w, ...), at most share_w + 1
     // of them (the word straddling R); ring slots padded for the unpack
@@ -816,10 +822,10 @@ static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool 
     case SNN_FIELD_HIST_DEV_HI:
         if (net.H <= 64) return sim->fail(SNN_E_STATE, "HIST_DEV_HI needs history_bits = 128");
         f.dev = st.hist_hi + base; f.elem = 8; break;
-    case SNN_FIELD_FPOS: f.dev = st.fpos + base; f.elem = 1; break;
+    case SNN_FIELD_FPOT: f.dev = st.fpot + base; f.elem = 4; break;
     default: break;
     }
-    if (f.elem > 1 || field == SNN_FIELD_FPOS) {
+    if (f.elem > 1) {
         f.bytes = f.elem * n;
     } else {
         switch (field) {

@@ -188,11 +188,24 @@ k_front(NetDev net, StateDev st) {
                 st.hist_hi[i] = hh;
             }
             recent = (h | hh) != 0ull;
-            // position of the window's only post spike (lean forced flush in k_stdp), 0xff: several
+            // potentiation factor of a forced flush (age H) for this target:
+            // fpot = sum over its spikes s in the window of D+[H - s], oldest
+            // first (k_stdp: w = min(w + A+ (x_pre fpot), w_max))
             if (recent) {
-                const uint32_t n1 = __popcll(h) + __popcll(hh);
-                st.fpos[i] = n1 > 1 ? (uint8_t)0xffu
-                                    : (uint8_t)(h ? 63 - __clzll((long long)h) : 127 - __clzll((long long)hh));
+                const float *dpl = net.stdp[p.post_stdp].dplus;
+                const int H = (int)net.H;
+                float f = 0.0f;
+                for (uint64_t m = hh; m; ) {
+                    const int b = 63 - __clzll((long long)m);
+                    m &= ~(1ull << b);
+                    f = __fadd_rn(f, dpl[H - 64 - b]);
+                }
+                for (uint64_t m = h; m; ) {
+                    const int b = 63 - __clzll((long long)m);
+                    m &= ~(1ull << b);
+                    f = __fadd_rn(f, dpl[H - b]);
+                }
+                st.fpot[i] = f;
             }
             const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
             st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
@@ -558,6 +571,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     constexpr uint32_t hi_on = kH128 ? 1u : 0u;
     constexpr bool lazy = kLazy;
     const float *__restrict__ gxpost = st.xpost;
+    const float *__restrict__ gfpot = st.fpot;
     float *__restrict__ gw = st.w;
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kStdpRows) {
         // ---- tabulate up to kStdpRows rows (one per thread), chunk prefix
@@ -637,7 +651,6 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 const uint32_t sa = stage_a + slot * (kStdpStageCh * 32);
                 uint32_t hm = 0, rm = 0, slots = 0;   // 16-bit masks: list the synapse / target may hold a post spike
                 uint32_t am = 0;                      // 16-bit mask: synapses of arriving rows (updated in place)
-                bool nonlean = false;                 // lazy schedule: the generic drain replays step by step
                 mbar_wait(full_a + 8 * slot, (g / kStdpStages) & 1u);
 #pragma unroll
                 for (int u = 0; u < kStdpChPerThr; u++) {
@@ -671,7 +684,6 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         hm |= sel << (4 * u);
                         am |= (arr ? inm : 0u) << (4 * u);
                         rm |= rec << (4 * u);
-                        nonlean |= sel != 0u && lazy;
                         slots |= o << (8 * u);
                     }
                 }
@@ -718,40 +730,85 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         }
                     }
                 }
-                // ---- list the selected synapses (warp-exclusive prefix of the counts)
-                const uint32_t k = __popc(hm);
-                uint32_t ex = k;
+                if constexpr (!kGeneric) {
+                    // ---- forced flushes (R3), in place.  Every forced flush of this
+                    //      step has age H, so all its synapses share the window
+                    //      (t - H, t]: a target j that fired in it gets
+                    //      w = min(w + A+ (x_pre fpot[j]), w_max) with fpot[j] = the sum
+                    //      over j's spikes s in the window of D+[H - s] (k_front; one
+                    //      spike: exactly the closed-form skip-ahead of Fig. 2c, P:284;
+                    //      several: their potentiations are all >= 0, so the sequential
+                    //      clamps are the one clamp of the sum).  The gathers of the
+                    //      thread's 16 synapses are in flight together, predicated off
+                    //      for the ~84 % of targets without a spike in the window.
+                    if (hm) {
+                        float fv[4 * kStdpChPerThr];
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, ex, d);
-                    if (lane >= (uint32_t)d) ex += y;
-                }
-                const uint32_t ntot = __shfl_sync(0xffffffffu, ex, 31);
-                ex -= k;
-                for (uint32_t base = 0; base < ntot; base += kStdpList) {
-                uint32_t n = ntot - base < kStdpList ? ntot - base : kStdpList;
-                {
-                    uint32_t m = hm, e = ex;
-                    while (m) {
-                        const uint32_t bpos = __ffs(m) - 1u;
-                        m &= m - 1u;
-                        const uint32_t u = bpos >> 2;
-                        const uint32_t p = 4u * (gt + kStdpGroupThr * u) + (bpos & 3u);     // element in the stage
-                        if (e - base < kStdpList)
-                            sts_u32(list_a + 4u * (e - base),
-                                    (p << 9) | (((rm >> bpos) & 1u) << 8) | ((slots >> (8 * u)) & 0xffu));
-                        e++;
+                        for (int u = 0; u < kStdpChPerThr; u++) {
+                            const uint32_t nib = (hm >> (4 * u)) & 0xfu;
+                            const uint4 j4 = nib ? lds_v4(sa + 16u * (gt + kStdpGroupThr * u)) : make_uint4(0, 0, 0, 0);
+                            fv[4 * u + 0] = ldg_f32_if(gfpot + j4.x, nib & 1u);
+                            fv[4 * u + 1] = ldg_f32_if(gfpot + j4.y, nib & 2u);
+                            fv[4 * u + 2] = ldg_f32_if(gfpot + j4.z, nib & 4u);
+                            fv[4 * u + 3] = ldg_f32_if(gfpot + j4.w, nib & 8u);
+                        }
+#pragma unroll
+                        for (int u = 0; u < kStdpChPerThr; u++) {
+                            const uint32_t nib = (hm >> (4 * u)) & 0xfu;
+                            if (!nib) continue;
+                            const uint32_t ch = gt + kStdpGroupThr * u;             // chunk in the stage
+                            const StdpRow &rr = sm.rows[(slots >> (8 * u)) & 0xffu];
+                            const float4 pr = sm.par[(rr.meta >> 12) & 0x3u];
+                            const uint4 w4 = lds_v4(sa + kStdpStageCh * 16 + 16u * ch);
+                            const float wv[4] = {__uint_as_float(w4.x), __uint_as_float(w4.y), __uint_as_float(w4.z),
+                                                 __uint_as_float(w4.w)};
+                            const int64_t off = rr.cb + 4ll * ((int64_t)(a + ch) - (int64_t)rr.first);
+#pragma unroll
+                            for (int e = 0; e < 4; e++) {
+                                if (!((nib >> e) & 1u)) continue;
+                                const float nw = __fadd_rn(wv[e], __fmul_rn(pr.x, __fmul_rn(rr.xp, fv[4 * u + e])));
+                                const float w = nw < pr.z ? nw : pr.z;
+                                const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
+                                stg_f32_if(gw + off + e, w, chg);
+                                n_w += chg;
+                            }
+                        }
                     }
-                }
-                __syncwarp();
-                if (!__any_sync(0xffffffffu, nonlean)) {
-                    // ---- lean drain (forced flushes, R3): potentiation by the window's
-                    //      post spikes; the only spike's position comes from fpos[j]
-                    //      (one byte), several spikes take the history loop
+                } else {
+                    // ---- list the selected synapses (warp-exclusive prefix of the counts)
+                    const uint32_t k = __popc(hm);
+                    uint32_t ex = k;
+    #pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, ex, d);
+                        if (lane >= (uint32_t)d) ex += y;
+                    }
+                    const uint32_t ntot = __shfl_sync(0xffffffffu, ex, 31);
+                    ex -= k;
+                    for (uint32_t base = 0; base < ntot; base += kStdpList) {
+                    uint32_t n = ntot - base < kStdpList ? ntot - base : kStdpList;
+                    {
+                        uint32_t m = hm, e = ex;
+                        while (m) {
+                            const uint32_t bpos = __ffs(m) - 1u;
+                            m &= m - 1u;
+                            const uint32_t u = bpos >> 2;
+                            const uint32_t p = 4u * (gt + kStdpGroupThr * u) + (bpos & 3u);     // element in the stage
+                            if (e - base < kStdpList)
+                                sts_u32(list_a + 4u * (e - base),
+                                        (p << 9) | (((rm >> bpos) & 1u) << 8) | ((slots >> (8 * u)) & 0xffu));
+                            e++;
+                        }
+                    }
+                    __syncwarp();
+                    // ---- drain the list, four entries per lane in flight
                     for (uint32_t b = 0; b < n; b += 128) {
-                        uint32_t ent[4], jv[4], pos[4];
+                        uint32_t ent[4];
+                        uint32_t jv[4];
                         float wv[4];
-#pragma unroll
+                        uint64_t hh[4], hh2[4];
+                        float xq[4];
+    #pragma unroll
                         for (int u = 0; u < 4; u++) {
                             const uint32_t q = b + 32 * u + lane;
                             const bool ok = q < n;
@@ -759,78 +816,33 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                             const uint32_t p = ent[u] >> 9;
                             jv[u] = lds_u32(sa + 4u * p);
                             wv[u] = lds_f32(sa + kStdpStageCh * 16 + 4u * p);
-                            pos[u] = ldg_u8_if(st.fpos + jv[u], ok ? 1u : 0u);
+                            const bool arr = ok && (sm.rows[ent[u] & 0xffu].meta & kMetaArr) != 0;
+                            hh[u] = ldg_u64_if(ghist + jv[u], ok && ((ent[u] >> 8) & 1u) ? 1u : 0u);
+                            hh2[u] = ldg_u64_if(ghist_hi + jv[u], ok && ((ent[u] >> 8) & 1u) ? hi_on : 0u);
+                            xq[u] = ldg_f32_if(gxpost + jv[u], arr ? 1u : 0u);
                         }
-#pragma unroll
+    #pragma unroll
                         for (int u = 0; u < 4; u++) {
                             if (b + 32 * u + lane >= n) continue;
                             const StdpRow &rr = sm.rows[ent[u] & 0xffu];
-                            const uint32_t si = (rr.meta >> 12) & 0x3u;
+                            const uint32_t meta = rr.meta;
+                            const bool arr = (meta & kMetaArr) != 0;
+                            const int age = (int)(meta & kMetaAge);
+                            const uint32_t si = (meta >> 12) & 0x3u;
                             const float4 pr = sm.par[si];
                             const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
-                            const int age = (int)(rr.meta & kMetaAge);
-                            float w = wv[u];
-                            if (pos[u] < (uint32_t)kMaxHist) {      // the history's only spike: in the window?
-                                if (pos[u] < (uint32_t)age) {
-                                    const float d = lds_f32(dp + 4u * ((uint32_t)age - pos[u]));
-                                    const float nw = __fadd_rn(wv[u], __fmul_rn(pr.x, __fmul_rn(rr.xp, d)));
-                                    w = nw < pr.z ? nw : pr.z;
-                                }
-                            } else {                                // several: replay the window
-                                w = stdp_synapse(wv[u], window_lo(__ldg(ghist + jv[u]), age), false, 0.0f, rr.xp, age,
-                                                 dp, pr.x, pr.y, pr.z,
-                                                 kH128 ? window_hi(__ldg(ghist_hi + jv[u]), age) : 0ull);
-                            }
+                            const float w = lazy ? stdp_synapse_lazy(wv[u], window_lo(hh[u], age), arr, xq[u], rr.xp, age,
+                                                                     dp, pr.x, pr.y, pr.z, window_hi(hh2[u], age))
+                                                 : stdp_synapse(wv[u], window_lo(hh[u], age), arr, xq[u], rr.xp, age,
+                                                                dp, pr.x, pr.y, pr.z, window_hi(hh2[u], age));   // (tlu, t], R2
                             const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
                             const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);
                             stg_f32_if(gw + off, w, chg);
                             n_w += chg;
                         }
                     }
-                    n = 0;
-                }
-                // ---- drain the list, four entries per lane in flight
-                if (!kGeneric) n = 0;       // (a step of the event schedule lists only age-H flushes)
-                for (uint32_t b = 0; b < n; b += 128) {
-                    uint32_t ent[4];
-                    uint32_t jv[4];
-                    float wv[4];
-                    uint64_t hh[4], hh2[4];
-                    float xq[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const uint32_t q = b + 32 * u + lane;
-                        const bool ok = q < n;
-                        ent[u] = ok ? lds_u32(list_a + 4u * q) : 0u;
-                        const uint32_t p = ent[u] >> 9;
-                        jv[u] = lds_u32(sa + 4u * p);
-                        wv[u] = lds_f32(sa + kStdpStageCh * 16 + 4u * p);
-                        const bool arr = ok && (sm.rows[ent[u] & 0xffu].meta & kMetaArr) != 0;
-                        hh[u] = ldg_u64_if(ghist + jv[u], ok && ((ent[u] >> 8) & 1u) ? 1u : 0u);
-                        hh2[u] = ldg_u64_if(ghist_hi + jv[u], ok && ((ent[u] >> 8) & 1u) ? hi_on : 0u);
-                        xq[u] = ldg_f32_if(gxpost + jv[u], arr ? 1u : 0u);
+                    __syncwarp();                              // list reused by the next pass
                     }
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        if (b + 32 * u + lane >= n) continue;
-                        const StdpRow &rr = sm.rows[ent[u] & 0xffu];
-                        const uint32_t meta = rr.meta;
-                        const bool arr = (meta & kMetaArr) != 0;
-                        const int age = (int)(meta & kMetaAge);
-                        const uint32_t si = (meta >> 12) & 0x3u;
-                        const float4 pr = sm.par[si];
-                        const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
-                        const float w = lazy ? stdp_synapse_lazy(wv[u], window_lo(hh[u], age), arr, xq[u], rr.xp, age,
-                                                                 dp, pr.x, pr.y, pr.z, window_hi(hh2[u], age))
-                                             : stdp_synapse(wv[u], window_lo(hh[u], age), arr, xq[u], rr.xp, age,
-                                                            dp, pr.x, pr.y, pr.z, window_hi(hh2[u], age));   // (tlu, t], R2
-                        const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[u]) ? 1u : 0u;
-                        const int64_t off = rr.cb + 4ll * ((int64_t)a - (int64_t)rr.first) + (ent[u] >> 9);
-                        stg_f32_if(gw + off, w, chg);
-                        n_w += chg;
-                    }
-                }
-                __syncwarp();                              // list reused by the next pass
                 }
                 if (lane == 0) mbar_arrive(empty_a + 8 * slot);   // stage and list free
             }

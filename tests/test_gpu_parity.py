@@ -2,6 +2,8 @@
 connectivity, pivots, spike rasters / bitfields bit-exact; V bit-exact for
 static networks (every op identical, integer accumulation); weights and V
 within 1e-4 relative for Brunel+ (DESIGN.md section 5 derives the tolerance)."""
+import math
+
 import numpy as np
 import pytest
 
@@ -447,25 +449,28 @@ def test_dense_slices_several_windows():
 
 
 # ------------------------------------------------- device bitfields
-def _expected_fpos(lo, hi):
-    """Index of the only set bit of the 128-bit window (hi:lo), 0xff if several."""
-    out = np.full(lo.shape, 0xFF, dtype=np.uint8)
-    n1 = np.array([bin(int(a)).count("1") + bin(int(b)).count("1") for a, b in zip(lo, hi)])
-    one = n1 == 1
-    for k in np.flatnonzero(one):
-        a, b = int(lo[k]), int(hi[k])
-        out[k] = a.bit_length() - 1 if a else 64 + b.bit_length() - 1
-    return out, n1 > 0
+def _expected_fpot(lo, hi, H, dt, tau_plus):
+    """Forced-flush factor of each target: the sum over its spikes s in the
+    H-step window (bit s of hi:lo) of D+[H - s] = fp32(exp(-(H - s) dt / tau+)),
+    accumulated in fp32 oldest first; and whether the window holds a spike."""
+    dplus = [np.float32(math.exp(-n * float(np.float32(dt)) / float(np.float32(tau_plus)))) for n in range(H + 1)]
+    out = np.zeros(lo.shape, dtype=np.float32)
+    for s in range(H - 1, -1, -1):
+        word = hi if s >= 64 else lo
+        on = ((word >> np.uint64(s % 64)) & np.uint64(1)).astype(bool)
+        out[on] = out[on] + dplus[H - s]          # fp32 adds, round to nearest even
+    return out, (lo | hi) != 0
 
 
 @pytest.mark.parametrize("H,delay", [(64, 15), (128, 15), (64, 0), (128, 3)])
 def test_device_history_bitfields_bit_exact_every_step(H, delay):
     """The bitfields k_stdp actually reads -- the per-neuron history words
     (Fig. 2 header: bit s = spike at step t - s), the second word at
-    H = 128, the one-byte position of a window's only spike and the
-    'fired in the last H steps' bitmap -- read out of device memory after every
-    step and compared bit-exactly with the oracle's history (bits 64..127 are
-    the oracle's words shifted out, kept by the test)."""
+    H = 128 (P:399), the 'fired in the last H steps' bitmap and the
+    forced-flush factor derived from the window (sum of D+[H - s]) -- read out
+    of device memory after every step and compared bit-exactly with the
+    oracle's history (bits 64..127 are the oracle's words shifted out, kept by
+    the test)."""
     rc = W.brunel(10000, p=0.05, plastic=True, delay=delay, seed=31)
     g, o = _pair(rc, slice_width=512, history_bits=H)
     ne = rc.pops[0].n                       # E = the post-synaptic population of P -> E STDP (R8)
@@ -483,9 +488,9 @@ def test_device_history_bitfields_bit_exact_every_step(H, delay):
             whi = hi
         else:
             whi = np.zeros_like(hi)
-        fpos_exp, nonempty = _expected_fpos(lo, whi)
-        fpos = g.read_state("FPOS", pop=0)
-        assert np.array_equal(fpos[nonempty], fpos_exp[nonempty]), f"fpos differs at step {t}"
+        fpot_exp, nonempty = _expected_fpot(lo, whi, H, rc.dt_ms, rc.projs[4].stdp["tau_plus"])
+        fpot = g.read_state("FPOT", pop=0)
+        assert np.array_equal(fpot[nonempty], fpot_exp[nonempty]), f"forced-flush factors differ at step {t}"
         bits = np.zeros(((N + 31) // 32) * 32, dtype=np.uint8)
         bits[:ne] = nonempty
         rec = np.packbits(bits, bitorder="little").view(np.uint32)
