@@ -43,7 +43,7 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 METRIC = "wall-s per bio-second & synaptic events/s at 1/2/4/8 B200; % HBM roofline"
-KERNEL_OF = {"front": "k_front", "stdp": "k_stdp", "deliver": "k_deliver"}
+KERNEL_OF = {"front": "k_front", "stdp": "k_stdp", "deliver": "k_deliver", "flush": "k_flush"}
 
 
 def parse(argv=None):
@@ -318,7 +318,7 @@ def main(argv=None):
         del sk
         spans = {"same_window": bool(reduce(0.0 if same else 1.0, MAX) == 0.0),
                  "ms_per_step_instrumented": ms_k / a.steps}
-        for k in ("front", "stdp", "deliver"):
+        for k in ("front", "stdp", "deliver", "flush"):
             st = k1[k]["steps"] - k0[k]["steps"]
             if st <= 0:
                 continue
@@ -368,16 +368,20 @@ def main(argv=None):
     nrcpt = 2 if any(pr.receptor == W.INH for pr in rc.projs) else 1
     K = a.steps
     # algorithmic HBM bytes per launch:
-    #   k_stdp:    4 B target id per visited plastic synapse + 8 B (weight read
-    #              and written) per synapse of an arriving row or whose target
-    #              fired in the window + 16 B per visited row
+    #   k_flush / k_stdp (forced flushes / plastic arrivals): 4 B target id per
+    #              visited plastic synapse + 8 B (weight read and written) per
+    #              synapse of an arriving row or whose target fired in the
+    #              window + 16 B per visited row
     #   k_deliver: 8 B per delivered event (id + weight; 6 B with --idx16) +
     #              8 B per (arriving row, slice) pivot pair + 4 B per slice
     #              neuron and receptor written back
     #   k_front:   32 B per LIF neuron, 16 B per Poisson neuron (8(a1))
     n_pois = sum(p.n for p in rc.pops if p.kind == W.POISSON)
+    fl_rows = dm_local["FLUSH_ROWS"] if dm_local["FLUSH_SYN"] else 0
     kb = {
-        "stdp": (4 * dm_local["STDP_SYN"] + 8 * dm_local["STDP_WRW"] + 16 * dm_local["STDP_ROWS"]) / K,
+        "flush": (4 * dm_local["FLUSH_SYN"] + 8 * dm_local["FLUSH_WRW"] + 16 * fl_rows) / K,
+        "stdp": (4 * (dm_local["STDP_SYN"] - dm_local["FLUSH_SYN"]) + 8 * (dm_local["STDP_WRW"] - dm_local["FLUSH_WRW"])
+                 + 16 * (dm_local["STDP_ROWS"] - fl_rows)) / K,
         "deliver": ((6 if a.idx16 else 8) * dm_local["EVENTS"] + 8 * dm_local["SPIKES"] * info["nslices"]) / K
                    + 4 * nrcpt * (info["tgt_hi"] - info["tgt_lo"]),
         "front": 32.0 * (info["N"] - n_pois) + 16.0 * n_pois,
@@ -400,7 +404,7 @@ def main(argv=None):
     if dom:
         dk = KERNEL_OF[dom] if not (dom == "deliver" and a.delivery == "rowwise") else "k_deliver_rowwise"
         traffic, traffic_src = ncu_traffic(dk, a.config, flags_s)
-        sd = [k for k in ("stdp", "deliver") if k in kern]
+        sd = [k for k in ("flush", "stdp", "deliver") if k in kern]
         sd_b = sum(kern[k]["bytes_per_launch"] for k in sd)
         sd_us = sum(kern[k]["us_per_launch"] for k in sd)
         step_b = sum(kb.values())

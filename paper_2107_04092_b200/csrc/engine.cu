@@ -34,6 +34,8 @@ cudaError_t kernels_configure(int);
 cudaError_t launch_kspan_reset(KSpan *, cudaStream_t);
 cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
 cudaError_t launch_deliver_rowwise(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
+cudaError_t launch_flush(const NetDev &, const StateDev &, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
+uint32_t flush_bufs(uint32_t, uint32_t);
 cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
@@ -112,6 +114,7 @@ struct snn_sim {
     uint32_t stdp_grid = 1;              // k_stdp CTAs
     uint32_t pp_lo = 0, pp_hi = 0;       // post-plastic neuron range (bitmap span)
     bool plastic = false;
+    bool flush_kernel = false;           // event schedule, flushes at age H: k_flush
     uint64_t *d_hist_tmp = nullptr;
     // kernel spans (SNN_FLAG_KTIME): device slots, host totals per kernel:
     // [sum(end - entry) ns, sum(end - wait) ns, steps, CTAs]
@@ -517,6 +520,10 @@ static snn_status finalize(snn_sim *sim) {
         return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory", C, deliver_smem_bytes(net));
     if (sim->plastic && stdp_smem_bytes(net, sim->pp_lo, sim->pp_hi) > 227 * 1024)
         return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for the shared bitmap");
+    sim->flush_kernel = sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 &&
+                        flush_bufs(sim->pp_lo, sim->pp_hi) >= 2;
+    if (sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 && !sim->flush_kernel)
+        return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for k_flush's shared bitmap");
     // k_stdp flattens up to 128 rows' plastic spans (16-byte chunks) per round
     // into one uint32 chunk index
     if (sim->plastic && 128ull * ((uint64_t)net.N / 4 + 2) >= (1ull << 32))
@@ -554,8 +561,12 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
         if (r != SNN_OK) return r;
     }
     if (ev) CK(cudaEventRecord(ev[1], s));
-    if (sim->plastic)                                               // (2) P:37-39
+    if (sim->plastic) {                                             // (2) P:37-39
+        // the event schedule's forced flushes (age H) stream in k_flush; the
+        // plastic arrivals (and every visit of the other schedules) in k_stdp
+        if (sim->flush_kernel) CK(launch_flush(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
         CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
+    }
     if (ev) CK(cudaEventRecord(ev[2], s));
     if (net.deliv_mode == SNN_DELIV_ROWWISE) CK(launch_deliver_rowwise(net, st, sim->stdp_grid, s, pdl));   // Fig. 3a
     else CK(launch_deliver(net, st, sim->splits, s, pdl));          // (3) P:41, Fig. 3b
@@ -770,7 +781,7 @@ struct FieldRef {
     size_t bytes = 0, elem = 1;
     bool ring = false;   // SPIKE_RING: rows of nwords words, device stride ring_stride
     int64_t host_i64[8];
-    unsigned long long host_u64[16];
+    unsigned long long host_u64[4 * kKSpanKernels];
     double host_f64[8];
 };
 
@@ -843,7 +854,7 @@ static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool 
         case SNN_FIELD_PHASE_TIMES: f.host = f.host_f64; f.elem = 8; f.bytes = 8 * 8; break;
         case SNN_FIELD_KTIME:
             if (!sim->kspan) return sim->fail(SNN_E_STATE, "KTIME needs SNN_FLAG_KTIME");
-            f.host = f.host_u64; f.elem = 8; f.bytes = 8 * 16; break;
+            f.host = f.host_u64; f.elem = 8; f.bytes = 8 * 4 * kKSpanKernels; break;
         case SNN_FIELD_TRACE:
             if (!st.trace) return sim->fail(SNN_E_STATE, "trace needs SNN_FLAG_TRACE");
             f.dev = st.trace; f.elem = 8; f.bytes = 8ull * kTraceKernels * kTraceCtas * 4; break;

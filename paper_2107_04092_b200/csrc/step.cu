@@ -543,7 +543,8 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Vl = readout ? st.rdesc : st.vdesc[par];
     const uint32_t *lens = readout ? st.ctr->rlst : st.ctr->lst[par];
-    const uint32_t nA = lens[0], nF = readout ? 0u : lens[2];     // (k_front(t) complete)
+    // (k_front(t) complete).  The event schedule's forced flushes are k_flush's
+    const uint32_t nA = lens[0], nF = (readout || !kGeneric) ? 0u : lens[2];
     const size_t cap_back = (size_t)st.nblk * kFrontThreads - 1;   // forced flushes: from the back
     const uint32_t bm_bytes = 16u * ((w_hi - w_lo + 3) >> 2);
     if (threadIdx.x == 0) {   // bitmap of recently fired post neurons (one bulk copy; the barrier's initialiser)
@@ -563,6 +564,8 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     const uint32_t dp_addr = smem_u32(sm.dplus);
     if (!readout) trace_mark(st.trace, 1, 1);
     uint32_t n_syn = 0, n_w = 0, n_rw = 0;
+    unsigned long long dbg_wait = 0, dbg_busy = 0, dbg_n = 0, dbg_first = 0;   // (SNN_FLAG_TRACE only)
+    unsigned long long dbg_filt = 0, dbg_arr = 0;
     uint32_t g0 = 0;             // global stage index of the round's first stage (ring position)
     bool bm_ready = false;
     const uint64_t *__restrict__ ghist = st.hist;
@@ -614,7 +617,9 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 uint32_t pr = 0;
                 for (uint32_t s = 0; s < nst; s++) {
                     const uint32_t g = g0 + s, slot = g % kStdpStages;
+                    const unsigned long long tw0 = st.trace ? clock64() : 0ull;
                     mbar_wait(empty_a + 8 * slot, ((g / kStdpStages) & 1u) ^ 1u);
+                    if (st.trace) { dbg_wait += clock64() - tw0; dbg_n++; }
                     const uint32_t a = s * kStdpStageCh, b = min(a + kStdpStageCh, T);
                     const uint32_t fb = full_a + 8 * slot;
                     mbar_expect_tx(fb, 32u * (b - a));
@@ -651,7 +656,10 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                 const uint32_t sa = stage_a + slot * (kStdpStageCh * 32);
                 uint32_t hm = 0, rm = 0, slots = 0;   // 16-bit masks: list the synapse / target may hold a post spike
                 uint32_t am = 0;                      // 16-bit mask: synapses of arriving rows (updated in place)
+                const unsigned long long tw0 = st.trace ? clock64() : 0ull;
                 mbar_wait(full_a + 8 * slot, (g / kStdpStages) & 1u);
+                const unsigned long long tw1 = st.trace ? clock64() : 0ull;
+                if (st.trace) { dbg_wait += tw1 - tw0; dbg_n++; if (!dbg_first) dbg_first = gtimer(); }
 #pragma unroll
                 for (int u = 0; u < kStdpChPerThr; u++) {
                     const uint32_t c = a + gt + kStdpGroupThr * u;
@@ -688,6 +696,8 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                     }
                 }
                 n_rw += __popc(am) + __popc(hm);     // 8(d): weights read + written (arrival / window hit)
+                const unsigned long long tf1 = st.trace ? clock64() : 0ull;
+                if (st.trace) dbg_filt += tf1 - tw1;
                 // ---- arrivals (every synapse: history window + depression, Fig. 2c):
                 //      in place, two chunks (8 synapses) of gathers in flight per lane
                 if (__any_sync(0xffffffffu, am != 0u)) {
@@ -730,51 +740,9 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                         }
                     }
                 }
-                if constexpr (!kGeneric) {
-                    // ---- forced flushes (R3), in place.  Every forced flush of this
-                    //      step has age H, so all its synapses share the window
-                    //      (t - H, t]: a target j that fired in it gets
-                    //      w = min(w + A+ (x_pre fpot[j]), w_max) with fpot[j] = the sum
-                    //      over j's spikes s in the window of D+[H - s] (k_front; one
-                    //      spike: exactly the closed-form skip-ahead of Fig. 2c, P:284;
-                    //      several: their potentiations are all >= 0, so the sequential
-                    //      clamps are the one clamp of the sum).  The gathers of the
-                    //      thread's 16 synapses are in flight together, predicated off
-                    //      for the ~84 % of targets without a spike in the window.
-                    if (hm) {
-                        float fv[4 * kStdpChPerThr];
-#pragma unroll
-                        for (int u = 0; u < kStdpChPerThr; u++) {
-                            const uint32_t nib = (hm >> (4 * u)) & 0xfu;
-                            const uint4 j4 = nib ? lds_v4(sa + 16u * (gt + kStdpGroupThr * u)) : make_uint4(0, 0, 0, 0);
-                            fv[4 * u + 0] = ldg_f32_if(gfpot + j4.x, nib & 1u);
-                            fv[4 * u + 1] = ldg_f32_if(gfpot + j4.y, nib & 2u);
-                            fv[4 * u + 2] = ldg_f32_if(gfpot + j4.z, nib & 4u);
-                            fv[4 * u + 3] = ldg_f32_if(gfpot + j4.w, nib & 8u);
-                        }
-#pragma unroll
-                        for (int u = 0; u < kStdpChPerThr; u++) {
-                            const uint32_t nib = (hm >> (4 * u)) & 0xfu;
-                            if (!nib) continue;
-                            const uint32_t ch = gt + kStdpGroupThr * u;             // chunk in the stage
-                            const StdpRow &rr = sm.rows[(slots >> (8 * u)) & 0xffu];
-                            const float4 pr = sm.par[(rr.meta >> 12) & 0x3u];
-                            const uint4 w4 = lds_v4(sa + kStdpStageCh * 16 + 16u * ch);
-                            const float wv[4] = {__uint_as_float(w4.x), __uint_as_float(w4.y), __uint_as_float(w4.z),
-                                                 __uint_as_float(w4.w)};
-                            const int64_t off = rr.cb + 4ll * ((int64_t)(a + ch) - (int64_t)rr.first);
-#pragma unroll
-                            for (int e = 0; e < 4; e++) {
-                                if (!((nib >> e) & 1u)) continue;
-                                const float nw = __fadd_rn(wv[e], __fmul_rn(pr.x, __fmul_rn(rr.xp, fv[4 * u + e])));
-                                const float w = nw < pr.z ? nw : pr.z;
-                                const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
-                                stg_f32_if(gw + off + e, w, chg);
-                                n_w += chg;
-                            }
-                        }
-                    }
-                } else {
+                const unsigned long long ta1 = st.trace ? clock64() : 0ull;
+                if (st.trace) dbg_arr += ta1 - tf1;
+                if constexpr (kGeneric) {
                     // ---- list the selected synapses (warp-exclusive prefix of the counts)
                     const uint32_t k = __popc(hm);
                     uint32_t ex = k;
@@ -844,6 +812,7 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
                     __syncwarp();                              // list reused by the next pass
                     }
                 }
+                if (st.trace) dbg_busy += clock64() - tw1;
                 if (lane == 0) mbar_arrive(empty_a + 8 * slot);   // stage and list free
             }
         }
@@ -859,11 +828,246 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
         if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
         if (n_rw) atomicAdd(&st.ctr->metric[8], (unsigned long long)n_rw);
     }
+    if (st.trace && !readout && lane == 0 && (warp == 0 || warp == kStdpConsWarps)) {
+        // debug: consumer warp 0 / the producer: cycles waiting on full / empty
+        // stages, cycles busy on stages, stages, time of the first stage
+        unsigned long long *tr = st.trace + ((size_t)3 * kTraceCtas + blockIdx.x) * 4;
+        if (warp == 0) { tr[0] = dbg_wait; tr[1] = dbg_busy; tr[2] = dbg_n; tr[3] = dbg_first; }
+        else st.trace[((size_t)3 * kTraceCtas + 2048 + blockIdx.x) * 4] = dbg_wait;
+        if (warp == 0) { st.trace[((size_t)3 * kTraceCtas + 1024 + blockIdx.x) * 4] = dbg_filt;
+                         st.trace[((size_t)3 * kTraceCtas + 1024 + blockIdx.x) * 4 + 1] = dbg_arr; }
+    }
     if (!readout) {
         __syncthreads();
         trace_mark(st.trace, 1, 3);
         kspan_end(st.kspan, t, 1);
     }
+}
+
+// ------------------------------------------------------------------ k_flush
+// Forced flushes of the event schedule (R3, "(up to) 64 update steps"):
+// every plastic row whose age reached H at step t is brought up to t without
+// a pre spike.  All of them share the window (t - H, t], so synapse i -> j
+// changes only if j fired in it, by
+//     w = min(w + A+ (x_pre_i fpot[j]), w_max),
+// fpot[j] = sum over j's spikes s in the window of D+[H - s] (k_front; one
+// spike: the closed-form skip-ahead of Fig. 2c; several: potentiations
+// only, so the sequential clamps are one clamp of the sum).  The kernel is the
+// step's largest stream (4 B target id per synapse, 8 B weight
+// read + write where the target fired in the window), so it is built for
+// bytes in flight: 32 warps per SM, each owning a ring of three 2 KB segment
+// buffers that its lane 0 fills with TMA bulk copies (cp.async.bulk +
+// mbarrier) of the target ids of its next segments (128 16-byte chunks of
+// one row) while the warp filters the current one through the shared bitmap
+// of recently fired targets; the weights of the hits (~16 % at the bench's
+// rates) are gathered and updated in place, predicated.
+#ifndef SNN_FL_THREADS
+#define SNN_FL_THREADS 1024
+#endif
+constexpr int kFlThreads = SNN_FL_THREADS;
+constexpr int kFlWarps = kFlThreads / 32;
+constexpr int kFlRows = 256;        // row table per round
+constexpr int kFlSegCh = 128;       // 16-byte chunks per segment (4 per lane)
+constexpr int kFlBufs = 3;          // segment buffers per warp (at most; 2 when the bitmap needs the room)
+
+struct __align__(16) FlushRow {
+    int64_t cb;      // 16-byte aligned CSR offset of the plastic span
+    uint32_t lo, hi; // valid elements [lo, hi) relative to cb
+    float xp;        // x_pre at tlu (age H before t)
+    uint32_t si;     // STDP projection
+    uint32_t nch;    // 16-byte chunks
+    uint32_t pad;
+};
+struct FlushSmem {
+    uint64_t mbar[kFlWarps][kFlBufs];
+    FlushRow rows[kFlRows];
+    uint32_t incl[kFlRows];          // inclusive prefix of the rows' segment counts
+    uint32_t wsum[kFlWarps];
+    float4 par[4];                   // per projection: a_plus, a_minus, w_max
+};
+
+size_t flush_smem_bytes(uint32_t pp_lo, uint32_t pp_hi, uint32_t nb) {
+    const size_t head = (sizeof(FlushSmem) + 127) & ~(size_t)127;
+    const size_t bufs = (size_t)kFlWarps * nb * kFlSegCh * 16;
+    return head + bufs + 16ull * ((((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 3) >> 2);
+}
+
+// segment buffers per warp: 3 if they fit beside the bitmap, else 2 (0: none fit)
+uint32_t flush_bufs(uint32_t pp_lo, uint32_t pp_hi) {
+    for (uint32_t nb = kFlBufs; nb >= 2; nb--)
+        if (flush_smem_bytes(pp_lo, pp_hi, nb) <= 227u * 1024u) return nb;
+    return 0;
+}
+
+// segment sg of the round -> row slot (first r with incl[r] > sg; warp-uniform)
+__device__ __forceinline__ uint32_t flush_row_of(const uint32_t *incl, uint32_t nrows, uint32_t sg) {
+    uint32_t a = 0, b = nrows;
+    while (a < b) {
+        const uint32_t m = (a + b) >> 1;
+        if (incl[m] <= sg) a = m + 1; else b = m;
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(kFlThreads, 1)
+k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi, uint32_t nb) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
+    FlushSmem &sm = *reinterpret_cast<FlushSmem *>(smem);
+    unsigned char *buf_base = smem + ((sizeof(FlushSmem) + 127) & ~(size_t)127);
+    uint32_t *recent_s = reinterpret_cast<uint32_t *>(buf_base + (size_t)kFlWarps * nb * kFlSegCh * 16);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t w_lo = (pp_lo >> 7) << 2, w_hi = (pp_hi + 31) >> 5;     // 16-byte aligned start
+    const uint32_t mbar_a = smem_u32(&sm.mbar[warp][0]);
+    const uint32_t buf_a = smem_u32(buf_base) + warp * (nb * kFlSegCh * 16);
+    if (lane == 0) {
+        for (uint32_t b = 0; b < nb; b++) mbar_init(mbar_a + 8 * b, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < net.nstdp)
+        sm.par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
+                                          st.stdp[threadIdx.x].w_max, 0.0f);
+    // the step counter was advanced by k_deliver(t-1), complete before
+    // k_front(t) triggered this launch
+    const int64_t t = *(volatile const int64_t *)&st.ctr->t;
+    pdl_wait();            // k_front(t): the flush list, the bitmap, fpot
+    pdl_launch();
+    if (st.kspan) kspan_begin(st.kspan, t, 3, t_entry, gtimer());
+    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t nF = st.ctr->lst[par][2];
+    const uint32_t f_begin = (uint32_t)(((uint64_t)nF * blockIdx.x) / gridDim.x);
+    const uint32_t f_end = (uint32_t)(((uint64_t)nF * (blockIdx.x + 1)) / gridDim.x);
+    const size_t cap_back = (size_t)st.nblk * kFrontThreads - 1;      // forced flushes: from the back
+    for (uint32_t x = threadIdx.x; x < (w_hi - w_lo + 3) >> 2; x += kFlThreads)     // bitmap -> shared
+        reinterpret_cast<uint4 *>(recent_s)[x] = __ldg(reinterpret_cast<const uint4 *>(st.recent + w_lo) + x);
+    const uint32_t rs_addr = smem_u32(recent_s) - 4u * w_lo;      // bitmap word of neuron j: + 4 (j >> 5)
+    const float *__restrict__ gfpot = st.fpot;
+    float *__restrict__ gw = st.w;
+    uint32_t n_syn = 0, n_w = 0, n_rw = 0;
+    uint32_t phase_bits = 0;     // per buffer: mbarrier phase parity
+    for (uint32_t r0 = f_begin; r0 < f_end; r0 += kFlRows) {
+        const uint32_t nrows = min(f_end - r0, (uint32_t)kFlRows);
+        uint32_t nseg = 0;
+        if (threadIdx.x < nrows) {
+            const RowDesc d = st.vdesc[par][cap_back - (r0 + threadIdx.x)];
+            const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
+            FlushRow fr;
+            fr.cb = cs & ~3ll;
+            fr.lo = (uint32_t)(cs - fr.cb);
+            fr.hi = (uint32_t)(ce - fr.cb);
+            fr.xp = d.xp;
+            fr.si = (d.meta >> 12) & 0x3u;
+            fr.nch = (fr.hi + 3) >> 2;
+            fr.pad = 0;
+            // a flush with x_pre == 0 changes no weight (potentiation adds A+ 0, R31)
+            if (cs < ce && d.xp != 0.0f) {
+                nseg = (fr.nch + kFlSegCh - 1) / kFlSegCh;
+                n_syn += (uint32_t)(ce - cs);
+            }
+            sm.rows[threadIdx.x] = fr;
+        }
+        uint32_t S = 0;
+        const uint32_t inc = block_incl_scan<kFlThreads>(nseg, sm.wsum, S);
+        if (threadIdx.x < kFlRows) sm.incl[threadIdx.x] = inc;
+        __syncthreads();
+        // the warp's segments: warp, warp + 32, ...; lane 0 keeps kFlBufs in flight
+        const uint32_t my = S > warp ? (S - warp + kFlWarps - 1) / kFlWarps : 0u;
+        auto issue = [&](uint32_t k) {        // segment k of this warp -> buffer k % kFlBufs
+            const uint32_t sg = warp + k * kFlWarps;
+            const uint32_t r = flush_row_of(sm.incl, nrows, sg);
+            const FlushRow &fr = sm.rows[r];
+            const uint32_t c0 = (sg - (r ? sm.incl[r - 1] : 0u)) * kFlSegCh;
+            const uint32_t nch = min((uint32_t)kFlSegCh, fr.nch - c0);
+            const uint32_t b = k % nb;
+            mbar_expect_tx(mbar_a + 8 * b, 16u * nch);
+            bulk_g2s(buf_a + b * (kFlSegCh * 16), st.idx + fr.cb + 4ll * c0, 16u * nch, mbar_a + 8 * b);
+        };
+        if (lane == 0)
+            for (uint32_t k = 0; k < my && k < nb; k++) issue(k);
+        for (uint32_t k = 0; k < my; k++) {
+            const uint32_t sg = warp + k * kFlWarps;
+            const uint32_t r = flush_row_of(sm.incl, nrows, sg);
+            const FlushRow fr = sm.rows[r];
+            const uint32_t c0 = (sg - (r ? sm.incl[r - 1] : 0u)) * kFlSegCh;
+            const uint32_t b = k % nb;
+            mbar_wait(mbar_a + 8 * b, (phase_bits >> b) & 1u);
+            phase_bits ^= 1u << b;
+            const uint32_t ba = buf_a + b * (kFlSegCh * 16);
+            // filter: lane takes chunks c0 + lane + 32 u of the segment
+            uint32_t hm = 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t c = c0 + lane + 32u * u;
+                const bool ok = c < fr.nch;
+                const uint4 j4 = ok ? lds_v4(ba + 16u * (lane + 32u * u)) : make_uint4(pp_lo, pp_lo, pp_lo, pp_lo);
+                const uint32_t jj[4] = {j4.x, j4.y, j4.z, j4.w};
+                uint32_t inm = ok ? 0xfu : 0u;
+                const uint32_t x0 = 4u * c;
+                if (ok && (x0 < fr.lo || x0 + 4 > fr.hi)) {          // a row's first / last chunk
+                    inm = 0;
+#pragma unroll
+                    for (int e = 0; e < 4; e++) inm |= (uint32_t)(x0 + e >= fr.lo && x0 + e < fr.hi) << e;
+                }
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const uint32_t j = jj[e];
+                    const uint32_t bit = (lds_u32(rs_addr + ((j >> 5) << 2)) >> (j & 31)) & 1u;
+                    hm |= (bit & (inm >> e)) << (4 * u + e);
+                }
+            }
+            n_rw += __popc(hm);
+            // the hits' factors and weights, gathered together (predicated; the
+            // ids are read again from the buffer, which is refilled once the
+            // gathers are issued)
+            float fv[16], wv[16];
+            if (hm) {
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t nib = (hm >> (4 * u)) & 0xfu;
+                    const uint4 j4 = nib ? lds_v4(ba + 16u * (lane + 32u * u)) : make_uint4(0, 0, 0, 0);
+                    const uint32_t jj[4] = {j4.x, j4.y, j4.z, j4.w};
+                    const int64_t base = fr.cb + 4ll * (c0 + lane + 32u * u);
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const uint32_t on = (nib >> e) & 1u;
+                        fv[4 * u + e] = ldg_f32_if(gfpot + jj[e], on);
+                        wv[4 * u + e] = ldg_f32_if(gw + base + e, on);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0 && k + nb < my) issue(k + nb);   // buffer b read by every lane: refill
+            if (hm) {
+                const float4 pr = sm.par[fr.si];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int64_t base = fr.cb + 4ll * (c0 + lane + 32u * u);
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int q = 4 * u + e;
+                        if (!((hm >> q) & 1u)) continue;
+                        const float nw = __fadd_rn(wv[q], __fmul_rn(pr.x, __fmul_rn(fr.xp, fv[q])));
+                        const float w = nw < pr.z ? nw : pr.z;
+                        const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[q]) ? 1u : 0u;
+                        stg_f32_if(gw + base + e, w, chg);
+                        n_w += chg;
+                    }
+                }
+            }
+        }
+        __syncthreads();                           // row table reused next round
+    }
+    n_syn = __reduce_add_sync(0xffffffffu, n_syn);
+    n_w = __reduce_add_sync(0xffffffffu, n_w);
+    n_rw = __reduce_add_sync(0xffffffffu, n_rw);
+    if (lane == 0) {
+        if (n_syn) atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
+        if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
+        if (n_rw) atomicAdd(&st.ctr->metric[8], (unsigned long long)n_rw);
+        if (n_syn) atomicAdd(&st.ctr->metric[9], (unsigned long long)n_syn);
+        if (n_rw) atomicAdd(&st.ctr->metric[10], (unsigned long long)n_rw);
+    }
+    kspan_end(st.kspan, t, 3);
 }
 
 // --------------------------------------------------------------- k_deliver
@@ -1360,6 +1564,7 @@ cudaError_t kernels_configure(int device) {
         k_stdp<false, true, true>, k_stdp<true, false, true>, k_stdp<true, true, true>};
     for (auto k : ks)
         if ((e = set_max((const void *)k)) != cudaSuccess) return e;
+    if ((e = set_max((const void *)k_flush)) != cudaSuccess) return e;
     done.insert(device);
     return cudaSuccess;
 }
@@ -1367,13 +1572,22 @@ cudaError_t kernels_configure(int device) {
 cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, uint32_t grid, uint32_t pp_lo,
                         uint32_t pp_hi, cudaStream_t s, bool pdl) {
     const bool lazy = net.plast_mode == 1u, h128 = net.H > kHistBits;
-    const bool generic = t_fixed >= 0 || net.plast_mode != 0u;   // read-out flush, lazy, naive
+    // read-out flush, lazy, naive, batched flushes (rows of several ages): the
+    // per-target forced-flush factor assumes age H
+    const bool generic = t_fixed >= 0 || net.plast_mode != 0u || net.flush_period != 0u;
     void (*k)(NetDev, StateDev, int64_t, uint32_t, uint32_t) =
         lazy ? (h128 ? k_stdp<true, true, true> : k_stdp<true, false, true>)
              : generic ? (h128 ? k_stdp<false, true, true> : k_stdp<false, false, true>)
                        : (h128 ? k_stdp<false, true, false> : k_stdp<false, false, false>);
     return launch_pdl(k, dim3(grid), dim3(kStdpThreads), stdp_smem_bytes(net, pp_lo, pp_hi), s, pdl, net, st,
                       t_fixed, pp_lo, pp_hi);
+}
+
+cudaError_t launch_flush(const NetDev &net, const StateDev &st, uint32_t grid, uint32_t pp_lo, uint32_t pp_hi,
+                         cudaStream_t s, bool pdl) {
+    const uint32_t nb = flush_bufs(pp_lo, pp_hi);
+    return launch_pdl(k_flush, dim3(grid), dim3(kFlThreads), flush_smem_bytes(pp_lo, pp_hi, nb), s, pdl, net, st,
+                      pp_lo, pp_hi, nb);
 }
 
 cudaError_t launch_deliver_rowwise(const NetDev &net, const StateDev &st, uint32_t grid, cudaStream_t s, bool pdl) {

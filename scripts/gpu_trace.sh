@@ -1,2 +1,3 @@
-python -c "import __graft_entry__ as g; g.build()"
-for C in 0 2048 512; do echo "== C=$C"; python scripts/trace.py 3 $C; done > gpurun_out/trace.log 2>&1
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 300 python scripts/trace.py 3 0 > gpurun_out/trace.log 2>&1; echo trace=$?
+cat gpurun_out/trace.log

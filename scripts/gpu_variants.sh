@@ -1,7 +1,20 @@
-# A/B of compile-time variants: bash scripts/gpu_variants.sh "" "-DSNN_X=1" ...
-# (each: rebuild with SNN_NVCC_EXTRA, GPU tests, one config-3 bench line)
-for v in "$@"; do
-  SNN_NVCC_EXTRA="$v" python paper_2107_04092_b200/build_ext.py --force > gpurun_out/build_variant.log 2>&1 || { echo "BUILD FAIL [$v]"; tail -5 gpurun_out/build_variant.log; continue; }
-  r=$(timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1)
-  timeout 300 python bench.py --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('[$v]', '$r', 'us/step', round(d['ms_per_step']*1e3,2), {k: round(v*1e3,2) for k,v in d['roofline']['phase_ms_per_step'].items() if k in ('FRONT','STDP','DELIVERY')})"
+# build + short bench of compile-time variants: VARIANTS="name1:-DX=1 name2:-DY=2"
+set -x
+for v in $VARIANTS; do
+  name=${v%%:*}; flags=${v#*:}; flags=${flags//,/ }
+  rm -f paper_2107_04092_b200/libsnn.so
+  SNN_NVCC_EXTRA="$flags" python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$name.log 2>&1 || { echo "$name build failed"; continue; }
+  timeout 300 python bench.py --steps ${VSTEPS:-3000} --warmup 300 --no-cpu-baseline --no-e2e ${BENCH_ARGS} > gpurun_out/var_$name.json 2> gpurun_out/var_$name.err
+  python - "$name" <<'PY'
+import json, sys
+n = sys.argv[1]
+try:
+    d = json.loads(open(f"gpurun_out/var_{n}.json").read().strip().splitlines()[-1])
+    ks = d["kernel_spans"]
+    print(f"VARIANT {n}: ms/step {d['ms_per_step']*1e3:.2f} us  " + " ".join(f"{k}={ks[k]['us_from_wait']:.2f}" for k in ks if isinstance(ks[k], dict)))
+except Exception as e:
+    print("VARIANT", n, "failed", e, open(f"gpurun_out/var_{n}.err").read()[-500:])
+PY
 done
+rm -f paper_2107_04092_b200/libsnn.so
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1

@@ -1,6 +1,7 @@
-"""Per-CTA phase trace of one simulation step (debug, SNN_FLAG_TRACE)."""
+"""Per-CTA phase trace of simulation steps (debug, SNN_FLAG_TRACE; direct launches)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import json as _json
 import numpy as np
 import torch
 import workloads as W
@@ -10,21 +11,16 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 C = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 rc = W.config(cfg)
 extra = int(os.environ.get("SNN_TRACE_FLAGS", "0"))
-import json as _json
 kw = _json.loads(os.environ.get("SNN_TRACE_KW", "{}"))      # e.g. {"flush_period": 16}
 g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, flags=FLAG_TRACE | extra, **kw)
 rc.apply(g)
-g.step(int(os.environ.get("SNN_TRACE_T0", "1500")))
+g.step(int(os.environ.get("SNN_TRACE_T0", "3000")))
 torch.cuda.synchronize()
-dbg = os.environ.pop("SNN_TRACE_DEBUG", None)
 for rep in range(3):
-    if dbg is not None:
-        os.environ["SNN_DEBUG_KERNELS"] = dbg     # kernel experiment on the traced steps only
     g.step(1)
-    os.environ.pop("SNN_DEBUG_KERNELS", None)
     tr = g.read_state("TRACE").reshape(4, 4096, 4).astype(np.int64)
     t0 = tr[0][tr[0][:, 0] > 0][:, 0].min()
-    for k, name in [(0, "front"), (3, "stdp_arr"), (2, "deliver"), (1, "stdp")]:
+    for k, name in [(0, "front"), (2, "deliver"), (1, "stdp")]:
         a = tr[k]
         a = a[a[:, 0] > 0]
         if len(a) == 0:
@@ -33,4 +29,12 @@ for rep in range(3):
         print(f"{name:8s} ctas={len(a):4d} start[min/med/max]={rel[:,0].min():7.2f}/{np.median(rel[:,0]):7.2f}/{rel[:,0].max():7.2f} "
               + " ".join(f"ph{p}[med/max]={np.median(rel[:,p]-rel[:,0]):6.2f}/{(rel[:,p]-rel[:,0]).max():6.2f}" for p in (1, 2, 3))
               + f" end_max={rel[:,3].max():7.2f}")
+    d = tr[3][:148]
+    prod = tr[3][2048:2048 + 148, 0]
+    ghz = 1.965
+    first = (d[:, 3] - t0) / 1000.0
+    print(f"stdp consumer warp0: wait_us med={np.median(d[:,0])/ghz/1e3:.2f} busy_us med={np.median(d[:,1])/ghz/1e3:.2f} "
+          f"stages med={np.median(d[:,2]):.0f} max={d[:,2].max()} first_stage_at med={np.median(first):.2f} "
+          f"producer empty-wait_us med={np.median(prod)/ghz/1e3:.2f} filter_us med={np.median(tr[3][1024:1172,0])/ghz/1e3:.2f} "
+          f"arrivals_us med={np.median(tr[3][1024:1172,1])/ghz/1e3:.2f}")
     print(g.metrics())
