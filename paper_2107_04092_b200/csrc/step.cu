@@ -1009,8 +1009,8 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi, uint32_t nb) {
                     for (int e = 0; e < 4; e++) inm |= (uint32_t)(x0 + e >= fr.lo && x0 + e < fr.hi) << e;
                 }
 #pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const uint32_t j = jj[e];
+                for (int e = 0; e < 4; e++) {       // (outside the span: a neighbour's target, maybe no post neuron)
+                    const uint32_t j = ((inm >> e) & 1u) ? jj[e] : pp_lo;
                     const uint32_t bit = (lds_u32(rs_addr + ((j >> 5) << 2)) >> (j & 31)) & 1u;
                     hm |= (bit & (inm >> e)) << (4 * u + e);
                 }
