@@ -43,7 +43,7 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 METRIC = "wall-s per bio-second & synaptic events/s at 1/2/4/8 B200; % HBM roofline"
-KERNEL_OF = {"front": "k_front", "stdp": "k_stdp", "deliver": "k_deliver", "flush": "k_flush"}
+KERNEL_OF = {"front": "k_front", "stdp": "k_stdp_ev", "deliver": "k_deliver"}
 
 
 def parse(argv=None):
@@ -318,7 +318,7 @@ def main(argv=None):
         del sk
         spans = {"same_window": bool(reduce(0.0 if same else 1.0, MAX) == 0.0),
                  "ms_per_step_instrumented": ms_k / a.steps}
-        for k in ("front", "stdp", "deliver", "flush"):
+        for k in ("front", "stdp", "deliver"):
             st = k1[k]["steps"] - k0[k]["steps"]
             if st <= 0:
                 continue
@@ -368,7 +368,7 @@ def main(argv=None):
     nrcpt = 2 if any(pr.receptor == W.INH for pr in rc.projs) else 1
     K = a.steps
     # algorithmic HBM bytes per launch:
-    #   k_flush / k_stdp (forced flushes / plastic arrivals): 4 B target id per
+    #   k_stdp_ev (k_stdp for the ablation schedules): 4 B target id per
     #              visited plastic synapse + 8 B (weight read and written) per
     #              synapse of an arriving row or whose target fired in the
     #              window + 16 B per visited row
@@ -377,11 +377,8 @@ def main(argv=None):
     #              neuron and receptor written back
     #   k_front:   32 B per LIF neuron, 16 B per Poisson neuron (8(a1))
     n_pois = sum(p.n for p in rc.pops if p.kind == W.POISSON)
-    fl_rows = dm_local["FLUSH_ROWS"] if dm_local["FLUSH_SYN"] else 0
     kb = {
-        "flush": (4 * dm_local["FLUSH_SYN"] + 8 * dm_local["FLUSH_WRW"] + 16 * fl_rows) / K,
-        "stdp": (4 * (dm_local["STDP_SYN"] - dm_local["FLUSH_SYN"]) + 8 * (dm_local["STDP_WRW"] - dm_local["FLUSH_WRW"])
-                 + 16 * (dm_local["STDP_ROWS"] - fl_rows)) / K,
+        "stdp": (4 * dm_local["STDP_SYN"] + 8 * dm_local["STDP_WRW"] + 16 * dm_local["STDP_ROWS"]) / K,
         "deliver": ((6 if a.idx16 else 8) * dm_local["EVENTS"] + 8 * dm_local["SPIKES"] * info["nslices"]) / K
                    + 4 * nrcpt * (info["tgt_hi"] - info["tgt_lo"]),
         "front": 32.0 * (info["N"] - n_pois) + 16.0 * n_pois,
@@ -402,9 +399,13 @@ def main(argv=None):
                        if on)
     roof = None
     if dom:
-        dk = KERNEL_OF[dom] if not (dom == "deliver" and a.delivery == "rowwise") else "k_deliver_rowwise"
+        dk = KERNEL_OF[dom]
+        if dom == "deliver" and a.delivery == "rowwise":
+            dk = "k_deliver_rowwise"
+        if dom == "stdp" and (a.plasticity != "event" or a.flush_period):
+            dk = "k_stdp"
         traffic, traffic_src = ncu_traffic(dk, a.config, flags_s)
-        sd = [k for k in ("flush", "stdp", "deliver") if k in kern]
+        sd = [k for k in ("stdp", "deliver") if k in kern]
         sd_b = sum(kern[k]["bytes_per_launch"] for k in sd)
         sd_us = sum(kern[k]["us_per_launch"] for k in sd)
         step_b = sum(kb.values())

@@ -232,7 +232,7 @@ enum {
     SNN_FIELD_RECENT = 25,      /* [u32 / ceil(N/32)] bit j: post-plastic neuron
                                    j fired in the last H steps                   */
     SNN_FIELD_KTIME = 26,       /* [u64 / 20] per kernel k (front, stdp, deliver,
-                                   flush, lists): [4k] sum over steps of (last CTA end -
+                                   spare, lists): [4k] sum over steps of (last CTA end -
                                    first CTA entry) ns, [4k+1] sum of (last end -
                                    first return from the dependency wait) ns,
                                    [4k+2] steps, [4k+3] CTAs; cumulative
@@ -255,14 +255,14 @@ enum {
                                     must read and write: every
                                     synapse of an arriving row, and forced-flush
                                     synapses whose target fired in the window     */
-    SNN_METRIC_FLUSH_SYN = 9,    /* of STDP_SYN: synapses streamed by k_flush      */
-    SNN_METRIC_FLUSH_WRW = 10    /* of STDP_WRW: k_flush's window hits             */
+    SNN_METRIC_FLUSH_SYN = 9,    /* of STDP_SYN: forced-flush synapses (event schedule) */
+    SNN_METRIC_FLUSH_WRW = 10    /* of STDP_WRW: their window hits                 */
 };
 
 /* SNN_FIELD_PHASE_TIMES layout: the kernels of a step */
 enum {
     SNN_PHASE_FRONT = 0,    /* neuron update + firing bits + work lists       */
-    SNN_PHASE_STDP = 1,     /* lazy + event-driven STDP (k_flush + k_stdp)     */
+    SNN_PHASE_STDP = 1,     /* lazy + event-driven STDP                       */
     SNN_PHASE_DELIVERY = 2, /* sliced shared-atomic delivery                  */
     SNN_PHASE_EXCHANGE = 3, /* spike-bitmask all-gather (world > 1)           */
     SNN_PHASE_TOTAL = 4,

@@ -155,7 +155,7 @@ struct KSpan {
     unsigned long long entry, wait, end, ctas;
 };
 constexpr uint32_t kKSpanSlots = 65536;   // steps between two read-outs
-constexpr int kKSpanKernels = 5;          // front, stdp, deliver, flush, lists (world > 1, D = 0)
+constexpr int kKSpanKernels = 5;          // front, stdp, deliver, (spare), lists (world > 1, D = 0)
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long g = 0;
 #ifdef __CUDA_ARCH__

@@ -34,8 +34,8 @@ cudaError_t kernels_configure(int);
 cudaError_t launch_kspan_reset(KSpan *, cudaStream_t);
 cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
 cudaError_t launch_deliver_rowwise(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
-cudaError_t launch_flush(const NetDev &, const StateDev &, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
-uint32_t flush_bufs(uint32_t, uint32_t);
+cudaError_t launch_stdp_ev(const NetDev &, const StateDev &, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
+uint32_t ev_bufs(uint32_t, uint32_t);
 cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
@@ -114,7 +114,7 @@ struct snn_sim {
     uint32_t stdp_grid = 1;              // k_stdp CTAs
     uint32_t pp_lo = 0, pp_hi = 0;       // post-plastic neuron range (bitmap span)
     bool plastic = false;
-    bool flush_kernel = false;           // event schedule, flushes at age H: k_flush
+    bool ev_kernel = false;              // event schedule, flushes at age H: k_stdp_ev
     uint64_t *d_hist_tmp = nullptr;
     // kernel spans (SNN_FLAG_KTIME): device slots, host totals per kernel:
     // [sum(end - entry) ns, sum(end - wait) ns, steps, CTAs]
@@ -520,10 +520,10 @@ static snn_status finalize(snn_sim *sim) {
         return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory", C, deliver_smem_bytes(net));
     if (sim->plastic && stdp_smem_bytes(net, sim->pp_lo, sim->pp_hi) > 227 * 1024)
         return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for the shared bitmap");
-    sim->flush_kernel = sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 &&
-                        flush_bufs(sim->pp_lo, sim->pp_hi) >= 2;
-    if (sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 && !sim->flush_kernel)
-        return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for k_flush's shared bitmap");
+    sim->ev_kernel = sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 &&
+                     ev_bufs(sim->pp_lo, sim->pp_hi) >= 2;
+    if (sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 && !sim->ev_kernel)
+        return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for k_stdp_ev's shared bitmap");
     // k_stdp flattens up to 128 rows' plastic spans (16-byte chunks) per round
     // into one uint32 chunk index
     if (sim->plastic && 128ull * ((uint64_t)net.N / 4 + 2) >= (1ull << 32))
@@ -562,10 +562,10 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     }
     if (ev) CK(cudaEventRecord(ev[1], s));
     if (sim->plastic) {                                             // (2) P:37-39
-        // the event schedule's forced flushes (age H) stream in k_flush; the
-        // plastic arrivals (and every visit of the other schedules) in k_stdp
-        if (sim->flush_kernel) CK(launch_flush(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
-        CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
+        // the event schedule (flushes at age H): k_stdp_ev; the ablation
+        // schedules and batched flushes: the generic k_stdp
+        if (sim->ev_kernel) CK(launch_stdp_ev(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
+        else CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
     }
     if (ev) CK(cudaEventRecord(ev[2], s));
     if (net.deliv_mode == SNN_DELIV_ROWWISE) CK(launch_deliver_rowwise(net, st, sim->stdp_grid, s, pdl));   // Fig. 3a
