@@ -35,7 +35,7 @@ cudaError_t launch_kspan_reset(KSpan *, cudaStream_t);
 cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
 cudaError_t launch_deliver_rowwise(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_stdp_ev(const NetDev &, const StateDev &, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
-uint32_t ev_bufs(uint32_t, uint32_t);
+size_t ev_smem_bytes(uint32_t, uint32_t);
 cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
 cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
@@ -521,7 +521,7 @@ static snn_status finalize(snn_sim *sim) {
     if (sim->plastic && stdp_smem_bytes(net, sim->pp_lo, sim->pp_hi) > 227 * 1024)
         return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for the shared bitmap");
     sim->ev_kernel = sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 &&
-                     ev_bufs(sim->pp_lo, sim->pp_hi) >= 2;
+                     ev_smem_bytes(sim->pp_lo, sim->pp_hi) <= 227 * 1024;
     if (sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 && !sim->ev_kernel)
         return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for k_stdp_ev's shared bitmap");
     // k_stdp flattens up to 128 rows' plastic spans (16-byte chunks) per round

@@ -845,14 +845,15 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
 }
 
 // --------------------------------------------------------------- k_stdp_ev
-// Lazy + event-driven STDP of the event schedule (Fig. 2c): the
-// step's visited plastic rows -- plastic arrivals A(t) and forced flushes F(t)
-// (R3) -- cut into segments of kEvSegCh 16-byte chunks (4 synapses each) of
-// one row.  The kernel is the step's largest stream (4 B target
-// id per visited synapse, 8 B weight read + write where it can change), so it
-// is built for bytes in flight: every warp owns a ring of segment buffers that
-// its lane 0 fills with TMA bulk copies (cp.async.bulk + mbarrier) of the next
-// segments' target ids and weights while the warp works on the current one.
+// Lazy + event-driven STDP of the event schedule (Fig. 2c) over the
+// step's visited plastic rows: plastic arrivals A(t), then forced flushes F(t)
+// (R3).  The kernel is the step's largest stream (4 B target id
+// per visited synapse, 8 B weight where it can change), so it is built as a
+// plain stream with many bytes in flight: each CTA flattens its share of the
+// rows into 16-byte chunks (4 synapses); thread x takes chunks x + kEvT u
+// (consecutive threads: consecutive chunks, coalesced 16-byte loads of ids
+// and weights), kEvU chunks per iteration, the next iteration's loads issued
+// before the current one's gathers (double-buffered registers).
 //  * forced flush (age H): every flush of the step shares the window
 //    (t - H, t], so synapse i -> j changes only if j fired in it (shared
 //    bitmap probe), by w = min(w + A+ (x_pre_i fpot[j]), w_max) with
@@ -861,79 +862,223 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
 //    so the sequential clamps are one clamp of the sum);
 //  * arrival: the window (tlu, t] of the target's history, oldest spike first
 //    with __clz, then the pre spike's depression by x_post[j].
-// Hits gather their factor / history and x_post (L2-resident per-neuron
-// arrays) predicated, and store the weights that changed.
+// Only weights that change are stored.
 #ifndef SNN_EV_THREADS
-#define SNN_EV_THREADS 768
+#define SNN_EV_THREADS 512
 #endif
-#ifndef SNN_EV_SEGCH
-#define SNN_EV_SEGCH 64
-#endif
-constexpr int kEvThreads = SNN_EV_THREADS;
-constexpr int kEvWarps = kEvThreads / 32;
+constexpr int kEvT = SNN_EV_THREADS;
+constexpr int kEvWarps = kEvT / 32;
 constexpr int kEvRows = 256;                 // row table per round
-constexpr int kEvSegCh = SNN_EV_SEGCH;       // 16-byte chunks per segment
-constexpr int kEvU = kEvSegCh / 32;          // chunks per lane and segment
-constexpr int kEvBufs = 3;                   // segment buffers per warp (at most; 2 when the bitmap needs the room)
-constexpr int kEvBufBytes = kEvSegCh * 32;   // ids + weights
+constexpr int kEvU = 2;                      // chunks per thread and iteration
 
 struct __align__(16) EvRow {
     int64_t cb;      // 16-byte aligned CSR offset of the plastic span
     uint32_t lo, hi; // valid elements [lo, hi) relative to cb
     float xp;        // x_pre at tlu
     uint32_t meta;   // age, arrival bit, STDP projection (RowDesc::meta)
-    uint32_t nch;    // 16-byte chunks
+    uint32_t first;  // flattened index of its first chunk
     uint32_t pad;
 };
 struct EvSmem {
-    uint64_t mbar[kEvWarps][kEvBufs];
     EvRow rows[kEvRows];
-    uint32_t incl[kEvRows];          // inclusive prefix of the rows' segment counts
+    uint32_t incl[kEvRows + 1];      // inclusive prefix of the rows' chunk counts
     uint32_t wsum[kEvWarps];
     float4 par[4];                   // per projection: a_plus, a_minus, w_max
     float dplus[4 * (kMaxHist + 1)];
 };
 
-size_t ev_smem_bytes(uint32_t pp_lo, uint32_t pp_hi, uint32_t nb) {
-    const size_t head = (sizeof(EvSmem) + 127) & ~(size_t)127;
-    const size_t bufs = (size_t)kEvWarps * nb * kEvBufBytes;
-    return head + bufs + 16ull * ((((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 3) >> 2);
+size_t ev_smem_bytes(uint32_t pp_lo, uint32_t pp_hi) {
+    return ((sizeof(EvSmem) + 15) & ~(size_t)15) + 16ull * ((((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 3) >> 2);
 }
 
-// segment buffers per warp: 3 if they fit beside the bitmap, else 2 (0: none fit)
-uint32_t ev_bufs(uint32_t pp_lo, uint32_t pp_hi) {
-    for (uint32_t nb = kEvBufs; nb >= 2; nb--)
-        if (ev_smem_bytes(pp_lo, pp_hi, nb) <= 227u * 1024u) return nb;
-    return 0;
-}
+// One iteration's loads: chunk c (c < T) of the CTA's flattened rows; r walks
+// forward (a thread's chunks increase).
+struct EvLoad {
+    uint4 j, w;
+    uint32_t r, x0;   // row slot, element offset of the chunk in the row (rel. cb)
+};
 
-// segment sg of the round -> row slot (first r with incl[r] > sg; warp-uniform)
-__device__ __forceinline__ uint32_t ev_row_of(const uint32_t *incl, uint32_t nrows, uint32_t sg) {
-    uint32_t a = 0, b = nrows;
-    while (a < b) {
-        const uint32_t m = (a + b) >> 1;
-        if (incl[m] <= sg) a = m + 1; else b = m;
+template <bool kH128, bool kArr>
+__device__ __forceinline__ void ev_load(const EvSmem &sm, const uint32_t *__restrict__ idx, const float *__restrict__ w,
+                                        uint32_t c, uint32_t T, uint32_t &cur, EvLoad &L) {
+    if (c < T) {
+        while (c >= sm.incl[cur]) cur++;
+        const EvRow &er = sm.rows[cur];
+        L.r = cur;
+        L.x0 = 4u * (c - er.first);
+        const int64_t off = er.cb + L.x0;
+        L.j = __ldg(reinterpret_cast<const uint4 *>(idx + off));
+        L.w = __ldg(reinterpret_cast<const uint4 *>(w + off));
+    } else {
+        L.r = 0xffffffffu;
+        L.x0 = 0;
+        L.j = make_uint4(0, 0, 0, 0);
+        L.w = make_uint4(0, 0, 0, 0);
     }
-    return a;
+}
+
+template <bool kH128, bool kArr>
+__device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st, const EvLoad (&L)[kEvU],
+                                           uint32_t rs_addr, uint32_t dp_addr, uint32_t pp_lo, uint32_t &n_w,
+                                           uint32_t &n_rw) {
+    // filter: hm = targets that fired in the last H steps, im = inside the row's span
+    uint32_t hm = 0, im = 0;
+#pragma unroll
+    for (int u = 0; u < kEvU; u++) {
+        if (L[u].r == 0xffffffffu) continue;
+        const EvRow &er = sm.rows[L[u].r];
+        uint32_t inm = 0xfu;
+        if (L[u].x0 < er.lo || L[u].x0 + 4 > er.hi) {                // a row's first / last chunk
+            inm = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) inm |= (uint32_t)(L[u].x0 + e >= er.lo && L[u].x0 + e < er.hi) << e;
+        }
+        const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {       // (outside the span: a neighbour's target, maybe no post neuron)
+            const uint32_t j = ((inm >> e) & 1u) ? jj[e] : pp_lo;
+            const uint32_t bit = (lds_u32(rs_addr + ((j >> 5) << 2)) >> (j & 31)) & 1u;
+            hm |= (bit & (inm >> e)) << (4 * u + e);
+        }
+        im |= inm << (4 * u);
+    }
+    if (!kArr) {
+        // ---- forced flushes: the hits' factors (predicated gathers), in place
+        if (!hm) return;
+        n_rw += __popc(hm);
+        float fv[4 * kEvU];
+#pragma unroll
+        for (int u = 0; u < kEvU; u++) {
+            const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) fv[4 * u + e] = ldg_f32_if(st.fpot + jj[e], (hm >> (4 * u + e)) & 1u);
+        }
+#pragma unroll
+        for (int u = 0; u < kEvU; u++) {
+            const uint32_t nib = (hm >> (4 * u)) & 0xfu;
+            if (!nib) continue;
+            const EvRow &er = sm.rows[L[u].r];
+            const float4 pr = sm.par[(er.meta >> 12) & 0x3u];
+            const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
+                                 __uint_as_float(L[u].w.w)};
+            float *wp = st.w + er.cb + L[u].x0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                if (!((nib >> e) & 1u)) continue;
+                const float nw = __fadd_rn(wv[e], __fmul_rn(pr.x, __fmul_rn(er.xp, fv[4 * u + e])));
+                const float w = nw < pr.z ? nw : pr.z;
+                const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
+                stg_f32_if(wp + e, w, chg);
+                n_w += chg;
+            }
+        }
+    } else {
+        // ---- arrivals (Fig. 2c): every synapse; the history window (tlu, t]
+        //      of the targets that fired lately, x_post of all
+        if (!im) return;
+        n_rw += __popc(im);
+        uint64_t hh[4 * kEvU], hh2[4 * kEvU];
+        float xq[4 * kEvU];
+#pragma unroll
+        for (int u = 0; u < kEvU; u++) {
+            const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const uint32_t on = (im >> (4 * u + e)) & 1u, rec = on & (hm >> (4 * u + e));
+                hh[4 * u + e] = ldg_u64_if(st.hist + jj[e], rec);
+                hh2[4 * u + e] = kH128 ? ldg_u64_if(st.hist_hi + jj[e], rec) : 0ull;
+                xq[4 * u + e] = ldg_f32_if(st.xpost + jj[e], on);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kEvU; u++) {
+            const uint32_t nib = (im >> (4 * u)) & 0xfu;
+            if (!nib) continue;
+            const EvRow &er = sm.rows[L[u].r];
+            const uint32_t si = (er.meta >> 12) & 0x3u;
+            const float4 pr = sm.par[si];
+            const int age = (int)(er.meta & kMetaAge);
+            const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+            const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
+                                 __uint_as_float(L[u].w.w)};
+            float *wp = st.w + er.cb + L[u].x0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                if (!((nib >> e) & 1u)) continue;
+                const int q = 4 * u + e;
+                const float w = stdp_synapse(wv[e], window_lo(hh[q], age), true, xq[q], er.xp, age, dp, pr.x, pr.y,
+                                             pr.z, window_hi(hh2[q], age));   // (tlu, t], R2
+                const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
+                stg_f32_if(wp + e, w, chg);
+                n_w += chg;
+            }
+        }
+    }
+}
+
+// The CTA's rows of one kind (arrivals or flushes) in rounds of kEvRows.
+template <bool kH128, bool kArr>
+__device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const RowDesc *Vl, uint32_t nrows_all,
+                                        bool from_back, size_t base, uint32_t rs_addr, uint32_t dp_addr,
+                                        uint32_t pp_lo, uint32_t &n_syn, uint32_t &n_w, uint32_t &n_rw) {
+    for (uint32_t r0 = 0; r0 < nrows_all; r0 += kEvRows) {
+        const uint32_t nrows = min(nrows_all - r0, (uint32_t)kEvRows);
+        uint32_t nch = 0;
+        EvRow er;
+        if (threadIdx.x < nrows) {
+            const RowDesc d = Vl[from_back ? base - (r0 + threadIdx.x) : base + r0 + threadIdx.x];
+            const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
+            er.cb = cs & ~3ll;
+            er.lo = (uint32_t)(cs - er.cb);
+            er.hi = (uint32_t)(ce - er.cb);
+            er.xp = d.xp;
+            er.meta = d.meta;
+            er.pad = 0;
+            // a flush with x_pre == 0 changes no weight (potentiation adds A+ 0, R31)
+            if (cs < ce && (kArr || d.xp != 0.0f)) {
+                nch = (er.hi + 3) >> 2;
+                n_syn += (uint32_t)(ce - cs);
+            }
+        }
+        uint32_t T = 0;
+        const uint32_t inc = block_incl_scan<kEvT>(nch, sm.wsum, T);
+        if (threadIdx.x < nrows) {
+            er.first = inc - nch;
+            sm.rows[threadIdx.x] = er;
+            sm.incl[threadIdx.x] = inc;
+        }
+        if (threadIdx.x == 0) sm.incl[nrows] = 0xffffffffu;      // (the walk never passes the last row)
+        __syncthreads();
+        uint32_t cur = 0;
+        EvLoad A[kEvU], B[kEvU];
+#pragma unroll
+        for (int u = 0; u < kEvU; u++) ev_load<kH128, kArr>(sm, st.idx, st.w, threadIdx.x + kEvT * u, T, cur, A[u]);
+        for (uint32_t c0 = 0; c0 < T; c0 += 2 * kEvT * kEvU) {
+            // B: the next iteration's loads in flight while A is processed, and back
+#pragma unroll
+            for (int u = 0; u < kEvU; u++)
+                ev_load<kH128, kArr>(sm, st.idx, st.w, c0 + kEvT * (kEvU + u) + threadIdx.x, T, cur, B[u]);
+            ev_process<kH128, kArr>(sm, st, A, rs_addr, dp_addr, pp_lo, n_w, n_rw);
+            if (c0 + kEvT * kEvU >= T) break;
+#pragma unroll
+            for (int u = 0; u < kEvU; u++)
+                ev_load<kH128, kArr>(sm, st.idx, st.w, c0 + kEvT * (2 * kEvU + u) + threadIdx.x, T, cur, A[u]);
+            ev_process<kH128, kArr>(sm, st, B, rs_addr, dp_addr, pp_lo, n_w, n_rw);
+        }
+        __syncthreads();                           // row table reused next round
+    }
 }
 
 template <bool kH128>
-__global__ void __launch_bounds__(kEvThreads, 1)
-k_stdp_ev(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi, uint32_t nb) {
+__global__ void __launch_bounds__(kEvT, 1)
+k_stdp_ev(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
     extern __shared__ __align__(16) unsigned char smem[];
     const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
     EvSmem &sm = *reinterpret_cast<EvSmem *>(smem);
-    unsigned char *buf_base = smem + ((sizeof(EvSmem) + 127) & ~(size_t)127);
-    uint32_t *recent_s = reinterpret_cast<uint32_t *>(buf_base + (size_t)kEvWarps * nb * kEvBufBytes);
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *recent_s = reinterpret_cast<uint32_t *>(smem + ((sizeof(EvSmem) + 15) & ~(size_t)15));
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t w_lo = (pp_lo >> 7) << 2, w_hi = (pp_hi + 31) >> 5;     // 16-byte aligned start
-    const uint32_t mbar_a = smem_u32(&sm.mbar[warp][0]);
-    const uint32_t buf_a = smem_u32(buf_base) + warp * (nb * kEvBufBytes);
-    if (lane == 0) {
-        for (uint32_t b = 0; b < nb; b++) mbar_init(mbar_a + 8 * b, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kEvThreads)
+    for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kEvT)
         sm.dplus[x] = st.stdp[x / (kMaxHist + 1)].dplus[x % (kMaxHist + 1)];
     if (threadIdx.x < net.nstdp)
         sm.par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
@@ -943,196 +1088,41 @@ k_stdp_ev(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi, uint32_t nb) 
     const int64_t t = *(volatile const int64_t *)&st.ctr->t;
     pdl_wait();            // k_front(t): lists, histories, bitmap, fpot
     pdl_launch();          // k_deliver may start its tabulation (k_front is complete)
+    trace_mark(st.trace, 1, 0);
     if (st.kspan) kspan_begin(st.kspan, t, 1, t_entry, gtimer());
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Vl = st.vdesc[par];
     const uint32_t nA = st.ctr->lst[par][0], nF = st.ctr->lst[par][2];
     const size_t cap_back = (size_t)st.nblk * kFrontThreads - 1;      // forced flushes: from the back
-    // even shares of each kind over the CTAs: [0, nAb) arrivals, then flushes
     const uint32_t a_begin = (uint32_t)(((uint64_t)nA * blockIdx.x) / gridDim.x);
     const uint32_t a_end = (uint32_t)(((uint64_t)nA * (blockIdx.x + 1)) / gridDim.x);
     const uint32_t f_begin = (uint32_t)(((uint64_t)nF * blockIdx.x) / gridDim.x);
     const uint32_t f_end = (uint32_t)(((uint64_t)nF * (blockIdx.x + 1)) / gridDim.x);
-    const uint32_t nAb = a_end - a_begin, r_end = nAb + (f_end - f_begin);
-    for (uint32_t x = threadIdx.x; x < (w_hi - w_lo + 3) >> 2; x += kEvThreads)     // bitmap -> shared
+    for (uint32_t x = threadIdx.x; x < (w_hi - w_lo + 3) >> 2; x += kEvT)     // bitmap -> shared
         reinterpret_cast<uint4 *>(recent_s)[x] = __ldg(reinterpret_cast<const uint4 *>(st.recent + w_lo) + x);
+    __syncthreads();
     const uint32_t rs_addr = smem_u32(recent_s) - 4u * w_lo;      // bitmap word of neuron j: + 4 (j >> 5)
     const uint32_t dp_addr = smem_u32(sm.dplus);
-    const float *__restrict__ gfpot = st.fpot;
-    const float *__restrict__ gxpost = st.xpost;
-    const uint64_t *__restrict__ ghist = st.hist;
-    const uint64_t *__restrict__ ghist_hi = st.hist_hi;
-    float *__restrict__ gw = st.w;
-    uint32_t n_syn = 0, n_w = 0, n_rw = 0, n_fsyn = 0, n_frw = 0;
-    uint32_t phase_bits = 0;     // per buffer: mbarrier phase parity
-    for (uint32_t r0 = 0; r0 < r_end; r0 += kEvRows) {
-        const uint32_t nrows = min(r_end - r0, (uint32_t)kEvRows);
-        uint32_t nseg = 0;
-        if (threadIdx.x < nrows) {
-            const uint32_t r = r0 + threadIdx.x;
-            const RowDesc d = Vl[r < nAb ? (size_t)(a_begin + r) : cap_back - (f_begin + (r - nAb))];
-            const bool arr = (d.meta & kMetaArr) != 0;
-            const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
-            EvRow er;
-            er.cb = cs & ~3ll;
-            er.lo = (uint32_t)(cs - er.cb);
-            er.hi = (uint32_t)(ce - er.cb);
-            er.xp = d.xp;
-            er.meta = d.meta;
-            er.nch = (er.hi + 3) >> 2;
-            er.pad = 0;
-            // a flush with x_pre == 0 changes no weight (potentiation adds A+ 0, R31)
-            if (cs < ce && (arr || d.xp != 0.0f)) {
-                nseg = (er.nch + kEvSegCh - 1) / kEvSegCh;
-                n_syn += (uint32_t)(ce - cs);
-                if (!arr) n_fsyn += (uint32_t)(ce - cs);
-            }
-            sm.rows[threadIdx.x] = er;
-        }
-        uint32_t S = 0;
-        const uint32_t inc = block_incl_scan<kEvThreads>(nseg, sm.wsum, S);
-        if (threadIdx.x < kEvRows) sm.incl[threadIdx.x] = inc;
-        __syncthreads();
-        // the warp's segments: warp, warp + W, ...; lane 0 keeps nb in flight
-        const uint32_t my = S > warp ? (S - warp + kEvWarps - 1) / kEvWarps : 0u;
-        auto issue = [&](uint32_t k) {        // segment k of this warp -> buffer k % nb
-            const uint32_t sg = warp + k * kEvWarps;
-            const uint32_t r = ev_row_of(sm.incl, nrows, sg);
-            const EvRow &er = sm.rows[r];
-            const uint32_t c0 = (sg - (r ? sm.incl[r - 1] : 0u)) * kEvSegCh;
-            const uint32_t nch = min((uint32_t)kEvSegCh, er.nch - c0);
-            const uint32_t b = k % nb;
-            const uint32_t dst = buf_a + b * kEvBufBytes;
-            mbar_expect_tx(mbar_a + 8 * b, 32u * nch);
-            bulk_g2s(dst, st.idx + er.cb + 4ll * c0, 16u * nch, mbar_a + 8 * b);
-            bulk_g2s(dst + kEvSegCh * 16, gw + er.cb + 4ll * c0, 16u * nch, mbar_a + 8 * b);
-        };
-        if (lane == 0)
-            for (uint32_t k = 0; k < my && k < nb; k++) issue(k);
-        for (uint32_t k = 0; k < my; k++) {
-            const uint32_t sg = warp + k * kEvWarps;
-            const uint32_t r = ev_row_of(sm.incl, nrows, sg);
-            const EvRow er = sm.rows[r];
-            const uint32_t c0 = (sg - (r ? sm.incl[r - 1] : 0u)) * kEvSegCh;
-            const uint32_t b = k % nb;
-            const uint32_t ba = buf_a + b * kEvBufBytes;          // ids; weights at + kEvSegCh * 16
-            const bool arr = (er.meta & kMetaArr) != 0;
-            const uint32_t si = (er.meta >> 12) & 0x3u;
-            const float4 pr = sm.par[si];
-            mbar_wait(mbar_a + 8 * b, (phase_bits >> b) & 1u);
-            phase_bits ^= 1u << b;
-            // filter: lane takes chunks c0 + lane + 32 u of the segment; hm: the
-            // targets that fired in the last H steps, in: inside the row's span
-            uint32_t hm = 0, im = 0;
-#pragma unroll
-            for (int u = 0; u < kEvU; u++) {
-                const uint32_t c = c0 + lane + 32u * u;
-                const bool ok = c < er.nch;
-                const uint4 j4 = ok ? lds_v4(ba + 16u * (lane + 32u * u)) : make_uint4(pp_lo, pp_lo, pp_lo, pp_lo);
-                const uint32_t jj[4] = {j4.x, j4.y, j4.z, j4.w};
-                uint32_t inm = ok ? 0xfu : 0u;
-                const uint32_t x0 = 4u * c;
-                if (ok && (x0 < er.lo || x0 + 4 > er.hi)) {          // a row's first / last chunk
-                    inm = 0;
-#pragma unroll
-                    for (int e = 0; e < 4; e++) inm |= (uint32_t)(x0 + e >= er.lo && x0 + e < er.hi) << e;
-                }
-#pragma unroll
-                for (int e = 0; e < 4; e++) {       // (outside the span: a neighbour's target, maybe no post neuron)
-                    const uint32_t j = ((inm >> e) & 1u) ? jj[e] : pp_lo;
-                    const uint32_t bit = (lds_u32(rs_addr + ((j >> 5) << 2)) >> (j & 31)) & 1u;
-                    hm |= (bit & (inm >> e)) << (4 * u + e);
-                }
-                im |= inm << (4 * u);
-            }
-            if (!arr) {
-                // ---- forced flush: the hits' factors (predicated gathers), in place
-                n_rw += __popc(hm);
-                n_frw += __popc(hm);
-                float fv[4 * kEvU];
-#pragma unroll
-                for (int u = 0; u < kEvU; u++) {
-                    const uint32_t nib = (hm >> (4 * u)) & 0xfu;
-                    const uint4 j4 = nib ? lds_v4(ba + 16u * (lane + 32u * u)) : make_uint4(0, 0, 0, 0);
-                    const uint32_t jj[4] = {j4.x, j4.y, j4.z, j4.w};
-#pragma unroll
-                    for (int e = 0; e < 4; e++) fv[4 * u + e] = ldg_f32_if(gfpot + jj[e], (nib >> e) & 1u);
-                }
-#pragma unroll
-                for (int u = 0; u < kEvU; u++) {
-                    const uint32_t nib = (hm >> (4 * u)) & 0xfu;
-                    if (!nib) continue;
-                    const uint4 w4 = lds_v4(ba + kEvSegCh * 16 + 16u * (lane + 32u * u));
-                    const float wv[4] = {__uint_as_float(w4.x), __uint_as_float(w4.y), __uint_as_float(w4.z),
-                                         __uint_as_float(w4.w)};
-                    const int64_t base = er.cb + 4ll * (c0 + lane + 32u * u);
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        if (!((nib >> e) & 1u)) continue;
-                        const float nw = __fadd_rn(wv[e], __fmul_rn(pr.x, __fmul_rn(er.xp, fv[4 * u + e])));
-                        const float w = nw < pr.z ? nw : pr.z;
-                        const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
-                        stg_f32_if(gw + base + e, w, chg);
-                        n_w += chg;
-                    }
-                }
-            } else {
-                // ---- arrival (Fig. 2c): every synapse; history window (tlu, t]
-                //      of the targets that fired lately, x_post of all
-                n_rw += __popc(im);
-                const int age = (int)(er.meta & kMetaAge);
-                const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
-                uint64_t hh[4 * kEvU], hh2[4 * kEvU];
-                float xq[4 * kEvU];
-#pragma unroll
-                for (int u = 0; u < kEvU; u++) {
-                    const uint32_t nib = (im >> (4 * u)) & 0xfu;
-                    const uint4 j4 = nib ? lds_v4(ba + 16u * (lane + 32u * u)) : make_uint4(0, 0, 0, 0);
-                    const uint32_t jj[4] = {j4.x, j4.y, j4.z, j4.w};
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        const uint32_t on = (nib >> e) & 1u, rec = on & (hm >> (4 * u + e));
-                        hh[4 * u + e] = ldg_u64_if(ghist + jj[e], rec);
-                        hh2[4 * u + e] = kH128 ? ldg_u64_if(ghist_hi + jj[e], rec) : 0ull;
-                        xq[4 * u + e] = ldg_f32_if(gxpost + jj[e], on);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < kEvU; u++) {
-                    const uint32_t nib = (im >> (4 * u)) & 0xfu;
-                    if (!nib) continue;
-                    const uint4 w4 = lds_v4(ba + kEvSegCh * 16 + 16u * (lane + 32u * u));
-                    const float wv[4] = {__uint_as_float(w4.x), __uint_as_float(w4.y), __uint_as_float(w4.z),
-                                         __uint_as_float(w4.w)};
-                    const int64_t base = er.cb + 4ll * (c0 + lane + 32u * u);
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        if (!((nib >> e) & 1u)) continue;
-                        const int q = 4 * u + e;
-                        const float w = stdp_synapse(wv[e], window_lo(hh[q], age), true, xq[q], er.xp, age, dp, pr.x,
-                                                     pr.y, pr.z, window_hi(hh2[q], age));   // (tlu, t], R2
-                        const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
-                        stg_f32_if(gw + base + e, w, chg);
-                        n_w += chg;
-                    }
-                }
-            }
-            __syncwarp();                                  // buffer b read by every lane: refill
-            if (lane == 0 && k + nb < my) issue(k + nb);
-        }
-        __syncthreads();                           // row table reused next round
-    }
-    n_syn = __reduce_add_sync(0xffffffffu, n_syn);
+    uint32_t n_syn = 0, n_w = 0, n_rw = 0;
+    ev_rows<kH128, true>(sm, st, Vl, a_end - a_begin, false, a_begin, rs_addr, dp_addr, pp_lo, n_syn, n_w, n_rw);
+    uint32_t f_syn = 0, f_rw = 0;
+    ev_rows<kH128, false>(sm, st, Vl, f_end - f_begin, true, cap_back - f_begin, rs_addr, dp_addr, pp_lo, f_syn, n_w,
+                          f_rw);
+    n_syn = __reduce_add_sync(0xffffffffu, n_syn + f_syn);
     n_w = __reduce_add_sync(0xffffffffu, n_w);
-    n_rw = __reduce_add_sync(0xffffffffu, n_rw);
-    n_fsyn = __reduce_add_sync(0xffffffffu, n_fsyn);
-    n_frw = __reduce_add_sync(0xffffffffu, n_frw);
+    n_rw = __reduce_add_sync(0xffffffffu, n_rw + f_rw);
+    f_syn = __reduce_add_sync(0xffffffffu, f_syn);
+    f_rw = __reduce_add_sync(0xffffffffu, f_rw);
     if (lane == 0) {
         if (n_syn) atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
         if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
         if (n_rw) atomicAdd(&st.ctr->metric[8], (unsigned long long)n_rw);
-        if (n_fsyn) atomicAdd(&st.ctr->metric[9], (unsigned long long)n_fsyn);
-        if (n_frw) atomicAdd(&st.ctr->metric[10], (unsigned long long)n_frw);
+        if (f_syn) atomicAdd(&st.ctr->metric[9], (unsigned long long)f_syn);
+        if (f_rw) atomicAdd(&st.ctr->metric[10], (unsigned long long)f_rw);
+    }
+    if (st.trace) {
+        __syncthreads();
+        trace_mark(st.trace, 1, 3);
     }
     kspan_end(st.kspan, t, 1);
 }
@@ -1653,10 +1643,8 @@ cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, 
 
 cudaError_t launch_stdp_ev(const NetDev &net, const StateDev &st, uint32_t grid, uint32_t pp_lo, uint32_t pp_hi,
                            cudaStream_t s, bool pdl) {
-    const uint32_t nb = ev_bufs(pp_lo, pp_hi);
-    void (*k)(NetDev, StateDev, uint32_t, uint32_t, uint32_t) = net.H > kHistBits ? k_stdp_ev<true> : k_stdp_ev<false>;
-    return launch_pdl(k, dim3(grid), dim3(kEvThreads), ev_smem_bytes(pp_lo, pp_hi, nb), s, pdl, net, st, pp_lo, pp_hi,
-                      nb);
+    void (*k)(NetDev, StateDev, uint32_t, uint32_t) = net.H > kHistBits ? k_stdp_ev<true> : k_stdp_ev<false>;
+    return launch_pdl(k, dim3(grid), dim3(kEvT), ev_smem_bytes(pp_lo, pp_hi), s, pdl, net, st, pp_lo, pp_hi);
 }
 
 cudaError_t launch_deliver_rowwise(const NetDev &net, const StateDev &st, uint32_t grid, cudaStream_t s, bool pdl) {

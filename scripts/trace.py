@@ -29,12 +29,11 @@ for rep in range(3):
         print(f"{name:8s} ctas={len(a):4d} start[min/med/max]={rel[:,0].min():7.2f}/{np.median(rel[:,0]):7.2f}/{rel[:,0].max():7.2f} "
               + " ".join(f"ph{p}[med/max]={np.median(rel[:,p]-rel[:,0]):6.2f}/{(rel[:,p]-rel[:,0]).max():6.2f}" for p in (1, 2, 3))
               + f" end_max={rel[:,3].max():7.2f}")
-    d = tr[3][:148]
-    prod = tr[3][2048:2048 + 148, 0]
+    d = tr[3][:148 * 4].reshape(148, 4, 4)
     ghz = 1.965
-    first = (d[:, 3] - t0) / 1000.0
-    print(f"stdp consumer warp0: wait_us med={np.median(d[:,0])/ghz/1e3:.2f} busy_us med={np.median(d[:,1])/ghz/1e3:.2f} "
-          f"stages med={np.median(d[:,2]):.0f} max={d[:,2].max()} first_stage_at med={np.median(first):.2f} "
-          f"producer empty-wait_us med={np.median(prod)/ghz/1e3:.2f} filter_us med={np.median(tr[3][1024:1172,0])/ghz/1e3:.2f} "
-          f"arrivals_us med={np.median(tr[3][1024:1172,1])/ghz/1e3:.2f}")
+    segs = d[:, :, 2] >> 40
+    flush = d[:, :, 2] & ((1 << 40) - 1)
+    us = lambda x: np.median(x) / ghz / 1e3
+    print(f"stdp_ev warps0-3: wait_us={us(d[:,:,0]):.2f} filter_us={us(d[:,:,1]):.2f} flush_us={us(flush):.2f} "
+          f"arrival_us={us(d[:,:,3]):.2f} segs med={np.median(segs):.0f} max={segs.max()}")
     print(g.metrics())
