@@ -238,7 +238,10 @@ enum {
                                    [4k+2] steps, [4k+3] CTAs; cumulative
                                    (SNN_FLAG_KTIME; read at least every 65,536
                                    steps)                                       */
-    SNN_FIELD_COUNT = 27
+    SNN_FIELD_FPOS = 27,        /* [u8 / n]    post-plastic neuron: 0xfe no spike
+                                   in its H-bit window, 0xff several, else the
+                                   bit index of the only one                     */
+    SNN_FIELD_COUNT = 28
 };
 
 /* SNN_FIELD_METRICS layout (device counters, cumulative over steps) */

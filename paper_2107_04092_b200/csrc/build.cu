@@ -169,6 +169,8 @@ __global__ void k_init_state(NetDev net, StateDev st) {
     st.in_i[i] = 0;
     st.hist[i] = 0ull;
     if (net.H > 64) st.hist_hi[i] = 0ull;
+    st.fpos[i] = 0xfeu;
+    st.fpot[i] = 0.0f;
     st.nspk[i] = 0u;
     st.xpre[i] = 0.0f;
     st.tlu[i] = -1;

@@ -118,6 +118,7 @@ struct StateDev {
     uint64_t *hist;          // bits 0..63 of the spike history (bit s: step t - s)
     uint64_t *hist_hi;       // H = 128: bits 64..127 (else unused)
     float *fpot;             // post-plastic j with spikes in its H-bit window: sum of D+[H - s] over them
+    uint8_t *fpos;           // post-plastic j: 0xfe no spike in its H-bit window, 0xff several, else the bit of the only one
     uint32_t *nspk;
     uint32_t *ring;          // [kRingSlots][ring_stride]
     // source rows

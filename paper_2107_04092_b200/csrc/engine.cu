@@ -395,6 +395,7 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.hist, uint64_t, N);
     ALLOC(st.hist_hi, uint64_t, cfg.history_bits > 64 ? N : 1);
     ALLOC(st.fpot, float, N);
+    ALLOC(st.fpos, uint8_t, (size_t)N + 16);
     ALLOC(st.nspk, uint32_t, N);
     // exchange geometry: rank r owns words [r share_w, ...), at most share_w + 1
     // of them (the word straddling R); ring slots padded for the unpack
@@ -817,6 +818,7 @@ static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool 
         n = sim->pops[pop_id].n;
     }
     cudaStream_t s = sim->stream;
+    bool per_neuron = true;
     switch (field) {
     case SNN_FIELD_V: f.dev = st.V + base; f.elem = 4; break;
     case SNN_FIELD_REFRACTORY: f.dev = st.ref + base; f.elem = 4; break;
@@ -834,9 +836,10 @@ static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool 
         if (net.H <= 64) return sim->fail(SNN_E_STATE, "HIST_DEV_HI needs history_bits = 128");
         f.dev = st.hist_hi + base; f.elem = 8; break;
     case SNN_FIELD_FPOT: f.dev = st.fpot + base; f.elem = 4; break;
-    default: break;
+    case SNN_FIELD_FPOS: f.dev = st.fpos + base; f.elem = 1; break;
+    default: per_neuron = false; break;
     }
-    if (f.elem > 1) {
+    if (per_neuron) {
         f.bytes = f.elem * n;
     } else {
         switch (field) {

@@ -188,6 +188,14 @@ k_front(NetDev net, StateDev st) {
                 st.hist_hi[i] = hh;
             }
             recent = (h | hh) != 0ull;
+            // the window's spike position (k_stdp_ev's shared table): 0xfe no
+            // spike in the last H steps, 0xff several, else the bit of the only one
+            {
+                const uint32_t n1 = __popcll(h) + __popcll(hh);
+                st.fpos[i] = n1 == 0 ? (uint8_t)0xfeu
+                           : n1 > 1 ? (uint8_t)0xffu
+                                    : (uint8_t)(h ? 63 - __clzll((long long)h) : 127 - __clzll((long long)hh));
+            }
             // potentiation factor of a forced flush (age H) for this target:
             // fpot = sum over its spikes s in the window of D+[H - s], oldest
             // first (k_stdp: w = min(w + A+ (x_pre fpot), w_max))
@@ -329,6 +337,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)_
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
@@ -854,14 +867,20 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
 // (consecutive threads: consecutive chunks, coalesced 16-byte loads of ids
 // and weights), kEvU chunks per iteration, the next iteration's loads issued
 // before the current one's gathers (double-buffered registers).
+// The CTA keeps the post population's one-byte spike positions (k_front:
+// 0xfe no spike in the last H steps, 0xff several, else the bit of the only
+// one -- the paper's regime has 0-1 spikes per window) in shared
+// memory, so a target is filtered by one shared byte and most updates need no
+// history gather:
 //  * forced flush (age H): every flush of the step shares the window
-//    (t - H, t], so synapse i -> j changes only if j fired in it (shared
-//    bitmap probe), by w = min(w + A+ (x_pre_i fpot[j]), w_max) with
-//    fpot[j] = sum over j's spikes s in the window of D+[H - s] (k_front; one
-//    spike: the closed-form skip-ahead of P:284; several: potentiations only,
-//    so the sequential clamps are one clamp of the sum);
-//  * arrival: the window (tlu, t] of the target's history, oldest spike first
-//    with __clz, then the pre spike's depression by x_post[j].
+//    (t - H, t], so synapse i -> j changes only if j fired in it, by
+//    w = min(w + A+ (x_pre_i D+[H - p]), w_max) for its one spike at bit p (the
+//    closed-form skip-ahead of P:284); several spikes: by the gathered
+//    fpot[j] = sum of D+[H - s] (potentiations only, so the sequential clamps
+//    are one clamp of the sum);
+//  * arrival: potentiation by the spikes in the window (tlu, t] (one: p < age;
+//    several: the gathered history, oldest first with __clz), then the
+//    pre spike's depression by x_post[j] (gathered).
 // Only weights that change are stored.
 #ifndef SNN_EV_THREADS
 #define SNN_EV_THREADS 512
@@ -887,8 +906,8 @@ struct EvSmem {
     float dplus[4 * (kMaxHist + 1)];
 };
 
-size_t ev_smem_bytes(uint32_t pp_lo, uint32_t pp_hi) {
-    return ((sizeof(EvSmem) + 15) & ~(size_t)15) + 16ull * ((((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 3) >> 2);
+size_t ev_smem_bytes(uint32_t pp_lo, uint32_t pp_hi) {     // + the post population's spike-position bytes
+    return ((sizeof(EvSmem) + 15) & ~(size_t)15) + (((size_t)pp_hi - (pp_lo & ~15u) + 15) & ~(size_t)15);
 }
 
 // One iteration's loads: chunk c (c < T) of the CTA's flattened rows; r walks
@@ -919,31 +938,39 @@ __device__ __forceinline__ void ev_load(const EvSmem &sm, const uint32_t *__rest
 
 template <bool kH128, bool kArr>
 __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st, const EvLoad (&L)[kEvU],
-                                           uint32_t rs_addr, uint32_t dp_addr, uint32_t pp_lo, uint32_t &n_w,
-                                           uint32_t &n_rw) {
-    // filter: hm = targets that fired in the last H steps, im = inside the row's span
-    uint32_t hm = 0, im = 0;
+                                           uint32_t fs_addr, uint32_t dp_addr, uint32_t pp_lo, uint32_t H,
+                                           uint32_t &n_w, uint32_t &n_rw, uint32_t net_debug) {
+    // filter: pos = the target's spike position in the last H steps (shared
+    // table: 0xfe none, 0xff several), im = inside the row's span
+    uint32_t im = 0, hm = 0, mm = 0;     // in span / window holds a spike / several spikes
+    uint32_t pos[4 * kEvU];
 #pragma unroll
     for (int u = 0; u < kEvU; u++) {
-        if (L[u].r == 0xffffffffu) continue;
-        const EvRow &er = sm.rows[L[u].r];
-        uint32_t inm = 0xfu;
-        if (L[u].x0 < er.lo || L[u].x0 + 4 > er.hi) {                // a row's first / last chunk
-            inm = 0;
+        uint32_t inm = 0;
+        if (L[u].r != 0xffffffffu) {
+            const EvRow &er = sm.rows[L[u].r];
+            inm = 0xfu;
+            if (L[u].x0 < er.lo || L[u].x0 + 4 > er.hi) {            // a row's first / last chunk
+                inm = 0;
 #pragma unroll
-            for (int e = 0; e < 4; e++) inm |= (uint32_t)(L[u].x0 + e >= er.lo && L[u].x0 + e < er.hi) << e;
+                for (int e = 0; e < 4; e++) inm |= (uint32_t)(L[u].x0 + e >= er.lo && L[u].x0 + e < er.hi) << e;
+            }
         }
         const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
 #pragma unroll
         for (int e = 0; e < 4; e++) {       // (outside the span: a neighbour's target, maybe no post neuron)
-            const uint32_t j = ((inm >> e) & 1u) ? jj[e] : pp_lo;
-            const uint32_t bit = (lds_u32(rs_addr + ((j >> 5) << 2)) >> (j & 31)) & 1u;
-            hm |= (bit & (inm >> e)) << (4 * u + e);
+            const uint32_t on = (inm >> e) & 1u;
+            const uint32_t p = lds_u8(fs_addr + (on ? jj[e] : pp_lo));
+            pos[4 * u + e] = p;
+            hm |= (on & (uint32_t)(p != 0xfeu)) << (4 * u + e);
+            mm |= (on & (uint32_t)(p == 0xffu)) << (4 * u + e);
         }
         im |= inm << (4 * u);
     }
+    if (net_debug & 1u) return;                  // (experiments: filter only)
     if (!kArr) {
-        // ---- forced flushes: the hits' factors (predicated gathers), in place
+        // ---- forced flushes (age H): the window's spike at bit p adds
+        //      A+ (x_pre D+[H - p]); several: the gathered fpot factor
         if (!hm) return;
         n_rw += __popc(hm);
         float fv[4 * kEvU];
@@ -951,21 +978,25 @@ __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st,
         for (int u = 0; u < kEvU; u++) {
             const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
 #pragma unroll
-            for (int e = 0; e < 4; e++) fv[4 * u + e] = ldg_f32_if(st.fpot + jj[e], (hm >> (4 * u + e)) & 1u);
+            for (int e = 0; e < 4; e++) fv[4 * u + e] = ldg_f32_if(st.fpot + jj[e], (mm >> (4 * u + e)) & 1u);
         }
 #pragma unroll
         for (int u = 0; u < kEvU; u++) {
             const uint32_t nib = (hm >> (4 * u)) & 0xfu;
             if (!nib) continue;
             const EvRow &er = sm.rows[L[u].r];
-            const float4 pr = sm.par[(er.meta >> 12) & 0x3u];
+            const uint32_t si = (er.meta >> 12) & 0x3u;
+            const float4 pr = sm.par[si];
+            const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
             const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
                                  __uint_as_float(L[u].w.w)};
             float *wp = st.w + er.cb + L[u].x0;
 #pragma unroll
             for (int e = 0; e < 4; e++) {
                 if (!((nib >> e) & 1u)) continue;
-                const float nw = __fadd_rn(wv[e], __fmul_rn(pr.x, __fmul_rn(er.xp, fv[4 * u + e])));
+                const int q = 4 * u + e;
+                const float f = pos[q] == 0xffu ? fv[q] : lds_f32(dp + 4u * (H - pos[q]));
+                const float nw = __fadd_rn(wv[e], __fmul_rn(pr.x, __fmul_rn(er.xp, f)));
                 const float w = nw < pr.z ? nw : pr.z;
                 const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
                 stg_f32_if(wp + e, w, chg);
@@ -973,8 +1004,10 @@ __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st,
             }
         }
     } else {
-        // ---- arrivals (Fig. 2c): every synapse; the history window (tlu, t]
-        //      of the targets that fired lately, x_post of all
+        // ---- arrivals (Fig. 2c): every synapse.  Potentiation by the spikes in
+        //      the window (tlu, t] (one: bit p < age, closed form; several:
+        //      the history word, oldest first with __clz), then the pre
+        //      spike's depression by x_post[j]
         if (!im) return;
         n_rw += __popc(im);
         uint64_t hh[4 * kEvU], hh2[4 * kEvU];
@@ -984,9 +1017,9 @@ __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st,
             const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                const uint32_t on = (im >> (4 * u + e)) & 1u, rec = on & (hm >> (4 * u + e));
-                hh[4 * u + e] = ldg_u64_if(st.hist + jj[e], rec);
-                hh2[4 * u + e] = kH128 ? ldg_u64_if(st.hist_hi + jj[e], rec) : 0ull;
+                const uint32_t on = (im >> (4 * u + e)) & 1u, sev = (mm >> (4 * u + e)) & 1u;
+                hh[4 * u + e] = ldg_u64_if(st.hist + jj[e], sev);
+                hh2[4 * u + e] = kH128 ? ldg_u64_if(st.hist_hi + jj[e], sev) : 0ull;
                 xq[4 * u + e] = ldg_f32_if(st.xpost + jj[e], on);
             }
         }
@@ -997,7 +1030,7 @@ __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st,
             const EvRow &er = sm.rows[L[u].r];
             const uint32_t si = (er.meta >> 12) & 0x3u;
             const float4 pr = sm.par[si];
-            const int age = (int)(er.meta & kMetaAge);
+            const uint32_t age = er.meta & kMetaAge;
             const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
             const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
                                  __uint_as_float(L[u].w.w)};
@@ -1006,8 +1039,18 @@ __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st,
             for (int e = 0; e < 4; e++) {
                 if (!((nib >> e) & 1u)) continue;
                 const int q = 4 * u + e;
-                const float w = stdp_synapse(wv[e], window_lo(hh[q], age), true, xq[q], er.xp, age, dp, pr.x, pr.y,
-                                             pr.z, window_hi(hh2[q], age));   // (tlu, t], R2
+                float w = wv[e];
+                if (pos[q] == 0xffu) {
+                    w = stdp_synapse(w, window_lo(hh[q], (int)age), true, xq[q], er.xp, (int)age, dp, pr.x, pr.y, pr.z,
+                                     window_hi(hh2[q], (int)age));   // (tlu, t], R2
+                } else {
+                    if (pos[q] < age) {                // the window's only post spike
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(er.xp, lds_f32(dp + 4u * (age - pos[q])))));
+                        w = nw < pr.z ? nw : pr.z;
+                    }
+                    const float dw = __fsub_rn(w, __fmul_rn(pr.y, xq[q]));
+                    w = dw > 0.0f ? dw : 0.0f;
+                }
                 const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
                 stg_f32_if(wp + e, w, chg);
                 n_w += chg;
@@ -1019,8 +1062,9 @@ __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st,
 // The CTA's rows of one kind (arrivals or flushes) in rounds of kEvRows.
 template <bool kH128, bool kArr>
 __device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const RowDesc *Vl, uint32_t nrows_all,
-                                        bool from_back, size_t base, uint32_t rs_addr, uint32_t dp_addr,
-                                        uint32_t pp_lo, uint32_t &n_syn, uint32_t &n_w, uint32_t &n_rw) {
+                                        bool from_back, size_t base, uint32_t fs_addr, uint32_t dp_addr,
+                                        uint32_t pp_lo, uint32_t H, uint32_t &n_syn, uint32_t &n_w, uint32_t &n_rw,
+                                        uint32_t net_debug) {
     for (uint32_t r0 = 0; r0 < nrows_all; r0 += kEvRows) {
         const uint32_t nrows = min(nrows_all - r0, (uint32_t)kEvRows);
         uint32_t nch = 0;
@@ -1058,12 +1102,12 @@ __device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const Ro
 #pragma unroll
             for (int u = 0; u < kEvU; u++)
                 ev_load<kH128, kArr>(sm, st.idx, st.w, c0 + kEvT * (kEvU + u) + threadIdx.x, T, cur, B[u]);
-            ev_process<kH128, kArr>(sm, st, A, rs_addr, dp_addr, pp_lo, n_w, n_rw);
+            ev_process<kH128, kArr>(sm, st, A, fs_addr, dp_addr, pp_lo, H, n_w, n_rw, net_debug);
             if (c0 + kEvT * kEvU >= T) break;
 #pragma unroll
             for (int u = 0; u < kEvU; u++)
                 ev_load<kH128, kArr>(sm, st.idx, st.w, c0 + kEvT * (2 * kEvU + u) + threadIdx.x, T, cur, A[u]);
-            ev_process<kH128, kArr>(sm, st, B, rs_addr, dp_addr, pp_lo, n_w, n_rw);
+            ev_process<kH128, kArr>(sm, st, B, fs_addr, dp_addr, pp_lo, H, n_w, n_rw, net_debug);
         }
         __syncthreads();                           // row table reused next round
     }
@@ -1075,9 +1119,9 @@ k_stdp_ev(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
     extern __shared__ __align__(16) unsigned char smem[];
     const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
     EvSmem &sm = *reinterpret_cast<EvSmem *>(smem);
-    uint32_t *recent_s = reinterpret_cast<uint32_t *>(smem + ((sizeof(EvSmem) + 15) & ~(size_t)15));
+    uint8_t *fpos_s = smem + ((sizeof(EvSmem) + 15) & ~(size_t)15);
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t w_lo = (pp_lo >> 7) << 2, w_hi = (pp_hi + 31) >> 5;     // 16-byte aligned start
+    const uint32_t f_lo = pp_lo & ~15u;                                     // 16-byte aligned start
     for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kEvT)
         sm.dplus[x] = st.stdp[x / (kMaxHist + 1)].dplus[x % (kMaxHist + 1)];
     if (threadIdx.x < net.nstdp)
@@ -1098,16 +1142,19 @@ k_stdp_ev(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
     const uint32_t a_end = (uint32_t)(((uint64_t)nA * (blockIdx.x + 1)) / gridDim.x);
     const uint32_t f_begin = (uint32_t)(((uint64_t)nF * blockIdx.x) / gridDim.x);
     const uint32_t f_end = (uint32_t)(((uint64_t)nF * (blockIdx.x + 1)) / gridDim.x);
-    for (uint32_t x = threadIdx.x; x < (w_hi - w_lo + 3) >> 2; x += kEvT)     // bitmap -> shared
-        reinterpret_cast<uint4 *>(recent_s)[x] = __ldg(reinterpret_cast<const uint4 *>(st.recent + w_lo) + x);
+    for (uint32_t x = threadIdx.x; x < (pp_hi - f_lo + 15) >> 4; x += kEvT)     // spike positions -> shared
+        reinterpret_cast<uint4 *>(fpos_s)[x] = __ldg(reinterpret_cast<const uint4 *>(st.fpos + f_lo) + x);
     __syncthreads();
-    const uint32_t rs_addr = smem_u32(recent_s) - 4u * w_lo;      // bitmap word of neuron j: + 4 (j >> 5)
+    const uint32_t fs_addr = smem_u32(fpos_s) - f_lo;             // position of post neuron j: + j
     const uint32_t dp_addr = smem_u32(sm.dplus);
     uint32_t n_syn = 0, n_w = 0, n_rw = 0;
-    ev_rows<kH128, true>(sm, st, Vl, a_end - a_begin, false, a_begin, rs_addr, dp_addr, pp_lo, n_syn, n_w, n_rw);
+    if (!(net.debug & 2u))                       // (experiments: no arrivals / no flushes)
+        ev_rows<kH128, true>(sm, st, Vl, a_end - a_begin, false, a_begin, fs_addr, dp_addr, pp_lo, net.H, n_syn, n_w,
+                             n_rw, net.debug);
     uint32_t f_syn = 0, f_rw = 0;
-    ev_rows<kH128, false>(sm, st, Vl, f_end - f_begin, true, cap_back - f_begin, rs_addr, dp_addr, pp_lo, f_syn, n_w,
-                          f_rw);
+    if (!(net.debug & 4u))
+        ev_rows<kH128, false>(sm, st, Vl, f_end - f_begin, true, cap_back - f_begin, fs_addr, dp_addr, pp_lo, net.H,
+                              f_syn, n_w, f_rw, net.debug);
     n_syn = __reduce_add_sync(0xffffffffu, n_syn + f_syn);
     n_w = __reduce_add_sync(0xffffffffu, n_w);
     n_rw = __reduce_add_sync(0xffffffffu, n_rw + f_rw);
@@ -1173,11 +1220,6 @@ __device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
 __device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
     uint64_t v;
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ void red_shared_add(uint32_t addr, int32_t v) {

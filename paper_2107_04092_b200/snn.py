@@ -35,14 +35,14 @@ ALL = 0xFFFFFFFF
 FIELD = dict(V=0, REFRACTORY=1, G_EXC=2, G_INH=3, INPUT_EXC=4, INPUT_INH=5, HIST=6, SPIKE_COUNT=7,
              XPOST=8, XPRE_ROW=9, TLU=10, ROW_PTR=11, IDX=12, WEIGHTS=13, PIVOTS=14, STEP=15,
              METRICS=16, SPIKE_RING=17, PHASE_TIMES=18, INFO=19, TRACE=20, IDX16=21, HIST_DEV=22,
-             HIST_DEV_HI=23, FPOT=24, RECENT=25, KTIME=26)
+             HIST_DEV_HI=23, FPOT=24, RECENT=25, KTIME=26, FPOS=27)
 FIELD_DTYPE = dict(V=np.float32, REFRACTORY=np.int32, G_EXC=np.float32, G_INH=np.float32,
                    INPUT_EXC=np.int32, INPUT_INH=np.int32, HIST=np.uint64, SPIKE_COUNT=np.uint32,
                    XPOST=np.float32, XPRE_ROW=np.float32, TLU=np.int32, ROW_PTR=np.int64,
                    IDX=np.uint32, WEIGHTS=np.float32, PIVOTS=np.uint32, STEP=np.int64,
                    METRICS=np.uint64, SPIKE_RING=np.uint32, PHASE_TIMES=np.float64, INFO=np.int64,
                    TRACE=np.uint64, IDX16=np.uint16, HIST_DEV=np.uint64, HIST_DEV_HI=np.uint64,
-                   FPOT=np.float32, RECENT=np.uint32, KTIME=np.uint64)
+                   FPOT=np.float32, RECENT=np.uint32, KTIME=np.uint64, FPOS=np.uint8)
 METRIC = dict(EVENTS=0, SPIKES=1, STDP_ROWS=2, STDP_SYN=3, STDP_WSTORE=4, FLUSH_ROWS=5, SEGMENTS=6, ELEMS=7,
               STDP_WRW=8, FLUSH_SYN=9, FLUSH_WRW=10)
 KTIME_KERNELS = ("front", "stdp", "deliver", "spare", "lists")

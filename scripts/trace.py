@@ -16,8 +16,12 @@ g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=C, flags=FLAG_TRA
 rc.apply(g)
 g.step(int(os.environ.get("SNN_TRACE_T0", "3000")))
 torch.cuda.synchronize()
+dbg = os.environ.get("SNN_TRACE_DEBUG")
 for rep in range(3):
+    if dbg is not None:
+        os.environ["SNN_DEBUG_KERNELS"] = dbg     # kernel experiment on the traced steps only
     g.step(1)
+    os.environ.pop("SNN_DEBUG_KERNELS", None)
     tr = g.read_state("TRACE").reshape(4, 4096, 4).astype(np.int64)
     t0 = tr[0][tr[0][:, 0] > 0][:, 0].min()
     for k, name in [(0, "front"), (2, "deliver"), (1, "stdp")]:
@@ -29,11 +33,4 @@ for rep in range(3):
         print(f"{name:8s} ctas={len(a):4d} start[min/med/max]={rel[:,0].min():7.2f}/{np.median(rel[:,0]):7.2f}/{rel[:,0].max():7.2f} "
               + " ".join(f"ph{p}[med/max]={np.median(rel[:,p]-rel[:,0]):6.2f}/{(rel[:,p]-rel[:,0]).max():6.2f}" for p in (1, 2, 3))
               + f" end_max={rel[:,3].max():7.2f}")
-    d = tr[3][:148 * 4].reshape(148, 4, 4)
-    ghz = 1.965
-    segs = d[:, :, 2] >> 40
-    flush = d[:, :, 2] & ((1 << 40) - 1)
-    us = lambda x: np.median(x) / ghz / 1e3
-    print(f"stdp_ev warps0-3: wait_us={us(d[:,:,0]):.2f} filter_us={us(d[:,:,1]):.2f} flush_us={us(flush):.2f} "
-          f"arrival_us={us(d[:,:,3]):.2f} segs med={np.median(segs):.0f} max={segs.max()}")
     print(g.metrics())

@@ -462,12 +462,26 @@ def _expected_fpot(lo, hi, H, dt, tau_plus):
     return out, (lo | hi) != 0
 
 
+def _expected_fpos(lo, hi):
+    """0xfe: no spike in the window (hi:lo), 0xff: several, else the bit index of the only one."""
+    out = np.full(lo.shape, 0xFE, dtype=np.uint8)
+    cnt = np.zeros(lo.shape, dtype=np.int64)
+    for s in range(128):
+        word = hi if s >= 64 else lo
+        on = ((word >> np.uint64(s % 64)) & np.uint64(1)).astype(bool)
+        cnt += on
+        out[on] = s
+    out[cnt > 1] = 0xFF
+    return out
+
+
 @pytest.mark.parametrize("H,delay", [(64, 15), (128, 15), (64, 0), (128, 3)])
 def test_device_history_bitfields_bit_exact_every_step(H, delay):
     """The bitfields k_stdp actually reads -- the per-neuron history words
     (Fig. 2 header: bit s = spike at step t - s), the second word at
-    H = 128 (P:399), the 'fired in the last H steps' bitmap and the
-    forced-flush factor derived from the window (sum of D+[H - s]) -- read out
+    H = 128, the 'fired in the last H steps' bitmap, the one-byte
+    position of a window's only spike and the forced-flush factor derived from
+    the window (sum of D+[H - s]) -- read out
     of device memory after every step and compared bit-exactly with the
     oracle's history (bits 64..127 are the oracle's words shifted out, kept by
     the test)."""
@@ -491,6 +505,7 @@ def test_device_history_bitfields_bit_exact_every_step(H, delay):
         fpot_exp, nonempty = _expected_fpot(lo, whi, H, rc.dt_ms, rc.projs[4].stdp["tau_plus"])
         fpot = g.read_state("FPOT", pop=0)
         assert np.array_equal(fpot[nonempty], fpot_exp[nonempty]), f"forced-flush factors differ at step {t}"
+        assert np.array_equal(g.read_state("FPOS", pop=0), _expected_fpos(lo, whi)), f"spike positions differ at {t}"
         bits = np.zeros(((N + 31) // 32) * 32, dtype=np.uint8)
         bits[:ne] = nonempty
         rec = np.packbits(bits, bitorder="little").view(np.uint32)
