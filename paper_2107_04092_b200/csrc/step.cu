@@ -883,12 +883,12 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
 //    pre spike's depression by x_post[j] (gathered).
 // Only weights that change are stored.
 #ifndef SNN_EV_THREADS
-#define SNN_EV_THREADS 512
+#define SNN_EV_THREADS 1024
 #endif
 constexpr int kEvT = SNN_EV_THREADS;
 constexpr int kEvWarps = kEvT / 32;
 constexpr int kEvRows = 256;                 // row table per round
-constexpr int kEvU = 2;                      // chunks per thread and iteration
+constexpr int kEvU = 2;                      // chunks per thread and iteration (flushes; arrivals: 1)
 
 struct __align__(16) EvRow {
     int64_t cb;      // 16-byte aligned CSR offset of the plastic span
@@ -936,119 +936,73 @@ __device__ __forceinline__ void ev_load(const EvSmem &sm, const uint32_t *__rest
     }
 }
 
-template <bool kH128, bool kArr>
-__device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st, const EvLoad (&L)[kEvU],
+template <bool kH128, bool kArr, int U>
+__device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st, const EvLoad (&L)[U],
                                            uint32_t fs_addr, uint32_t dp_addr, uint32_t pp_lo, uint32_t H,
                                            uint32_t &n_w, uint32_t &n_rw, uint32_t net_debug) {
-    // filter: pos = the target's spike position in the last H steps (shared
-    // table: 0xfe none, 0xff several), im = inside the row's span
-    uint32_t im = 0, hm = 0, mm = 0;     // in span / window holds a spike / several spikes
-    uint32_t pos[4 * kEvU];
 #pragma unroll
-    for (int u = 0; u < kEvU; u++) {
-        uint32_t inm = 0;
-        if (L[u].r != 0xffffffffu) {
-            const EvRow &er = sm.rows[L[u].r];
-            inm = 0xfu;
-            if (L[u].x0 < er.lo || L[u].x0 + 4 > er.hi) {            // a row's first / last chunk
-                inm = 0;
+    for (int u = 0; u < U; u++) {
+        if (L[u].r == 0xffffffffu) continue;
+        const EvRow &er = sm.rows[L[u].r];
+        uint32_t inm = 0xfu;
+        if (L[u].x0 < er.lo || L[u].x0 + 4 > er.hi) {                // a row's first / last chunk
+            inm = 0;
 #pragma unroll
-                for (int e = 0; e < 4; e++) inm |= (uint32_t)(L[u].x0 + e >= er.lo && L[u].x0 + e < er.hi) << e;
-            }
+            for (int e = 0; e < 4; e++) inm |= (uint32_t)(L[u].x0 + e >= er.lo && L[u].x0 + e < er.hi) << e;
         }
         const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
+        uint32_t pos[4];
+        uint32_t hm = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) {       // (outside the span: a neighbour's target, maybe no post neuron)
-            const uint32_t on = (inm >> e) & 1u;
-            const uint32_t p = lds_u8(fs_addr + (on ? jj[e] : pp_lo));
-            pos[4 * u + e] = p;
-            hm |= (on & (uint32_t)(p != 0xfeu)) << (4 * u + e);
-            mm |= (on & (uint32_t)(p == 0xffu)) << (4 * u + e);
+            pos[e] = lds_u8(fs_addr + (((inm >> e) & 1u) ? jj[e] : pp_lo));
+            hm |= (uint32_t)(((inm >> e) & 1u) && pos[e] != 0xfeu) << e;
         }
-        im |= inm << (4 * u);
-    }
-    if (net_debug & 1u) return;                  // (experiments: filter only)
-    if (!kArr) {
-        // ---- forced flushes (age H): the window's spike at bit p adds
-        //      A+ (x_pre D+[H - p]); several: the gathered fpot factor
-        if (!hm) return;
-        n_rw += __popc(hm);
-        float fv[4 * kEvU];
-#pragma unroll
-        for (int u = 0; u < kEvU; u++) {
-            const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
-#pragma unroll
-            for (int e = 0; e < 4; e++) fv[4 * u + e] = ldg_f32_if(st.fpot + jj[e], (mm >> (4 * u + e)) & 1u);
-        }
-#pragma unroll
-        for (int u = 0; u < kEvU; u++) {
-            const uint32_t nib = (hm >> (4 * u)) & 0xfu;
-            if (!nib) continue;
-            const EvRow &er = sm.rows[L[u].r];
-            const uint32_t si = (er.meta >> 12) & 0x3u;
-            const float4 pr = sm.par[si];
-            const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
-            const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
-                                 __uint_as_float(L[u].w.w)};
-            float *wp = st.w + er.cb + L[u].x0;
+        if (net_debug & 1u) continue;            // (experiments: filter only)
+        const uint32_t si = (er.meta >> 12) & 0x3u;
+        const float4 pr = sm.par[si];
+        const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+        const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
+                             __uint_as_float(L[u].w.w)};
+        float *wp = st.w + er.cb + L[u].x0;
+        if (!kArr) {
+            // ---- forced flush (age H): the window's spike at bit p adds
+            //      A+ (x_pre D+[H - p]); several spikes: the fpot factor (gathered)
+            n_rw += __popc(hm);
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                if (!((nib >> e) & 1u)) continue;
-                const int q = 4 * u + e;
-                const float f = pos[q] == 0xffu ? fv[q] : lds_f32(dp + 4u * (H - pos[q]));
+                const bool hit = (hm >> e) & 1u;
+                float f = lds_f32(dp + 4u * (pos[e] < H ? H - pos[e] : 0u));
+                if (hit && pos[e] == 0xffu) f = __ldg(st.fpot + jj[e]);
                 const float nw = __fadd_rn(wv[e], __fmul_rn(pr.x, __fmul_rn(er.xp, f)));
                 const float w = nw < pr.z ? nw : pr.z;
-                const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
+                const uint32_t chg = (hit && __float_as_uint(w) != __float_as_uint(wv[e])) ? 1u : 0u;
                 stg_f32_if(wp + e, w, chg);
                 n_w += chg;
             }
-        }
-    } else {
-        // ---- arrivals (Fig. 2c): every synapse.  Potentiation by the spikes in
-        //      the window (tlu, t] (one: bit p < age, closed form; several:
-        //      the history word, oldest first with __clz), then the pre
-        //      spike's depression by x_post[j]
-        if (!im) return;
-        n_rw += __popc(im);
-        uint64_t hh[4 * kEvU], hh2[4 * kEvU];
-        float xq[4 * kEvU];
-#pragma unroll
-        for (int u = 0; u < kEvU; u++) {
-            const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const uint32_t on = (im >> (4 * u + e)) & 1u, sev = (mm >> (4 * u + e)) & 1u;
-                hh[4 * u + e] = ldg_u64_if(st.hist + jj[e], sev);
-                hh2[4 * u + e] = kH128 ? ldg_u64_if(st.hist_hi + jj[e], sev) : 0ull;
-                xq[4 * u + e] = ldg_f32_if(st.xpost + jj[e], on);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kEvU; u++) {
-            const uint32_t nib = (im >> (4 * u)) & 0xfu;
-            if (!nib) continue;
-            const EvRow &er = sm.rows[L[u].r];
-            const uint32_t si = (er.meta >> 12) & 0x3u;
-            const float4 pr = sm.par[si];
+        } else {
+            // ---- arrival (Fig. 2c): every synapse.  Potentiation by the spikes
+            //      in the window (tlu, t] (one: bit p < age, closed form; several:
+            //      the history word, oldest first with __clz), then the pre spike's
+            //      depression by x_post[j] (gathered)
+            n_rw += __popc(inm);
             const uint32_t age = er.meta & kMetaAge;
-            const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
-            const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
-                                 __uint_as_float(L[u].w.w)};
-            float *wp = st.w + er.cb + L[u].x0;
+            float xq[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) xq[e] = ldg_f32_if(st.xpost + jj[e], (inm >> e) & 1u);
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                if (!((nib >> e) & 1u)) continue;
-                const int q = 4 * u + e;
+                if (!((inm >> e) & 1u)) continue;
                 float w = wv[e];
-                if (pos[q] == 0xffu) {
-                    w = stdp_synapse(w, window_lo(hh[q], (int)age), true, xq[q], er.xp, (int)age, dp, pr.x, pr.y, pr.z,
-                                     window_hi(hh2[q], (int)age));   // (tlu, t], R2
+                if (pos[e] == 0xffu) {
+                    w = stdp_synapse(w, window_lo(__ldg(st.hist + jj[e]), (int)age), true, xq[e], er.xp, (int)age, dp,
+                                     pr.x, pr.y, pr.z, kH128 ? window_hi(__ldg(st.hist_hi + jj[e]), (int)age) : 0ull);
                 } else {
-                    if (pos[q] < age) {                // the window's only post spike
-                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(er.xp, lds_f32(dp + 4u * (age - pos[q])))));
+                    if (pos[e] < age) {                // the window's only post spike
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(er.xp, lds_f32(dp + 4u * (age - pos[e])))));
                         w = nw < pr.z ? nw : pr.z;
                     }
-                    const float dw = __fsub_rn(w, __fmul_rn(pr.y, xq[q]));
+                    const float dw = __fsub_rn(w, __fmul_rn(pr.y, xq[e]));
                     w = dw > 0.0f ? dw : 0.0f;
                 }
                 const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
@@ -1094,20 +1048,12 @@ __device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const Ro
         if (threadIdx.x == 0) sm.incl[nrows] = 0xffffffffu;      // (the walk never passes the last row)
         __syncthreads();
         uint32_t cur = 0;
-        EvLoad A[kEvU], B[kEvU];
+        constexpr int U = kArr ? 1 : kEvU;
+        for (uint32_t c0 = 0; c0 < T; c0 += kEvT * U) {
+            EvLoad L[U];
 #pragma unroll
-        for (int u = 0; u < kEvU; u++) ev_load<kH128, kArr>(sm, st.idx, st.w, threadIdx.x + kEvT * u, T, cur, A[u]);
-        for (uint32_t c0 = 0; c0 < T; c0 += 2 * kEvT * kEvU) {
-            // B: the next iteration's loads in flight while A is processed, and back
-#pragma unroll
-            for (int u = 0; u < kEvU; u++)
-                ev_load<kH128, kArr>(sm, st.idx, st.w, c0 + kEvT * (kEvU + u) + threadIdx.x, T, cur, B[u]);
-            ev_process<kH128, kArr>(sm, st, A, fs_addr, dp_addr, pp_lo, H, n_w, n_rw, net_debug);
-            if (c0 + kEvT * kEvU >= T) break;
-#pragma unroll
-            for (int u = 0; u < kEvU; u++)
-                ev_load<kH128, kArr>(sm, st.idx, st.w, c0 + kEvT * (2 * kEvU + u) + threadIdx.x, T, cur, A[u]);
-            ev_process<kH128, kArr>(sm, st, B, fs_addr, dp_addr, pp_lo, H, n_w, n_rw, net_debug);
+            for (int u = 0; u < U; u++) ev_load<kH128, kArr>(sm, st.idx, st.w, c0 + kEvT * u + threadIdx.x, T, cur, L[u]);
+            ev_process<kH128, kArr, U>(sm, st, L, fs_addr, dp_addr, pp_lo, H, n_w, n_rw, net_debug);
         }
         __syncthreads();                           // row table reused next round
     }
