@@ -936,10 +936,10 @@ __device__ __forceinline__ void ev_load(const EvSmem &sm, const uint32_t *__rest
     }
 }
 
-template <bool kH128, bool kArr, int U>
+template <bool kH128, int U>
 __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st, const EvLoad (&L)[U],
                                            uint32_t fs_addr, uint32_t dp_addr, uint32_t pp_lo, uint32_t H,
-                                           uint32_t &n_w, uint32_t &n_rw, uint32_t net_debug) {
+                                           uint32_t &n_w, uint32_t &n_rw, uint32_t &n_frw, uint32_t net_debug) {
 #pragma unroll
     for (int u = 0; u < U; u++) {
         if (L[u].r == 0xffffffffu) continue;
@@ -965,10 +965,11 @@ __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st,
         const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
                              __uint_as_float(L[u].w.w)};
         float *wp = st.w + er.cb + L[u].x0;
-        if (!kArr) {
+        if (!(er.meta & kMetaArr)) {
             // ---- forced flush (age H): the window's spike at bit p adds
             //      A+ (x_pre D+[H - p]); several spikes: the fpot factor (gathered)
             n_rw += __popc(hm);
+            n_frw += __popc(hm);
 #pragma unroll
             for (int e = 0; e < 4; e++) {
                 const bool hit = (hm >> e) & 1u;
@@ -1013,18 +1014,22 @@ __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st,
     }
 }
 
-// The CTA's rows of one kind (arrivals or flushes) in rounds of kEvRows.
-template <bool kH128, bool kArr>
-__device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const RowDesc *Vl, uint32_t nrows_all,
-                                        bool from_back, size_t base, uint32_t fs_addr, uint32_t dp_addr,
-                                        uint32_t pp_lo, uint32_t H, uint32_t &n_syn, uint32_t &n_w, uint32_t &n_rw,
+// The CTA's rows -- its arrivals, then its forced flushes -- flattened into one
+// chunk stream, in rounds of kEvRows rows.
+template <bool kH128>
+__device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const RowDesc *Vl, uint32_t a_begin,
+                                        uint32_t nAb, size_t f_back, uint32_t r_end, uint32_t fs_addr,
+                                        uint32_t dp_addr, uint32_t pp_lo, uint32_t H, uint32_t &n_syn,
+                                        uint32_t &n_fsyn, uint32_t &n_w, uint32_t &n_rw, uint32_t &n_frw,
                                         uint32_t net_debug) {
-    for (uint32_t r0 = 0; r0 < nrows_all; r0 += kEvRows) {
-        const uint32_t nrows = min(nrows_all - r0, (uint32_t)kEvRows);
+    for (uint32_t r0 = 0; r0 < r_end; r0 += kEvRows) {
+        const uint32_t nrows = min(r_end - r0, (uint32_t)kEvRows);
         uint32_t nch = 0;
         EvRow er;
         if (threadIdx.x < nrows) {
-            const RowDesc d = Vl[from_back ? base - (r0 + threadIdx.x) : base + r0 + threadIdx.x];
+            const uint32_t r = r0 + threadIdx.x;
+            const RowDesc d = Vl[r < nAb ? (size_t)(a_begin + r) : f_back - (r - nAb)];
+            const bool arr = (d.meta & kMetaArr) != 0;
             const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
             er.cb = cs & ~3ll;
             er.lo = (uint32_t)(cs - er.cb);
@@ -1033,9 +1038,10 @@ __device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const Ro
             er.meta = d.meta;
             er.pad = 0;
             // a flush with x_pre == 0 changes no weight (potentiation adds A+ 0, R31)
-            if (cs < ce && (kArr || d.xp != 0.0f)) {
+            if (cs < ce && (arr || d.xp != 0.0f)) {
                 nch = (er.hi + 3) >> 2;
                 n_syn += (uint32_t)(ce - cs);
+                if (!arr) n_fsyn += (uint32_t)(ce - cs);
             }
         }
         uint32_t T = 0;
@@ -1048,12 +1054,11 @@ __device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const Ro
         if (threadIdx.x == 0) sm.incl[nrows] = 0xffffffffu;      // (the walk never passes the last row)
         __syncthreads();
         uint32_t cur = 0;
-        constexpr int U = kArr ? 1 : kEvU;
-        for (uint32_t c0 = 0; c0 < T; c0 += kEvT * U) {
-            EvLoad L[U];
+        for (uint32_t c0 = 0; c0 < T; c0 += kEvT * kEvU) {
+            EvLoad L[kEvU];
 #pragma unroll
-            for (int u = 0; u < U; u++) ev_load<kH128, kArr>(sm, st.idx, st.w, c0 + kEvT * u + threadIdx.x, T, cur, L[u]);
-            ev_process<kH128, kArr, U>(sm, st, L, fs_addr, dp_addr, pp_lo, H, n_w, n_rw, net_debug);
+            for (int u = 0; u < kEvU; u++) ev_load<kH128, false>(sm, st.idx, st.w, c0 + kEvT * u + threadIdx.x, T, cur, L[u]);
+            ev_process<kH128, kEvU>(sm, st, L, fs_addr, dp_addr, pp_lo, H, n_w, n_rw, n_frw, net_debug);
         }
         __syncthreads();                           // row table reused next round
     }
@@ -1093,17 +1098,14 @@ k_stdp_ev(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
     __syncthreads();
     const uint32_t fs_addr = smem_u32(fpos_s) - f_lo;             // position of post neuron j: + j
     const uint32_t dp_addr = smem_u32(sm.dplus);
-    uint32_t n_syn = 0, n_w = 0, n_rw = 0;
-    if (!(net.debug & 2u))                       // (experiments: no arrivals / no flushes)
-        ev_rows<kH128, true>(sm, st, Vl, a_end - a_begin, false, a_begin, fs_addr, dp_addr, pp_lo, net.H, n_syn, n_w,
-                             n_rw, net.debug);
-    uint32_t f_syn = 0, f_rw = 0;
-    if (!(net.debug & 4u))
-        ev_rows<kH128, false>(sm, st, Vl, f_end - f_begin, true, cap_back - f_begin, fs_addr, dp_addr, pp_lo, net.H,
-                              f_syn, n_w, f_rw, net.debug);
-    n_syn = __reduce_add_sync(0xffffffffu, n_syn + f_syn);
+    uint32_t n_syn = 0, n_w = 0, n_rw = 0, f_syn = 0, f_rw = 0;
+    // (experiments: net.debug 2 = no arrivals, 4 = no flushes)
+    const uint32_t nAb = (net.debug & 2u) ? 0u : a_end - a_begin, nFb = (net.debug & 4u) ? 0u : f_end - f_begin;
+    ev_rows<kH128>(sm, st, Vl, a_begin, nAb, cap_back - f_begin, nAb + nFb, fs_addr, dp_addr, pp_lo, net.H, n_syn,
+                   f_syn, n_w, n_rw, f_rw, net.debug);
+    n_syn = __reduce_add_sync(0xffffffffu, n_syn);
     n_w = __reduce_add_sync(0xffffffffu, n_w);
-    n_rw = __reduce_add_sync(0xffffffffu, n_rw + f_rw);
+    n_rw = __reduce_add_sync(0xffffffffu, n_rw);
     f_syn = __reduce_add_sync(0xffffffffu, f_syn);
     f_rw = __reduce_add_sync(0xffffffffu, f_rw);
     if (lane == 0) {
