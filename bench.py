@@ -43,7 +43,8 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 METRIC = "wall-s per bio-second & synaptic events/s at 1/2/4/8 B200; % HBM roofline"
-KERNEL_OF = {"front": "k_front", "stdp": "k_stdp_ev", "deliver": "k_deliver"}
+KERNEL_OF = {"front": "k_front", "stdp": "k_stdp_ev<arrivals>", "flush": "k_stdp_ev<flushes> (k_flush)",
+             "deliver": "k_deliver"}
 
 
 def parse(argv=None):
@@ -236,6 +237,20 @@ def main(argv=None):
     stream = torch.cuda.Stream(dev)
     pre_steps = a.settle + a.warmup
 
+    def prepare(s, chunks):
+        """The untimed settle + warm-up steps, issued so that the step graphs the
+        timed region replays (one per distinct call size in `chunks`, captured
+        and instantiated by the library on first use) already exist."""
+        sizes = sorted({min(c, 64) for c in chunks if c > 0})
+        head = pre_steps - a.warmup - sum(sizes)
+        if head > 0:
+            s.step(head)
+            for c in sizes:
+                s.step(c)
+        else:
+            s.step(pre_steps - a.warmup)
+        s.step(a.warmup)
+
     def make(flags=0):
         if a.idx16:
             flags |= FLAG_IDX16
@@ -271,7 +286,7 @@ def main(argv=None):
     setup_s = time.perf_counter() - t0
     info = sim.info()
     build_ms = sim.phase_times()["BUILD"]      # device time of count + scan + fill + segments (f4)
-    sim.step(pre_steps)                        # settle + warm-up (untimed)
+    prepare(sim, [a.steps])                    # settle + warm-up (untimed)
     barrier()
     m0 = sim.metrics()
     spk0 = sim.read_state("SPIKE_COUNT").astype(np.int64)
@@ -301,7 +316,7 @@ def main(argv=None):
     spans = None
     if not a.no_ktime:
         sk = make(FLAG_KTIME)
-        sk.step(pre_steps)
+        prepare(sk, [a.steps])
         k0 = sk.ktime()                         # folds (and discards) the settle / warm-up steps
         mk0 = sk.metrics()
         barrier()
@@ -318,7 +333,7 @@ def main(argv=None):
         del sk
         spans = {"same_window": bool(reduce(0.0 if same else 1.0, MAX) == 0.0),
                  "ms_per_step_instrumented": ms_k / a.steps}
-        for k in ("front", "stdp", "deliver"):
+        for k in ("front", "stdp", "flush", "deliver"):
             st = k1[k]["steps"] - k0[k]["steps"]
             if st <= 0:
                 continue
@@ -330,7 +345,7 @@ def main(argv=None):
     e2e = None
     if not a.no_e2e:
         se = make()
-        se.step(pre_steps)
+        prepare(se, [64, a.steps % 64])
         nw = (info["N"] + 31) // 32
         chunk = 64
         # the steps' rasters land in a pinned host buffer the caller owns
@@ -371,14 +386,20 @@ def main(argv=None):
     #   k_stdp_ev (k_stdp for the ablation schedules): 4 B target id per
     #              visited plastic synapse + 8 B (weight read and written) per
     #              synapse of an arriving row or whose target fired in the
-    #              window + 16 B per visited row
+    #              window + 16 B per visited row; split into the arrivals
+    #              ("stdp", critical path) and the forced flushes ("flush",
+    #              side branch) when the step graph runs them apart
     #   k_deliver: 8 B per delivered event (id + weight; 6 B with --idx16) +
     #              8 B per (arriving row, slice) pivot pair + 4 B per slice
     #              neuron and receptor written back
     #   k_front:   32 B per LIF neuron, 16 B per Poisson neuron (8(a1))
     n_pois = sum(p.n for p in rc.pops if p.kind == W.POISSON)
+    stdp_b = (4 * dm_local["STDP_SYN"] + 8 * dm_local["STDP_WRW"] + 16 * dm_local["STDP_ROWS"]) / K
+    flush_b = (4 * dm_local["FLUSH_SYN"] + 8 * dm_local["FLUSH_WRW"] + 16 * dm_local["FLUSH_ROWS"]) / K
+    split = bool(spans and "flush" in spans)
     kb = {
-        "stdp": (4 * dm_local["STDP_SYN"] + 8 * dm_local["STDP_WRW"] + 16 * dm_local["STDP_ROWS"]) / K,
+        "stdp": stdp_b - flush_b if split else stdp_b,
+        "flush": flush_b if split else 0.0,
         "deliver": ((6 if a.idx16 else 8) * dm_local["EVENTS"] + 8 * dm_local["SPIKES"] * info["nslices"]) / K
                    + 4 * nrcpt * (info["tgt_hi"] - info["tgt_lo"]),
         "front": 32.0 * (info["N"] - n_pois) + 16.0 * n_pois,
@@ -405,7 +426,7 @@ def main(argv=None):
         if dom == "stdp" and (a.plasticity != "event" or a.flush_period):
             dk = "k_stdp"
         traffic, traffic_src = ncu_traffic(dk, a.config, flags_s)
-        sd = [k for k in ("stdp", "deliver") if k in kern]
+        sd = [k for k in ("stdp", "flush", "deliver") if k in kern]
         sd_b = sum(kern[k]["bytes_per_launch"] for k in sd)
         sd_us = sum(kern[k]["us_per_launch"] for k in sd)
         step_b = sum(kb.values())
@@ -446,7 +467,7 @@ def main(argv=None):
                           "allocation excluded; the paper quotes ~200M synapses/ms on its GPU (P:391, context)"},
         "rates_hz": rates,
         "per_step": {k.lower(): v / a.steps for k, v in dm.items()},
-        "gpu_launches": a.steps * (3 if rc.plastic else 2) + (a.steps if world > 1 else 0),
+        "gpu_launches": a.steps * ((4 if split else 3) if rc.plastic else 2) + (a.steps if world > 1 else 0),
         "roofline": roof,
         "kernel_spans": spans,
         "e2e": e2e,

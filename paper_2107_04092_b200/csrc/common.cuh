@@ -85,10 +85,16 @@ constexpr int kFrontThreads = 1024;   // k_front CTA = one list region
 
 struct Counters {
     int64_t t;               // next step to simulate
+    int64_t tfl;             // the step of the next k_flush launch (k_flush runs once per step, in order;
+                             // its last CTA advances it)
+    uint32_t fticket;        // CTA-completion ticket of k_flush
+    uint32_t pad2;
     uint32_t ticket;         // CTA-completion ticket of the slice kernel
     uint32_t pad;
     unsigned long long metric[16];
-    uint32_t lst[2][4];      // by step parity: list lengths (plastic arrivals, arrivals, forced flushes, 0)
+    alignas(16) uint32_t lst[8][4];      // by step t & 7: list lengths (plastic arrivals, arrivals, forced flushes, 0);
+                             // several slots: the forced flushes of step t are read by k_flush(t), which runs
+                             // beside the next steps' k_deliver / k_front (engine.cu, side branch)
     uint32_t rlst[4];        // read-out flush list length
 };
 
@@ -117,8 +123,12 @@ struct StateDev {
     int32_t *ref, *in_e, *in_i;
     uint64_t *hist;          // bits 0..63 of the spike history (bit s: step t - s)
     uint64_t *hist_hi;       // H = 128: bits 64..127 (else unused)
+    // four buffers by step (buffer t & 3 at + (t & 3) * fstride / rstride): k_flush(t) reads step t's
+    // while k_front(t+1), k_front(t+2) write theirs
     float *fpot;             // post-plastic j with spikes in its H-bit window: sum of D+[H - s] over them
     uint8_t *fpos;           // post-plastic j: 0xfe no spike in its H-bit window, 0xff several, else the bit of the only one
+    uint32_t fstride;        // elements per fpos / fpot buffer
+    uint32_t rstride;        // words per `recent` buffer
     uint32_t *nspk;
     uint32_t *ring;          // [kRingSlots][ring_stride]
     // source rows
@@ -134,11 +144,11 @@ struct StateDev {
     // work lists (by step parity), appended by k_front CTAs (one atomic per
     // CTA and list, lengths in Counters::lst): plastic visits (arrivals from
     // the front, forced flushes from the back: entry cap - 1 - r) and arrivals
-    RowDesc *vdesc[2], *adesc[2];
+    RowDesc *vdesc[4], *adesc[2];   // visits by t & 3; arrivals by the parity of their step
     RowDesc *rdesc;          // read-out flush rows (length Counters::rlst[0])
     uint32_t nblk;           // k_front CTAs (list capacity nblk * kFrontThreads)
     uint32_t *vmask[2];      // [nwords] rows visited at the step of that parity
-    uint32_t *recent;        // [nwords] bit i: post-plastic neuron i fired in the last 64 steps
+    uint32_t *recent;        // [4][rstride] bit i: post-plastic neuron i fired in the last H steps
     uint32_t *sendbuf;       // [wmax] this rank's spike words of the step (world > 1)
     uint32_t *gath;          // [2][world][wmax] all ranks' words (NCCL: slot 0; local group: by step parity)
     Counters *ctr;

@@ -5,8 +5,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <iterator>
 #include <map>
 #include <mutex>
 #include <cstdarg>
@@ -27,17 +29,20 @@ cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, ui
 cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
 cudaError_t build_idx16(const NetDev &, const uint32_t *, uint16_t *, int64_t, cudaStream_t);
 uint32_t front_blocks(const NetDev &);
-cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool);
+cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool, bool);
 size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
-size_t deliver_smem_bytes(const NetDev &);
+size_t deliver_smem_bytes(const NetDev &, bool);
 cudaError_t kernels_configure(int);
 cudaError_t launch_kspan_reset(KSpan *, cudaStream_t);
 cudaError_t launch_stdp(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
 cudaError_t launch_deliver_rowwise(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
-cudaError_t launch_stdp_ev(const NetDev &, const StateDev &, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
+cudaError_t launch_stdp_ev(const NetDev &, const StateDev &, uint32_t, uint32_t, uint32_t, cudaStream_t, bool, int);
+uint32_t flush_ctas_per_sm();
+void set_launch_priority(int);
 size_t ev_smem_bytes(uint32_t, uint32_t);
-cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool);
-cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t);
+size_t flush_smem_bytes(uint32_t, uint32_t);
+cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool, bool);
+cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
 cudaError_t launch_unpack(const NetDev &, const StateDev &, const uint32_t *, int64_t, cudaStream_t);
 }  // namespace snn
@@ -108,7 +113,21 @@ struct snn_sim {
     int64_t nsyn = 0;
     int64_t t = 0;  // steps enqueued so far
     cudaStream_t stream = nullptr, cap_stream = nullptr;
-    cudaGraphExec_t g_many = nullptr, g_one = nullptr;
+    // the ahead step: k_front(t) builds the arrival list
+    // of t+1, k_deliver(t) runs the plastic arrivals' STDP, k_flush(t) the
+    // forced flushes after it
+    bool ahead = false;
+    uint32_t flush_grid = 1, flush_grid_side = 1;   // k_flush CTAs: serial step / side branch
+    // step graph (SNN_PIPE, experiments): 0 serial; 1 ahead + k_flush(t) on a
+    // side branch joined before k_deliver(t + fl_lag); 2 no ahead list, k_stdp_arr
+    // + k_flush(t) on a side branch joined before k_stdp_arr(t+1)
+    int pipe = 0, fl_lag = 2, prio_hi = 0, prio_lo = 0;
+    bool use_prio = false;
+    cudaStream_t cap_side = nullptr;
+    cudaEvent_t ev_front = nullptr, ev_flush[2] = {nullptr, nullptr};
+    // captured step graphs by step count (<= kGraphSteps): a call of n steps
+    // replays ceil(n / 64) graphs, so a step's side branch is joined once per call
+    std::map<uint32_t, cudaGraphExec_t> graphs;
     std::vector<void *> allocs;
     uint32_t splits = 1;                 // k_deliver CTAs per slice
     uint32_t stdp_grid = 1;              // k_stdp CTAs
@@ -126,7 +145,7 @@ struct snn_sim {
     bool local_group = false;
     // phase timing
     std::vector<cudaEvent_t> ev_pool;
-    std::vector<std::vector<cudaEvent_t>> ev_steps;  // per step: 5 boundary events
+    std::vector<std::vector<cudaEvent_t>> ev_steps;  // per step: 5 boundary events (front, STDP, delivery, flushes)
     size_t ev_used = 0;
     double phase_ms[8] = {0};
 
@@ -394,8 +413,9 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.in_i, int32_t, N);
     ALLOC(st.hist, uint64_t, N);
     ALLOC(st.hist_hi, uint64_t, cfg.history_bits > 64 ? N : 1);
-    ALLOC(st.fpot, float, N);
-    ALLOC(st.fpos, uint8_t, (size_t)N + 16);
+    st.fstride = (N + 16 + 15) & ~15u;
+    ALLOC(st.fpot, float, 4ull * st.fstride);
+    ALLOC(st.fpos, uint8_t, 4ull * st.fstride);
     ALLOC(st.nspk, uint32_t, N);
     // exchange geometry: rank r owns words [r share_w, ...), at most share_w + 1
     // of them (the word straddling R); ring slots padded for the unpack
@@ -418,13 +438,14 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.seg, uint2, N);
     st.nblk = front_blocks(net);
     const size_t nreg = (size_t)st.nblk * kFrontThreads;
+    for (int b = 0; b < 4; b++) ALLOC(st.vdesc[b], RowDesc, net.nstdp ? nreg : 1);
     for (int b = 0; b < 2; b++) {
-        ALLOC(st.vdesc[b], RowDesc, net.nstdp ? nreg : 1);
         ALLOC(st.adesc[b], RowDesc, nreg);
         ALLOC(st.vmask[b], uint32_t, net.nwords);
     }
     ALLOC(st.rdesc, RowDesc, net.nstdp ? nreg : 1);
-    ALLOC(st.recent, uint32_t, net.nwords + 4);   // + the tail of its 16-byte bulk copy
+    st.rstride = (net.nwords + 4 + 3) & ~3u;      // + the tail of its 16-byte bulk copy
+    ALLOC(st.recent, uint32_t, 4ull * st.rstride);
     st.trace = nullptr;
     if (cfg.flags & SNN_FLAG_TRACE) {
         ALLOC(st.trace, unsigned long long, (size_t)kTraceKernels * kTraceCtas * 4);
@@ -447,7 +468,7 @@ static snn_status finalize(snn_sim *sim) {
         snn_status r = exchange_setup(sim);
         if (r != SNN_OK) return r;
     }
-    CK(cudaMemsetAsync(st.recent, 0, sizeof(uint32_t) * net.nwords, s));
+    CK(cudaMemsetAsync(st.recent, 0, sizeof(uint32_t) * 4ull * st.rstride, s));
     for (int b = 0; b < 2; b++) {
         CK(cudaMemsetAsync(st.vmask[b], 0, sizeof(uint32_t) * net.nwords, s));
     }
@@ -517,14 +538,48 @@ static snn_status finalize(snn_sim *sim) {
     if (sim->pp_hi <= sim->pp_lo) sim->pp_lo = sim->pp_hi = 0;
     net.pp_lo = sim->pp_lo;
     net.pp_hi = sim->pp_hi;
-    if (deliver_smem_bytes(net) > 200 * 1024)
-        return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory", C, deliver_smem_bytes(net));
+    // the split step (k_front's arrival list one step ahead, the plastic
+    // arrivals inside the delivery, k_flush beside it): the event schedule
+    // with flushes at age H and sliced delivery; the arrivals of t + 2 must be
+    // known at t (D >= 2; D >= 3 across ranks, whose words of t - 1 arrive
+    // during step t - 1).  Otherwise the unsplit step (front -> STDP -> delivery).
+    {
+        const uint32_t dmin = (cfg.world > 1 ? 1u : 0u) + (sim->plastic ? 2u : 1u);
+        sim->ahead = cfg.delivery == SNN_DELIV_SLICED && net.D >= dmin &&
+                     (!sim->plastic || (cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0)) &&
+                     !getenv("SNN_NO_AHEAD");   // (tuning knob: the unsplit step)
+    }
+    if (deliver_smem_bytes(net, sim->ahead) > 200 * 1024)
+        return sim->fail(SNN_E_INVALID, "slice width %u needs %zu B of shared memory", C,
+                         deliver_smem_bytes(net, sim->ahead));
     if (sim->plastic && stdp_smem_bytes(net, sim->pp_lo, sim->pp_hi) > 227 * 1024)
         return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for the shared bitmap");
     sim->ev_kernel = sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 &&
                      ev_smem_bytes(sim->pp_lo, sim->pp_hi) <= 227 * 1024;
     if (sim->plastic && cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0 && !sim->ev_kernel)
         return sim->fail(SNN_E_UNSUPPORTED, "post-synaptic population of STDP too large for k_stdp_ev's shared bitmap");
+    if (sim->plastic && (!sim->ev_kernel || flush_smem_bytes(sim->pp_lo, sim->pp_hi) > 227 * 1024))
+        sim->ahead = false;      // (k_flush needs its table in shared memory)
+    // default (graph steps): the ahead step with k_flush on a side branch on
+    // half of the SMs (measured on cfg3: 42.2 us/step vs 58.2 serial, 49.4 on
+    // every SM -- the critical-path kernels are latency-bound, and a full-width
+    // flush slows them more than it gains)
+    sim->pipe = sim->ahead && sim->plastic ? 1 : 0;
+    if (const char *e = getenv("SNN_PIPE")) sim->pipe = atoi(e);          // (experiments)
+    if (const char *e = getenv("SNN_FL_LAG")) sim->fl_lag = atoi(e) < 2 ? 1 : 2;
+    if (sim->pipe == 2) sim->ahead = false;
+    if (sim->pipe == 1 && !sim->ahead) sim->pipe = 0;
+    if (!sim->plastic || !sim->ev_kernel || flush_smem_bytes(sim->pp_lo, sim->pp_hi) > 227 * 1024)
+        if (sim->pipe == 2) sim->pipe = 0;
+    if (sim->pipe != 0) {
+        CK(cudaStreamCreateWithFlags(&sim->cap_side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&sim->ev_front, cudaEventDisableTiming));
+        for (auto &e : sim->ev_flush) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        if (getenv("SNN_PRIO")) {
+            sim->use_prio = true;
+            CK(cudaDeviceGetStreamPriorityRange(&sim->prio_lo, &sim->prio_hi));
+        }
+    }
     // k_stdp flattens up to 128 rows' plastic spans (16-byte chunks) per round
     // into one uint32 chunk index
     if (sim->plastic && 128ull * ((uint64_t)net.N / 4 + 2) >= (1ull << 32))
@@ -537,13 +592,18 @@ static snn_status finalize(snn_sim *sim) {
     sim->splits = std::max(1u, (uint32_t)(2 * nsm) / ns);   // <= 2 CTAs per SM, one wave
     if (const char *sp = getenv("SNN_DELIVER_SPLITS")) sim->splits = std::max(1, atoi(sp));  // tuning knob
     sim->stdp_grid = (uint32_t)nsm;                 // k_stdp: one CTA per SM
+    sim->flush_grid = (uint32_t)nsm * flush_ctas_per_sm();
+    sim->flush_grid_side = std::max(1, nsm / 2);
+    if (const char *e = getenv("SNN_FL_CTAS")) sim->flush_grid_side = std::max(1, atoi(e));   // (experiments)
+
     CK(cudaStreamSynchronize(s));
     sim->state = 1;
     return SNN_OK;
 }
 
 // ---------------------------------------------------------------- the step
-static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bool first, int64_t step_k = 0) {
+static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bool first, int64_t step_k = 0,
+                               cudaStream_t side = nullptr, uint32_t gk = 0) {
     NetDev net = sim->net;
     if ((sim->cfg.flags & SNN_FLAG_TRACE) && getenv("SNN_DEBUG_KERNELS"))   // kernel experiments (trace runs only)
         net.debug = (uint32_t)atoi(getenv("SNN_DEBUG_KERNELS"));
@@ -556,7 +616,8 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     const int64_t t = sim->t + step_k;                              // host copy (direct mode only)
     if (multi && sim->local_group && t > 0)                         // peers' spikes of t-1 -> ring
         CK(launch_unpack(net, st, st.gath + (size_t)((t - 1) & 1) * sim->cfg.world * sim->wmax, t - 1, s));
-    CK(launch_front(net, st, s, pdl && !first));                    // (1) P:36 + work lists
+    if (sim->use_prio) set_launch_priority(sim->prio_hi);
+    CK(launch_front(net, st, s, pdl && !first, sim->ahead));        // (1) P:36 + work lists
     if (multi) {                                                    // spike words of t -> peers
         snn_status r = exchange_enqueue(sim, s, t);
         if (r != SNN_OK) return r;
@@ -565,12 +626,35 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     if (sim->plastic) {                                             // (2) P:37-39
         // the event schedule (flushes at age H): k_stdp_ev; the ablation
         // schedules and batched flushes: the generic k_stdp
-        if (sim->ev_kernel) CK(launch_stdp_ev(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
-        else CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
+        if (side && (sim->pipe == 1 || sim->pipe == 2)) {
+            // (experiments) the forced flushes on a side branch of the graph
+            CK(cudaEventRecord(sim->ev_front, s));
+            const uint32_t lag = sim->pipe == 1 ? (uint32_t)sim->fl_lag : 1u;
+            if (gk >= lag) CK(cudaStreamWaitEvent(s, sim->ev_flush[(gk - lag) & 1], 0));
+            if (sim->pipe == 2) CK(launch_stdp_ev(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl, 1));
+            CK(cudaStreamWaitEvent(side, sim->ev_front, 0));
+            if (sim->use_prio) set_launch_priority(sim->prio_lo);
+            CK(launch_stdp_ev(net, st, sim->flush_grid_side, sim->pp_lo, sim->pp_hi, side, false, 2));
+            if (sim->use_prio) set_launch_priority(sim->prio_hi);
+            CK(cudaEventRecord(sim->ev_flush[gk & 1], side));
+        } else if (sim->ahead) {
+            // the plastic arrivals run inside k_deliver(t), the forced flushes of t
+            // in k_flush(t) after it (below)
+        } else if (sim->pipe == 2) {
+            CK(launch_stdp_ev(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl, 1));
+        } else if (sim->ev_kernel) {
+            CK(launch_stdp_ev(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl, 0));
+        } else {
+            CK(launch_stdp(net, st, -1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl));
+        }
     }
     if (ev) CK(cudaEventRecord(ev[2], s));
     if (net.deliv_mode == SNN_DELIV_ROWWISE) CK(launch_deliver_rowwise(net, st, sim->stdp_grid, s, pdl));   // Fig. 3a
-    else CK(launch_deliver(net, st, sim->splits, s, pdl));          // (3) P:41, Fig. 3b
+    else CK(launch_deliver(net, st, sim->splits, s, pdl, sim->ahead));   // (3) P:41, Fig. 3b
+    if (sim->plastic && (sim->ahead || sim->pipe == 2) && !(side && sim->pipe != 0))   // (2') forced flushes of t (R3)
+        CK(launch_stdp_ev(net, st, sim->flush_grid, sim->pp_lo, sim->pp_hi, s, pdl, 2));
+    if (sim->use_prio) set_launch_priority(0);
+    if (ev) CK(cudaEventRecord(ev[4], s));
     if (ev) CK(cudaEventRecord(ev[3], s));
     return SNN_OK;
 }
@@ -579,13 +663,16 @@ static snn_status capture(snn_sim *sim, uint32_t nsteps, cudaGraphExec_t *out) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(sim->cap_stream, cudaStreamCaptureModeThreadLocal));
     for (uint32_t k = 0; k < nsteps; k++) {
-        snn_status r = enqueue_step(sim, sim->cap_stream, nullptr, k == 0);
+        snn_status r = enqueue_step(sim, sim->cap_stream, nullptr, k == 0, 0, sim->cap_side, k);
         if (r != SNN_OK) {
             cudaStreamEndCapture(sim->cap_stream, &g);
             if (g) cudaGraphDestroy(g);
             return r;
         }
     }
+    if (sim->cap_side && sim->pipe != 0)                            // join the side branch
+        for (uint32_t k = nsteps > 2 ? nsteps - 2 : 0; k < nsteps; k++)
+            CK(cudaStreamWaitEvent(sim->cap_stream, sim->ev_flush[k & 1], 0));
     CK(cudaStreamEndCapture(sim->cap_stream, &g));
     CK(cudaGraphInstantiate(out, g, 0));
     CK(cudaGraphDestroy(g));
@@ -739,7 +826,7 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
             cudaEvent_t *ev = nullptr;
             if (timing) {
                 if (sim->ev_used == sim->ev_steps.size()) {
-                    std::vector<cudaEvent_t> v(4);
+                    std::vector<cudaEvent_t> v(5);
                     for (auto &e : v) CK(cudaEventCreate(&e));
                     sim->ev_steps.push_back(v);
                 }
@@ -751,15 +838,24 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
         }
         return SNN_OK;
     }
-    if (!sim->g_many) {
-        snn_status r = capture(sim, kGraphSteps, &sim->g_many);
-        if (r != SNN_OK) return r;
-        r = capture(sim, 1, &sim->g_one);
-        if (r != SNN_OK) return r;
+    for (uint32_t k = 0; k < n_steps;) {
+        const uint32_t n = std::min(kGraphSteps, n_steps - k);
+        auto it = sim->graphs.find(n);
+        if (it == sim->graphs.end()) {
+            if (sim->graphs.size() >= 16) {              // (bounded cache: drop the others, keep 64)
+                for (auto &g : sim->graphs)
+                    if (g.first != kGraphSteps) cudaGraphExecDestroy(g.second);
+                for (auto g = sim->graphs.begin(); g != sim->graphs.end();)
+                    g = g->first != kGraphSteps ? sim->graphs.erase(g) : std::next(g);
+            }
+            cudaGraphExec_t ge = nullptr;
+            snn_status r = capture(sim, n, &ge);
+            if (r != SNN_OK) return r;
+            it = sim->graphs.emplace(n, ge).first;
+        }
+        CK(cudaGraphLaunch(it->second, sim->stream));
+        k += n;
     }
-    uint32_t k = 0;
-    for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(sim->g_many, sim->stream));
-    for (; k < n_steps; k++) CK(cudaGraphLaunch(sim->g_one, sim->stream));
     sim->t += n_steps;
     return SNN_OK;
 }
@@ -768,7 +864,7 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
 // plastic row up to t_last without a pre spike.
 static snn_status readout_flush(snn_sim *sim) {
     if (!sim->plastic || sim->t == 0) return SNN_OK;
-    CK(launch_readout(sim->net, sim->st, sim->t - 1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, sim->stream));
+    CK(launch_readout(sim->net, sim->st, sim->t - 1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, sim->stream, sim->ahead));
     return SNN_OK;
 }
 
@@ -835,8 +931,8 @@ static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool 
     case SNN_FIELD_HIST_DEV_HI:
         if (net.H <= 64) return sim->fail(SNN_E_STATE, "HIST_DEV_HI needs history_bits = 128");
         f.dev = st.hist_hi + base; f.elem = 8; break;
-    case SNN_FIELD_FPOT: f.dev = st.fpot + base; f.elem = 4; break;
-    case SNN_FIELD_FPOS: f.dev = st.fpos + base; f.elem = 1; break;
+    case SNN_FIELD_FPOT: f.dev = st.fpot + (size_t)((sim->t + 3) & 3) * st.fstride + base; f.elem = 4; break;   // step t-1's
+    case SNN_FIELD_FPOS: f.dev = st.fpos + (size_t)((sim->t + 3) & 3) * st.fstride + base; f.elem = 1; break;
     default: per_neuron = false; break;
     }
     if (per_neuron) {
@@ -851,7 +947,8 @@ static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool 
         case SNN_FIELD_WEIGHTS: f.dev = st.w; f.elem = 4; f.bytes = 4ull * sim->nsyn; break;
         case SNN_FIELD_PIVOTS: f.dev = st.piv; f.elem = 4; f.bytes = 4ull * sim->N * (net.nslices + 1); break;
         case SNN_FIELD_SPIKE_RING: f.dev = st.ring; f.elem = 4; f.bytes = 4ull * kRingSlots * net.nwords; f.ring = true; break;
-        case SNN_FIELD_RECENT: f.dev = st.recent; f.elem = 4; f.bytes = 4ull * net.nwords; break;
+        case SNN_FIELD_RECENT:
+            f.dev = st.recent + (size_t)((sim->t + 3) & 3) * st.rstride; f.elem = 4; f.bytes = 4ull * net.nwords; break;
         case SNN_FIELD_STEP: f.host_i64[0] = sim->t; f.host = f.host_i64; f.elem = 8; f.bytes = 8; break;
         case SNN_FIELD_METRICS: f.dev = st.ctr->metric; f.elem = 8; f.bytes = 8 * 16; break;
         case SNN_FIELD_PHASE_TIMES: f.host = f.host_f64; f.elem = 8; f.bytes = 8 * 8; break;
@@ -894,12 +991,12 @@ static snn_status field_ref(snn_sim *sim, uint32_t field, uint32_t pop_id, bool 
     if (field == SNN_FIELD_PHASE_TIMES) {
         CK(cudaStreamSynchronize(s));
         for (size_t k = 0; k < sim->ev_used; k++) {
-            float ms[3];
-            for (int p = 0; p < 3; p++) CK(cudaEventElapsedTime(&ms[p], sim->ev_steps[k][p], sim->ev_steps[k][p + 1]));
+            float ms[4];
+            for (int p = 0; p < 4; p++) CK(cudaEventElapsedTime(&ms[p], sim->ev_steps[k][p], sim->ev_steps[k][p + 1]));
             sim->phase_ms[SNN_PHASE_FRONT] += ms[0];
-            sim->phase_ms[SNN_PHASE_STDP] += ms[1];
+            sim->phase_ms[SNN_PHASE_STDP] += ms[1] + ms[3];     // (ahead step: the forced flushes after delivery)
             sim->phase_ms[SNN_PHASE_DELIVERY] += ms[2];
-            sim->phase_ms[SNN_PHASE_TOTAL] += ms[0] + ms[1] + ms[2];
+            sim->phase_ms[SNN_PHASE_TOTAL] += ms[0] + ms[1] + ms[2] + ms[3];
         }
         sim->ev_used = 0;
         for (int k = 0; k < 8; k++) f.host_f64[k] = sim->phase_ms[k];
@@ -993,8 +1090,7 @@ void snn_destroy(snn_sim *sim) {
     if (sim->comm) g_nccl.commDestroy(sim->comm);
     if (sim->stream) cudaStreamSynchronize(sim->stream);
     cudaDeviceSynchronize();
-    if (sim->g_many) cudaGraphExecDestroy(sim->g_many);
-    if (sim->g_one) cudaGraphExecDestroy(sim->g_one);
+    for (auto &g : sim->graphs) cudaGraphExecDestroy(g.second);
     for (auto &v : sim->ev_steps)
         for (auto e : v) cudaEventDestroy(e);
     for (void *p : sim->allocs) {
@@ -1002,6 +1098,11 @@ void snn_destroy(snn_sim *sim) {
         else cudaFree(p);
     }
     if (sim->cap_stream) cudaStreamDestroy(sim->cap_stream);
+    if (sim->cap_side) cudaStreamDestroy(sim->cap_side);
+    if (sim->ev_front) cudaEventDestroy(sim->ev_front);
+    for (auto e : sim->ev_flush)
+        if (e) cudaEventDestroy(e);
+
     delete sim;
 }
 

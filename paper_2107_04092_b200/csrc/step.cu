@@ -23,6 +23,8 @@
 //
 // Floating point: every fp32 op is an explicit __f*_rn intrinsic, so there is no
 // FMA contraction (R19); accumulators are int32 fixed point (R18).
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 
@@ -54,7 +56,8 @@ struct Compact2 {
     uint32_t wa[kFrontThreads / 32], wb[kFrontThreads / 32], wc[kFrontThreads / 32];
     uint32_t tot[3], base[3];
 };
-__device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *lens, bool a, bool b, bool c, uint32_t &slot_a,
+__device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *len_a, uint32_t *len_b, uint32_t *len_c, bool a,
+                                         bool b, bool c, uint32_t &slot_a,
                                          uint32_t &slot_b, uint32_t &slot_c, uint32_t &tot_a, uint32_t &tot_b,
                                          uint32_t &tot_c) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -89,9 +92,9 @@ __device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *lens, bool a, b
             sm.tot[0] = ia;
             sm.tot[1] = ib;
             sm.tot[2] = ic;
-            sm.base[0] = ia ? atomicAdd(lens + 0, ia) : 0u;
-            sm.base[1] = ib ? atomicAdd(lens + 1, ib) : 0u;
-            sm.base[2] = ic ? atomicAdd(lens + 2, ic) : 0u;
+            sm.base[0] = ia ? atomicAdd(len_a, ia) : 0u;
+            sm.base[1] = ib ? atomicAdd(len_b, ib) : 0u;
+            sm.base[2] = ic ? atomicAdd(len_c, ic) : 0u;
         }
     }
     __syncthreads();
@@ -107,6 +110,7 @@ __device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *lens, bool a, b
 // ------------------------------------------------------------------ k_front
 // One thread per neuron i (it also owns source row i); warps cover 32
 // consecutive ids = one ring word.  P:36 "Update neurons, note which ones fire".
+template <bool kAhead>
 __global__ void __launch_bounds__(kFrontThreads)
 k_front(NetDev net, StateDev st) {
     __shared__ Compact2 cs;
@@ -192,7 +196,7 @@ k_front(NetDev net, StateDev st) {
             // spike in the last H steps, 0xff several, else the bit of the only one
             {
                 const uint32_t n1 = __popcll(h) + __popcll(hh);
-                st.fpos[i] = n1 == 0 ? (uint8_t)0xfeu
+                st.fpos[(size_t)(t & 3) * st.fstride + i] = n1 == 0 ? (uint8_t)0xfeu
                            : n1 > 1 ? (uint8_t)0xffu
                                     : (uint8_t)(h ? 63 - __clzll((long long)h) : 127 - __clzll((long long)hh));
             }
@@ -213,7 +217,7 @@ k_front(NetDev net, StateDev st) {
                     m &= ~(1ull << b);
                     f = __fadd_rn(f, dpl[H - b]);
                 }
-                st.fpot[i] = f;
+                st.fpot[(size_t)(t & 3) * st.fstride + i] = f;
             }
             const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
             st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
@@ -228,26 +232,29 @@ k_front(NetDev net, StateDev st) {
                                                            : (i >= net.tgt_lo && net.tgt_hi == net.R));
     if (lane == 0 && valid && wown) {
         st.ring[(size_t)(t & (kRingSlots - 1)) * net.ring_stride + (i >> 5)] = fword;
-        if (net.nstdp) st.recent[i >> 5] = rword;
+        if (net.nstdp) st.recent[(size_t)(t & 3) * st.rstride + (i >> 5)] = rword;
         // this rank's share of the step's input-neuron words, for the exchange
         const uint32_t w = i >> 5, w0 = net.rank * net.share_w;
         if (net.world > 1 && i < net.R && w >= w0 && w < w0 + net.wmax) st.sendbuf[w - w0] = fword;
     }
 
     // ---- (2) arrival of row i at step t: its spike of step t - D (hist[delay])
-    bool arr = false;
+    bool arr = false, arr1 = false, arr2 = false;
     if (valid) {
         if (net.D == 0) arr = fired;
         else if (t >= (int64_t)net.D) arr = ring_bit(st.ring, net.ring_stride, t - net.D, i);
+        // kAhead (D >= 2): the arrivals of t + 1 and t + 2 are spikes of steps <= t - 1
+        if (kAhead && t + 1 >= (int64_t)net.D) arr1 = ring_bit(st.ring, net.ring_stride, t + 1 - net.D, i);
+        if (kAhead && t + 2 >= (int64_t)net.D) arr2 = ring_bit(st.ring, net.ring_stride, t + 2 - net.D, i);
     }
     const bool plastic_row = valid && (p.flags & PF_PRE_PLASTIC);
-    bool visit = false;
-    RowDesc d;
+    bool visit = false, flush = false;
+    RowDesc d, a;
     if (plastic_row) {
         const StdpDev &sd = net.stdp[p.stdp];
         int32_t tl = st.tlu[i];
         float xp = st.xpre[i];
-        // finalise a visit of step t-1 (its synapses were updated by k_stdp(t-1))
+        // finalise a visit of step t-1 (its synapses were updated at t-1)
         if (t >= 1 && ((st.vmask[par ^ 1u][i >> 5] >> (i & 31)) & 1u)) {
             const bool arr_prev = (t - 1 >= (int64_t)net.D) && ring_bit(st.ring, net.ring_stride, t - 1 - net.D, i);
             xp = xpre_after(sd, xp, (int)(t - 1 - tl), arr_prev);
@@ -256,12 +263,25 @@ k_front(NetDev net, StateDev st) {
             st.tlu[i] = tl;
         }
         const int age = (int)(t - tl);
-        // forced flush (R3): at age H, or -- batched schedule (R33) -- every
-        // flush_period steps for the rows of age >= H - flush_period
-        const uint32_t K = net.flush_period;
-        visit = arr || (K == 0 ? age >= (int)net.H : ((uint32_t)(t % K) == K - 1 && age >= (int)(net.H - K)));
-        if (net.plast_mode == 2u) visit = true;   // SNN_PLAST_NAIVE: every row every step (Fig. 2a schedule)
-        if (visit) {
+        const int H = (int)net.H;
+        if (kAhead) {
+            // forced flush (R3) of the split step graph: k_flush(t) runs beside
+            // the delivery (and arrival STDP) of steps t and t+1, so a row it
+            // flushes must not arrive at t + 1.  A row of age H arriving at t + 1
+            // waits for that arrival (age H there); a row of age H - 1 arriving at
+            // t + 2 is flushed one step early (age H - 1) -- then no row of age H
+            // arrives at t + 1 (D >= 2: known one step ahead).  Exact by R4.
+            flush = !arr && !arr1 && (age >= H || (age == H - 1 && arr2));
+            visit = arr || flush;
+        } else {
+            // forced flush (R3): at age H, or -- batched schedule (R33) -- every
+            // flush_period steps for the rows of age >= H - flush_period
+            const uint32_t K = net.flush_period;
+            visit = arr || (K == 0 ? age >= H : ((uint32_t)(t % K) == K - 1 && age >= (int)(H - K)));
+            if (net.plast_mode == 2u) visit = true;   // SNN_PLAST_NAIVE: every row every step (Fig. 2a schedule)
+            flush = visit && !arr;
+        }
+        if (visit && (!kAhead || flush)) {
             const uint2 sg = st.seg[i];
             d.start = st.row_ptr[i];
             d.row = i;
@@ -272,31 +292,66 @@ k_front(NetDev net, StateDev st) {
             d.s1 = sg.y;
             d.pad = 0;
         }
+        if (kAhead && arr1) {
+            // the row's STDP state at t + 1 for the arrival (delivery of t + 1):
+            // after this step's visit, if any (its x_pre / tlu are finalised by
+            // k_front(t+1), identically)
+            const float xp1 = visit ? xpre_after(sd, xp, age, arr) : xp;
+            const int32_t tl1 = visit ? (int32_t)t : tl;
+            const uint2 sg = st.seg[i];
+            a.meta = (uint32_t)(t + 1 - tl1) | kMetaPlastic | ((uint32_t)p.stdp << 12);
+            a.xp = xp1;
+            a.s0 = sg.x;
+            a.s1 = sg.y;
+        }
     }
     const uint32_t vword = __ballot_sync(0xffffffffu, visit);
     if (net.nstdp && lane == 0 && valid) st.vmask[par][i >> 5] = vword;
-    // plastic visits -> k_stdp: the arrivals from the front of the list, the
-    // forced flushes from its back (so k_stdp can share each kind evenly);
-    // every arrival -> k_deliver
-    const bool parr = visit && arr, flush = visit && !arr;
     uint32_t sp, sa, sf, np, na, nf;
-    compact3(cs, st.ctr->lst[par], parr, arr, flush, sp, sa, sf, np, na, nf);
-    if (parr) st.vdesc[par][sp] = d;
-    if (flush) st.vdesc[par][(size_t)st.nblk * kFrontThreads - 1 - sf] = d;
-    if (arr) {                                       // every arriving row is delivered
-        RowDesc a;
-        a.start = st.row_ptr[i];
-        a.row = i;
-        a.meta = kMetaArr | ((uint32_t)(p.rcpt_uniform & 3) << 8);
-        if (p.rcpt_uniform < 0) a.meta |= (uint32_t)pi << 16;
-        a.xp = 0.0f;
-        a.s0 = a.s1 = 0;
-        a.pad = 0;
-        st.adesc[par][sa] = a;
+    if (kAhead) {
+        // forced flushes of t -> k_flush(t); arrivals of t + 1 -> k_deliver(t+1)
+        // (which runs the plastic arrivals' STDP, Fig. 2c, before delivering)
+        compact3(cs, st.ctr->lst[t & 7], st.ctr->lst[(t + 1) & 7] + 1, st.ctr->lst[t & 7] + 2, false, arr1, flush,
+                 sp, sa, sf, np, na, nf);
+        if (flush) st.vdesc[t & 3][(size_t)st.nblk * kFrontThreads - 1 - sf] = d;
+        if (arr1) {
+            a.start = st.row_ptr[i];
+            a.row = i;
+            a.meta |= kMetaArr | ((uint32_t)(p.rcpt_uniform & 3) << 8);
+            if (p.rcpt_uniform < 0) a.meta |= (uint32_t)pi << 16;
+            if (!plastic_row) {
+                a.xp = 0.0f;
+                a.s0 = a.s1 = 0;
+            }
+            a.pad = 0;
+            st.adesc[(t + 1) & 1][sa] = a;
+        }
+        np = __syncthreads_count(visit && arr);      // (metrics: plastic arrivals visited at t)
+        na = 0;                                      // (arrivals are counted by k_deliver)
+    } else {
+        // plastic visits -> k_stdp: the arrivals from the front of the list, the
+        // forced flushes from its back (so k_stdp can share each kind evenly);
+        // every arrival -> k_deliver
+        const bool parr = visit && arr;
+        compact3(cs, st.ctr->lst[t & 7], st.ctr->lst[t & 7] + 1, st.ctr->lst[t & 7] + 2, parr, arr, flush, sp, sa, sf,
+                 np, na, nf);
+        if (parr) st.vdesc[t & 3][sp] = d;
+        if (flush) st.vdesc[t & 3][(size_t)st.nblk * kFrontThreads - 1 - sf] = d;
+        if (arr) {                                       // every arriving row is delivered
+            a.start = st.row_ptr[i];
+            a.row = i;
+            a.meta = kMetaArr | ((uint32_t)(p.rcpt_uniform & 3) << 8);
+            if (p.rcpt_uniform < 0) a.meta |= (uint32_t)pi << 16;
+            a.xp = 0.0f;
+            a.s0 = a.s1 = 0;
+            a.pad = 0;
+            st.adesc[par][sa] = a;
+        }
     }
     if (threadIdx.x == 0) {
-        // the lists of step t-1 are consumed (k_deliver(t-1) completed): reset for t+1
-        if (blockIdx.x == 0) *reinterpret_cast<uint4 *>(st.ctr->lst[par ^ 1u]) = make_uint4(0u, 0u, 0u, 0u);
+        // slot (t + 2) & 7 was last used by step t - 6 (long consumed): reset it
+        // for the lists of t + 2 (kAhead: its arrivals are appended by k_front(t+1))
+        if (blockIdx.x == 0) *reinterpret_cast<uint4 *>(st.ctr->lst[(t + 2) & 7]) = make_uint4(0u, 0u, 0u, 0u);
         // metrics (fire-and-forget reductions): spikes arriving, plastic rows
         // visited (arrivals + forced flushes), forced flushes
         if (na) atomicAdd(&st.ctr->metric[1], (unsigned long long)na);
@@ -398,6 +453,10 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
+}
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
 }
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -554,15 +613,15 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     if (!readout) trace_mark(st.trace, 1, 0);
     if (!readout && st.kspan) kspan_begin(st.kspan, t, 1, t_entry, gtimer());
     const uint32_t par = (uint32_t)(t & 1);
-    const RowDesc *Vl = readout ? st.rdesc : st.vdesc[par];
-    const uint32_t *lens = readout ? st.ctr->rlst : st.ctr->lst[par];
+    const RowDesc *Vl = readout ? st.rdesc : st.vdesc[t & 3];
+    const uint32_t *lens = readout ? st.ctr->rlst : st.ctr->lst[t & 7];
     // (k_front(t) complete).  The event schedule's forced flushes are k_flush's
     const uint32_t nA = lens[0], nF = (readout || !kGeneric) ? 0u : lens[2];
     const size_t cap_back = (size_t)st.nblk * kFrontThreads - 1;   // forced flushes: from the back
     const uint32_t bm_bytes = 16u * ((w_hi - w_lo + 3) >> 2);
     if (threadIdx.x == 0) {   // bitmap of recently fired post neurons (one bulk copy; the barrier's initialiser)
         mbar_expect_tx(bmap_a, bm_bytes);
-        bulk_g2s(smem_u32(recent_s), st.recent + w_lo, bm_bytes, bmap_a);
+        bulk_g2s(smem_u32(recent_s), st.recent + (size_t)(t & 3) * st.rstride + w_lo, bm_bytes, bmap_a);
     }
     __syncthreads();       // barrier init visible
     // even shares of each kind: plastic arrivals (front of the list; read-out
@@ -587,7 +646,6 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
     constexpr uint32_t hi_on = kH128 ? 1u : 0u;
     constexpr bool lazy = kLazy;
     const float *__restrict__ gxpost = st.xpost;
-    const float *__restrict__ gfpot = st.fpot;
     float *__restrict__ gw = st.w;
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kStdpRows) {
         // ---- tabulate up to kStdpRows rows (one per thread), chunk prefix
@@ -859,36 +917,37 @@ k_stdp(NetDev net, StateDev st, int64_t t_fixed, uint32_t pp_lo, uint32_t pp_hi)
 
 // --------------------------------------------------------------- k_stdp_ev
 // Lazy + event-driven STDP of the event schedule (Fig. 2c) over the
-// step's visited plastic rows: plastic arrivals A(t), then forced flushes F(t)
-// (R3).  The kernel is the step's largest stream (4 B target id
-// per visited synapse, 8 B weight where it can change), so it is built as a
-// plain stream with many bytes in flight: each CTA flattens its share of the
-// rows into 16-byte chunks (4 synapses); thread x takes chunks x + kEvT u
-// (consecutive threads: consecutive chunks, coalesced 16-byte loads of ids
-// and weights), kEvU chunks per iteration, the next iteration's loads issued
-// before the current one's gathers (double-buffered registers).
-// The CTA keeps the post population's one-byte spike positions (k_front:
-// 0xfe no spike in the last H steps, 0xff several, else the bit of the only
-// one -- the paper's regime has 0-1 spikes per window) in shared
-// memory, so a target is filtered by one shared byte and most updates need no
-// history gather:
+// step's visited plastic rows: the plastic arrivals A(t) and the forced flushes
+// F(t) (R3).
+//  * kMode 2 (k_flush, the ahead step, engine.cu): the forced flushes of t,
+//    after k_deliver(t) -- which ran the plastic arrivals' STDP itself
+//    (deliver_stdp) -- so that k_deliver(t) follows k_front(t) directly.  It
+//    reads step t's tables (fpos / fpot / recent: four buffers by t & 3; lists
+//    by t & 7) and no delivery of t reads a flushed row (a forced flush is a
+//    row that does not arrive at t).
+//  * kMode 0: both kinds between k_front(t) and k_deliver(t) (the step without
+//    the ahead list: D < 2).
+// Both stream their share of the rows' plastic spans as 16-byte chunks (4
+// synapses): thread x takes chunks x + kT u, coalesced 16-byte loads of ids and
+// weights, the next iteration's loads issued before the current one's gathers.
+// A synapse i -> j is filtered by the bit of j in the shared-memory copy of the
+// `recent` bitmap (j fired in the last H steps); only then is the one-byte
+// spike position fpos[j] gathered (0xff: several spikes) -- the paper's regime
+// has 0-1 post spikes per window:
 //  * forced flush (age H): every flush of the step shares the window
-//    (t - H, t], so synapse i -> j changes only if j fired in it, by
-//    w = min(w + A+ (x_pre_i D+[H - p]), w_max) for its one spike at bit p (the
-//    closed-form skip-ahead of P:284); several spikes: by the gathered
-//    fpot[j] = sum of D+[H - s] (potentiations only, so the sequential clamps
-//    are one clamp of the sum);
+//    (t - H, t], so w = min(w + A+ (x_pre_i D+[H - p]), w_max) for j's one
+//    spike at bit p (the closed-form skip-ahead of P:284); several spikes: by
+//    the gathered fpot[j] = sum of D+[H - s] (potentiations only, so the
+//    sequential clamps are one clamp of the sum);
 //  * arrival: potentiation by the spikes in the window (tlu, t] (one: p < age;
 //    several: the gathered history, oldest first with __clz), then the
 //    pre spike's depression by x_post[j] (gathered).
 // Only weights that change are stored.
-#ifndef SNN_EV_THREADS
-#define SNN_EV_THREADS 1024
+#ifndef SNN_FL_GRID
+#define SNN_FL_GRID 1        // k_flush CTAs per SM
 #endif
-constexpr int kEvT = SNN_EV_THREADS;
-constexpr int kEvWarps = kEvT / 32;
-constexpr int kEvRows = 256;                 // row table per round
-constexpr int kEvU = 2;                      // chunks per thread and iteration (flushes; arrivals: 1)
+constexpr int kEvRowsMax = 256;              // row table per round
+constexpr int kEvU = 2;                      // chunks per thread and iteration
 
 struct __align__(16) EvRow {
     int64_t cb;      // 16-byte aligned CSR offset of the plastic span
@@ -899,15 +958,21 @@ struct __align__(16) EvRow {
     uint32_t pad;
 };
 struct EvSmem {
-    EvRow rows[kEvRows];
-    uint32_t incl[kEvRows + 1];      // inclusive prefix of the rows' chunk counts
-    uint32_t wsum[kEvWarps];
+    uint64_t bmap;                   // mbarrier of the bitmap's bulk copy
+    EvRow rows[kEvRowsMax];
+    uint32_t incl[kEvRowsMax + 1];   // inclusive prefix of the rows' chunk counts
+    uint32_t wsum[32];
     float4 par[4];                   // per projection: a_plus, a_minus, w_max
     float dplus[4 * (kMaxHist + 1)];
 };
 
-size_t ev_smem_bytes(uint32_t pp_lo, uint32_t pp_hi) {     // + the post population's spike-position bytes
-    return ((sizeof(EvSmem) + 15) & ~(size_t)15) + (((size_t)pp_hi - (pp_lo & ~15u) + 15) & ~(size_t)15);
+// bitmap words [pp_lo / 128 * 4, ceil(pp_hi / 32)): 16-byte aligned, whole 16-byte units
+__host__ __device__ inline uint32_t ev_bm_lo(uint32_t pp_lo) { return (pp_lo >> 7) << 2; }
+__host__ __device__ inline uint32_t ev_bm_bytes(uint32_t pp_lo, uint32_t pp_hi) {
+    return 16u * ((((pp_hi + 31) >> 5) - ev_bm_lo(pp_lo) + 3) >> 2);
+}
+size_t ev_smem_bytes(uint32_t pp_lo, uint32_t pp_hi) {
+    return ((sizeof(EvSmem) + 15) & ~(size_t)15) + ev_bm_bytes(pp_lo, pp_hi);
 }
 
 // One iteration's loads: chunk c (c < T) of the CTA's flattened rows; r walks
@@ -917,9 +982,9 @@ struct EvLoad {
     uint32_t r, x0;   // row slot, element offset of the chunk in the row (rel. cb)
 };
 
-template <bool kH128, bool kArr>
-__device__ __forceinline__ void ev_load(const EvSmem &sm, const uint32_t *__restrict__ idx, const float *__restrict__ w,
-                                        uint32_t c, uint32_t T, uint32_t &cur, EvLoad &L) {
+__device__ __forceinline__ void ev_load(const EvSmem &sm, const uint32_t *__restrict__ idx,
+                                        const float *__restrict__ w, uint32_t c, uint32_t T, uint32_t &cur,
+                                        EvLoad &L) {
     if (c < T) {
         while (c >= sm.incl[cur]) cur++;
         const EvRow &er = sm.rows[cur];
@@ -936,94 +1001,145 @@ __device__ __forceinline__ void ev_load(const EvSmem &sm, const uint32_t *__rest
     }
 }
 
-template <bool kH128, int U>
+// A flush of age < H whose target fired several times in the H window: the
+// window's spikes from the history word (potentiation only, no pre spike).
+template <bool kH128>
+__device__ __noinline__ float flush_hist(const uint64_t *hist, const uint64_t *hist_hi, uint32_t j, float w, float xp,
+                                         uint32_t age, uint32_t dp, float4 pr) {
+    return stdp_synapse(w, window_lo(__ldg(hist + j), (int)age), false, 0.0f, xp, (int)age, dp, pr.x, pr.y, pr.z,
+                        kH128 ? window_hi(__ldg(hist_hi + j), (int)age) : 0ull);
+}
+
+// Per-iteration counters (metrics, 8(d) bytes).
+struct EvCount {
+    uint32_t syn = 0, fsyn = 0, w = 0, rw = 0, frw = 0;
+};
+
+// The U chunks of one iteration, in phases so that each phase's gathers of all
+// U x 4 synapses are in flight together: (1) span mask and bitmap filter, (2)
+// fpos (+ x_post for arrivals), (3) fpot / history where several spikes, (4)
+// the updates and the stores of changed weights.
+template <bool kH128, int U, bool kArr, bool kFl>
 __device__ __forceinline__ void ev_process(const EvSmem &sm, const StateDev &st, const EvLoad (&L)[U],
-                                           uint32_t fs_addr, uint32_t dp_addr, uint32_t pp_lo, uint32_t H,
-                                           uint32_t &n_w, uint32_t &n_rw, uint32_t &n_frw, uint32_t net_debug) {
+                                           uint32_t bm_addr, const uint8_t *__restrict__ fpos,
+                                           const float *__restrict__ fpot, uint32_t dp_addr, uint32_t H,
+                                           EvCount &n) {
+    uint32_t inm[U], hm[U];
+    bool arr[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
+        inm[u] = 0;
+        hm[u] = 0;
+        arr[u] = false;
         if (L[u].r == 0xffffffffu) continue;
         const EvRow &er = sm.rows[L[u].r];
-        uint32_t inm = 0xfu;
+        arr[u] = kArr && (!kFl || (er.meta & kMetaArr) != 0);
+        uint32_t m = 0xfu;
         if (L[u].x0 < er.lo || L[u].x0 + 4 > er.hi) {                // a row's first / last chunk
-            inm = 0;
+            m = 0;
 #pragma unroll
-            for (int e = 0; e < 4; e++) inm |= (uint32_t)(L[u].x0 + e >= er.lo && L[u].x0 + e < er.hi) << e;
+            for (int e = 0; e < 4; e++) m |= (uint32_t)(L[u].x0 + e >= er.lo && L[u].x0 + e < er.hi) << e;
         }
+        inm[u] = m;
         const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
-        uint32_t pos[4];
-        uint32_t hm = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) {       // (outside the span: a neighbour's target, maybe no post neuron)
-            pos[e] = lds_u8(fs_addr + (((inm >> e) & 1u) ? jj[e] : pp_lo));
-            hm |= (uint32_t)(((inm >> e) & 1u) && pos[e] != 0xfeu) << e;
+            const uint32_t j = ((m >> e) & 1u) ? jj[e] : (bm_addr & 0u);
+            const uint32_t bit = ((m >> e) & 1u) ? (lds_u32(bm_addr + ((j >> 5) << 2)) >> (j & 31)) & 1u : 0u;
+            hm[u] |= bit << e;
         }
-        if (net_debug & 1u) continue;            // (experiments: filter only)
+        n.rw += __popc(arr[u] ? m : hm[u]);
+        if (!arr[u]) n.frw += __popc(hm[u]);
+    }
+    uint32_t pos[U][4];
+    float xq[U][4];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            pos[u][e] = ldg_u8_if(fpos + jj[e], (hm[u] >> e) & 1u);          // 0xff where not gathered
+            xq[u][e] = kArr ? ldg_f32_if(st.xpost + jj[e], arr[u] ? (inm[u] >> e) & 1u : 0u) : 0.0f;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        if (!inm[u]) continue;
+        const EvRow &er = sm.rows[L[u].r];
         const uint32_t si = (er.meta >> 12) & 0x3u;
         const float4 pr = sm.par[si];
         const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+        const uint32_t jj[4] = {L[u].j.x, L[u].j.y, L[u].j.z, L[u].j.w};
         const float wv[4] = {__uint_as_float(L[u].w.x), __uint_as_float(L[u].w.y), __uint_as_float(L[u].w.z),
                              __uint_as_float(L[u].w.w)};
         float *wp = st.w + er.cb + L[u].x0;
-        if (!(er.meta & kMetaArr)) {
-            // ---- forced flush (age H): the window's spike at bit p adds
-            //      A+ (x_pre D+[H - p]); several spikes: the fpot factor (gathered)
-            n_rw += __popc(hm);
-            n_frw += __popc(hm);
+        if (kFl && !arr[u]) {
+            // ---- forced flush (age H, or H - 1 when flushed a step early,
+            //      k_front): the window's spike at bit p < age adds
+            //      A+ (x_pre D+[age - p]); several spikes at age H: the fpot
+            //      factor (gathered); several at age H - 1: the history word
+            if (!hm[u]) continue;
+            const uint32_t age = er.meta & kMetaAge;
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                const bool hit = (hm >> e) & 1u;
-                float f = lds_f32(dp + 4u * (pos[e] < H ? H - pos[e] : 0u));
-                if (hit && pos[e] == 0xffu) f = __ldg(st.fpot + jj[e]);
-                const float nw = __fadd_rn(wv[e], __fmul_rn(pr.x, __fmul_rn(er.xp, f)));
-                const float w = nw < pr.z ? nw : pr.z;
+                const bool hit = (hm[u] >> e) & 1u;
+                const uint32_t p = pos[u][e];
+                float w = wv[e];
+                if (hit && (p < age || (p == 0xffu && age == H))) {
+                    const float f = p < age ? lds_f32(dp + 4u * (age - p)) : __ldg(fpot + jj[e]);
+                    const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(er.xp, f)));
+                    w = nw < pr.z ? nw : pr.z;
+                } else if (hit && p == 0xffu) {
+                    w = flush_hist<kH128>(st.hist, st.hist_hi, jj[e], w, er.xp, age, dp, pr);
+                }
                 const uint32_t chg = (hit && __float_as_uint(w) != __float_as_uint(wv[e])) ? 1u : 0u;
                 stg_f32_if(wp + e, w, chg);
-                n_w += chg;
+                n.w += chg;
             }
-        } else {
+        } else if (kArr) {
             // ---- arrival (Fig. 2c): every synapse.  Potentiation by the spikes
             //      in the window (tlu, t] (one: bit p < age, closed form; several:
             //      the history word, oldest first with __clz), then the pre spike's
-            //      depression by x_post[j] (gathered)
-            n_rw += __popc(inm);
+            //      depression by x_post[j]
             const uint32_t age = er.meta & kMetaAge;
-            float xq[4];
-#pragma unroll
-            for (int e = 0; e < 4; e++) xq[e] = ldg_f32_if(st.xpost + jj[e], (inm >> e) & 1u);
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                if (!((inm >> e) & 1u)) continue;
+                if (!((inm[u] >> e) & 1u)) continue;
                 float w = wv[e];
-                if (pos[e] == 0xffu) {
-                    w = stdp_synapse(w, window_lo(__ldg(st.hist + jj[e]), (int)age), true, xq[e], er.xp, (int)age, dp,
-                                     pr.x, pr.y, pr.z, kH128 ? window_hi(__ldg(st.hist_hi + jj[e]), (int)age) : 0ull);
+                const uint32_t p = ((hm[u] >> e) & 1u) ? pos[u][e] : 0xfeu;
+                if (p == 0xffu) {
+                    w = stdp_synapse(w, window_lo(__ldg(st.hist + jj[e]), (int)age), true, xq[u][e], er.xp, (int)age,
+                                     dp, pr.x, pr.y, pr.z,
+                                     kH128 ? window_hi(__ldg(st.hist_hi + jj[e]), (int)age) : 0ull);
                 } else {
-                    if (pos[e] < age) {                // the window's only post spike
-                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(er.xp, lds_f32(dp + 4u * (age - pos[e])))));
+                    if (p < age) {                     // the window's only post spike
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(er.xp, lds_f32(dp + 4u * (age - p)))));
                         w = nw < pr.z ? nw : pr.z;
                     }
-                    const float dw = __fsub_rn(w, __fmul_rn(pr.y, xq[e]));
+                    const float dw = __fsub_rn(w, __fmul_rn(pr.y, xq[u][e]));
                     w = dw > 0.0f ? dw : 0.0f;
                 }
                 const uint32_t chg = __float_as_uint(w) != __float_as_uint(wv[e]) ? 1u : 0u;
                 stg_f32_if(wp + e, w, chg);
-                n_w += chg;
+                n.w += chg;
             }
         }
     }
 }
 
-// The CTA's rows -- its arrivals, then its forced flushes -- flattened into one
-// chunk stream, in rounds of kEvRows rows.
-template <bool kH128>
+// The CTA's rows -- [0, nAb) from the front of the visit list at a_begin, then
+// nFb from its back at f_back downwards -- flattened into one chunk stream, in
+// rounds of kRows rows.  The bitmap copy (mbarrier bmap_a) is awaited once,
+// after the first round's table.
+template <bool kH128, int kT, int kMode>
 __device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const RowDesc *Vl, uint32_t a_begin,
-                                        uint32_t nAb, size_t f_back, uint32_t r_end, uint32_t fs_addr,
-                                        uint32_t dp_addr, uint32_t pp_lo, uint32_t H, uint32_t &n_syn,
-                                        uint32_t &n_fsyn, uint32_t &n_w, uint32_t &n_rw, uint32_t &n_frw,
-                                        uint32_t net_debug) {
-    for (uint32_t r0 = 0; r0 < r_end; r0 += kEvRows) {
-        const uint32_t nrows = min(r_end - r0, (uint32_t)kEvRows);
+                                        uint32_t nAb, size_t f_back, uint32_t r_end, uint32_t bm_addr,
+                                        uint32_t bmap_a, const uint8_t *fpos, const float *fpot, uint32_t dp_addr,
+                                        uint32_t H, EvCount &n) {
+    constexpr int kRows = kT < kEvRowsMax ? kT : kEvRowsMax;
+    bool bm_ready = false;
+    for (uint32_t r0 = 0; r0 < r_end; r0 += kRows) {
+        const uint32_t nrows = min(r_end - r0, (uint32_t)kRows);
         uint32_t nch = 0;
         EvRow er;
         if (threadIdx.x < nrows) {
@@ -1040,12 +1156,12 @@ __device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const Ro
             // a flush with x_pre == 0 changes no weight (potentiation adds A+ 0, R31)
             if (cs < ce && (arr || d.xp != 0.0f)) {
                 nch = (er.hi + 3) >> 2;
-                n_syn += (uint32_t)(ce - cs);
-                if (!arr) n_fsyn += (uint32_t)(ce - cs);
+                n.syn += (uint32_t)(ce - cs);
+                if (!arr) n.fsyn += (uint32_t)(ce - cs);
             }
         }
         uint32_t T = 0;
-        const uint32_t inc = block_incl_scan<kEvT>(nch, sm.wsum, T);
+        const uint32_t inc = block_incl_scan<kT>(nch, sm.wsum, T);
         if (threadIdx.x < nrows) {
             er.first = inc - nch;
             sm.rows[threadIdx.x] = er;
@@ -1053,73 +1169,369 @@ __device__ __forceinline__ void ev_rows(EvSmem &sm, const StateDev &st, const Ro
         }
         if (threadIdx.x == 0) sm.incl[nrows] = 0xffffffffu;      // (the walk never passes the last row)
         __syncthreads();
+        if (!bm_ready) {
+            mbar_wait(bmap_a, 0);
+            bm_ready = true;
+        }
         uint32_t cur = 0;
-        for (uint32_t c0 = 0; c0 < T; c0 += kEvT * kEvU) {
-            EvLoad L[kEvU];
+        constexpr bool kArr = kMode != 2, kFl = kMode != 1;
+        if constexpr (kMode == 2) {
+            // forced flushes (the long stream): the next iteration's loads are
+            // issued before the current one's gathers
+            EvLoad L[kEvU], Ln[kEvU];
 #pragma unroll
-            for (int u = 0; u < kEvU; u++) ev_load<kH128, false>(sm, st.idx, st.w, c0 + kEvT * u + threadIdx.x, T, cur, L[u]);
-            ev_process<kH128, kEvU>(sm, st, L, fs_addr, dp_addr, pp_lo, H, n_w, n_rw, n_frw, net_debug);
+            for (int u = 0; u < kEvU; u++) ev_load(sm, st.idx, st.w, kT * u + threadIdx.x, T, cur, L[u]);
+            for (uint32_t c0 = 0; c0 < T; c0 += kT * kEvU) {
+#pragma unroll
+                for (int u = 0; u < kEvU; u++)
+                    ev_load(sm, st.idx, st.w, c0 + kT * (kEvU + u) + threadIdx.x, T, cur, Ln[u]);
+                ev_process<kH128, kEvU, kArr, kFl>(sm, st, L, bm_addr, fpos, fpot, dp_addr, H, n);
+#pragma unroll
+                for (int u = 0; u < kEvU; u++) L[u] = Ln[u];
+            }
+        } else {
+            for (uint32_t c0 = 0; c0 < T; c0 += kT * kEvU) {
+                EvLoad L[kEvU];
+#pragma unroll
+                for (int u = 0; u < kEvU; u++) ev_load(sm, st.idx, st.w, c0 + kT * u + threadIdx.x, T, cur, L[u]);
+                ev_process<kH128, kEvU, kArr, kFl>(sm, st, L, bm_addr, fpos, fpot, dp_addr, H, n);
+            }
         }
         __syncthreads();                           // row table reused next round
     }
+    if (!bm_ready && threadIdx.x == 0) mbar_wait(bmap_a, 0);   // (no rows) the copy has landed
 }
 
-template <bool kH128>
-__global__ void __launch_bounds__(kEvT, 1)
+// kMode: 0 arrivals + forced flushes, 1 arrivals (k_stdp_arr), 2 forced flushes (k_flush)
+template <bool kH128, int kMode, int kT>
+__global__ void __launch_bounds__(kT, 65536 / (kT * 64))
 k_stdp_ev(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
     extern __shared__ __align__(16) unsigned char smem[];
     const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
     EvSmem &sm = *reinterpret_cast<EvSmem *>(smem);
-    uint8_t *fpos_s = smem + ((sizeof(EvSmem) + 15) & ~(size_t)15);
+    uint32_t *bm_s = reinterpret_cast<uint32_t *>(smem + ((sizeof(EvSmem) + 15) & ~(size_t)15));
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t f_lo = pp_lo & ~15u;                                     // 16-byte aligned start
-    for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kEvT)
+    const uint32_t bmap_a = smem_u32(&sm.bmap);
+    // ---- prologue independent of k_front(t): barrier, STDP constants
+    if (threadIdx.x == 0) {
+        mbar_init(bmap_a, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kT)
         sm.dplus[x] = st.stdp[x / (kMaxHist + 1)].dplus[x % (kMaxHist + 1)];
     if (threadIdx.x < net.nstdp)
         sm.par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
                                           st.stdp[threadIdx.x].w_max, 0.0f);
-    // the step counter was advanced by k_deliver(t-1), complete before
-    // k_front(t) triggered this launch
-    const int64_t t = *(volatile const int64_t *)&st.ctr->t;
-    pdl_wait();            // k_front(t): lists, histories, bitmap, fpot
-    pdl_launch();          // k_deliver may start its tabulation (k_front is complete)
-    trace_mark(st.trace, 1, 0);
-    if (st.kspan) kspan_begin(st.kspan, t, 1, t_entry, gtimer());
+    // kMode 0 / 1: after k_front(t); kMode 2 (flushes on a side branch): its
+    // step from the flush sequence counter (advanced by its last CTA)
+    pdl_wait();            // k_front(t): lists, bitmap, fpos / fpot
+    const int64_t t = kMode == 2 ? *(volatile const int64_t *)&st.ctr->tfl : *(volatile const int64_t *)&st.ctr->t;
+    pdl_launch();          // the next kernel may start its prologue
+    trace_mark(st.trace, kMode == 2 ? 3 : 1, 0);
+    if (st.kspan) kspan_begin(st.kspan, t, kMode == 2 ? 3 : 1, t_entry, gtimer());
     const uint32_t par = (uint32_t)(t & 1);
-    const RowDesc *Vl = st.vdesc[par];
-    const uint32_t nA = st.ctr->lst[par][0], nF = st.ctr->lst[par][2];
+    const uint32_t wlo = ev_bm_lo(pp_lo), bm_bytes = ev_bm_bytes(pp_lo, pp_hi);
+    __syncthreads();       // barrier init visible
+    if (threadIdx.x == 0) {    // bitmap of recently fired post neurons (one bulk copy)
+        mbar_expect_tx(bmap_a, bm_bytes);
+        bulk_g2s(smem_u32(bm_s), st.recent + (size_t)(t & 3) * st.rstride + wlo, bm_bytes, bmap_a);
+    }
+    const RowDesc *Vl = st.vdesc[t & 3];
+    const uint32_t *lens = st.ctr->lst[t & 7];
+    const uint32_t nA = kMode == 2 ? 0u : lens[0], nF = kMode == 1 ? 0u : lens[2];
     const size_t cap_back = (size_t)st.nblk * kFrontThreads - 1;      // forced flushes: from the back
     const uint32_t a_begin = (uint32_t)(((uint64_t)nA * blockIdx.x) / gridDim.x);
     const uint32_t a_end = (uint32_t)(((uint64_t)nA * (blockIdx.x + 1)) / gridDim.x);
     const uint32_t f_begin = (uint32_t)(((uint64_t)nF * blockIdx.x) / gridDim.x);
     const uint32_t f_end = (uint32_t)(((uint64_t)nF * (blockIdx.x + 1)) / gridDim.x);
-    for (uint32_t x = threadIdx.x; x < (pp_hi - f_lo + 15) >> 4; x += kEvT)     // spike positions -> shared
-        reinterpret_cast<uint4 *>(fpos_s)[x] = __ldg(reinterpret_cast<const uint4 *>(st.fpos + f_lo) + x);
-    __syncthreads();
-    const uint32_t fs_addr = smem_u32(fpos_s) - f_lo;             // position of post neuron j: + j
+    const uint32_t bm_addr = smem_u32(bm_s) - 4u * wlo;          // bitmap word of neuron j: + 4 (j >> 5)
     const uint32_t dp_addr = smem_u32(sm.dplus);
-    uint32_t n_syn = 0, n_w = 0, n_rw = 0, f_syn = 0, f_rw = 0;
+    const uint8_t *fpos = st.fpos + (size_t)(t & 3) * st.fstride;
+    const float *fpot = st.fpot + (size_t)(t & 3) * st.fstride;
+    EvCount n;
     // (experiments: net.debug 2 = no arrivals, 4 = no flushes)
     const uint32_t nAb = (net.debug & 2u) ? 0u : a_end - a_begin, nFb = (net.debug & 4u) ? 0u : f_end - f_begin;
-    ev_rows<kH128>(sm, st, Vl, a_begin, nAb, cap_back - f_begin, nAb + nFb, fs_addr, dp_addr, pp_lo, net.H, n_syn,
-                   f_syn, n_w, n_rw, f_rw, net.debug);
-    n_syn = __reduce_add_sync(0xffffffffu, n_syn);
-    n_w = __reduce_add_sync(0xffffffffu, n_w);
-    n_rw = __reduce_add_sync(0xffffffffu, n_rw);
-    f_syn = __reduce_add_sync(0xffffffffu, f_syn);
-    f_rw = __reduce_add_sync(0xffffffffu, f_rw);
+    ev_rows<kH128, kT, kMode>(sm, st, Vl, a_begin, nAb, cap_back - f_begin, nAb + nFb, bm_addr, bmap_a, fpos, fpot,
+                       dp_addr, net.H, n);
+    n.syn = __reduce_add_sync(0xffffffffu, n.syn);
+    n.w = __reduce_add_sync(0xffffffffu, n.w);
+    n.rw = __reduce_add_sync(0xffffffffu, n.rw);
+    n.fsyn = __reduce_add_sync(0xffffffffu, n.fsyn);
+    n.frw = __reduce_add_sync(0xffffffffu, n.frw);
     if (lane == 0) {
-        if (n_syn) atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
-        if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
-        if (n_rw) atomicAdd(&st.ctr->metric[8], (unsigned long long)n_rw);
-        if (f_syn) atomicAdd(&st.ctr->metric[9], (unsigned long long)f_syn);
-        if (f_rw) atomicAdd(&st.ctr->metric[10], (unsigned long long)f_rw);
+        if (n.syn) atomicAdd(&st.ctr->metric[3], (unsigned long long)n.syn);
+        if (n.w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n.w);
+        if (n.rw) atomicAdd(&st.ctr->metric[8], (unsigned long long)n.rw);
+        if (n.fsyn) atomicAdd(&st.ctr->metric[9], (unsigned long long)n.fsyn);
+        if (n.frw) atomicAdd(&st.ctr->metric[10], (unsigned long long)n.frw);
     }
     if (st.trace) {
         __syncthreads();
-        trace_mark(st.trace, 1, 3);
+        trace_mark(st.trace, kMode == 2 ? 3 : 1, 3);
     }
-    kspan_end(st.kspan, t, 1);
+    kspan_end(st.kspan, t, kMode == 2 ? 3 : 1);
+    if (kMode == 2) {
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(&st.ctr->fticket, 1u) == gridDim.x - 1) {   // the last CTA: next step
+            st.ctr->fticket = 0;
+            st.ctr->tfl = t + 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ k_flush
+// The forced flushes F(t) of the ahead step (R3).  A forced flush changes w_ij
+// only where the target j fired in the row's window (0-1 spikes per
+// window, most targets none), so the kernel is a stream whose only memory
+// round trip is the stream itself: everything a synapse needs besides its id
+// and weight is in shared memory --
+//  * kStaged: the post population's one-byte spike positions fpos (k_front:
+//    0xfe none in the H window, 0xff several, else the bit of the only one),
+//    TMA bulk copies (cfg3: 126 KB);
+//  * else (a post population too large for shared memory): the `recent`
+//    bitmap (1 bit per neuron) and fpos gathered (L2) for the set bits.
+// Work unit: a piece = 32 kFlQ 16-byte chunks (128 kFlQ synapses) of one row's
+// plastic span; warp w takes the CTA's pieces w, w + 32, ... with the row's
+// state in registers; lane l loads chunks l + 32 q (q < kFlQ) -- ids and
+// weights, all 2 kFlQ 16-byte loads in flight together (the other warps'
+// pieces cover the latency).  A synapse i -> j whose target's only spike is at
+// bit p < age (age H, or H - 1 when flushed a step early, k_front's rule)
+// becomes w = min(w + A+ (x_pre D+[age - p]), w_max) -- the closed-form
+// skip-ahead of P:284 -- stored in place; several spikes: the fpot[j] factor
+// (age H: sum of D+[H - s] over them, potentiations only, so the sequential
+// clamps are one clamp of the sum) or the history word (age H - 1).
+// Its inputs are k_front(t)'s (lists, fpos / fpot / bitmap, the rows' x_pre)
+// and no k_deliver(t) access touches a flushed row (a forced flush is a row
+// that does not arrive at t, and k_deliver(t) updates only arriving rows), so
+// the whole kernel runs before its dependency wait: its CTAs start as
+// k_deliver(t)'s retire; the wait at the end only orders k_front(t+1) after
+// k_deliver(t) (PDL chain).
+// 8(d) bytes: 4 B per visited synapse (its id) + 8 B per hit (weight read and
+// written) + 16 B per row.
+#ifndef SNN_FL_Q
+#define SNN_FL_Q 4
+#endif
+#ifndef SNN_FL_T
+#define SNN_FL_T 1024
+#endif
+#ifndef SNN_FL_STAGED
+#define SNN_FL_STAGED 1          // 0: always the bitmap filter (smaller shared memory)
+#endif
+constexpr int kFlT = SNN_FL_T;
+constexpr int kFlWarps = kFlT / 32;
+constexpr int kFlRows = 256;
+constexpr int kFlQ = SNN_FL_Q;          // chunks per lane and piece
+constexpr int kFlPieceCh = 32 * kFlQ;   // chunks per piece
+
+struct FlSmem {
+    uint64_t bmap;                      // mbarrier of the table's bulk copies
+    EvRow rows[kFlRows];                // EvRow::first = the row's first piece
+    uint32_t incl[kFlRows + 1];         // inclusive prefix of the rows' piece counts
+    uint32_t wsum[kFlWarps];
+    float4 par[4];
+    float dplus[4 * (kMaxHist + 1)];
+};
+
+// table: fpos bytes [pp_lo & ~15, pp_hi) (16-byte units), else the bitmap
+__host__ __device__ inline uint32_t fl_tab_bytes(uint32_t pp_lo, uint32_t pp_hi, bool staged) {
+    return staged ? ((pp_hi - (pp_lo & ~15u) + 15u) & ~15u) : ev_bm_bytes(pp_lo, pp_hi);
+}
+bool flush_staged(uint32_t pp_lo, uint32_t pp_hi) {
+    return SNN_FL_STAGED && ((sizeof(FlSmem) + 15) & ~(size_t)15) + fl_tab_bytes(pp_lo, pp_hi, true) <= 227u * 1024u;
+}
+size_t flush_smem_bytes(uint32_t pp_lo, uint32_t pp_hi) {
+    return ((sizeof(FlSmem) + 15) & ~(size_t)15) + fl_tab_bytes(pp_lo, pp_hi, flush_staged(pp_lo, pp_hi));
+}
+
+template <bool kH128, bool kStaged>
+__global__ void __launch_bounds__(kFlT, kFlT >= 1024 ? 1 : 1024 / kFlT)
+k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
+    FlSmem &sm = *reinterpret_cast<FlSmem *>(smem);
+    unsigned char *tab = smem + ((sizeof(FlSmem) + 15) & ~(size_t)15);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t bmap_a = smem_u32(&sm.bmap);
+    pdl_launch();          // k_front(t+1) may be scheduled (it waits for this grid)
+    // the step of the flushes: k_flush runs once per step, in order (one
+    // stream); the previous launch's last CTA advanced the counter
+    const int64_t t = *(volatile const int64_t *)&st.ctr->tfl;
+    trace_mark(st.trace, 3, 0);
+    if (st.kspan) kspan_begin(st.kspan, t, 3, t_entry, t_entry);
+    const uint8_t *__restrict__ fpos = st.fpos + (size_t)(t & 3) * st.fstride;
+    const float *__restrict__ fpot = st.fpot + (size_t)(t & 3) * st.fstride;
+    const uint32_t f_lo = pp_lo & ~15u, wlo = ev_bm_lo(pp_lo);
+    const uint32_t tab_bytes = fl_tab_bytes(pp_lo, pp_hi, kStaged);
+    if (threadIdx.x == 0) {
+        mbar_init(bmap_a, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bmap_a, tab_bytes);
+        const unsigned char *src = kStaged ? (const unsigned char *)(fpos + f_lo)
+                                           : (const unsigned char *)(st.recent + (size_t)(t & 3) * st.rstride + wlo);
+        for (uint32_t off = 0; off < tab_bytes; off += 32768u)      // (bulk copies of at most 32 KB)
+            bulk_g2s(smem_u32(tab) + off, src + off, min(32768u, tab_bytes - off), bmap_a);
+    }
+    for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kFlT)
+        sm.dplus[x] = st.stdp[x / (kMaxHist + 1)].dplus[x % (kMaxHist + 1)];
+    if (threadIdx.x < net.nstdp)
+        sm.par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
+                                          st.stdp[threadIdx.x].w_max, 0.0f);
+    const RowDesc *Vl = st.vdesc[t & 3];
+    const uint32_t nF = st.ctr->lst[t & 7][2];
+    const size_t cap_back = (size_t)st.nblk * kFrontThreads - 1;      // forced flushes: from the back
+    const uint32_t f_begin = (uint32_t)(((uint64_t)nF * blockIdx.x) / gridDim.x);
+    const uint32_t f_end = (uint32_t)(((uint64_t)nF * (blockIdx.x + 1)) / gridDim.x);
+    // kStaged: fpos of neuron j at + j; else the bitmap word of j at + 4 (j >> 5)
+    const uint32_t tab_a = kStaged ? smem_u32(tab) - f_lo : smem_u32(tab) - 4u * wlo;
+    const uint32_t dp_addr = smem_u32(sm.dplus);
+    const uint32_t *__restrict__ gidx = st.idx;
+    float *__restrict__ gw = st.w;
+    const uint32_t H = net.H;
+    uint32_t n_syn = 0, n_w = 0, n_hit = 0;
+    bool tab_ready = false;
+    const uint32_t nrows_all = f_end - f_begin;
+    for (uint32_t r0 = 0; r0 < nrows_all; r0 += (kFlRows < kFlT ? kFlRows : kFlT)) {
+        // ---- row table: plastic spans as pieces (x_pre = 0: no change, R31)
+        const uint32_t nrows = min(nrows_all - r0, (uint32_t)(kFlRows < kFlT ? kFlRows : kFlT));
+        uint32_t npc = 0;
+        EvRow er;
+        if (threadIdx.x < nrows) {
+            const RowDesc d = Vl[cap_back - (f_begin + r0 + threadIdx.x)];
+            const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
+            er.cb = cs & ~3ll;
+            er.lo = (uint32_t)(cs - er.cb);
+            er.hi = (uint32_t)(ce - er.cb);
+            er.xp = d.xp;
+            er.meta = d.meta;
+            er.pad = 0;
+            if (cs < ce && d.xp != 0.0f) {
+                npc = (((er.hi + 3) >> 2) + kFlPieceCh - 1) / kFlPieceCh;
+                n_syn += (uint32_t)(ce - cs);
+            }
+        }
+        // (warp-level prefix + one pass over the warp totals)
+        uint32_t inc = npc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
+        }
+        if (lane == 31) sm.wsum[warp] = inc;
+        __syncthreads();                             // (also: the barrier's init, the constants)
+        uint32_t wpre = 0, P = 0;
+        {
+            const uint32_t v = lane < (uint32_t)kFlWarps ? sm.wsum[lane] : 0u;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            wpre = __shfl_sync(0xffffffffu, x - v, warp);
+            P = __shfl_sync(0xffffffffu, x, 31);
+        }
+        inc += wpre;
+        if (threadIdx.x < nrows) {
+            er.first = inc - npc;
+            sm.rows[threadIdx.x] = er;
+            sm.incl[threadIdx.x] = inc;
+        }
+        if (threadIdx.x == 0) sm.incl[nrows] = 0xffffffffu;
+        __syncthreads();
+        if (!tab_ready) {
+            trace_mark(st.trace, 3, 1);
+            mbar_wait(bmap_a, 0);
+            tab_ready = true;
+            trace_mark(st.trace, 3, 2);
+        }
+        // ---- the warp's pieces: p = warp + 32 i
+        uint32_t cur = 0;
+        for (uint32_t p = warp; p < P; p += kFlWarps) {
+            while (p >= sm.incl[cur]) cur++;
+            const EvRow &rr = sm.rows[cur];
+            const uint32_t c0 = (p - rr.first) * kFlPieceCh;
+            const uint32_t lo = rr.lo, hi = rr.hi, nch = (hi + 3) >> 2;
+            const int64_t cb = rr.cb;
+            uint4 J[kFlQ], Wt[kFlQ];
+#pragma unroll
+            for (int q = 0; q < kFlQ; q++) {
+                const uint32_t c = c0 + lane + 32u * q;
+                const bool ok = c < nch;
+                J[q] = ok ? __ldg(reinterpret_cast<const uint4 *>(gidx + cb + 4ll * c))
+                          : make_uint4(pp_lo, pp_lo, pp_lo, pp_lo);
+                Wt[q] = ok ? __ldg(reinterpret_cast<const uint4 *>(gw + cb + 4ll * c)) : make_uint4(0, 0, 0, 0);
+            }
+            const uint32_t age = rr.meta & kMetaAge, si = (rr.meta >> 12) & 0x3u;
+            const float4 pr = sm.par[si];
+            const float xp = rr.xp;
+            const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+#pragma unroll
+            for (int q = 0; q < kFlQ; q++) {
+                const uint32_t x0 = 4u * (c0 + lane + 32u * q);
+                const bool edge = x0 < lo || x0 + 4 > hi;       // a row's first / last chunk (or past it)
+                const uint32_t jj[4] = {J[q].x, J[q].y, J[q].z, J[q].w};
+                const uint32_t wb[4] = {Wt[q].x, Wt[q].y, Wt[q].z, Wt[q].w};
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    // (outside the span: a neighbour's target, maybe outside the table)
+                    const bool in = !edge || (x0 + e >= lo && x0 + e < hi);
+                    const uint32_t j = in ? jj[e] : pp_lo;
+                    uint32_t pos;
+                    if (kStaged) {
+                        pos = in ? lds_u8(tab_a + j) : 0xfeu;
+                    } else {
+                        const uint32_t b = (lds_u32(tab_a + ((j >> 5) << 2)) >> (j & 31)) & 1u;
+                        pos = (in && b) ? ldg_u8_if(fpos + j, 1u) : 0xfeu;
+                    }
+                    const float w0 = __uint_as_float(wb[e]);
+                    float w = w0;
+                    if (pos < age) {
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, lds_f32(dp + 4u * (age - pos)))));
+                        w = nw < pr.z ? nw : pr.z;
+                    } else if (pos == 0xffu) {
+                        if (age == H) {
+                            const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, __ldg(fpot + j))));
+                            w = nw < pr.z ? nw : pr.z;
+                        } else {
+                            w = flush_hist<kH128>(st.hist, st.hist_hi, j, w, xp, age, dp, pr);
+                        }
+                    }
+                    n_hit += pos != 0xfeu ? 1u : 0u;
+                    if (__float_as_uint(w) != __float_as_uint(w0)) {
+                        gw[cb + x0 + e] = w;
+                        n_w++;
+                    }
+                }
+            }
+        }
+        __syncthreads();                           // row table reused next round
+    }
+    if (!tab_ready && threadIdx.x == 0) mbar_wait(bmap_a, 0);   // (no rows) the copy has landed
+    n_syn = __reduce_add_sync(0xffffffffu, n_syn);
+    n_w = __reduce_add_sync(0xffffffffu, n_w);
+    n_hit = __reduce_add_sync(0xffffffffu, n_hit);
+    if (lane == 0) {
+        if (n_syn) {
+            atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
+            atomicAdd(&st.ctr->metric[9], (unsigned long long)n_syn);
+        }
+        if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
+        if (n_hit) {
+            atomicAdd(&st.ctr->metric[8], (unsigned long long)n_hit);
+            atomicAdd(&st.ctr->metric[10], (unsigned long long)n_hit);
+        }
+    }
+    pdl_wait();            // k_deliver(t) complete: k_front(t+1), which waits for this grid, reads its inputs
+    if (st.trace) {
+        __syncthreads();
+        trace_mark(st.trace, 3, 3);
+    }
+    kspan_end(st.kspan, t, 3);
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&st.ctr->fticket, 1u) == gridDim.x - 1) {   // the last CTA: next step
+        st.ctr->fticket = 0;
+        st.ctr->tfl = t + 1;
+    }
 }
 
 // --------------------------------------------------------------- k_deliver
@@ -1184,6 +1596,56 @@ __device__ __forceinline__ float ldg_nc_f32(uint64_t a) {
     return v;
 }
 
+// Plastic arrivals inside the delivery (kPl, the split step graph): the
+// (row, slice) segment's plastic part [pl.x, pl.y) (flattened) is updated by
+// Fig. 2c before it is delivered (plasticity before delivery) -- its
+// window (tlu, t] from the target's one-byte spike position (0xff: several
+// spikes -> the history word, oldest first with __clz), then the pre
+// spike's depression by x_post[j]; the slice's x_post / fpos are staged in
+// shared memory.  The changed weight is stored and the new one delivered.
+// Per-segment STDP tables of k_deliver (namespace-scope shared memory: fixed
+// addresses, no registers to hold them)
+__shared__ uint2 g_del_pl[kDelRows];            // segment g: plastic part, flattened [x, y)
+__shared__ uint2 g_del_row[kDelRows];           // segment g: (x_pre at tlu, meta: age, projection)
+__shared__ float g_del_dp[4 * (kMaxHist + 1)];  // D+ tables
+__shared__ float4 g_del_par[4];                 // per projection: a_plus, a_minus, w_max
+struct DelStdp {
+    uint32_t xq_a;             // shared: the slice's x_post (by offset j - slo), then its fpos bytes at + 4 C
+    uint32_t n_syn, n_w;       // metrics
+};
+
+// (several post spikes in the H window: rare in the paper's regime)
+template <bool kH128>
+__device__ __noinline__ float deliver_stdp_hist(const uint64_t *hist, const uint64_t *hist_hi, uint32_t j, float w,
+                                                float xq, float xp, uint32_t age, uint32_t dp, float4 pr) {
+    return stdp_synapse(w, window_lo(__ldg(hist + j), (int)age), true, xq, xp, (int)age, dp, pr.x, pr.y, pr.z,
+                        kH128 ? window_hi(__ldg(hist_hi + j), (int)age) : 0ull);
+}
+
+template <bool kH128>
+__device__ __forceinline__ float deliver_stdp(const StateDev &st, uint32_t xq_a, uint32_t C, uint32_t jl, uint32_t j,
+                                              float w0, uint32_t g) {
+    const uint2 rw = g_del_row[g];                         // (x_pre bits, meta)
+    const float xp = __uint_as_float(rw.x);
+    const uint32_t age = rw.y & kMetaAge, si = (rw.y >> 12) & 0x3u;
+    const uint32_t pos = lds_u8(xq_a + 4u * C + jl);
+    const float xq = lds_f32(xq_a + 4u * jl);
+    const uint32_t dp = smem_u32(g_del_dp) + si * 4u * (kMaxHist + 1);
+    const float4 pr = g_del_par[si];
+    float w = w0;
+    if (pos == 0xffu) {
+        w = deliver_stdp_hist<kH128>(st.hist, st.hist_hi, j, w, xq, xp, age, dp, pr);
+    } else {
+        if (pos < age) {                     // the window's only post spike (0xfe: none)
+            const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, lds_f32(dp + 4u * (age - pos)))));
+            w = nw < pr.z ? nw : pr.z;
+        }
+        const float dw = __fsub_rn(w, __fmul_rn(pr.y, xq));
+        w = dw > 0.0f ? dw : 0.0f;
+    }
+    return w;
+}
+
 // Owner-window pass (k_deliver): thread x takes elements w0 + x + 512 u of the
 // window.  Segment of element x: bw.y + popc(start bits <= x) (s_bw word).
 // s_ptr holds per segment the byte address of idx[c] for flattened element 0.
@@ -1196,11 +1658,11 @@ __device__ __forceinline__ uint32_t ldg_nc_u16(uint64_t a) {
 // kIdx16 (SNN_FLAG_IDX16): s_ptr addresses the 16-bit
 // slice-local offsets (2 B per element, the weight at 2 a + dw) and the target
 // is already local to the slice; else the 32-bit ids (4 B, weight at a + dw).
-template <bool kMulti, bool kCheck, bool kIdx16>
-__device__ __forceinline__ void deliver_pass(const NetDev &net, uint32_t x0, uint32_t wlen, uint32_t w0,
-                                             uint32_t bw_a, uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a,
-                                             uint64_t dw, float scale, uint32_t slo) {
-    uint32_t jj[kDelU], rr[kDelU];
+template <bool kMulti, bool kCheck, bool kIdx16, bool kPl, bool kH128>
+__device__ __forceinline__ void deliver_pass(const NetDev &net, const StateDev &st, uint32_t x0, uint32_t wlen,
+                                             uint32_t w0, uint32_t bw_a, uint32_t ptr_a, uint32_t rc_a,
+                                             uint32_t acc_a, uint64_t dw, float scale, uint32_t slo, DelStdp &ps) {
+    uint32_t jj[kDelU], rr[kDelU], gg[kDelU];
     float ww[kDelU];
 #pragma unroll
     for (int u = 0; u < kDelU; u++) {
@@ -1211,6 +1673,7 @@ __device__ __forceinline__ void deliver_pass(const NetDev &net, uint32_t x0, uin
                                   : x0 + u * kDelThreads + threadIdx.x;
         const uint2 bw = lds_u2(bw_a + ((x >> 5) << 3));
         const uint32_t gi = bw.y + __popc(bw.x & (0xffffffffu >> (31u - (x & 31u))));
+        gg[u] = gi;
         if (kIdx16) {
             const uint64_t a = lds_u64(ptr_a + (gi << 3)) + 2ull * (w0 + x);
             jj[u] = ldg_nc_u16(a);
@@ -1227,21 +1690,40 @@ __device__ __forceinline__ void deliver_pass(const NetDev &net, uint32_t x0, uin
         const uint32_t x = x0 + u * kDelThreads + threadIdx.x;
         if (!kCheck || x < wlen) {
             uint32_t r2 = rr[u];
+            float wv = ww[u];
+            if (kPl) {
+                const uint2 pl = g_del_pl[gg[u]];
+                if (w0 + x >= pl.x && w0 + x < pl.y) {
+                    const uint32_t jl = kIdx16 ? jj[u] : jj[u] - slo;
+                    const float wn = deliver_stdp<kH128>(st, ps.xq_a, net.C, jl, slo + jl, wv, gg[u]);
+                    ps.n_syn++;
+                    if (__float_as_uint(wn) != __float_as_uint(wv)) {
+                        const uint64_t a = lds_u64(ptr_a + (gg[u] << 3));
+                        float *wp = reinterpret_cast<float *>(kIdx16 ? 2ull * (a + 2ull * (w0 + x)) + dw
+                                                                     : a + 4ull * (w0 + x) + dw);
+                        *wp = wn;
+                        ps.n_w++;
+                        wv = wn;
+                    }
+                }
+            }
             if (kMulti && r2 >= 3u) r2 = (uint32_t)net.rcpt[r2 >> 2][find_pop(net, kIdx16 ? slo + jj[u] : jj[u])];
-            red_shared_add(acc_a + ((r2 * net.C + jj[u]) << 2), __float2int_rn(__fmul_rn(ww[u], scale)));
+            red_shared_add(acc_a + ((r2 * net.C + jj[u]) << 2), __float2int_rn(__fmul_rn(wv, scale)));
         }
     }
 }
 
-template <bool kMulti, bool kIdx16>
-__device__ __forceinline__ void deliver_window(const NetDev &net, uint32_t wlen, uint32_t w0, uint32_t bw_a,
-                                               uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a, uint64_t dw,
-                                               float scale, uint32_t slo) {
+template <bool kMulti, bool kIdx16, bool kPl, bool kH128>
+__device__ __forceinline__ void deliver_window(const NetDev &net, const StateDev &st, uint32_t wlen, uint32_t w0,
+                                               uint32_t bw_a, uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a,
+                                               uint64_t dw, float scale, uint32_t slo, DelStdp &ps) {
     for (uint32_t x0 = 0; x0 < wlen; x0 += kDelThreads * kDelU) {
         if (x0 + kDelThreads * kDelU <= wlen)
-            deliver_pass<kMulti, false, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+            deliver_pass<kMulti, false, kIdx16, kPl, kH128>(net, st, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw,
+                                                            scale, slo, ps);
         else
-            deliver_pass<kMulti, true, kIdx16>(net, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+            deliver_pass<kMulti, true, kIdx16, kPl, kH128>(net, st, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw,
+                                                           scale, slo, ps);
     }
 }
 
@@ -1254,8 +1736,12 @@ __device__ __forceinline__ void deliver_window(const NetDev &net, uint32_t wlen,
 // consecutive synapses -- and each element adds q(w) = RNE(w 2^F) to the slice
 // accumulator with a shared atomic.
 // kMulti: two receptor accumulators (a receptor code per segment); kIdx16:
-// SNN_FLAG_IDX16 -- compile-time variants, so a kernel carries only its path.
-template <bool kMulti, bool kIdx16>
+// SNN_FLAG_IDX16; kAhead: the arrival list of step t was written by
+// k_front(t-1) (D >= 2), so the CTA tabulates it while k_front(t) still runs
+// and waits for k_front(t) only before the elements; with STDP it also runs the
+// plastic arrivals' update (kPl = kAhead && STDP, see deliver_stdp) --
+// compile-time variants, so a kernel carries only its path.
+template <bool kMulti, bool kIdx16, bool kAhead, bool kH128>
 __global__ void __launch_bounds__(kDelThreads, SNN_DEL_MINB)
 k_deliver(NetDev net, StateDev st) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1264,6 +1750,7 @@ k_deliver(NetDev net, StateDev st) {
     __shared__ uint64_t s_ptr[kDelRows];     // segment g: byte address of idx[c] of flattened element 0
     __shared__ uint8_t s_rc[kDelRows];       // segment g: receptor code
     __shared__ uint2 s_bw[kDelWin / 32];     // window word: (segment-start bits, segments begun before it - 1)
+    constexpr bool kPlT = kAhead;            // (runtime: net.nstdp != 0)
     const uint32_t C = net.C;
     int32_t *acc = reinterpret_cast<int32_t *>(smem);                           // [nrcpt][C]
     const uint32_t k = blockIdx.x;
@@ -1274,18 +1761,31 @@ k_deliver(NetDev net, StateDev st) {
     const uint32_t lane = threadIdx.x & 31;
     const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
     unsigned long long t_wait = 0ull;
+    const bool pl_on = kAhead && net.nstdp != 0;
     trace_mark(st.trace, 2, 0);
 
-    // prologue: reads only k_front(t)'s lists -- complete before k_stdp(t)
-    // triggered this launch; without STDP the primary IS k_front(t), so wait
-    if (net.nstdp == 0) pdl_wait();
-    // the step and both parities' arrival counts in one round trip
+    // prologue: reads only the arrival list -- kAhead: k_front(t-1)'s, complete
+    // before k_front(t) triggered this launch; else k_front(t)'s, complete before
+    // k_stdp(t) triggered it (without STDP the primary IS k_front(t), so wait)
+    if (!kAhead && net.nstdp == 0) pdl_wait();
+    // the step and every slot's arrival count in one round trip
     const int64_t t = st.ctr->t;
-    const uint32_t nA0 = st.ctr->lst[0][1], nA1 = st.ctr->lst[1][1];
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Al = st.adesc[par];
-    const uint32_t nA = k < net.nslices ? (par ? nA1 : nA0) : 0u;
+    const uint32_t nAs = st.ctr->lst[t & 7][1];
+    const uint32_t nA = k < net.nslices ? nAs : 0u;
     for (uint32_t x = threadIdx.x; x < net.nrcpt * C; x += kDelThreads) acc[x] = 0;
+    DelStdp ps;
+    ps.n_syn = ps.n_w = 0;
+    ps.xq_a = 0;
+    if (kPlT && pl_on) {
+        for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kDelThreads)
+            g_del_dp[x] = st.stdp[x / (kMaxHist + 1)].dplus[x % (kMaxHist + 1)];
+        if (threadIdx.x < net.nstdp)
+            g_del_par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
+                                                 st.stdp[threadIdx.x].w_max, 0.0f);
+        ps.xq_a = smem_u32(acc + net.nrcpt * C);
+    }
     __syncthreads();
     const uint32_t r_begin = (uint32_t)(((uint64_t)nA * split) / nsplit);
     const uint32_t r_end = (uint32_t)(((uint64_t)nA * (split + 1)) / nsplit);
@@ -1346,6 +1846,12 @@ k_deliver(NetDev net, StateDev st) {
             s_rc[g] = (uint8_t)rcq[q];
             s_ptr[g] = idx16 ? (uint64_t)(st.idx16 + c0q[q]) - 2ull * est[q]
                              : (uint64_t)(st.idx + c0q[q]) - 4ull * est[q];
+            if (kPlT && pl_on) {
+                // the segment's plastic part: row-relative [max(piv, s0), min(piv', s1))
+                const uint32_t a0 = max(pp[q].x, d2[q].s0), a1 = min(pp[q].y, d2[q].s1);
+                g_del_pl[g] = a0 < a1 ? make_uint2(est[q] + a0 - pp[q].x, est[q] + a1 - pp[q].x) : make_uint2(0u, 0u);
+                g_del_row[g] = make_uint2(__float_as_uint(d2[q].xp), d2[q].meta);
+            }
             g++;
         }
         for (uint32_t w0 = 0; w0 < T; w0 += kDelWin) {
@@ -1365,13 +1871,28 @@ k_deliver(NetDev net, StateDev st) {
             s_bw[threadIdx.x].y = before + winc - pc - 1u;
             __syncthreads();
             if (r0 == r_begin && w0 == 0) {   // (the segment tables and the bitmap are ready)
-                pdl_wait();    // k_stdp(t): updated weights of plastic arrivals
+                pdl_wait();    // kAhead: k_front(t) (x_post, histories; inputs consumed); else k_stdp(t)
                 pdl_launch();
                 if (st.kspan) t_wait = gtimer();
                 trace_mark(st.trace, 2, 1);
+                if (kPlT && pl_on) {
+                    // the slice's x_post and spike positions (k_front(t)) -> shared
+                    const uint32_t plo = net.pp_lo > slo ? net.pp_lo : slo, phi = net.pp_hi < shi ? net.pp_hi : shi;
+                    const uint8_t *fpos = st.fpos + (size_t)(t & 3) * st.fstride;
+                    for (uint32_t j = plo + threadIdx.x; j < phi; j += kDelThreads) {
+                        reinterpret_cast<float *>(acc + net.nrcpt * C)[j - slo] = st.xpost[j];
+                        reinterpret_cast<uint8_t *>(acc + (net.nrcpt + 1) * C)[j - slo] = fpos[j];
+                    }
+                    __syncthreads();
+                }
             }
             // ---- elements: thread x takes w0 + x + 512 u (coalesced)
-            deliver_window<kMulti, kIdx16>(net, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale, slo);
+            if (kPlT && pl_on)
+                deliver_window<kMulti, kIdx16, kPlT, kH128>(net, st, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale,
+                                                            slo, ps);
+            else
+                deliver_window<kMulti, kIdx16, false, false>(net, st, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale,
+                                                             slo, ps);
             if (w0 + kDelWin < T) __syncthreads();  // bitmap reused by the next window
         }
         __syncthreads();                           // table reused next round
@@ -1387,14 +1908,25 @@ k_deliver(NetDev net, StateDev st) {
     }
     n_ev = __reduce_add_sync(0xffffffffu, n_ev);
     n_seg = __reduce_add_sync(0xffffffffu, n_seg);
+    if (kPlT && pl_on) {
+        ps.n_syn = __reduce_add_sync(0xffffffffu, ps.n_syn);
+        ps.n_w = __reduce_add_sync(0xffffffffu, ps.n_w);
+    }
     if (lane == 0) {
         if (n_ev) {
             atomicAdd(&st.ctr->metric[0], (unsigned long long)n_ev);
             atomicAdd(&st.ctr->metric[7], (unsigned long long)n_ev);
         }
         if (n_seg) atomicAdd(&st.ctr->metric[6], (unsigned long long)n_seg);
+        if (kPlT && ps.n_syn) {
+            atomicAdd(&st.ctr->metric[3], (unsigned long long)ps.n_syn);
+            atomicAdd(&st.ctr->metric[8], (unsigned long long)ps.n_syn);    // 8(d): every arrival weight r+w
+        }
+        if (kPlT && ps.n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)ps.n_w);
     }
-    pdl_wait();            // (no segments) this grid still completes after k_stdp(t)
+    // kAhead: the arriving rows of the step (k_front counts the arrivals of t + 1)
+    if (kAhead && k == 0 && split == 0 && threadIdx.x == 0 && nAs) atomicAdd(&st.ctr->metric[1], (unsigned long long)nAs);
+    pdl_wait();            // (no segments) this grid still completes after its primary
     pdl_launch();
     if (st.kspan) kspan_begin(st.kspan, t, 2, t_entry, t_wait ? t_wait : gtimer());
     // ---- step completion: the last CTA advances t
@@ -1425,7 +1957,7 @@ k_deliver_rowwise(NetDev net, StateDev st) {
     const int64_t t = st.ctr->t;
     const uint32_t par = (uint32_t)(t & 1);
     const RowDesc *Al = st.adesc[par];
-    const uint32_t nA = st.ctr->lst[par][1];
+    const uint32_t nA = st.ctr->lst[t & 7][1];
     pdl_wait();            // k_stdp(t): updated weights of plastic arrivals
     pdl_launch();
     const float scale = net.scale;
@@ -1499,7 +2031,8 @@ k_readout_prepare(NetDev net, StateDev st, int64_t t_last) {
     __syncwarp();
     if (valid && lane == 0 && net.nstdp) st.vmask[par][i >> 5] = 0u;
     uint32_t s0, s1, s2, n0, n1, n2;
-    compact3(cs, st.ctr->rlst, stale, false, false, s0, s1, s2, n0, n1, n2);   // (rlst zeroed by the launcher)
+    compact3(cs, st.ctr->rlst, st.ctr->rlst + 1, st.ctr->rlst + 2, stale, false, false, s0, s1, s2, n0, n1,
+             n2);   // (rlst zeroed by the launcher)
     if (stale) st.rdesc[s0] = d;
 }
 
@@ -1512,6 +2045,21 @@ k_readout_finish(NetDev net, StateDev st, int64_t t_last) {
         const StdpDev &sd = net.stdp[(d.meta >> 12) & 0xfu];
         st.xpre[d.row] = xpre_after(sd, d.xp, (int)(d.meta & kMetaAge), false);
         st.tlu[d.row] = (int32_t)t_last;
+    }
+}
+
+// (4) kAhead: the arrivals of t_last + 1 were listed by k_front(t_last) with
+// their rows' state at t_last + 1; after the read-out flush every plastic row
+// has tlu = t_last: age 1 and the flushed x_pre.
+__global__ void k_readout_ahead(NetDev net, StateDev st, int64_t t_last) {
+    const uint32_t n = st.ctr->lst[(t_last + 1) & 7][1];
+    RowDesc *A = st.adesc[(t_last + 1) & 1];
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        RowDesc d = A[r];
+        if (!(d.meta & kMetaPlastic)) continue;
+        d.meta = (d.meta & ~kMetaAge) | (uint32_t)(t_last + 1 - st.tlu[d.row]);
+        d.xp = st.xpre[d.row];
+        A[r] = d;
     }
 }
 
@@ -1555,7 +2103,10 @@ __global__ void k_hist_from_ring(NetDev net, const uint32_t *ring, int64_t t_las
 // ---------------------------------------------------------------- launchers
 uint32_t front_blocks(const NetDev &net) { return (net.N + kFrontThreads - 1) / kFrontThreads; }
 
-// Launch with the programmatic-stream-serialization attribute (PDL).
+// Launch with the programmatic-stream-serialization attribute (PDL) and, when
+// set (g_prio: a step graph with a side branch), a scheduling priority.
+static int g_prio = 0;   // 0: none, else the priority of the next launches (set per launch by the engine)
+void set_launch_priority(int p) { g_prio = p; }
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               bool pdl, Args... args) {
@@ -1564,25 +2115,48 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        na++;
+    }
+    if (g_prio) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na].val.priority = g_prio;
+        na++;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, bool pdl) {
-    return launch_pdl(k_front, dim3(front_blocks(net)), dim3(kFrontThreads), 0, s, pdl, net, st);
+cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, bool pdl, bool ahead) {
+    return launch_pdl(ahead ? k_front<true> : k_front<false>, dim3(front_blocks(net)), dim3(kFrontThreads), 0, s, pdl,
+                      net, st);
 }
+
+// k_deliver variants by (two receptors, 16-bit ids, ahead list, H = 128)
+static void (*const g_deliver[16])(NetDev, StateDev) = {
+    k_deliver<false, false, false, false>, k_deliver<false, false, false, true>,
+    k_deliver<false, false, true, false>,  k_deliver<false, false, true, true>,
+    k_deliver<false, true, false, false>,  k_deliver<false, true, false, true>,
+    k_deliver<false, true, true, false>,   k_deliver<false, true, true, true>,
+    k_deliver<true, false, false, false>,  k_deliver<true, false, false, true>,
+    k_deliver<true, false, true, false>,   k_deliver<true, false, true, true>,
+    k_deliver<true, true, false, false>,   k_deliver<true, true, false, true>,
+    k_deliver<true, true, true, false>,    k_deliver<true, true, true, true>};
 
 size_t stdp_smem_bytes(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
     (void)net;
     return ((sizeof(StdpSmem) + 127) & ~(size_t)127) + (size_t)kStdpStages * kStdpStageCh * 32 + 16ull * ((((pp_hi + 31) >> 5) - ((pp_lo >> 7) << 2) + 3) >> 2);
 }
 
-size_t deliver_smem_bytes(const NetDev &net) {
-    return 4ull * net.nrcpt * net.C;
+// accumulators [nrcpt][C]; + the slice's x_post [C] and fpos [C] with the
+// plastic arrivals' STDP (kAhead with STDP)
+size_t deliver_smem_bytes(const NetDev &net, bool ahead) {
+    return 4ull * net.nrcpt * net.C + (ahead && net.nstdp ? 5ull * net.C + 16 : 0ull);
 }
 
 // The dynamic shared-memory limit is an attribute of the kernel function, not
@@ -1602,17 +2176,22 @@ cudaError_t kernels_configure(int device) {
         if (r != cudaSuccess) return r;
         return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
     };
-    void (*kd[4])(NetDev, StateDev) = {k_deliver<false, false>, k_deliver<false, true>, k_deliver<true, false>,
-                                       k_deliver<true, true>};
-    for (auto k : kd)
+    for (auto k : g_deliver)
         if ((e = set_max((const void *)k)) != cudaSuccess) return e;
     void (*ks[6])(NetDev, StateDev, int64_t, uint32_t, uint32_t) = {
         k_stdp<false, false, false>, k_stdp<false, true, false>, k_stdp<false, false, true>,
         k_stdp<false, true, true>, k_stdp<true, false, true>, k_stdp<true, true, true>};
     for (auto k : ks)
         if ((e = set_max((const void *)k)) != cudaSuccess) return e;
-    if ((e = set_max((const void *)k_stdp_ev<false>)) != cudaSuccess) return e;
-    if ((e = set_max((const void *)k_stdp_ev<true>)) != cudaSuccess) return e;
+    void (*ke[6])(NetDev, StateDev, uint32_t, uint32_t) = {k_stdp_ev<false, 0, 1024>, k_stdp_ev<true, 0, 1024>,
+                                                          k_stdp_ev<false, 1, 512>, k_stdp_ev<true, 1, 512>,
+                                                          k_stdp_ev<false, 2, 512>, k_stdp_ev<true, 2, 512>};
+    for (auto k : ke)
+        if ((e = set_max((const void *)k)) != cudaSuccess) return e;
+    void (*kf[4])(NetDev, StateDev, uint32_t, uint32_t) = {k_flush<false, true>, k_flush<true, true>,
+                                                                    k_flush<false, false>, k_flush<true, false>};
+    for (auto k : kf)
+        if ((e = set_max((const void *)k)) != cudaSuccess) return e;
     done.insert(device);
     return cudaSuccess;
 }
@@ -1631,26 +2210,43 @@ cudaError_t launch_stdp(const NetDev &net, const StateDev &st, int64_t t_fixed, 
                       t_fixed, pp_lo, pp_hi);
 }
 
+// mode 0: arrivals + forced flushes (the step without the ahead list), 1: the
+// plastic arrivals only (a step whose flushes run on a side branch), 2: the
+// forced flushes (k_flush)
+uint32_t stdp_ev_threads(int mode) { return mode == 2 ? kFlT : mode == 1 ? 512u : 1024u; }
+uint32_t flush_ctas_per_sm() { return SNN_FL_GRID; }
 cudaError_t launch_stdp_ev(const NetDev &net, const StateDev &st, uint32_t grid, uint32_t pp_lo, uint32_t pp_hi,
-                           cudaStream_t s, bool pdl) {
-    void (*k)(NetDev, StateDev, uint32_t, uint32_t) = net.H > kHistBits ? k_stdp_ev<true> : k_stdp_ev<false>;
-    return launch_pdl(k, dim3(grid), dim3(kEvT), ev_smem_bytes(pp_lo, pp_hi), s, pdl, net, st, pp_lo, pp_hi);
+                           cudaStream_t s, bool pdl, int mode) {
+    const bool h = net.H > kHistBits;
+    if (mode == 2 && getenv("SNN_FLUSH_EV"))    // (experiments: the per-thread-chunk flush stream)
+        return launch_pdl(h ? k_stdp_ev<true, 2, 512> : k_stdp_ev<false, 2, 512>, dim3(grid), dim3(512),
+                          ev_smem_bytes(pp_lo, pp_hi), s, pdl, net, st, pp_lo, pp_hi);
+    if (mode == 2) {
+        const bool stg = flush_staged(pp_lo, pp_hi);
+        return launch_pdl(h ? (stg ? k_flush<true, true> : k_flush<true, false>)
+                            : (stg ? k_flush<false, true> : k_flush<false, false>),
+                          dim3(grid), dim3(kFlT), flush_smem_bytes(pp_lo, pp_hi), s, pdl, net, st, pp_lo, pp_hi);
+    }
+    void (*k)(NetDev, StateDev, uint32_t, uint32_t) =
+        mode == 1 ? (h ? k_stdp_ev<true, 1, 512> : k_stdp_ev<false, 1, 512>)
+                  : (h ? k_stdp_ev<true, 0, 1024> : k_stdp_ev<false, 0, 1024>);
+    return launch_pdl(k, dim3(grid), dim3(stdp_ev_threads(mode)), ev_smem_bytes(pp_lo, pp_hi), s, pdl, net, st,
+                      pp_lo, pp_hi);
 }
 
 cudaError_t launch_deliver_rowwise(const NetDev &net, const StateDev &st, uint32_t grid, cudaStream_t s, bool pdl) {
     return launch_pdl(k_deliver_rowwise, dim3(grid), dim3(kRowThreads), 0, s, pdl, net, st);
 }
 
-cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s, bool pdl) {
+cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s, bool pdl,
+                           bool ahead) {
     dim3 grid(net.nslices > 0 ? net.nslices : 1, splits);
-    const bool multi = net.nrcpt > 1, idx16 = st.idx16 != nullptr;
-    void (*k)(NetDev, StateDev) = multi ? (idx16 ? k_deliver<true, true> : k_deliver<true, false>)
-                                        : (idx16 ? k_deliver<false, true> : k_deliver<false, false>);
-    return launch_pdl(k, grid, dim3(kDelThreads), deliver_smem_bytes(net), s, pdl, net, st);
+    const uint32_t v = (net.nrcpt > 1 ? 8u : 0u) | (st.idx16 ? 4u : 0u) | (ahead ? 2u : 0u) | (net.H > kHistBits ? 1u : 0u);
+    return launch_pdl(g_deliver[v], grid, dim3(kDelThreads), deliver_smem_bytes(net, ahead), s, pdl, net, st);
 }
 
 cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last, uint32_t grid, uint32_t pp_lo,
-                           uint32_t pp_hi, cudaStream_t s) {
+                           uint32_t pp_hi, cudaStream_t s, bool ahead) {
     cudaError_t e = cudaMemsetAsync(st.ctr->rlst, 0, sizeof(st.ctr->rlst), s);
     if (e != cudaSuccess) return e;
     k_readout_prepare<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
@@ -1658,6 +2254,7 @@ cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last
     if (e != cudaSuccess) return e;
     if ((e = launch_stdp(net, st, t_last, grid, pp_lo, pp_hi, s, false)) != cudaSuccess) return e;
     k_readout_finish<<<front_blocks(net), kFrontThreads, 0, s>>>(net, st, t_last);
+    if (ahead) k_readout_ahead<<<64, 256, 0, s>>>(net, st, t_last);
     return cudaGetLastError();
 }
 

@@ -9,7 +9,7 @@ import torch
 import workloads as W
 from paper_2107_04092_b200 import Snn
 rc = W.config(int(os.environ.get("NCU_CONFIG", "3")))
-g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, flags=1)   # NO_GRAPH: individual launches
+g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, flags=int(os.environ.get("NCU_FLAGS", "1")))   # 1 = NO_GRAPH: individual launches; 0 = graph nodes
 rc.apply(g)
 g.step(int(os.environ.get("NCU_STEPS", "3200")))
 torch.cuda.synchronize()

@@ -24,7 +24,7 @@ for rep in range(3):
     os.environ.pop("SNN_DEBUG_KERNELS", None)
     tr = g.read_state("TRACE").reshape(4, 4096, 4).astype(np.int64)
     t0 = tr[0][tr[0][:, 0] > 0][:, 0].min()
-    for k, name in [(0, "front"), (2, "deliver"), (1, "stdp")]:
+    for k, name in [(0, "front"), (2, "deliver"), (1, "stdp"), (3, "flush")]:
         a = tr[k]
         a = a[a[:, 0] > 0]
         if len(a) == 0:
@@ -34,3 +34,17 @@ for rep in range(3):
               + " ".join(f"ph{p}[med/max]={np.median(rel[:,p]-rel[:,0]):6.2f}/{(rel[:,p]-rel[:,0]).max():6.2f}" for p in (1, 2, 3))
               + f" end_max={rel[:,3].max():7.2f}")
     print(g.metrics())
+# deliver: element-phase duration by slice (E slices carry the plastic arrivals' STDP in the ahead step)
+a = tr[2][:g.info()["nslices"] * 2] if False else None
+tr = g.read_state("TRACE").reshape(4, 4096, 4).astype(np.int64)
+ns = g.info()["nslices"]
+d = tr[2][: ns * 2]
+ok = d[:, 0] > 0
+ph = (d[:, 2] - d[:, 1]) / 1000.0
+cta = np.arange(len(d))
+sl = cta % ns                      # blockIdx.y * gridDim.x + blockIdx.x
+nE = rc.pops[0].n
+C = g.info()["C"]
+isE = (sl + 1) * C <= nE
+print("deliver element phase (us): E slices med/max %.2f/%.2f   other slices med/max %.2f/%.2f" %
+      (np.median(ph[ok & isE]), ph[ok & isE].max(), np.median(ph[ok & ~isE]), ph[ok & ~isE].max()))
