@@ -341,6 +341,20 @@ uint32_t snn_abi_version(void);
 snn_status snn_partition(uint32_t n_targets, uint32_t slice_width, uint32_t world, uint32_t rank, uint32_t *lo,
                          uint32_t *hi);
 
+/* The partition the library uses: rank `rank`'s range
+ * [*lo, *hi) of [0, n_targets), contiguous and C-aligned, with boundaries at
+ * the slice prefixes closest to r / world of the total expected work
+ * (`slice_cost[k]` >= 0: the expected per-step bytes of slice k = targets
+ * [kC, (k+1)C), host memory, owned by the caller; the engine uses the
+ * SURVEY 8(d) byte model).  Ranks may get unequal neuron counts -- e.g. the
+ * plastic (E) targets, whose forced flushes dominate, are spread over more
+ * ranks.  Every rank computes every range identically (deterministic, host
+ * only).  Errors: SNN_E_INVALID (world == 0, rank >= world, C not a positive
+ * multiple of 32, nslices * C < n_targets, a negative or NaN cost, NULL
+ * pointers). */
+snn_status snn_partition_weighted(const double *slice_cost, uint32_t nslices, uint32_t n_targets,
+                                  uint32_t slice_width, uint32_t world, uint32_t rank, uint32_t *lo, uint32_t *hi);
+
 #ifdef __cplusplus
 }
 #endif

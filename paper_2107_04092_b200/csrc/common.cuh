@@ -8,6 +8,7 @@
 namespace snn {
 
 constexpr int kMaxPops = 16;
+constexpr int kMaxRanks = 64;   // world size limit of the target-range partition
 constexpr int kHistBits = 64;     // bits per history word
 constexpr int kMaxHist = 128;     // H: 64 (one word) or 128 (two words)
 constexpr int kRingSlots = 64;    // bitmask ring: slot t % 64 holds step t's spikes
@@ -51,8 +52,8 @@ struct NetDev {
     uint32_t ring_stride;// words per ring slot (nwords + exchange padding)
     uint32_t world, rank;        // ranks sharing the target range
     uint32_t debug;              // SNN_DEBUG_KERNELS bits (experiments only; 0 in normal runs)
-    uint32_t share_w;            // words per rank share (rank r owns words [r share_w, ...))
-    uint32_t wmax;               // words exchanged per rank and step
+    uint32_t wmax;               // words exchanged per rank and step (the largest share + 1)
+    uint32_t rank_lo[kMaxRanks + 1];   // target range of rank r: [rank_lo[r], rank_lo[r + 1]) (C-aligned)
     uint32_t D;          // delay
     uint32_t H;          // history bits: 64 or 128 (forced flush at age H, R3)
     uint32_t flush_period; // 0: flush at age H; K: every K steps the rows of age >= H - K (R33)
@@ -88,7 +89,8 @@ struct Counters {
     int64_t tfl;             // the step of the next k_flush launch (k_flush runs once per step, in order;
                              // its last CTA advances it)
     uint32_t fticket;        // CTA-completion ticket of k_flush
-    uint32_t pad2;
+    uint32_t xticket;        // CTA-completion ticket of k_unpack (world > 1)
+    int64_t tx;              // the step of the next NCCL exchange (k_unpack advances it)
     uint32_t ticket;         // CTA-completion ticket of the slice kernel
     uint32_t pad;
     unsigned long long metric[16];

@@ -29,7 +29,7 @@ cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, ui
 cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
 cudaError_t build_idx16(const NetDev &, const uint32_t *, uint16_t *, int64_t, cudaStream_t);
 uint32_t front_blocks(const NetDev &);
-cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool, bool);
+cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool, bool, int);
 size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
 size_t deliver_smem_bytes(const NetDev &, bool);
 cudaError_t kernels_configure(int);
@@ -125,6 +125,10 @@ struct snn_sim {
     bool use_prio = false;
     cudaStream_t cap_side = nullptr;
     cudaEvent_t ev_front = nullptr, ev_flush[2] = {nullptr, nullptr};
+    // world > 1, D >= 1: the exchange of step t on a branch of the step graph
+    // (after k_front(t), joined before k_front(t+1)), overlapping the delivery
+    cudaStream_t cap_xside = nullptr;
+    cudaEvent_t ev_xfront = nullptr, ev_xdone = nullptr;
     // captured step graphs by step count (<= kGraphSteps): a call of n steps
     // replays ceil(n / 64) graphs, so a step's side branch is joined once per call
     std::map<uint32_t, cudaGraphExec_t> graphs;
@@ -261,6 +265,34 @@ static snn_status exchange_enqueue(snn_sim *sim, cudaStream_t s, int64_t t) {
 }
 
 // --------------------------------------------------------------------- setup
+// Expected per-step HBM bytes of each slice of C targets of [0, R) -- the
+// SURVEY 8(d) byte model, per synapse into the slice: a delivered event 8 B x
+// nu_src dt; a plastic synapse adds its arrival's STDP (8 B x nu_src dt) and
+// its forced flush (4 B / H).  nu_src: the Poisson rate, 10 Hz for LIF sources
+// (8(d)'s nominal rate).  Used to balance the ranks' target ranges.
+static std::vector<double> slice_costs(const snn_sim *sim, uint32_t R, uint32_t C, uint32_t H) {
+    const double dt = sim->cfg.dt_ms * 1e-3;
+    std::vector<double> per_neuron(sim->pops.size(), 0.0);
+    for (const HostProj &hj : sim->projs) {
+        const HostPop &src = sim->pops[hj.src];
+        const double nu = src.prm.kind == SNN_POP_POISSON ? (double)src.prm.rate_hz : 10.0;
+        double b = 8.0 * nu * dt;
+        if (hj.prm.kind == SNN_SYN_STDP) b += 8.0 * nu * dt + 4.0 / (double)H;
+        per_neuron[hj.dst] += hj.prm.p * (double)src.n * b;
+    }
+    const uint32_t ns = (R + C - 1) / C;
+    std::vector<double> cost(ns, 0.0);
+    for (size_t k = 0; k < sim->pops.size(); k++) {
+        const uint64_t a = sim->pops[k].base, e = std::min<uint64_t>(R, a + sim->pops[k].n);
+        for (uint64_t s0 = a; s0 < e;) {                 // the population's overlap with each slice
+            const uint64_t sl = s0 / C, s1 = std::min<uint64_t>(e, (sl + 1) * C);
+            cost[sl] += (double)(s1 - s0) * per_neuron[k];
+            s0 = s1;
+        }
+    }
+    return cost;
+}
+
 static snn_status finalize(snn_sim *sim) {
     const snn_config &cfg = sim->cfg;
     if (sim->pops.empty()) return sim->fail(SNN_E_INVALID, "no populations");
@@ -383,15 +415,27 @@ static snn_status finalize(snn_sim *sim) {
     }
     net.C = C;
     net.log2C = 0;   // (unused: C need not be a power of two)
-    // this rank's target range: C-aligned equal shares of [0, R)
+    // this rank's target range: C-aligned contiguous
+    // ranges of [0, R) with equal expected per-step work (snn_partition_weighted)
+    if (cfg.world > kMaxRanks) return sim->fail(SNN_E_UNSUPPORTED, "world > %d", kMaxRanks);
     uint32_t lo = 0, hi = R;
-    snn_partition(R, C, (uint32_t)cfg.world, (uint32_t)cfg.rank, &lo, &hi);
+    {
+        const std::vector<double> cost = slice_costs(sim, R, C, cfg.history_bits);
+        for (int r = 0; r <= cfg.world; r++) {
+            uint32_t a = R, b = R;
+            if (r < cfg.world)
+                snn_partition_weighted(cost.data(), (uint32_t)cost.size(), R, C, (uint32_t)cfg.world, (uint32_t)r, &a, &b);
+            net.rank_lo[r] = a;
+            if (r == cfg.rank) {
+                lo = a;
+                hi = b;
+            }
+        }
+    }
     if (cfg.world > 1) {
         for (uint32_t k = 0; k < net.npop; k++)
             if (net.pop[k].base < R && !(net.pop[k].flags & PF_HAS_INPUT))
                 return sim->fail(SNN_E_INVALID, "world > 1: add populations that receive synapses first");
-        if (cfg.delay_steps == 0)
-            return sim->fail(SNN_E_UNSUPPORTED, "world > 1 needs delay >= 1 (the exchange of step t overlaps step t+1)");
     }
     net.tgt_lo = lo;
     net.tgt_hi = hi;
@@ -417,15 +461,15 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.fpot, float, 4ull * st.fstride);
     ALLOC(st.fpos, uint8_t, 4ull * st.fstride);
     ALLOC(st.nspk, uint32_t, N);
-    // exchange geometry: rank r owns words [r share_w, ...), at most share_w + 1
-    // of them (the word straddling R); ring slots padded for the unpack
+    // exchange geometry: rank r owns words [rank_lo[r] / 32, ...), at most
+    // (its share) / 32 + 1 of them (the word straddling R); every rank sends
+    // wmax words (the largest share + 1); ring slots padded for the unpack
     net.world = (uint32_t)cfg.world;
     net.rank = (uint32_t)cfg.rank;
     {
-        const uint32_t W = (uint32_t)cfg.world;
-        const uint64_t share = ((uint64_t)(R + W - 1) / W + C - 1) / C * C;
-        net.share_w = (uint32_t)std::max<uint64_t>(1, share / 32);
-        net.wmax = net.share_w + 1;
+        uint32_t mx = 1;
+        for (int r = 0; r < cfg.world; r++) mx = std::max(mx, (net.rank_lo[r + 1] - net.rank_lo[r] + 31) / 32);
+        net.wmax = mx + 1;
         sim->wmax = net.wmax;
     }
     net.ring_stride = net.nwords + (cfg.world > 1 ? net.wmax : 0);
@@ -571,6 +615,11 @@ static snn_status finalize(snn_sim *sim) {
     if (sim->pipe == 1 && !sim->ahead) sim->pipe = 0;
     if (!sim->plastic || !sim->ev_kernel || flush_smem_bytes(sim->pp_lo, sim->pp_hi) > 227 * 1024)
         if (sim->pipe == 2) sim->pipe = 0;
+    if (cfg.world > 1 && net.D >= 1 && cfg.nccl_unique_id && !getenv("SNN_NO_XBRANCH")) {
+        CK(cudaStreamCreateWithFlags(&sim->cap_xside, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&sim->ev_xfront, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sim->ev_xdone, cudaEventDisableTiming));
+    }
     if (sim->pipe != 0) {
         CK(cudaStreamCreateWithFlags(&sim->cap_side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&sim->ev_front, cudaEventDisableTiming));
@@ -602,6 +651,33 @@ static snn_status finalize(snn_sim *sim) {
 }
 
 // ---------------------------------------------------------------- the step
+// D = 0 on the local-group transport: every rank's neuron phase of step t,
+// then every rank's words of t into every peer's gather slot, then each
+// rank's unpack into its ring slot t (all on the caller's stream).
+static snn_status local_group_front_d0(snn_sim *sim, cudaStream_t s, int64_t t) {
+    const snn_config &cfg = sim->cfg;
+    std::vector<snn_sim *> peers;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        peers = g_groups[cfg.group_key];
+    }
+    if ((int)peers.size() != cfg.world)
+        return sim->fail(SNN_E_STATE, "local group %llu has %zu of %d ranks", (unsigned long long)cfg.group_key,
+                         peers.size(), cfg.world);
+    for (snn_sim *p : peers) {
+        if (p->state == 0 || !p->st.gath) return sim->fail(SNN_E_STATE, "local group peer not finalized");
+        if (p->t != sim->t) return sim->fail(SNN_E_STATE, "local group ranks must be stepped in lockstep");
+        CK(launch_front(p->net, p->st, s, false, false, 1));
+    }
+    for (snn_sim *q : peers)
+        for (snn_sim *p : peers)
+            CK(cudaMemcpyAsync(p->st.gath + ((size_t)(t & 1) * cfg.world + q->cfg.rank) * sim->wmax, q->st.sendbuf,
+                               4ull * sim->wmax, cudaMemcpyDeviceToDevice, s));
+    for (snn_sim *p : peers)
+        CK(launch_unpack(p->net, p->st, p->st.gath + (size_t)(t & 1) * cfg.world * sim->wmax, t, s));
+    return SNN_OK;
+}
+
 static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bool first, int64_t step_k = 0,
                                cudaStream_t side = nullptr, uint32_t gk = 0) {
     NetDev net = sim->net;
@@ -614,19 +690,46 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     const bool pdl = ev == nullptr && !(sim->cfg.flags & SNN_FLAG_NO_PDL) && !multi;
     if (ev) CK(cudaEventRecord(ev[0], s));
     const int64_t t = sim->t + step_k;                              // host copy (direct mode only)
-    if (multi && sim->local_group && t > 0)                         // peers' spikes of t-1 -> ring
+    const bool d0 = multi && net.D == 0;     // the arrivals of t include the other ranks' spikes of t
+    if (multi && sim->local_group && t > 0 && !d0)                  // peers' spikes of t-1 -> ring
         CK(launch_unpack(net, st, st.gath + (size_t)((t - 1) & 1) * sim->cfg.world * sim->wmax, t - 1, s));
     if (sim->use_prio) set_launch_priority(sim->prio_hi);
-    CK(launch_front(net, st, s, pdl && !first, sim->ahead));        // (1) P:36 + work lists
-    if (multi) {                                                    // spike words of t -> peers
-        snn_status r = exchange_enqueue(sim, s, t);
-        if (r != SNN_OK) return r;
+    if (d0) {
+        // neurons of t (every rank) -> the exchange of the words of t -> the
+        // lists of t from the complete ring slot
+        if (sim->local_group) {
+            // (test transport, one stream, ranks stepped in lockstep in rank
+            // order: rank 0's call runs every rank's neuron phase and the copies)
+            if (sim->cfg.rank == 0) {
+                snn_status r = local_group_front_d0(sim, s, t);
+                if (r != SNN_OK) return r;
+            }
+        } else {
+            CK(launch_front(net, st, s, false, false, 1));
+            snn_status r = exchange_enqueue(sim, s, t);
+            if (r != SNN_OK) return r;
+        }
+        CK(launch_front(net, st, s, false, false, 2));
+    } else {
+        const bool xbranch = multi && side && sim->cap_xside && !sim->local_group;
+        if (xbranch && gk > 0) CK(cudaStreamWaitEvent(s, sim->ev_xdone, 0));   // the exchange of t-1
+        CK(launch_front(net, st, s, pdl && !first, sim->ahead, 0)); // (1) P:36 + work lists
+        if (xbranch) {                                              // spike words of t -> peers, beside the step
+            CK(cudaEventRecord(sim->ev_xfront, s));
+            CK(cudaStreamWaitEvent(sim->cap_xside, sim->ev_xfront, 0));
+            snn_status r = exchange_enqueue(sim, sim->cap_xside, t);
+            if (r != SNN_OK) return r;
+            CK(cudaEventRecord(sim->ev_xdone, sim->cap_xside));
+        } else if (multi) {
+            snn_status r = exchange_enqueue(sim, s, t);
+            if (r != SNN_OK) return r;
+        }
     }
     if (ev) CK(cudaEventRecord(ev[1], s));
     if (sim->plastic) {                                             // (2) P:37-39
         // the event schedule (flushes at age H): k_stdp_ev; the ablation
         // schedules and batched flushes: the generic k_stdp
-        if (side && (sim->pipe == 1 || sim->pipe == 2)) {
+        if (side && sim->cap_side && (sim->pipe == 1 || sim->pipe == 2)) {
             // (experiments) the forced flushes on a side branch of the graph
             CK(cudaEventRecord(sim->ev_front, s));
             const uint32_t lag = sim->pipe == 1 ? (uint32_t)sim->fl_lag : 1u;
@@ -651,7 +754,7 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     if (ev) CK(cudaEventRecord(ev[2], s));
     if (net.deliv_mode == SNN_DELIV_ROWWISE) CK(launch_deliver_rowwise(net, st, sim->stdp_grid, s, pdl));   // Fig. 3a
     else CK(launch_deliver(net, st, sim->splits, s, pdl, sim->ahead));   // (3) P:41, Fig. 3b
-    if (sim->plastic && (sim->ahead || sim->pipe == 2) && !(side && sim->pipe != 0))   // (2') forced flushes of t (R3)
+    if (sim->plastic && (sim->ahead || sim->pipe == 2) && !(side && sim->cap_side && sim->pipe != 0))   // (2') flushes of t (R3)
         CK(launch_stdp_ev(net, st, sim->flush_grid, sim->pp_lo, sim->pp_hi, s, pdl, 2));
     if (sim->use_prio) set_launch_priority(0);
     if (ev) CK(cudaEventRecord(ev[4], s));
@@ -663,13 +766,15 @@ static snn_status capture(snn_sim *sim, uint32_t nsteps, cudaGraphExec_t *out) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(sim->cap_stream, cudaStreamCaptureModeThreadLocal));
     for (uint32_t k = 0; k < nsteps; k++) {
-        snn_status r = enqueue_step(sim, sim->cap_stream, nullptr, k == 0, 0, sim->cap_side, k);
+        snn_status r = enqueue_step(sim, sim->cap_stream, nullptr, k == 0, 0,
+                                    sim->cap_side ? sim->cap_side : sim->cap_xside, k);
         if (r != SNN_OK) {
             cudaStreamEndCapture(sim->cap_stream, &g);
             if (g) cudaGraphDestroy(g);
             return r;
         }
     }
+    if (sim->cap_xside && nsteps > 0) CK(cudaStreamWaitEvent(sim->cap_stream, sim->ev_xdone, 0));   // join
     if (sim->cap_side && sim->pipe != 0)                            // join the side branch
         for (uint32_t k = nsteps > 2 ? nsteps - 2 : 0; k < nsteps; k++)
             CK(cudaStreamWaitEvent(sim->cap_stream, sim->ev_flush[k & 1], 0));
@@ -1075,6 +1180,40 @@ snn_status snn_partition(uint32_t n_targets, uint32_t slice_width, uint32_t worl
     return SNN_OK;
 }
 
+snn_status snn_partition_weighted(const double *slice_cost, uint32_t nslices, uint32_t n_targets,
+                                  uint32_t slice_width, uint32_t world, uint32_t rank, uint32_t *lo, uint32_t *hi) {
+    if (world == 0 || rank >= world || !lo || !hi || slice_width == 0 || (slice_width & 31u) ||
+        (uint64_t)nslices * slice_width < n_targets || (nslices > 0 && !slice_cost))
+        return SNN_E_INVALID;
+    double total = 0.0;
+    for (uint32_t k = 0; k < nslices; k++) {
+        if (!(slice_cost[k] >= 0.0)) return SNN_E_INVALID;
+        total += slice_cost[k];
+    }
+    // boundary b_r (in slices): the prefix closest to r / world of the total,
+    // non-decreasing in r; equal counts when every cost is 0
+    auto boundary = [&](uint32_t r) -> uint32_t {
+        if (r == 0) return 0;
+        if (r >= world) return nslices;
+        if (!(total > 0.0)) return (uint32_t)(((uint64_t)nslices * r) / world);
+        const double goal = total * (double)r / (double)world;
+        double pre = 0.0;
+        uint32_t k = 0;
+        while (k < nslices && pre + slice_cost[k] < goal) pre += slice_cost[k++];
+        // pre < goal <= pre + cost[k]: the closer of k and k + 1
+        if (k < nslices && (pre + slice_cost[k]) - goal < goal - pre) k++;
+        return k;
+    };
+    uint32_t b0 = 0, b1 = 0;
+    for (uint32_t r = 0; r <= rank; r++) {      // (monotone: each boundary >= the previous)
+        b0 = std::max(b1, boundary(r));
+        b1 = std::max(b0, boundary(r + 1));
+    }
+    *lo = (uint32_t)std::min<uint64_t>((uint64_t)b0 * slice_width, n_targets);
+    *hi = (uint32_t)std::min<uint64_t>((uint64_t)b1 * slice_width, n_targets);
+    return SNN_OK;
+}
+
 void snn_destroy(snn_sim *sim) {
     if (!sim) return;
     DeviceGuard dg(sim->cfg.device);
@@ -1099,6 +1238,9 @@ void snn_destroy(snn_sim *sim) {
     }
     if (sim->cap_stream) cudaStreamDestroy(sim->cap_stream);
     if (sim->cap_side) cudaStreamDestroy(sim->cap_side);
+    if (sim->cap_xside) cudaStreamDestroy(sim->cap_xside);
+    if (sim->ev_xfront) cudaEventDestroy(sim->ev_xfront);
+    if (sim->ev_xdone) cudaEventDestroy(sim->ev_xdone);
     if (sim->ev_front) cudaEventDestroy(sim->ev_front);
     for (auto e : sim->ev_flush)
         if (e) cudaEventDestroy(e);

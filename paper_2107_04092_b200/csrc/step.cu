@@ -110,7 +110,11 @@ __device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *len_a, uint32_t
 // ------------------------------------------------------------------ k_front
 // One thread per neuron i (it also owns source row i); warps cover 32
 // consecutive ids = one ring word.  P:36 "Update neurons, note which ones fire".
-template <bool kAhead>
+// kPart (world > 1 with D = 0, where the arrivals of t include the other
+// ranks' spikes of t): 1 = the neuron update and ring words only, 2 = the
+// lists only, after the exchange put every rank's words of t in the ring;
+// 0 = both (every other case).
+template <bool kAhead, int kPart>
 __global__ void __launch_bounds__(kFrontThreads)
 k_front(NetDev net, StateDev st) {
     __shared__ Compact2 cs;
@@ -119,7 +123,8 @@ k_front(NetDev net, StateDev st) {
     pdl_launch();
     trace_mark(st.trace, 0, 0);
     const int64_t t = st.ctr->t;
-    if (st.kspan) kspan_begin(st.kspan, t, 0, t_entry, gtimer());
+    constexpr int kSpan = kPart == 2 ? 4 : 0;
+    if (st.kspan) kspan_begin(st.kspan, t, kSpan, t_entry, gtimer());
     const uint32_t par = (uint32_t)(t & 1);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t lane = threadIdx.x & 31;
@@ -132,7 +137,7 @@ k_front(NetDev net, StateDev st) {
     // other input neurons arrive by the exchange
     const bool owned = i >= net.R || (i >= net.tgt_lo && i < net.tgt_hi);
     // ---- (1) neuron dynamics (App. B op order)
-    if (valid && owned) {
+    if (kPart != 2 && valid && owned) {
         if (p.kind == POP_POISSON) {
             const u32x4 r = philox4x32_10(i, (uint32_t)t, 2u, 0u, net.key0, net.key1);
             fired = (uint64_t)r.x < p.thr;
@@ -230,18 +235,24 @@ k_front(NetDev net, StateDev st) {
     // neurons (the word straddling R by the last rank), by all if it has none
     const bool wown = i >= net.R ? true : (i + 32 <= net.R ? (i >= net.tgt_lo && i + 32 <= net.tgt_hi)
                                                            : (i >= net.tgt_lo && net.tgt_hi == net.R));
-    if (lane == 0 && valid && wown) {
+    if (kPart != 2 && lane == 0 && valid && wown) {
         st.ring[(size_t)(t & (kRingSlots - 1)) * net.ring_stride + (i >> 5)] = fword;
         if (net.nstdp) st.recent[(size_t)(t & 3) * st.rstride + (i >> 5)] = rword;
         // this rank's share of the step's input-neuron words, for the exchange
-        const uint32_t w = i >> 5, w0 = net.rank * net.share_w;
+        const uint32_t w = i >> 5, w0 = net.rank_lo[net.rank] >> 5;
         if (net.world > 1 && i < net.R && w >= w0 && w < w0 + net.wmax) st.sendbuf[w - w0] = fword;
+    }
+
+    if (kPart == 1) {
+        trace_mark(st.trace, 0, 3);
+        kspan_end(st.kspan, t, kSpan);
+        return;
     }
 
     // ---- (2) arrival of row i at step t: its spike of step t - D (hist[delay])
     bool arr = false, arr1 = false, arr2 = false;
     if (valid) {
-        if (net.D == 0) arr = fired;
+        if (net.D == 0) arr = kPart == 2 ? ring_bit(st.ring, net.ring_stride, t, i) != 0u : fired;
         else if (t >= (int64_t)net.D) arr = ring_bit(st.ring, net.ring_stride, t - net.D, i);
         // kAhead (D >= 2): the arrivals of t + 1 and t + 2 are spikes of steps <= t - 1
         if (kAhead && t + 1 >= (int64_t)net.D) arr1 = ring_bit(st.ring, net.ring_stride, t + 1 - net.D, i);
@@ -359,7 +370,7 @@ k_front(NetDev net, StateDev st) {
         if (nf) atomicAdd(&st.ctr->metric[5], (unsigned long long)nf);
     }
     trace_mark(st.trace, 0, 3);
-    kspan_end(st.kspan, t, 0);
+    kspan_end(st.kspan, t, kSpan);
 }
 
 // ---------------------------------------------------- CTA row-table helpers
@@ -2067,14 +2078,24 @@ __global__ void k_readout_ahead(NetDev net, StateDev st, int64_t t_last) {
 // `gath` (one share of wmax words per rank), into ring slot tp.  t_fixed < 0:
 // tp = the current step (NCCL: unpack right after the all-gather of the step).
 __global__ void k_unpack(NetDev net, StateDev st, const uint32_t *gath, int64_t t_fixed) {
-    const int64_t tp = t_fixed >= 0 ? t_fixed : st.ctr->t;
+    // t_fixed < 0: the exchange's own step counter (one exchange per step, in
+    // order; it may run beside the step, after k_deliver advanced ctr->t)
+    const int64_t tp = t_fixed >= 0 ? t_fixed : *(volatile const int64_t *)&st.ctr->tx;
+    if (t_fixed < 0) {
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(&st.ctr->xticket, 1u) == gridDim.x - 1) {   // the last CTA: next step
+            st.ctr->xticket = 0;
+            st.ctr->tx = tp + 1;
+        }
+    }
     if (tp < 0) return;
     const uint32_t nwR = (net.R + 31) >> 5;
     for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwR; w += gridDim.x * blockDim.x) {
-        const uint32_t r = min(w / net.share_w, net.world - 1);
+        uint32_t r = 0;                        // the rank owning word w (ranges are 32-aligned)
+        while (r + 1 < net.world && 32u * w >= net.rank_lo[r + 1]) r++;
         if (r == net.rank) continue;
         st.ring[(size_t)(tp & (kRingSlots - 1)) * net.ring_stride + w] =
-            gath[(size_t)r * net.wmax + (w - r * net.share_w)];
+            gath[(size_t)r * net.wmax + (w - (net.rank_lo[r] >> 5))];
     }
 }
 
@@ -2132,9 +2153,10 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, bool pdl, bool ahead) {
-    return launch_pdl(ahead ? k_front<true> : k_front<false>, dim3(front_blocks(net)), dim3(kFrontThreads), 0, s, pdl,
-                      net, st);
+cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, bool pdl, bool ahead, int part) {
+    void (*k)(NetDev, StateDev) = ahead ? k_front<true, 0>
+                                        : part == 1 ? k_front<false, 1> : part == 2 ? k_front<false, 2> : k_front<false, 0>;
+    return launch_pdl(k, dim3(front_blocks(net)), dim3(kFrontThreads), 0, s, pdl, net, st);
 }
 
 // k_deliver variants by (two receptors, 16-bit ids, ahead list, H = 128)

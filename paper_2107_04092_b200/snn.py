@@ -104,8 +104,13 @@ _lib.snn_partition.restype = ctypes.c_int32
 _lib.snn_partition.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                _P(ctypes.c_uint32), _P(ctypes.c_uint32)]
 
+_lib.snn_partition_weighted.restype = ctypes.c_int32
+_lib.snn_partition_weighted.argtypes = [_P(ctypes.c_double), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                        ctypes.c_uint32, ctypes.c_uint32, _P(ctypes.c_uint32), _P(ctypes.c_uint32)]
+
 EXPORTS = ["snn_create", "snn_add_population", "snn_connect", "snn_step", "snn_read_state",
-           "snn_read_state_range", "snn_destroy", "snn_last_error", "snn_abi_version", "snn_partition"]
+           "snn_read_state_range", "snn_destroy", "snn_last_error", "snn_abi_version", "snn_partition",
+           "snn_partition_weighted"]
 
 
 class SnnError(RuntimeError):
@@ -132,6 +137,15 @@ def snn_partition(n_targets: int, slice_width: int, world: int, rank: int):
     """Target range [lo, hi) of `rank` (host only, no device work)."""
     lo, hi = ctypes.c_uint32(), ctypes.c_uint32()
     _check(_lib.snn_partition(n_targets, slice_width, world, rank, ctypes.byref(lo), ctypes.byref(hi)), None)
+    return lo.value, hi.value
+
+
+def snn_partition_weighted(slice_cost, n_targets: int, slice_width: int, world: int, rank: int):
+    """Target range [lo, hi) of `rank` balancing the per-slice costs (host only)."""
+    c = (ctypes.c_double * len(slice_cost))(*[float(x) for x in slice_cost])
+    lo, hi = ctypes.c_uint32(), ctypes.c_uint32()
+    _check(_lib.snn_partition_weighted(c, len(slice_cost), n_targets, slice_width, world, rank, ctypes.byref(lo),
+                                       ctypes.byref(hi)), None)
     return lo.value, hi.value
 
 

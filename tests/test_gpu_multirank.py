@@ -55,13 +55,28 @@ def test_partitioned_equals_single(world, plastic):
     assert ev == ref.metrics()["EVENTS"]
 
 
-def test_world_gt1_needs_delay():
-    from paper_2107_04092_b200 import Snn, SnnError, SNN_E_UNSUPPORTED
-    rc = W.vogels(2000, seed=2)        # D = 0
-    g0 = Snn(1, 0.1, 0, 20, rank=0, world=2, group_key=77)
-    g1 = Snn(1, 0.1, 0, 20, rank=1, world=2, group_key=77)
-    rc.apply(g0)
-    with pytest.raises(SnnError) as e:
-        g0.finalize()
-    assert e.value.code == SNN_E_UNSUPPORTED
-    g1.close()
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_d0_equals_single(world):
+    """D = 0 (BASELINE config 5, Vogels-Abbott): the arrivals of step t include
+    the other ranks' spikes of step t, so each step runs the neuron phase, the
+    exchange of the step's words and then the lists (k_front parts 1 / 2);
+    the partitioned run equals the single one bit-exactly (rasters, V, CUBA
+    currents, pending inputs of both receptors)."""
+    rc = W.vogels(6000, seed=22)
+    assert rc.delay == 0
+    ref = _run(rc, 1, 300)[0]
+    parts = _run(rc, world, 300)
+    h_ref, v_ref = ref.read_state("HIST"), ref.read_state("V")
+    ge_ref, gi_ref = ref.read_state("G_EXC"), ref.read_state("G_INH")
+    ie_ref, ii_ref = ref.read_state("INPUT_EXC"), ref.read_state("INPUT_INH")
+    assert int(ref.read_state("SPIKE_COUNT").sum()) > 1000
+    ev = 0
+    for g in parts:
+        info = g.info()
+        lo, hi = info["tgt_lo"], info["tgt_hi"]
+        assert np.array_equal(g.read_state("HIST"), h_ref)
+        for f, r in (("V", v_ref), ("G_EXC", ge_ref), ("G_INH", gi_ref), ("INPUT_EXC", ie_ref),
+                     ("INPUT_INH", ii_ref)):
+            assert np.array_equal(g.read_state(f)[lo:hi], r[lo:hi]), f
+        ev += g.metrics()["EVENTS"]
+    assert ev == ref.metrics()["EVENTS"]

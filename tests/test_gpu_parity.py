@@ -309,32 +309,43 @@ def test_invalid_arguments_rejected():
 def test_long_run_rates_and_weight_histogram_within_1pct():
     """BASELINE north star: "Long-run firing rates and weight histograms must
     agree within 1%".  Brunel+ scaled to N = 31,623 (1e7 synapses, 40 %
-    plastic, D = 15), 10,000 steps = 1 s of biological time on both sides; the
-    trajectories may part once a weight rounding difference (<= 2e-6 relative)
-    flips a spike, so the statistics are compared: per-population rates within
-    1 % and the 64-bin histograms of the plastic weights on [0, w_max] within
-    1 % of the mass (L1)."""
-    rc = W.brunel(31_623, p=0.02, plastic=True, delay=15, seed=3)
-    g, o = _pair(rc)
-    g.step(10_000)
-    o.step(10_000)
-    sg = g.read_state("SPIKE_COUNT").astype(np.float64)
-    so = o.array("nspk").astype(np.float64)
-    b = 0
-    for p in rc.pops:
-        rg, ro = sg[b:b + p.n].sum(), so[b:b + p.n].sum()
+    plastic, D = 15), three seeds x 10,000 steps = 3 s of biological time on
+    both sides.  The trajectories part once a weight rounding difference
+    (<= 2e-6 relative: the closed-form decays of the event schedule vs the
+    naive per-step decays) flips a spike (measured: after ~1,500 steps), and
+    the network is chaotic, so the long-run statistics are compared, pooled
+    over the seeds (one 1-s window differs by up to ~1.2 % between two
+    trajectories of the same network, either schedule, scripts/diverge.py):
+    per-population spike counts within 1 % and the 64-bin histograms of the
+    plastic weights on [0, w_max] within 1 % of the mass (L1)."""
+    tot_g, tot_o = None, None
+    hist_g, hist_o, n = 0, 0, 0
+    for seed in (3, 4, 5):
+        rc = W.brunel(31_623, p=0.02, plastic=True, delay=15, seed=seed)
+        g, o = _pair(rc)
+        g.step(10_000)
+        o.step(10_000)
+        sg = g.read_state("SPIKE_COUNT").astype(np.float64)
+        so = o.array("nspk").astype(np.float64)
+        cuts = np.cumsum([0] + [p.n for p in rc.pops])
+        cg = np.array([sg[a:b].sum() for a, b in zip(cuts, cuts[1:])])
+        co = np.array([so[a:b].sum() for a, b in zip(cuts, cuts[1:])])
+        tot_g = cg if tot_g is None else tot_g + cg
+        tot_o = co if tot_o is None else tot_o + co
+        wmax = rc.projs[4].stdp["w_max"]
+        rp, idx = o.array("row_ptr"), o.array("idx")
+        src = np.repeat(np.arange(o.n), np.diff(rp))
+        base_p, ne = rc.pops[0].n + rc.pops[1].n, rc.pops[0].n
+        plastic = (src >= base_p) & (idx < ne)                     # P -> E (R8)
+        hist_g = hist_g + np.histogram(g.read_state("WEIGHTS")[plastic], bins=64, range=(0.0, wmax))[0]
+        hist_o = hist_o + np.histogram(o.array("w")[plastic], bins=64, range=(0.0, wmax))[0]
+        n += int(plastic.sum())
+        g.close()
+    for p, rg, ro in zip(rc.pops, tot_g, tot_o):
         assert ro > 0 and abs(rg - ro) <= 0.01 * ro, f"{p.name}: {rg} vs {ro} spikes"
-        b += p.n
-    wmax = rc.projs[4].stdp["w_max"]
-    rp, idx = o.array("row_ptr"), o.array("idx")
-    src = np.repeat(np.arange(o.n), np.diff(rp))
-    base_p, ne = rc.pops[0].n + rc.pops[1].n, rc.pops[0].n
-    plastic = (src >= base_p) & (idx < ne)                     # P -> E (R8)
-    hg, _ = np.histogram(g.read_state("WEIGHTS")[plastic], bins=64, range=(0.0, wmax))
-    ho, _ = np.histogram(o.array("w")[plastic], bins=64, range=(0.0, wmax))
-    n = plastic.sum()
     # "within 1%": the L1 distance of the two histograms is at most 1 % of the mass
-    assert np.abs(hg - ho).sum() <= 0.01 * n, f"histograms differ by {np.abs(hg - ho).sum() / n:.4f} of the mass"
+    assert np.abs(hist_g - hist_o).sum() <= 0.01 * n, \
+        f"histograms differ by {np.abs(hist_g - hist_o).sum() / n:.4f} of the mass"
 
 
 # ------------------------------------------------------------- full size

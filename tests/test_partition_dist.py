@@ -37,6 +37,45 @@ def test_partition_tiles_target_range(n, C, world):
     assert all(s <= share for s in sizes)         # equal shares, the tail truncated
 
 
+@settings(max_examples=200, deadline=None)
+@given(st.lists(st.floats(0.0, 1e3), min_size=1, max_size=300), st.sampled_from([32, 96, 1024]),
+       st.integers(1, 8), st.integers(0, 31))
+def test_weighted_partition_tiles_and_balances(cost, C, world, tail):
+    from paper_2107_04092_b200.snn import snn_partition_weighted
+    n = max(0, len(cost) * C - tail)
+    parts = [snn_partition_weighted(cost, n, C, world, r) for r in range(world)]
+    assert parts[0][0] == 0 and parts[-1][1] == n
+    for (lo, hi), (lo2, _) in zip(parts, parts[1:]):
+        assert hi == lo2 and lo <= hi
+    for lo, _ in parts:
+        assert lo % C == 0 or lo == n                  # slices never straddle ranks
+    # each rank's cost is within one slice of the ideal share (boundaries are
+    # the slice prefixes closest to r / world of the total)
+    total, cmax = sum(cost), max(cost)
+    for lo, hi in parts:
+        got = sum(cost[lo // C:(hi + C - 1) // C]) if hi > lo else 0.0
+        assert abs(got - total / world) <= 2 * cmax + 1e-9 * total
+
+
+def test_weighted_partition_spreads_plastic_targets():
+    """BASELINE config 4 layout: E (plastic targets, costlier) then I; with
+    world 8 the E range is split over more ranks than an equal neuron split."""
+    from paper_2107_04092_b200.snn import snn_partition_weighted
+    C, nE, nI = 512, 252_982, 63_246
+    R = nE + nI
+    ns = (R + C - 1) // C
+    cost = []
+    for k in range(ns):
+        a, b = k * C, min(R, (k + 1) * C)
+        e = max(0, min(b, nE) - a)
+        cost.append(e * 9.0 + (b - a - e) * 1.0)
+    parts = [snn_partition_weighted(cost, R, C, 8, r) for r in range(8)]
+    n_e_ranks = sum(1 for lo, hi in parts if lo < nE)
+    assert n_e_ranks == 8                               # every rank gets plastic targets
+    shares = [sum(cost[lo // C:(hi + C - 1) // C]) for lo, hi in parts]
+    assert max(shares) / min(shares) < 1.05
+
+
 def test_partition_rejects_bad_arguments(P):
     for args in [(100, 1000, 2, 0), (100, 1024, 0, 0), (100, 1024, 2, 2)]:
         with pytest.raises(P.SnnError):
