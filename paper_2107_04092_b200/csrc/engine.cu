@@ -112,6 +112,7 @@ struct snn_sim {
     uint32_t N = 0;
     int64_t nsyn = 0;
     int64_t t = 0;  // steps enqueued so far
+    int64_t readout_t = -1;              // the step of the last read-out flush (R11)
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     // the ahead step: k_front(t) builds the arrival list
     // of t+1, k_deliver(t) runs the plastic arrivals' STDP, k_flush(t) the
@@ -968,7 +969,8 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
 // Read-out flush (R11): finalise pending row visits and bring every stale
 // plastic row up to t_last without a pre spike.
 static snn_status readout_flush(snn_sim *sim) {
-    if (!sim->plastic || sim->t == 0) return SNN_OK;
+    if (!sim->plastic || sim->t == 0 || sim->readout_t == sim->t) return SNN_OK;   // (already flushed at t)
+    sim->readout_t = sim->t;
     CK(launch_readout(sim->net, sim->st, sim->t - 1, sim->stdp_grid, sim->pp_lo, sim->pp_hi, sim->stream, sim->ahead));
     return SNN_OK;
 }

@@ -349,18 +349,23 @@ def test_long_run_rates_and_weight_histogram_within_1pct():
 
 
 # ------------------------------------------------------------- full size
-def test_full_size_cfg3_sampled_against_oracle():
-    """BASELINE config 3 at full size (316,228 neurons, 1.0e9 synapses, 40 %
-    plastic, D = 15), in the launch configuration bench.py times (captured-graph
-    replay, PDL, C = 1024, H = 64): sampled outputs the oracle computes one by
-    one -- 48 rows and their pivots bit-exact; after 130 steps (forced flushes
-    at t = 63 and 127) the pending input of 64 sampled targets bit-exact
-    against the row-wise sum of the step's arrivals (Fig. 3a), 300 sampled
-    plastic synapses within 1e-4 of the naive oracle replayed on their own
-    spike trains, and the event count equal to the out-degrees of all
-    arrivals."""
+@pytest.mark.parametrize("cfg", [3, 4, 5, "4x"])
+def test_full_size_sampled_against_oracle(cfg):
+    """BASELINE configs 3 (Brunel+, 316,228 neurons, 1.0e9 synapses), 4
+    (Brunel+, 632,456 neurons, 4.0e9 synapses: CSR offsets beyond 2^31) and 5
+    (Vogels-Abbott, 316,228 neurons, 2.0e9 synapses, D = 0, two receptors) at
+    full size, and "4x" = Brunel+ at 700,000 neurons (4.9e9 synapses: CSR
+    offsets beyond 2^32), in the launch configuration bench.py times (captured-graph
+    replay, the ahead step where it applies, C auto, H = 64), read back by
+    ranges (snn_read_state_range): sampled outputs the oracle computes one by
+    one -- 32 rows and their pivots bit-exact; after 130 steps (forced flushes
+    at t = 63 and 127) the pending input of 48 sampled targets (both receptors)
+    bit-exact against the row-wise sum of the step's arrivals (Fig. 3a), the
+    event count equal to the out-degrees of all arrivals, and (Brunel+) 200
+    sampled plastic synapses within 1e-4 of the naive oracle replayed on
+    their own spike trains."""
     from paper_2107_04092_b200 import Snn
-    rc = W.config(3)
+    rc = W.brunel(700_000, plastic=True, seed=1) if cfg == "4x" else W.config(cfg)
     g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits)
     rc.apply(g)
     g.finalize()
@@ -368,15 +373,19 @@ def test_full_size_cfg3_sampled_against_oracle():
     rc.apply(o)
     info = g.info()
     N, C, ns, R = info["N"], info["C"], info["nslices"], info["R"]
-    assert info["S"] > 0.99e9
+    assert info["S"] > {3: 0.99e9, 4: 3.99e9, 5: 1.99e9, "4x": 4.8e9}[cfg]
     rp = g.read_state("ROW_PTR")
-    idx = g.read_state("IDX")
-    piv = g.read_state("PIVOTS").reshape(N, ns + 1)
-    rng = np.random.default_rng(0)
-    for i in rng.choice(N, 48, replace=False):
+    assert int(rp[-1]) > {3: 2 ** 29, 4: 2 ** 31, 5: 2 ** 30, "4x": 2 ** 32}[cfg]
+
+    def row(i, field="IDX"):
+        return g.read_range(field, int(rp[i]), int(rp[i + 1] - rp[i]))
+
+    rng = np.random.default_rng(7 if cfg == "4x" else cfg)
+    for i in rng.choice(N, 32, replace=False):
         ref = o.build_row(int(i))
-        assert np.array_equal(idx[rp[i]:rp[i + 1]], ref), f"row {i}"
-        assert np.array_equal(piv[i].astype(np.int64), O.pivots(ref, 0, C, ns)), f"pivots of row {i}"
+        assert np.array_equal(row(i), ref), f"row {i}"
+        piv = g.read_range("PIVOTS", int(i) * (ns + 1), ns + 1)
+        assert np.array_equal(piv.astype(np.int64), O.pivots(ref, 0, C, ns)), f"pivots of row {i}"
     T, D = 130, rc.delay
     raster = np.zeros((T, N), dtype=np.uint8)
     done = 0
@@ -387,37 +396,45 @@ def test_full_size_cfg3_sampled_against_oracle():
         for tt in range(done, done + n):
             raster[tt] = np.unpackbits(ring[tt % 64].view(np.uint8), bitorder="little")[:N]
         done += n
-    pending = g.read_state("INPUT_EXC")
-    w = g.read_state("WEIGHTS")          # read-out flush (R11): the naive state
+    assert raster.sum() > 1000
+    pend = [g.read_state("INPUT_EXC"), g.read_state("INPUT_INH")]
     # events: every arrival (spike of t - D) delivers its whole row (R24)
     outdeg = np.diff(rp)
     ev = sum(int(outdeg[np.flatnonzero(raster[t - D])].sum()) for t in range(D, T))
     assert g.metrics()["EVENTS"] == ev
-    # pending input of step T - 1 = sum over its arrivals of q(w) (fixed point, R18)
+    # pending input of step T - 1 = sum over its arrivals of q(w) (fixed point,
+    # R18), into the receptor of the source population
+    cuts = np.cumsum([0] + [p.n for p in rc.pops])
+    rcpt = {(pr.src, pr.dst): pr.receptor for pr in rc.projs}
     arrivals = np.flatnonzero(raster[T - 1 - D])
-    for j in rng.choice(R, 64, replace=False):
-        tot = 0
-        for a in arrivals:
-            row = idx[rp[a]:rp[a + 1]]
-            k = np.searchsorted(row, j)
-            if k < len(row) and row[k] == j:
-                tot += int(np.rint(np.float64(w[rp[a] + k]) * 2.0 ** rc.frac_bits))
-        assert pending[j] == tot, f"target {j}: {pending[j]} vs {tot}"
+    rows = {int(a): (row(a), row(a, "WEIGHTS")) for a in arrivals}     # (WEIGHTS: read-out flush, R11)
+    for j in rng.choice(R, 48, replace=False):
+        dpop = int(np.searchsorted(cuts, j, side="right") - 1)
+        tot = [0, 0]
+        for a, (ids, ws) in rows.items():
+            k = np.searchsorted(ids, j)
+            if k < len(ids) and ids[k] == j:
+                spop = int(np.searchsorted(cuts, a, side="right") - 1)
+                tot[rcpt[(spop, dpop)]] += int(np.rint(np.float64(ws[k]) * 2.0 ** rc.frac_bits))
+        for r in (0, 1):
+            assert pend[r][j] == tot[r], f"target {j} receptor {r}: {pend[r][j]} vs {tot[r]}"
+    if not rc.plastic:
+        return
     # plastic synapses P -> E against the naive oracle on their own spike trains
     ne, base_p = rc.pops[0].n, rc.pops[0].n + rc.pops[1].n
     wmax = rc.projs[4].stdp["w_max"]
     pre = np.zeros_like(raster)
     pre[D:] = raster[:T - D]
     checked = 0
-    for i in rng.choice(np.arange(base_p, N), 60, replace=False):
-        b = rp[i]
-        plen = int(np.searchsorted(idx[b:rp[i + 1]], ne))     # the plastic (E) prefix of the row
+    for i in rng.choice(np.arange(base_p, N), 40, replace=False):
+        ids, ws = row(i), row(i, "WEIGHTS")
+        plen = int(np.searchsorted(ids, ne))                   # the plastic (E) prefix of the row
         for c in rng.choice(plen, 5, replace=False):
-            j = idx[b + c]
+            j = ids[c]
             ref = o.synapse_replay(2, 0, pre[:, i], raster[:, j])
-            assert abs(float(w[b + c]) - ref) <= 1e-4 * max(abs(ref), 1e-2 * wmax), (i, j, w[b + c], ref)
+            assert abs(float(ws[c]) - ref) <= 1e-4 * max(abs(ref), 1e-2 * wmax), (i, j, ws[c], ref)
             checked += 1
-    assert checked == 300
+    assert checked == 200
 
 
 def _dense_recipe(n_p, n_e, p, delay, seed):
