@@ -128,6 +128,7 @@ struct StateDev {
     // four buffers by step (buffer t & 3 at + (t & 3) * fstride / rstride): k_flush(t) reads step t's
     // while k_front(t+1), k_front(t+2) write theirs
     float *fpot;             // post-plastic j with spikes in its H-bit window: sum of D+[H - s] over them
+                             // (buffers 0-3), and of D+[H - 1 - s] over those with s <= H - 2 (4-7)
     uint8_t *fpos;           // post-plastic j: 0xfe no spike in its H-bit window, 0xff several, else the bit of the only one
     uint32_t fstride;        // elements per fpos / fpot buffer
     uint32_t rstride;        // words per `recent` buffer

@@ -459,7 +459,7 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.hist, uint64_t, N);
     ALLOC(st.hist_hi, uint64_t, cfg.history_bits > 64 ? N : 1);
     st.fstride = (N + 16 + 15) & ~15u;
-    ALLOC(st.fpot, float, 4ull * st.fstride);
+    ALLOC(st.fpot, float, 8ull * st.fstride);         // [4] fpot (age H) + [4] fpot1 (age H - 1) by t & 3
     ALLOC(st.fpos, uint8_t, 4ull * st.fstride);
     ALLOC(st.nspk, uint32_t, N);
     // exchange geometry: rank r owns words [rank_lo[r] / 32, ...), at most

@@ -205,24 +205,30 @@ k_front(NetDev net, StateDev st) {
                            : n1 > 1 ? (uint8_t)0xffu
                                     : (uint8_t)(h ? 63 - __clzll((long long)h) : 127 - __clzll((long long)hh));
             }
-            // potentiation factor of a forced flush (age H) for this target:
-            // fpot = sum over its spikes s in the window of D+[H - s], oldest
-            // first (k_stdp: w = min(w + A+ (x_pre fpot), w_max))
+            // potentiation factors of a forced flush for this target, oldest
+            // spike first (k_flush: w = min(w + A+ (x_pre f), w_max)): age H --
+            // fpot = sum over its spikes s in the window of D+[H - s]; age H - 1
+            // (flushed a step early) -- fpot1 = sum over s <= H - 2 of
+            // D+[H - 1 - s].  k_flush(t) runs beside k_front(t+1), so it reads
+            // these step-t buffers, never the live history words
             if (recent) {
                 const float *dpl = net.stdp[p.post_stdp].dplus;
                 const int H = (int)net.H;
-                float f = 0.0f;
+                float f = 0.0f, f1 = 0.0f;
                 for (uint64_t m = hh; m; ) {
                     const int b = 63 - __clzll((long long)m);
                     m &= ~(1ull << b);
                     f = __fadd_rn(f, dpl[H - 64 - b]);
+                    if (64 + b <= H - 2) f1 = __fadd_rn(f1, dpl[H - 1 - 64 - b]);
                 }
                 for (uint64_t m = h; m; ) {
                     const int b = 63 - __clzll((long long)m);
                     m &= ~(1ull << b);
                     f = __fadd_rn(f, dpl[H - b]);
+                    if (b <= H - 2) f1 = __fadd_rn(f1, dpl[H - 1 - b]);
                 }
                 st.fpot[(size_t)(t & 3) * st.fstride + i] = f;
+                st.fpot[(size_t)(4 + (t & 3)) * st.fstride + i] = f1;
             }
             const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
             st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
@@ -1371,6 +1377,7 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
     if (st.kspan) kspan_begin(st.kspan, t, 3, t_entry, t_entry);
     const uint8_t *__restrict__ fpos = st.fpos + (size_t)(t & 3) * st.fstride;
     const float *__restrict__ fpot = st.fpot + (size_t)(t & 3) * st.fstride;
+    const float *__restrict__ fpot1 = st.fpot + (size_t)(4 + (t & 3)) * st.fstride;
     const uint32_t f_lo = pp_lo & ~15u, wlo = ev_bm_lo(pp_lo);
     const uint32_t tab_bytes = fl_tab_bytes(pp_lo, pp_hi, kStaged);
     if (threadIdx.x == 0) {
@@ -1500,12 +1507,9 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
                         const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, lds_f32(dp + 4u * (age - pos)))));
                         w = nw < pr.z ? nw : pr.z;
                     } else if (pos == 0xffu) {
-                        if (age == H) {
-                            const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, __ldg(fpot + j))));
-                            w = nw < pr.z ? nw : pr.z;
-                        } else {
-                            w = flush_hist<kH128>(st.hist, st.hist_hi, j, w, xp, age, dp, pr);
-                        }
+                        // several spikes: the step's factor for age H or H - 1 (k_front)
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, __ldg((age == H ? fpot : fpot1) + j))));
+                        w = nw < pr.z ? nw : pr.z;
                     }
                     n_hit += pos != 0xfeu ? 1u : 0u;
                     if (__float_as_uint(w) != __float_as_uint(w0)) {
