@@ -8,6 +8,7 @@
 // counts whose exclusive prefix IS the pivot row -- an independent route to the
 // same table, so the two cross-check each other.
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "philox.cuh"
@@ -57,6 +58,175 @@ __device__ __forceinline__ void geo_row(const NetDev &net, const BuildTabs &tabs
             f(j, d);
         }
     }
+}
+
+// ---- warp-cooperative rows: the same draws as geo_row, a warp
+// per row.  Lane l of an iteration draws n = n0 + 4 l .. n0 + 4 l + 3 (one
+// Philox call, counter (i, n0 / 4 + l, 4, d)); the gap of a draw comes from
+// the inverse CDF, g - 1 = #{k in [1, kGapTab] : gap[k-1] > x}, estimated as
+// ceil(log(x 2^-32) / log(1 - p)) - 1 and corrected against the table (exact:
+// the table decides); a warp prefix sum of the gaps gives every draw's
+// candidate position.  Kept targets in [lo, hi) are passed, ascending, to
+// emit(lane's j[4], mask, rank of its first one among the row's kept targets,
+// d) once per iteration (every lane; uniform call).
+__device__ __forceinline__ uint32_t geo_gap_count(const uint32_t *__restrict__ tab, float inv_l2q, uint32_t x) {
+    // #{k in [1, kGapTab] : tab[k-1] > x} (tab non-increasing)
+    int k;
+    if (x == 0u) {
+        k = kGapTab;
+    } else {
+        const float e = __log2f((float)x) - 32.0f;          // log2(x 2^-32) < 0
+        const float ks = ceilf(e * inv_l2q) - 1.0f;         // inv_l2q = 1 / log2(1 - p) < 0
+        k = ks < 0.0f ? 0 : ks > (float)kGapTab ? kGapTab : (int)ks;
+    }
+    // correct: want tab[k-1] > x (or k == 0) and (k == kGapTab or tab[k] <= x)
+    int steps = 0;
+    while (k < kGapTab && __ldg(tab + k) > x && steps < 4) { k++; steps++; }
+    while (k > 0 && __ldg(tab + k - 1) <= x && steps < 4) { k--; steps++; }
+    if (steps >= 4) {                                         // (far off: x tiny) -- binary search
+        uint32_t lo = 0, up = kGapTab;
+        while (lo < up) {
+            const uint32_t mid = (lo + up) >> 1;
+            if (__ldg(tab + mid) > x) lo = mid + 1; else up = mid;
+        }
+        k = (int)lo;
+    }
+    return (uint32_t)k;
+}
+
+template <typename F>
+__device__ __forceinline__ void geo_row_warp(const NetDev &net, const BuildTabs &tabs, uint32_t i, int sp, uint32_t lo,
+                                             uint32_t hi, F &&emit) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t kept_before = 0;                         // kept synapses of the row so far
+    for (int d = 0; d < (int)net.npop; d++) {
+        const int slot = tabs.gap_slot[sp * kMaxPops + d];
+        if (slot < 0) continue;
+        const PopDev &dp = net.pop[d];
+        if (dp.base >= hi) break;
+        const uint32_t *tab = tabs.gap + (size_t)slot * kGapTab;
+        const float inv_l2q = tabs.inv_l2q[sp * kMaxPops + d];
+        const bool excl = !tabs.autapse[sp * kMaxPops + d] && i >= dp.base && i < dp.base + dp.n;
+        const uint32_t il = i - dp.base;
+        const int64_t M = (int64_t)dp.n - (excl ? 1 : 0);
+        int64_t c0 = -1;                              // candidate position of the last draw so far
+        for (uint32_t n0 = 0;; n0 += 128) {
+            const u32x4 r = philox4x32_10(i, (n0 >> 2) + lane, 4u, (uint32_t)d, net.key0, net.key1);
+            uint32_t g[4], keep = 0;
+            int64_t gs = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const uint32_t k = geo_gap_count(tab, inv_l2q, lane_of(r, (uint32_t)e));
+                const bool beyond = k == (uint32_t)kGapTab;   // advance kGapTab, keep nothing
+                g[e] = beyond ? (uint32_t)kGapTab : k + 1;
+                keep |= (beyond ? 0u : 1u) << e;
+                gs += g[e];
+            }
+            // warp exclusive prefix of the lanes' gap sums (64-bit: rows beyond 2^32 candidates never occur,
+            // but the sum of 128 gaps stays < 2^20)
+            uint32_t inc = (uint32_t)gs;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= (uint32_t)o) inc += y;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            int64_t c = c0 + (int64_t)(inc - (uint32_t)gs);
+            uint32_t jv[4], mask = 0;
+            bool stop = false;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                c += g[e];
+                jv[e] = 0;
+                if (c >= M) { stop = true; continue; }
+                if (!((keep >> e) & 1u)) continue;
+                const uint32_t jl = (uint32_t)c + ((excl && (uint32_t)c >= il) ? 1u : 0u);
+                const uint32_t j = dp.base + jl;
+                if (j >= hi) { stop = true; continue; }         // (and every later one: the row ends)
+                if (j < lo) continue;
+                jv[e] = j;
+                mask |= 1u << e;
+            }
+            // (a stop condition is monotone in n: every later draw is stopped too)
+            const uint32_t nk = __popc(mask);
+            uint32_t kin = nk;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, kin, o);
+                if (lane >= (uint32_t)o) kin += y;
+            }
+            emit(jv, mask, kept_before + kin - nk, d);
+            kept_before += __shfl_sync(0xffffffffu, kin, 31);
+            if (__any_sync(0xffffffffu, stop)) break;    // (a stop is monotone in n: every later draw stops too)
+            c0 += tot;
+        }
+    }
+}
+
+constexpr int kGeoWarpThreads = 256;   // 8 rows per CTA
+
+// Pass 1 (warp per row): the pivots directly -- piv[i][k] = #kept targets
+// below tgt_lo + kC (Fig. 1) -- and the row length.  Slices are
+// non-decreasing along the row, so a kept target at rank q in slice kj after
+// one in slice kp writes piv[k] = q for kp < k <= kj.
+__global__ void __launch_bounds__(kGeoWarpThreads)
+k_count_warp(NetDev net, BuildTabs tabs, uint32_t *piv, int64_t *len) {
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (i >= net.N) return;                           // (warp-uniform)
+    const int sp = find_pop(net, i);
+    uint32_t *prow = piv + (size_t)i * (net.nslices + 1);
+    int last = -1;                                    // slice of the row's last kept target so far (warp-uniform)
+    uint32_t total = 0;
+    geo_row_warp(net, tabs, i, sp, net.tgt_lo, net.tgt_hi, [&](const uint32_t (&jv)[4], uint32_t mask, uint32_t q0, int) {
+        // the lane's last kept slice, and the max over the lanes before it (slices ascend along the row)
+        int mine = -1;
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if ((mask >> e) & 1u) mine = (int)((jv[e] - net.tgt_lo) / net.C);
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl = max(incl, y);
+        }
+        int prev = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) prev = -1;
+        prev = max(prev, last);
+        uint32_t q = q0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            if (!((mask >> e) & 1u)) continue;
+            const int kj = (int)((jv[e] - net.tgt_lo) / net.C);
+            for (int k = prev + 1; k <= kj; k++) prow[k] = q;
+            prev = max(prev, kj);
+            q++;
+        }
+        last = max(last, __shfl_sync(0xffffffffu, incl, 31));
+        total = __shfl_sync(0xffffffffu, q, 31);          // (lane 31's q = the ranks so far)
+    });
+    // slices after the last kept target: the row length
+    for (int k = last + 1 + (int)lane; k <= (int)net.nslices; k += 32) prow[k] = total;
+    if (lane == 0) len[i] = total;
+}
+
+// Pass 3 (warp per row): targets (sorted by construction) and initial weights.
+__global__ void __launch_bounds__(kGeoWarpThreads)
+k_fill_warp(NetDev net, BuildTabs tabs, const int64_t *row_ptr, uint32_t *idx, float *w) {
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= net.N) return;
+    const int sp = find_pop(net, i);
+    const int64_t base = row_ptr[i];
+    geo_row_warp(net, tabs, i, sp, net.tgt_lo, net.tgt_hi, [&](const uint32_t (&jv)[4], uint32_t mask, uint32_t q0, int d) {
+        const float wd = tabs.weight[sp * kMaxPops + d];
+        uint32_t q = q0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            if (!((mask >> e) & 1u)) continue;
+            idx[base + q] = jv[e];
+            w[base + q] = wd;
+            q++;
+        }
+    });
 }
 
 // Pass 1: per (row, slice) counts -> piv[i][k+1]; piv[i][0] = 0 (thread per row;
@@ -177,19 +347,28 @@ __global__ void k_init_state(NetDev net, StateDev st) {
 }
 
 // ---------------------------------------------------------------- launchers
-cudaError_t build_count(const NetDev &net, const BuildTabs &tabs, uint32_t *piv, cudaStream_t s) {
-    k_count<<<(net.N + kGeoThreads - 1) / kGeoThreads, kGeoThreads, 0, s>>>(net, tabs, piv);
+// (SNN_BUILD_THREAD_PER_ROW: the round-1 thread-per-row builder, for comparison)
+static bool build_thread_per_row() { return getenv("SNN_BUILD_THREAD_PER_ROW") != nullptr; }
+
+cudaError_t build_count(const NetDev &net, const BuildTabs &tabs, uint32_t *piv, int64_t *len, cudaStream_t s) {
+    if (build_thread_per_row()) {
+        k_count<<<(net.N + kGeoThreads - 1) / kGeoThreads, kGeoThreads, 0, s>>>(net, tabs, piv);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        k_pivot_scan<<<(net.N * 32 + 255) / 256, 256, 0, s>>>(net, piv, len, net.N);
+    } else {
+        const uint32_t per = kGeoWarpThreads / 32;
+        k_count_warp<<<(net.N + per - 1) / per, kGeoWarpThreads, 0, s>>>(net, tabs, piv, len);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t build_scan(const NetDev &net, uint32_t *piv, int64_t *len, int64_t *row_ptr,
                        void *tmp, size_t *tmp_bytes, cudaStream_t s) {
+    (void)piv;
     if (tmp == nullptr) {
         return cub::DeviceScan::ExclusiveSum(nullptr, *tmp_bytes, len, row_ptr, (int)net.N + 1, s);
     }
-    k_pivot_scan<<<(net.N * 32 + 255) / 256, 256, 0, s>>>(net, piv, len, net.N);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
     // len[N] = 0 was set by the caller; row_ptr = exclusive scan over N+1 entries
     return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, len, row_ptr, (int)net.N + 1, s);
 }
@@ -197,7 +376,12 @@ cudaError_t build_scan(const NetDev &net, uint32_t *piv, int64_t *len, int64_t *
 cudaError_t build_fill(const NetDev &net, const BuildTabs &tabs, const uint32_t *piv,
                        const int64_t *row_ptr, uint32_t *idx, float *w, cudaStream_t s) {
     (void)piv;
-    k_fill<<<(net.N + kGeoThreads - 1) / kGeoThreads, kGeoThreads, 0, s>>>(net, tabs, row_ptr, idx, w);
+    if (build_thread_per_row()) {
+        k_fill<<<(net.N + kGeoThreads - 1) / kGeoThreads, kGeoThreads, 0, s>>>(net, tabs, row_ptr, idx, w);
+    } else {
+        const uint32_t per = kGeoWarpThreads / 32;
+        k_fill_warp<<<(net.N + per - 1) / per, kGeoWarpThreads, 0, s>>>(net, tabs, row_ptr, idx, w);
+    }
     return cudaGetLastError();
 }
 

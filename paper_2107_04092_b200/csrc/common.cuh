@@ -79,10 +79,14 @@ struct BuildTabs {
     uint8_t autapse[kMaxPops * kMaxPops];
     float weight[kMaxPops * kMaxPops];     // initial (final, caller-scaled) weight
     int16_t gap_slot[kMaxPops * kMaxPops]; // projection (src, dst) -> its gap table, -1 = none
+    float inv_l2q[kMaxPops * kMaxPops];    // 1 / log2(1 - p): the inverse-CDF estimate of a gap (warp builder)
     const uint32_t *gap;                   // [projections][kGapTab]: floor((1-p)^k 2^32), k = 1..kGapTab
 };
 
-constexpr int kFrontThreads = 1024;   // k_front CTA = one list region
+#ifndef SNN_FRONT_T
+#define SNN_FRONT_T 1024
+#endif
+constexpr int kFrontThreads = SNN_FRONT_T;   // k_front CTA = one list region
 
 struct Counters {
     int64_t t;               // next step to simulate

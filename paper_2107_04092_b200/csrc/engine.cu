@@ -21,7 +21,7 @@
 #include "common.cuh"
 
 namespace snn {
-cudaError_t build_count(const NetDev &, const BuildTabs &, uint32_t *, cudaStream_t);
+cudaError_t build_count(const NetDev &, const BuildTabs &, uint32_t *, int64_t *, cudaStream_t);
 cudaError_t build_scan(const NetDev &, uint32_t *, int64_t *, int64_t *, void *, size_t *, cudaStream_t);
 cudaError_t build_fill(const NetDev &, const BuildTabs &, const uint32_t *, const int64_t *, uint32_t *,
                        float *, cudaStream_t);
@@ -352,6 +352,7 @@ static snn_status finalize(snn_sim *sim) {
         tabs.autapse[hj.src * kMaxPops + hj.dst] = q.allow_autapses ? 1 : 0;
         tabs.weight[hj.src * kMaxPops + hj.dst] = q.weight;
         if (q.p > 0.0) {
+            tabs.inv_l2q[hj.src * kMaxPops + hj.dst] = q.p < 1.0 ? (float)(1.0 / std::log2(1.0 - q.p)) : -0.0f;
             tabs.gap_slot[hj.src * kMaxPops + hj.dst] = (int16_t)(gap_host.size() / kGapTab);
             for (int k = 1; k <= kGapTab; k++) {
                 const double v = std::floor(std::pow(1.0 - q.p, (double)k) * 4294967296.0);
@@ -533,7 +534,7 @@ static snn_status finalize(snn_sim *sim) {
     cudaEvent_t bev[4];
     for (auto &e : bev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(bev[0], s));
-    CK(build_count(net, tabs, st.piv, s));
+    CK(build_count(net, tabs, st.piv, len, s));
     size_t tmp_bytes = 0;
     CK(build_scan(net, st.piv, len, st.row_ptr, nullptr, &tmp_bytes, s));
     void *tmp = sim->dalloc(tmp_bytes);
