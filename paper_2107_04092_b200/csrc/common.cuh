@@ -96,7 +96,8 @@ struct Counters {
     uint32_t xticket;        // CTA-completion ticket of k_unpack (world > 1)
     int64_t tx;              // the step of the next NCCL exchange (k_unpack advances it)
     uint32_t ticket;         // CTA-completion ticket of the slice kernel
-    uint32_t pad;
+    uint32_t fr_ticket;      // CTA-completion ticket of k_front
+    int64_t tf;              // the step of the next k_front (its last CTA advances it)
     unsigned long long metric[16];
     alignas(16) uint32_t lst[8][4];      // by step t & 7: list lengths (plastic arrivals, arrivals, forced flushes, 0);
                              // several slots: the forced flushes of step t are read by k_flush(t), which runs
@@ -159,6 +160,7 @@ struct StateDev {
     uint32_t *sendbuf;       // [wmax] this rank's spike words of the step (world > 1)
     uint32_t *gath;          // [2][world][wmax] all ranks' words (NCCL: slot 0; local group: by step parity)
     Counters *ctr;
+    uint32_t *slice_ticket;  // [nslices] CTA-completion tickets of a slice's splits (the fused step's epilogue)
     const StdpDev *stdp;     // device copy of NetDev::stdp (coalesced table loads into shared memory)
     unsigned long long *trace;   // optional (SNN_FLAG_TRACE): per-CTA phase timestamps
     struct KSpan *kspan;         // optional (SNN_FLAG_KTIME): per-step kernel spans, [slot][kernel]

@@ -29,7 +29,7 @@ cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, ui
 cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
 cudaError_t build_idx16(const NetDev &, const uint32_t *, uint16_t *, int64_t, cudaStream_t);
 uint32_t front_blocks(const NetDev &);
-cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool, bool, int);
+cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool, bool, int, bool);
 size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
 size_t deliver_smem_bytes(const NetDev &, bool);
 cudaError_t kernels_configure(int);
@@ -41,7 +41,7 @@ uint32_t flush_ctas_per_sm();
 void set_launch_priority(int);
 size_t ev_smem_bytes(uint32_t, uint32_t);
 size_t flush_smem_bytes(uint32_t, uint32_t);
-cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool, bool);
+cudaError_t launch_deliver(const NetDev &, const StateDev &, uint32_t, cudaStream_t, bool, bool, bool);
 cudaError_t launch_readout(const NetDev &, const StateDev &, int64_t, uint32_t, uint32_t, uint32_t, cudaStream_t, bool);
 cudaError_t launch_hist_from_ring(const NetDev &, const uint32_t *, int64_t, uint64_t *, cudaStream_t);
 cudaError_t launch_unpack(const NetDev &, const StateDev &, const uint32_t *, int64_t, cudaStream_t);
@@ -118,6 +118,12 @@ struct snn_sim {
     // of t+1, k_deliver(t) runs the plastic arrivals' STDP, k_flush(t) the
     // forced flushes after it
     bool ahead = false;
+    // the fused step (captured graphs of the ahead step, world 1): k_deliver(t)'s
+    // epilogue updates the neurons of t + 1; k_front(t+1) (neurons >= R, lists)
+    // and k_flush on branches -- DESIGN.md section 2
+    bool fused = false;
+    cudaStream_t cap_front = nullptr;
+    cudaEvent_t ev_fr[2] = {nullptr, nullptr}, ev_del[2] = {nullptr, nullptr}, ev_fl_f[2] = {nullptr, nullptr};
     uint32_t flush_grid = 1, flush_grid_side = 1;   // k_flush CTAs: serial step / side branch
     // step graph (SNN_PIPE, experiments): 0 serial; 1 ahead + k_flush(t) on a
     // side branch joined before k_deliver(t + fl_lag); 2 no ahead list, k_stdp_arr
@@ -617,6 +623,31 @@ static snn_status finalize(snn_sim *sim) {
     if (sim->pipe == 1 && !sim->ahead) sim->pipe = 0;
     if (!sim->plastic || !sim->ev_kernel || flush_smem_bytes(sim->pp_lo, sim->pp_hi) > 227 * 1024)
         if (sim->pipe == 2) sim->pipe = 0;
+    // the fused step: the ahead step on one rank (the epilogue writes the ring
+    // words of [0, R) and of the Poisson neurons sharing R's word)
+    {
+        bool straddle_ok = (net.R & 31u) == 0 || net.R >= net.N;
+        for (uint32_t k = 0; k < net.npop && !straddle_ok; k++) {
+            const PopDev &pp = net.pop[k];
+            if (pp.base <= net.R && net.R < pp.base + pp.n)
+                straddle_ok = pp.kind == POP_POISSON && pp.base + pp.n >= std::min((net.R + 31u) & ~31u, net.N);
+        }
+        // (opt-in, SNN_FUSE: measured slower on cfg3, 50.8 vs 42.8 us/step -- one CTA per
+        // slice runs the slice's neuron update in k_deliver's tail)
+        sim->fused = sim->ahead && cfg.world == 1 && straddle_ok && getenv("SNN_FUSE") && sim->pipe != 2;
+        if (sim->fused) sim->pipe = 0;     // (the fused graph has its own branches)
+    }
+    ALLOC(st.slice_ticket, uint32_t, std::max(1u, net.nslices));
+    CK(cudaMemsetAsync(st.slice_ticket, 0, 4ull * std::max(1u, net.nslices), s));
+    if (sim->fused) {
+        CK(cudaStreamCreateWithFlags(&sim->cap_front, cudaStreamNonBlocking));
+        for (int q = 0; q < 2; q++) {
+            CK(cudaEventCreateWithFlags(&sim->ev_fr[q], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&sim->ev_del[q], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&sim->ev_fl_f[q], cudaEventDisableTiming));
+        }
+        if (sim->plastic && !sim->cap_side) CK(cudaStreamCreateWithFlags(&sim->cap_side, cudaStreamNonBlocking));
+    }
     if (cfg.world > 1 && net.D >= 1 && cfg.nccl_unique_id && !getenv("SNN_NO_XBRANCH")) {
         CK(cudaStreamCreateWithFlags(&sim->cap_xside, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&sim->ev_xfront, cudaEventDisableTiming));
@@ -669,7 +700,7 @@ static snn_status local_group_front_d0(snn_sim *sim, cudaStream_t s, int64_t t) 
     for (snn_sim *p : peers) {
         if (p->state == 0 || !p->st.gath) return sim->fail(SNN_E_STATE, "local group peer not finalized");
         if (p->t != sim->t) return sim->fail(SNN_E_STATE, "local group ranks must be stepped in lockstep");
-        CK(launch_front(p->net, p->st, s, false, false, 1));
+        CK(launch_front(p->net, p->st, s, false, false, 1, false));
     }
     for (snn_sim *q : peers)
         for (snn_sim *p : peers)
@@ -707,15 +738,15 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
                 if (r != SNN_OK) return r;
             }
         } else {
-            CK(launch_front(net, st, s, false, false, 1));
+            CK(launch_front(net, st, s, false, false, 1, false));
             snn_status r = exchange_enqueue(sim, s, t);
             if (r != SNN_OK) return r;
         }
-        CK(launch_front(net, st, s, false, false, 2));
+        CK(launch_front(net, st, s, false, false, 2, false));
     } else {
         const bool xbranch = multi && side && sim->cap_xside && !sim->local_group;
         if (xbranch && gk > 0) CK(cudaStreamWaitEvent(s, sim->ev_xdone, 0));   // the exchange of t-1
-        CK(launch_front(net, st, s, pdl && !first, sim->ahead, 0)); // (1) P:36 + work lists
+        CK(launch_front(net, st, s, pdl && !first, sim->ahead, 0, sim->fused)); // (1) P:36 + work lists
         if (xbranch) {                                              // spike words of t -> peers, beside the step
             CK(cudaEventRecord(sim->ev_xfront, s));
             CK(cudaStreamWaitEvent(sim->cap_xside, sim->ev_xfront, 0));
@@ -755,7 +786,7 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     }
     if (ev) CK(cudaEventRecord(ev[2], s));
     if (net.deliv_mode == SNN_DELIV_ROWWISE) CK(launch_deliver_rowwise(net, st, sim->stdp_grid, s, pdl));   // Fig. 3a
-    else CK(launch_deliver(net, st, sim->splits, s, pdl, sim->ahead));   // (3) P:41, Fig. 3b
+    else CK(launch_deliver(net, st, sim->splits, s, pdl, sim->ahead, false));   // (3) P:41, Fig. 3b
     if (sim->plastic && (sim->ahead || sim->pipe == 2) && !(side && sim->cap_side && sim->pipe != 0))   // (2') flushes of t (R3)
         CK(launch_stdp_ev(net, st, sim->flush_grid, sim->pp_lo, sim->pp_hi, s, pdl, 2));
     if (sim->use_prio) set_launch_priority(0);
@@ -764,7 +795,76 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     return SNN_OK;
 }
 
+// The fused step graph of n steps t0 .. t0 + n - 1:
+//   main   : k_front(t0) (all neurons), then k_deliver(t) for every t, the
+//            epilogue (neurons of t + 1) on all but the last
+//   branch F: k_front(t) for t > t0 (neurons >= R, lists), after k_deliver(t-1)
+//   branch X: k_flush(t) after the front of t; k_deliver(t+2) waits for it
+// k_deliver(t) waits for the front of t-1 (its arrival list) -- so the critical
+// path is one kernel per step; state between two calls is the unfused one.
+static snn_status capture_fused(snn_sim *sim, uint32_t n, cudaGraphExec_t *out) {
+    cudaGraph_t g = nullptr;
+    const NetDev &net = sim->net;
+    const StateDev &st = sim->st;
+    cudaStream_t m = sim->cap_stream, F = sim->cap_front, X = sim->cap_side;
+    const bool pl = sim->plastic;
+    CK(cudaStreamBeginCapture(m, cudaStreamCaptureModeThreadLocal));
+    auto fail = [&](snn_status r) {
+        cudaStreamEndCapture(m, &g);
+        if (g) cudaGraphDestroy(g);
+        return r;
+    };
+#define CKF(call)                                                                                     \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess)                                                                        \
+            return fail(sim->fail(SNN_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                  __FILE__, __LINE__));                                               \
+    } while (0)
+    const bool dbg_serial = getenv("SNN_FUSE_SERIAL") != nullptr;   // (debug: k_front(t) after k_deliver(t))
+    for (uint32_t k = 0; k < n; k++) {
+        if (k > 0 && !dbg_serial) {                                   // F: the front of t0 + k
+            CKF(cudaStreamWaitEvent(F, sim->ev_del[(k - 1) & 1], 0));
+            CKF(launch_front(net, st, F, false, true, 3, true));
+            CKF(cudaEventRecord(sim->ev_fr[k & 1], F));
+        }
+        if (k > 0 && dbg_serial) {
+            CKF(launch_front(net, st, m, false, true, 3, true));
+            CKF(cudaEventRecord(sim->ev_fr[k & 1], m));
+        }
+        // main: [k_front(t0)] k_deliver(t0 + k)
+        if (k == 0) {
+            CKF(launch_front(net, st, m, false, true, 0, true));
+            CKF(cudaEventRecord(sim->ev_fr[0], m));
+        } else if (k >= 2) {
+            CKF(cudaStreamWaitEvent(m, sim->ev_fr[(k - 1) & 1], 0));  // the arrival list of t (front of t-1)
+        } else {
+            CKF(cudaStreamWaitEvent(m, sim->ev_fr[0], 0));
+        }
+        if (pl && k >= 2) CKF(cudaStreamWaitEvent(m, sim->ev_fl_f[k & 1], 0));   // k_flush(t-2)
+        // (PDL only behind the first front: with the joins of the branches, stream
+        // capture makes every incoming edge programmatic, and k_deliver(t) reads
+        // the arrival list of the front of t-1 before its dependency wait)
+        CKF(launch_deliver(net, st, sim->splits, m, k == 0, true, k + 1 < n));
+        CKF(cudaEventRecord(sim->ev_del[k & 1], m));
+        if (pl) {                                                     // X: the forced flushes of t0 + k
+            CKF(cudaStreamWaitEvent(X, sim->ev_fr[k & 1], 0));
+            CKF(launch_stdp_ev(net, st, sim->flush_grid_side, sim->pp_lo, sim->pp_hi, X, false, 2));
+            CKF(cudaEventRecord(sim->ev_fl_f[k & 1], X));
+        }
+    }
+    if (n > 1) CKF(cudaStreamWaitEvent(m, sim->ev_fr[(n - 1) & 1], 0));   // join the branches
+    if (pl)
+        for (uint32_t k = n > 2 ? n - 2 : 0; k < n; k++) CKF(cudaStreamWaitEvent(m, sim->ev_fl_f[k & 1], 0));
+#undef CKF
+    CK(cudaStreamEndCapture(m, &g));
+    CK(cudaGraphInstantiate(out, g, 0));
+    CK(cudaGraphDestroy(g));
+    return SNN_OK;
+}
+
 static snn_status capture(snn_sim *sim, uint32_t nsteps, cudaGraphExec_t *out) {
+    if (sim->fused) return capture_fused(sim, nsteps, out);
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(sim->cap_stream, cudaStreamCaptureModeThreadLocal));
     for (uint32_t k = 0; k < nsteps; k++) {
@@ -1242,6 +1342,12 @@ void snn_destroy(snn_sim *sim) {
     if (sim->cap_stream) cudaStreamDestroy(sim->cap_stream);
     if (sim->cap_side) cudaStreamDestroy(sim->cap_side);
     if (sim->cap_xside) cudaStreamDestroy(sim->cap_xside);
+    if (sim->cap_front) cudaStreamDestroy(sim->cap_front);
+    for (int q = 0; q < 2; q++) {
+        if (sim->ev_fr[q]) cudaEventDestroy(sim->ev_fr[q]);
+        if (sim->ev_del[q]) cudaEventDestroy(sim->ev_del[q]);
+        if (sim->ev_fl_f[q]) cudaEventDestroy(sim->ev_fl_f[q]);
+    }
     if (sim->ev_xfront) cudaEventDestroy(sim->ev_xfront);
     if (sim->ev_xdone) cudaEventDestroy(sim->ev_xdone);
     if (sim->ev_front) cudaEventDestroy(sim->ev_front);

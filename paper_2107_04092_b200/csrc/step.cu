@@ -110,19 +110,133 @@ __device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *len_a, uint32_t
 // ------------------------------------------------------------------ k_front
 // One thread per neuron i (it also owns source row i); warps cover 32
 // consecutive ids = one ring word.  P:36 "Update neurons, note which ones fire".
+// One neuron's update at step t (App. B op order, "Update neurons, note
+// which ones fire"): Poisson draw or Euler LIF step (consuming the fixed-point
+// input delivered at t-1), then for post-synaptic STDP targets the history
+// push, the window's spike position / flush factors (buffers t & 3) and
+// the x_post trace.  Returns `fired`; `recent`: a spike in the last H steps.
+// Shared by k_front and k_deliver's epilogue (the fused step), so both compute
+// exactly the same operations.
+__device__ __forceinline__ bool neuron_update(const NetDev &net, const StateDev &st, uint32_t i, const PopDev &p,
+                                              int64_t t, bool &recent) {
+    bool fired = false;
+    recent = false;
+    if (p.kind == POP_POISSON) {
+        const u32x4 r = philox4x32_10(i, (uint32_t)t, 2u, 0u, net.key0, net.key1);
+        fired = (uint64_t)r.x < p.thr;
+    } else if (p.kind == POP_LIF_DELTA) {
+        const int32_t q = st.in_e[i];
+        const float I = __fmul_rn(__int2float_rn(q), net.inv_scale);
+        if (q != 0) st.in_e[i] = 0;
+        int32_t ref = st.ref[i];
+        float V = st.V[i];
+        const float V0 = V;
+        const int32_t ref0 = ref;
+        if (ref > 0) ref--;
+        else V = __fadd_rn(__fmul_rn(V, p.k_m), I);
+        if (ref == 0 && V >= p.v_th) {
+            fired = true;
+            V = p.v_reset;
+            ref = p.n_ref;
+        }
+        if (__float_as_uint(V) != __float_as_uint(V0)) st.V[i] = V;
+        if (ref != ref0) st.ref[i] = ref;
+    } else {  // POP_LIF_CUBA
+        const int32_t qe = st.in_e[i], qi = st.in_i[i];
+        float ge = __fadd_rn(st.ge[i], __fmul_rn(__int2float_rn(qe), net.inv_scale));
+        float gi = __fadd_rn(st.gi[i], __fmul_rn(__int2float_rn(qi), net.inv_scale));
+        if (qe != 0) st.in_e[i] = 0;
+        if (qi != 0) st.in_i[i] = 0;
+        int32_t ref = st.ref[i];
+        const int32_t ref0 = ref;
+        float V = st.V[i];
+        if (ref > 0) {
+            ref--;
+        } else {
+            const float t1 = __fsub_rn(p.v_rest, V);
+            const float t2 = __fadd_rn(t1, ge);
+            const float t3 = __fadd_rn(t2, gi);
+            V = __fadd_rn(V, __fmul_rn(p.a_m, t3));
+        }
+        ge = __fmul_rn(ge, p.d_e);
+        gi = __fmul_rn(gi, p.d_i);
+        if (ref == 0 && V >= p.v_th) {
+            fired = true;
+            V = p.v_reset;
+            ref = p.n_ref;
+        }
+        st.V[i] = V;
+        if (ref != ref0) st.ref[i] = ref;
+        st.ge[i] = ge;
+        st.gi[i] = gi;
+    }
+    if (p.flags & PF_POST_PLASTIC) {
+        const uint64_t h0 = st.hist[i];
+        const uint64_t h = (h0 << 1) | (uint64_t)fired;
+        st.hist[i] = h;
+        uint64_t hh = 0ull;
+        if (net.H > kHistBits) {                 // H = 128: second word, bits 64..127
+            hh = (st.hist_hi[i] << 1) | (h0 >> 63);
+            st.hist_hi[i] = hh;
+        }
+        recent = (h | hh) != 0ull;
+        // the window's spike position (k_stdp_ev's shared table): 0xfe no
+        // spike in the last H steps, 0xff several, else the bit of the only one
+        {
+            const uint32_t n1 = __popcll(h) + __popcll(hh);
+            st.fpos[(size_t)(t & 3) * st.fstride + i] = n1 == 0 ? (uint8_t)0xfeu
+                       : n1 > 1 ? (uint8_t)0xffu
+                                : (uint8_t)(h ? 63 - __clzll((long long)h) : 127 - __clzll((long long)hh));
+        }
+        // potentiation factors of a forced flush for this target, oldest
+        // spike first (k_flush: w = min(w + A+ (x_pre f), w_max)): age H --
+        // fpot = sum over its spikes s in the window of D+[H - s]; age H - 1
+        // (flushed a step early) -- fpot1 = sum over s <= H - 2 of
+        // D+[H - 1 - s].  k_flush(t) runs beside k_front(t+1), so it reads
+        // these step-t buffers, never the live history words
+        if (recent) {
+            const float *dpl = net.stdp[p.post_stdp].dplus;
+            const int H = (int)net.H;
+            float f = 0.0f, f1 = 0.0f;
+            for (uint64_t m = hh; m; ) {
+                const int b = 63 - __clzll((long long)m);
+                m &= ~(1ull << b);
+                f = __fadd_rn(f, dpl[H - 64 - b]);
+                if (64 + b <= H - 2) f1 = __fadd_rn(f1, dpl[H - 1 - 64 - b]);
+            }
+            for (uint64_t m = h; m; ) {
+                const int b = 63 - __clzll((long long)m);
+                m &= ~(1ull << b);
+                f = __fadd_rn(f, dpl[H - b]);
+                if (b <= H - 2) f1 = __fadd_rn(f1, dpl[H - 1 - b]);
+            }
+            st.fpot[(size_t)(t & 3) * st.fstride + i] = f;
+            st.fpot[(size_t)(4 + (t & 3)) * st.fstride + i] = f1;
+        }
+        const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
+        st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
+    }
+    if (fired) st.nspk[i] += 1u;
+    return fired;
+}
+
 // kPart (world > 1 with D = 0, where the arrivals of t include the other
 // ranks' spikes of t): 1 = the neuron update and ring words only, 2 = the
 // lists only, after the exchange put every rank's words of t in the ring;
-// 0 = both (every other case).
+// 3 = the fused step's front (the neurons without inputs, >= R, and every
+// row's lists; k_deliver(t-1)'s epilogue updated [0, R) and wrote their ring
+// words); 0 = all (every other case).  The step comes from the front's own
+// counter in the fused step (use_tf: ctr->tf, advanced by the last CTA), where
+// k_front(t) runs beside k_deliver(t), which advances ctr->t; else ctr->t.
 template <bool kAhead, int kPart>
-__global__ void __launch_bounds__(kFrontThreads)
-k_front(NetDev net, StateDev st) {
+__global__ void __launch_bounds__(kFrontThreads, 2048 / kFrontThreads)   // two CTAs per SM: <= 32 registers
+k_front(NetDev net, StateDev st, uint32_t use_tf) {
     __shared__ Compact2 cs;
     const unsigned long long t_entry = st.kspan ? gtimer() : 0ull;
     pdl_wait();            // k_deliver(t-1): inputs, step counter
     pdl_launch();
     trace_mark(st.trace, 0, 0);
-    const int64_t t = st.ctr->t;
+    const int64_t t = use_tf ? *(volatile const int64_t *)&st.ctr->tf : st.ctr->t;
     constexpr int kSpan = kPart == 2 ? 4 : 0;
     if (st.kspan) kspan_begin(st.kspan, t, kSpan, t_entry, gtimer());
     const uint32_t par = (uint32_t)(t & 1);
@@ -136,112 +250,16 @@ k_front(NetDev net, StateDev st) {
     // (Poisson: counter-based, identical on all ranks); the spike bits of the
     // other input neurons arrive by the exchange
     const bool owned = i >= net.R || (i >= net.tgt_lo && i < net.tgt_hi);
-    // ---- (1) neuron dynamics (App. B op order)
-    if (kPart != 2 && valid && owned) {
-        if (p.kind == POP_POISSON) {
-            const u32x4 r = philox4x32_10(i, (uint32_t)t, 2u, 0u, net.key0, net.key1);
-            fired = (uint64_t)r.x < p.thr;
-        } else if (p.kind == POP_LIF_DELTA) {
-            const int32_t q = st.in_e[i];
-            const float I = __fmul_rn(__int2float_rn(q), net.inv_scale);
-            if (q != 0) st.in_e[i] = 0;
-            int32_t ref = st.ref[i];
-            float V = st.V[i];
-            const float V0 = V;
-            const int32_t ref0 = ref;
-            if (ref > 0) ref--;
-            else V = __fadd_rn(__fmul_rn(V, p.k_m), I);
-            if (ref == 0 && V >= p.v_th) {
-                fired = true;
-                V = p.v_reset;
-                ref = p.n_ref;
-            }
-            if (__float_as_uint(V) != __float_as_uint(V0)) st.V[i] = V;
-            if (ref != ref0) st.ref[i] = ref;
-        } else {  // POP_LIF_CUBA
-            const int32_t qe = st.in_e[i], qi = st.in_i[i];
-            float ge = __fadd_rn(st.ge[i], __fmul_rn(__int2float_rn(qe), net.inv_scale));
-            float gi = __fadd_rn(st.gi[i], __fmul_rn(__int2float_rn(qi), net.inv_scale));
-            if (qe != 0) st.in_e[i] = 0;
-            if (qi != 0) st.in_i[i] = 0;
-            int32_t ref = st.ref[i];
-            const int32_t ref0 = ref;
-            float V = st.V[i];
-            if (ref > 0) {
-                ref--;
-            } else {
-                const float t1 = __fsub_rn(p.v_rest, V);
-                const float t2 = __fadd_rn(t1, ge);
-                const float t3 = __fadd_rn(t2, gi);
-                V = __fadd_rn(V, __fmul_rn(p.a_m, t3));
-            }
-            ge = __fmul_rn(ge, p.d_e);
-            gi = __fmul_rn(gi, p.d_i);
-            if (ref == 0 && V >= p.v_th) {
-                fired = true;
-                V = p.v_reset;
-                ref = p.n_ref;
-            }
-            st.V[i] = V;
-            if (ref != ref0) st.ref[i] = ref;
-            st.ge[i] = ge;
-            st.gi[i] = gi;
-        }
-        if (p.flags & PF_POST_PLASTIC) {
-            const uint64_t h0 = st.hist[i];
-            const uint64_t h = (h0 << 1) | (uint64_t)fired;
-            st.hist[i] = h;
-            uint64_t hh = 0ull;
-            if (net.H > kHistBits) {                 // H = 128: second word, bits 64..127
-                hh = (st.hist_hi[i] << 1) | (h0 >> 63);
-                st.hist_hi[i] = hh;
-            }
-            recent = (h | hh) != 0ull;
-            // the window's spike position (k_stdp_ev's shared table): 0xfe no
-            // spike in the last H steps, 0xff several, else the bit of the only one
-            {
-                const uint32_t n1 = __popcll(h) + __popcll(hh);
-                st.fpos[(size_t)(t & 3) * st.fstride + i] = n1 == 0 ? (uint8_t)0xfeu
-                           : n1 > 1 ? (uint8_t)0xffu
-                                    : (uint8_t)(h ? 63 - __clzll((long long)h) : 127 - __clzll((long long)hh));
-            }
-            // potentiation factors of a forced flush for this target, oldest
-            // spike first (k_flush: w = min(w + A+ (x_pre f), w_max)): age H --
-            // fpot = sum over its spikes s in the window of D+[H - s]; age H - 1
-            // (flushed a step early) -- fpot1 = sum over s <= H - 2 of
-            // D+[H - 1 - s].  k_flush(t) runs beside k_front(t+1), so it reads
-            // these step-t buffers, never the live history words
-            if (recent) {
-                const float *dpl = net.stdp[p.post_stdp].dplus;
-                const int H = (int)net.H;
-                float f = 0.0f, f1 = 0.0f;
-                for (uint64_t m = hh; m; ) {
-                    const int b = 63 - __clzll((long long)m);
-                    m &= ~(1ull << b);
-                    f = __fadd_rn(f, dpl[H - 64 - b]);
-                    if (64 + b <= H - 2) f1 = __fadd_rn(f1, dpl[H - 1 - 64 - b]);
-                }
-                for (uint64_t m = h; m; ) {
-                    const int b = 63 - __clzll((long long)m);
-                    m &= ~(1ull << b);
-                    f = __fadd_rn(f, dpl[H - b]);
-                    if (b <= H - 2) f1 = __fadd_rn(f1, dpl[H - 1 - b]);
-                }
-                st.fpot[(size_t)(t & 3) * st.fstride + i] = f;
-                st.fpot[(size_t)(4 + (t & 3)) * st.fstride + i] = f1;
-            }
-            const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
-            st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
-        }
-        if (fired) st.nspk[i] += 1u;
-    }
+    // ---- (1) neuron dynamics (App. B op order); kPart 3 (the fused step):
+    //      the input neurons [0, R) were updated by k_deliver(t-1)'s epilogue
+    if (kPart != 2 && valid && owned && (kPart != 3 || i >= net.R)) fired = neuron_update(net, st, i, p, t, recent);
     const uint32_t fword = __ballot_sync(0xffffffffu, fired);
     const uint32_t rword = __ballot_sync(0xffffffffu, recent);
     // ring word of ids [i, i + 32): written by the rank owning its input
     // neurons (the word straddling R by the last rank), by all if it has none
     const bool wown = i >= net.R ? true : (i + 32 <= net.R ? (i >= net.tgt_lo && i + 32 <= net.tgt_hi)
                                                            : (i >= net.tgt_lo && net.tgt_hi == net.R));
-    if (kPart != 2 && lane == 0 && valid && wown) {
+    if (kPart != 2 && lane == 0 && valid && wown && (kPart != 3 || i >= net.R)) {   // (kPart 3: i = the warp's first)
         st.ring[(size_t)(t & (kRingSlots - 1)) * net.ring_stride + (i >> 5)] = fword;
         if (net.nstdp) st.recent[(size_t)(t & 3) * st.rstride + (i >> 5)] = rword;
         // this rank's share of the step's input-neuron words, for the exchange
@@ -249,7 +267,7 @@ k_front(NetDev net, StateDev st) {
         if (net.world > 1 && i < net.R && w >= w0 && w < w0 + net.wmax) st.sendbuf[w - w0] = fword;
     }
 
-    if (kPart == 1) {
+    if (kPart == 1) {                            // (the list part, kPart 2, advances ctr->tf)
         trace_mark(st.trace, 0, 3);
         kspan_end(st.kspan, t, kSpan);
         return;
@@ -262,7 +280,12 @@ k_front(NetDev net, StateDev st) {
         else if (t >= (int64_t)net.D) arr = ring_bit(st.ring, net.ring_stride, t - net.D, i);
         // kAhead (D >= 2): the arrivals of t + 1 and t + 2 are spikes of steps <= t - 1
         if (kAhead && t + 1 >= (int64_t)net.D) arr1 = ring_bit(st.ring, net.ring_stride, t + 1 - net.D, i);
-        if (kAhead && t + 2 >= (int64_t)net.D) arr2 = ring_bit(st.ring, net.ring_stride, t + 2 - net.D, i);
+        if (kAhead && t + 2 >= (int64_t)net.D) {
+            // (D = 2: the spike of this step -- this thread's own `fired` where it
+            // updated neuron i, the other CTAs of this grid write the ring slot)
+            const bool own = owned && (kPart != 3 || i >= net.R);
+            arr2 = (net.D == 2 && own) ? fired : ring_bit(st.ring, net.ring_stride, t + 2 - net.D, i) != 0u;
+        }
     }
     const bool plastic_row = valid && (p.flags & PF_PRE_PLASTIC);
     bool visit = false, flush = false;
@@ -377,6 +400,13 @@ k_front(NetDev net, StateDev st) {
     }
     trace_mark(st.trace, 0, 3);
     kspan_end(st.kspan, t, kSpan);
+    if (use_tf) {
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(&st.ctr->fr_ticket, 1u) == gridDim.x - 1) {   // the last CTA: next step
+            st.ctr->fr_ticket = 0;
+            st.ctr->tf = t + 1;
+        }
+    }
 }
 
 // ---------------------------------------------------- CTA row-table helpers
@@ -1758,7 +1788,7 @@ __device__ __forceinline__ void deliver_window(const NetDev &net, const StateDev
 // compile-time variants, so a kernel carries only its path.
 template <bool kMulti, bool kIdx16, bool kAhead, bool kH128>
 __global__ void __launch_bounds__(kDelThreads, SNN_DEL_MINB)
-k_deliver(NetDev net, StateDev st) {
+k_deliver(NetDev net, StateDev st, uint32_t epi) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t wsum[kDelWarps];
     __shared__ unsigned long long wsum64[kDelWarps];
@@ -1943,6 +1973,42 @@ k_deliver(NetDev net, StateDev st) {
     if (kAhead && k == 0 && split == 0 && threadIdx.x == 0 && nAs) atomicAdd(&st.ctr->metric[1], (unsigned long long)nAs);
     pdl_wait();            // (no segments) this grid still completes after its primary
     pdl_launch();
+    if (kAhead && epi && k < net.nslices) {
+        // ---- the fused step (SURVEY 8(a4) fusion lever 2): the last CTA of
+        //      the slice to finish its write-back updates the slice's neurons
+        //      for step t + 1 (neuron_update, the same operations as k_front)
+        //      and writes their ring / recent words -- the input never waits
+        //      for a separate neuron kernel.  The Poisson neurons of the word
+        //      straddling R get their (stateless) draw here too; k_front(t+1)
+        //      updates every other neuron >= R.
+        __shared__ uint32_t s_last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(st.slice_ticket + k, 1u) == nsplit - 1 ? 1u : 0u;
+        __syncthreads();
+        if (s_last) {
+            if (threadIdx.x == 0) st.slice_ticket[k] = 0;
+            __threadfence();                       // the other splits' write-backs
+            const int64_t t1 = t + 1;
+            const uint32_t hi32 = shi == net.R ? min((net.R + 31u) & ~31u, net.N) : shi;
+            for (uint32_t x0 = 0; slo + x0 < hi32; x0 += kDelThreads) {
+                const uint32_t i = slo + x0 + threadIdx.x;
+                bool fired = false, recent = false;
+                if (i < shi) {
+                    fired = neuron_update(net, st, i, net.pop[find_pop(net, i)], t1, recent);
+                } else if (i < hi32) {
+                    const PopDev &pp = net.pop[find_pop(net, i)];
+                    const u32x4 r = philox4x32_10(i, (uint32_t)t1, 2u, 0u, net.key0, net.key1);
+                    fired = (uint64_t)r.x < pp.thr;
+                }
+                const uint32_t fw = __ballot_sync(0xffffffffu, fired), rw = __ballot_sync(0xffffffffu, recent);
+                if (lane == 0 && i < hi32) {
+                    st.ring[(size_t)(t1 & (kRingSlots - 1)) * net.ring_stride + (i >> 5)] = fw;
+                    if (net.nstdp) st.recent[(size_t)(t1 & 3) * st.rstride + (i >> 5)] = rw;
+                }
+            }
+        }
+    }
     if (st.kspan) kspan_begin(st.kspan, t, 2, t_entry, t_wait ? t_wait : gtimer());
     // ---- step completion: the last CTA advances t
     __syncthreads();
@@ -2157,14 +2223,17 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, bool pdl, bool ahead, int part) {
-    void (*k)(NetDev, StateDev) = ahead ? k_front<true, 0>
+// use_tf: the step from the front's own counter (the fused step graph, where
+// k_front(t) runs beside k_deliver(t), which advances ctr->t)
+cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, bool pdl, bool ahead, int part,
+                         bool use_tf) {
+    void (*k)(NetDev, StateDev, uint32_t) = ahead ? (part == 3 ? k_front<true, 3> : k_front<true, 0>)
                                         : part == 1 ? k_front<false, 1> : part == 2 ? k_front<false, 2> : k_front<false, 0>;
-    return launch_pdl(k, dim3(front_blocks(net)), dim3(kFrontThreads), 0, s, pdl, net, st);
+    return launch_pdl(k, dim3(front_blocks(net)), dim3(kFrontThreads), 0, s, pdl, net, st, use_tf ? 1u : 0u);
 }
 
 // k_deliver variants by (two receptors, 16-bit ids, ahead list, H = 128)
-static void (*const g_deliver[16])(NetDev, StateDev) = {
+static void (*const g_deliver[16])(NetDev, StateDev, uint32_t) = {
     k_deliver<false, false, false, false>, k_deliver<false, false, false, true>,
     k_deliver<false, false, true, false>,  k_deliver<false, false, true, true>,
     k_deliver<false, true, false, false>,  k_deliver<false, true, false, true>,
@@ -2264,11 +2333,13 @@ cudaError_t launch_deliver_rowwise(const NetDev &net, const StateDev &st, uint32
     return launch_pdl(k_deliver_rowwise, dim3(grid), dim3(kRowThreads), 0, s, pdl, net, st);
 }
 
+// epi: the fused step's epilogue (the neurons of t + 1 by the slices' last CTAs)
 cudaError_t launch_deliver(const NetDev &net, const StateDev &st, uint32_t splits, cudaStream_t s, bool pdl,
-                           bool ahead) {
+                           bool ahead, bool epi) {
     dim3 grid(net.nslices > 0 ? net.nslices : 1, splits);
     const uint32_t v = (net.nrcpt > 1 ? 8u : 0u) | (st.idx16 ? 4u : 0u) | (ahead ? 2u : 0u) | (net.H > kHistBits ? 1u : 0u);
-    return launch_pdl(g_deliver[v], grid, dim3(kDelThreads), deliver_smem_bytes(net, ahead), s, pdl, net, st);
+    return launch_pdl(g_deliver[v], grid, dim3(kDelThreads), deliver_smem_bytes(net, ahead), s, pdl, net, st,
+                      epi ? 1u : 0u);
 }
 
 cudaError_t launch_readout(const NetDev &net, const StateDev &st, int64_t t_last, uint32_t grid, uint32_t pp_lo,

@@ -109,6 +109,38 @@ def _compare_weights(g, o, rc):
     return err.max()
 
 
+@pytest.mark.parametrize("plastic,delay,H", [(True, 15, 64), (True, 2, 64), (True, 15, 128), (False, 15, 64),
+                                              (True, 3, 64)])
+def test_fused_step_graph_parity(plastic, delay, H):
+    """Multi-step calls (snn_step(37)) with the fused step graph (SNN_FUSE: the
+    neurons of t + 1 updated in k_deliver(t)'s epilogue, k_front (neurons
+    without inputs, lists) and k_flush on branches) against the oracle at
+    every call boundary: rasters and history bit-exact, V within 1e-4, the
+    pending inputs bit-exact for static networks; weights within 1e-4 at the
+    end.  D = 2: the arrivals of t + 2 are the spikes of t itself."""
+    import os
+    rc = W.brunel(10000, p=0.05, plastic=plastic, delay=delay, seed=17)
+    os.environ["SNN_FUSE"] = "1"          # (read when the handle is finalized)
+    try:
+        g, o = _pair(rc, slice_width=512, history_bits=H)
+    finally:
+        del os.environ["SNN_FUSE"]
+    for _ in range(8):
+        g.step(37)
+        o.step(37)
+        hg, ho = g.read_state("HIST"), o.array("hist")
+        assert np.array_equal(hg, ho), f"raster differs: {np.flatnonzero(hg != ho)[:10]}"
+        if plastic:
+            assert np.allclose(g.read_state("V"), o.array("V"), rtol=1e-4, atol=1e-4)
+        else:
+            assert np.array_equal(g.read_state("V"), o.array("V"))
+            assert np.array_equal(g.read_state("INPUT_EXC"), o.array("in_e"))
+    if plastic:
+        _compare_weights(g, o, rc)
+        assert g.metrics()["FLUSH_ROWS"] > 0
+    assert g.metrics()["EVENTS"] == o.events
+
+
 @pytest.mark.parametrize("delay,H", [(0, 64), (15, 64), (0, 128), (15, 128)])
 def test_brunel_plus_stdp_parity(delay, H):
     """Lazy+event STDP (GPU) vs naive STDP (oracle), 400 steps: forced flushes
