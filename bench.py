@@ -162,7 +162,8 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ oracle
-def run_oracle(cfg: int, seed: int, steps: int, warmup: int, budget_s: float, threads: int = 0):
+def run_oracle(cfg: int, seed: int, steps: int, warmup: int, budget_s: float, threads: int = 0,
+               budget_1thread: float = 0.0):
     """Time the oracle as it stands (test infrastructure; only this leg of
     bench.py runs it) on the FULL network of the BASELINE config: build the
     graph (untimed), `warmup` untimed steps, then up to `steps` timed steps or
@@ -177,17 +178,25 @@ def run_oracle(cfg: int, seed: int, steps: int, warmup: int, budget_s: float, th
     o.finalize()
     build_s = time.perf_counter() - t0
     o.step(warmup)
-    e0 = o.events
-    t0 = time.perf_counter()
-    done = 0
-    while done < steps:
-        o.step(1)
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    ev = o.events - e0
+
+    def timed(budget):
+        e0 = o.events
+        t0 = time.perf_counter()
+        done = 0
+        while done < steps:
+            o.step(1)
+            done += 1
+            if time.perf_counter() - t0 > budget:
+                break
+        return done, time.perf_counter() - t0, o.events - e0
+
+    done, dt, ev = timed(budget_s)
     per_step = dt / done
+    one = None
+    if cores > 1 and budget_1thread > 0:          # the same oracle on one host thread (a shorter sample)
+        o.set_threads(1)
+        d1, t1, _ = timed(budget_1thread)
+        one = dict(value=t1 / d1 / (rc.dt_ms * 1e-3), steps=d1, ms_per_step=1e3 * t1 / d1)
     return dict(value=per_step / (rc.dt_ms * 1e-3), unit="wall-s per bio-second (extrapolated)", cores=cores,
                 kind="oracle",
                 sample=(f"BASELINE config {cfg} at full size ({rc.name}, {o.nsyn:,} synapses; graph build "
@@ -195,7 +204,8 @@ def run_oracle(cfg: int, seed: int, steps: int, warmup: int, budget_s: float, th
                         f"on {cores} host threads, per-step time x 10,000 = 1 bio-second (extrapolated).  The "
                         f"naive STDP sweep (Fig. 2a, every plastic synapse every step) dominates the oracle's "
                         f"step and does not depend on activity; delivery runs at the cold network's rates"),
-                events_per_s=ev / dt, steps=done, seconds=dt, synapses=int(o.nsyn), ms_per_step=1e3 * per_step)
+                events_per_s=ev / dt, steps=done, seconds=dt, synapses=int(o.nsyn), ms_per_step=1e3 * per_step,
+                one_thread=one)
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -397,10 +407,15 @@ def main(argv=None):
     stdp_b = (4 * dm_local["STDP_SYN"] + 8 * dm_local["STDP_WRW"] + 16 * dm_local["STDP_ROWS"]) / K
     flush_b = (4 * dm_local["FLUSH_SYN"] + 8 * dm_local["FLUSH_WRW"] + 16 * dm_local["FLUSH_ROWS"]) / K
     split = bool(spans and "flush" in spans)
+    # the ahead step runs the plastic arrivals' STDP inside k_deliver: their
+    # weights are read as delivered events and written back where they change
+    fused_arr = split and not (spans and "stdp" in spans)
+    arr_stores = dm_local["STDP_WSTORE"] - dm_local["FLUSH_WSTORE"]
     kb = {
-        "stdp": stdp_b - flush_b if split else stdp_b,
+        "stdp": 0.0 if fused_arr else (stdp_b - flush_b if split else stdp_b),
         "flush": flush_b if split else 0.0,
-        "deliver": ((6 if a.idx16 else 8) * dm_local["EVENTS"] + 8 * dm_local["SPIKES"] * info["nslices"]) / K
+        "deliver": ((6 if a.idx16 else 8) * dm_local["EVENTS"] + 8 * dm_local["SPIKES"] * info["nslices"]
+                    + ((4 * arr_stores + 16 * (dm_local["STDP_ROWS"] - dm_local["FLUSH_ROWS"])) if fused_arr else 0)) / K
                    + 4 * nrcpt * (info["tgt_hi"] - info["tgt_lo"]),
         "front": 32.0 * (info["N"] - n_pois) + 16.0 * n_pois,
     }
@@ -474,9 +489,12 @@ def main(argv=None):
         "clocks": clk.summary(),
     }
     if not a.no_cpu_baseline and rank == 0 and world == 1:
-        r = run_oracle(a.config, a.seed, 1000, 1, budget_s=a.cpu_budget, threads=a.cpu_threads)
+        r = run_oracle(a.config, a.seed, 1000, 1, budget_s=a.cpu_budget, threads=a.cpu_threads,
+                       budget_1thread=a.cpu_budget / 2)
         out["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
         out["cpu_baseline"]["ms_per_step"] = r["ms_per_step"]
+        if r.get("one_thread"):
+            out["cpu_baseline"]["one_thread"] = dict(r["one_thread"], unit=r["unit"], cores=1)
     if rank == 0:
         print(json.dumps(out))
     if world > 1:

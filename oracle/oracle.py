@@ -163,6 +163,10 @@ class Oracle:
         return float(lib().oracle_synapse_replay(self._s, src_pop, dst_pop, pre.ctypes.data_as(P8),
                                                   post.ctypes.data_as(P8), len(pre)))
 
+    def set_threads(self, threads: int):
+        """Host threads of the following steps (OpenMP-style row / neuron loops)."""
+        lib().oracle_set_threads(self._s, threads)
+
     def finalize(self):
         if lib().oracle_finalize(self._s) != 0:
             raise RuntimeError("oracle_finalize failed")

@@ -1560,7 +1560,10 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
             atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
             atomicAdd(&st.ctr->metric[9], (unsigned long long)n_syn);
         }
-        if (n_w) atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
+        if (n_w) {
+            atomicAdd(&st.ctr->metric[4], (unsigned long long)n_w);
+            atomicAdd(&st.ctr->metric[11], (unsigned long long)n_w);
+        }
         if (n_hit) {
             atomicAdd(&st.ctr->metric[8], (unsigned long long)n_hit);
             atomicAdd(&st.ctr->metric[10], (unsigned long long)n_hit);
