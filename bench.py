@@ -43,8 +43,7 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 METRIC = "wall-s per bio-second & synaptic events/s at 1/2/4/8 B200; % HBM roofline"
-KERNEL_OF = {"front": "k_front", "stdp": "k_stdp_ev<arrivals>", "flush": "k_stdp_ev<flushes> (k_flush)",
-             "deliver": "k_deliver"}
+KERNEL_OF = {"front": "k_front", "stdp": "k_stdp_ev", "flush": "k_flush", "deliver": "k_deliver"}
 
 
 def parse(argv=None):

@@ -88,8 +88,10 @@ for d in data:
     v = float(d["Metric Value"].replace(",", "")) * UNIT.get(d["Metric Unit"], 1.0)
     agg[d["Kernel Name"].split("(")[0]][d["Metric Name"]].append(v)
 tot = sum(sum(m["gpu__time_duration.sum"]) for m in agg.values())
-lines = ["ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
-         "-s 3000 -c 300 on `python bench.py --steps 1000 --warmup 1000` (graph replay; cold-cache, serialised)"]
+lines = [os.environ.get("NCU_LAUNCH_CMD",
+                        "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+                        "--clock-control none -s 3000 -c 300 on `python bench.py --steps 1000 --warmup 1000`")
+         + " (graph replay; cold-cache, serialised)"]
 for k, m in agg.items():
     t = m["gpu__time_duration.sum"]
     lines.append(f"{k:20s} launches={len(t):4d} mean_us={sum(t) / len(t):8.2f} share={sum(t) / tot:.3f} "
