@@ -342,7 +342,7 @@ def main(argv=None):
         del sk
         spans = {"same_window": bool(reduce(0.0 if same else 1.0, MAX) == 0.0),
                  "ms_per_step_instrumented": ms_k / a.steps}
-        for k in ("front", "stdp", "flush", "deliver"):
+        for k in ("front", "front2", "stdp", "flush", "deliver"):
             st = k1[k]["steps"] - k0[k]["steps"]
             if st <= 0:
                 continue

@@ -124,6 +124,11 @@ struct snn_sim {
     bool fused = false;
     cudaStream_t cap_front = nullptr;
     cudaEvent_t ev_fr[2] = {nullptr, nullptr}, ev_del[2] = {nullptr, nullptr}, ev_fl_f[2] = {nullptr, nullptr};
+    cudaEvent_t ev_lif[2] = {nullptr, nullptr};
+    // the split step (a variant of the fused graph): k_deliver without the
+    // epilogue, the neurons [0, R) of t in a slim k_front (kPart 4) on the
+    // critical path, the rest of k_front (neurons >= R, lists) on a branch
+    bool split_front = false;
     uint32_t flush_grid = 1, flush_grid_side = 1;   // k_flush CTAs: serial step / side branch
     // step graph (SNN_PIPE, experiments): 0 serial; 1 ahead + k_flush(t) on a
     // side branch joined before k_deliver(t + fl_lag); 2 no ahead list, k_stdp_arr
@@ -635,6 +640,15 @@ static snn_status finalize(snn_sim *sim) {
         // (opt-in, SNN_FUSE: measured slower on cfg3, 50.8 vs 42.8 us/step -- one CTA per
         // slice runs the slice's neuron update in k_deliver's tail)
         sim->fused = sim->ahead && cfg.world == 1 && straddle_ok && getenv("SNN_FUSE") && sim->pipe != 2;
+        // the split step (opt-in, SNN_SPLIT; needs D >= 3: the front of t reads
+        // the ring up to t - 1 while kPart 4 of t writes slot t).  Measured on
+        // cfg3: 45.9 vs 42.9 us/step -- k_deliver's CTAs fill the register files
+        // of the SMs k_flush leaves, so the branch front waits for them
+        if (!sim->fused && sim->ahead && cfg.world == 1 && straddle_ok && net.D >= 3 && sim->pipe != 2 &&
+            getenv("SNN_SPLIT")) {
+            sim->fused = true;
+            sim->split_front = true;
+        }
         if (sim->fused) sim->pipe = 0;     // (the fused graph has its own branches)
     }
     ALLOC(st.slice_ticket, uint32_t, std::max(1u, net.nslices));
@@ -645,6 +659,7 @@ static snn_status finalize(snn_sim *sim) {
             CK(cudaEventCreateWithFlags(&sim->ev_fr[q], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&sim->ev_del[q], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&sim->ev_fl_f[q], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&sim->ev_lif[q], cudaEventDisableTiming));
         }
         if (sim->plastic && !sim->cap_side) CK(cudaStreamCreateWithFlags(&sim->cap_side, cudaStreamNonBlocking));
     }
@@ -822,6 +837,7 @@ static snn_status capture_fused(snn_sim *sim, uint32_t n, cudaGraphExec_t *out) 
                                   __FILE__, __LINE__));                                               \
     } while (0)
     const bool dbg_serial = getenv("SNN_FUSE_SERIAL") != nullptr;   // (debug: k_front(t) after k_deliver(t))
+    const bool split = sim->split_front;
     for (uint32_t k = 0; k < n; k++) {
         if (k > 0 && !dbg_serial) {                                   // F: the front of t0 + k
             CKF(cudaStreamWaitEvent(F, sim->ev_del[(k - 1) & 1], 0));
@@ -842,12 +858,21 @@ static snn_status capture_fused(snn_sim *sim, uint32_t n, cudaGraphExec_t *out) 
             CKF(cudaStreamWaitEvent(m, sim->ev_fr[0], 0));
         }
         if (pl && k >= 2) CKF(cudaStreamWaitEvent(m, sim->ev_fl_f[k & 1], 0));   // k_flush(t-2)
-        // (PDL only behind the first front: with the joins of the branches, stream
-        // capture makes every incoming edge programmatic, and k_deliver(t) reads
-        // the arrival list of the front of t-1 before its dependency wait)
-        CKF(launch_deliver(net, st, sim->splits, m, k == 0, true, k + 1 < n));
+        if (split && k > 0) {
+            // the split step: the neurons [0, R) of t (kPart 4) after k_deliver(t-1),
+            // PDL -- its dependency wait also covers the joins above (front of
+            // t-1, k_flush(t-2)), and k_deliver(t) launches only after it waited
+            CKF(launch_front(net, st, m, true, true, 4, false));
+            CKF(cudaEventRecord(sim->ev_lif[k & 1], m));
+        }
+        // (fused: PDL only behind the first front -- with the joins of the
+        // branches, stream capture makes every incoming edge programmatic, and
+        // k_deliver(t) reads the arrival list of the front of t-1 before its
+        // dependency wait; split: behind kPart 4, which waited for them)
+        CKF(launch_deliver(net, st, sim->splits, m, k == 0 || split, true, !split && k + 1 < n));
         CKF(cudaEventRecord(sim->ev_del[k & 1], m));
         if (pl) {                                                     // X: the forced flushes of t0 + k
+            if (split && k > 0) CKF(cudaStreamWaitEvent(X, sim->ev_lif[k & 1], 0));   // fpos of t (kPart 4)
             CKF(cudaStreamWaitEvent(X, sim->ev_fr[k & 1], 0));
             CKF(launch_stdp_ev(net, st, sim->flush_grid_side, sim->pp_lo, sim->pp_hi, X, false, 2));
             CKF(cudaEventRecord(sim->ev_fl_f[k & 1], X));
@@ -1347,6 +1372,7 @@ void snn_destroy(snn_sim *sim) {
         if (sim->ev_fr[q]) cudaEventDestroy(sim->ev_fr[q]);
         if (sim->ev_del[q]) cudaEventDestroy(sim->ev_del[q]);
         if (sim->ev_fl_f[q]) cudaEventDestroy(sim->ev_fl_f[q]);
+        if (sim->ev_lif[q]) cudaEventDestroy(sim->ev_lif[q]);
     }
     if (sim->ev_xfront) cudaEventDestroy(sim->ev_xfront);
     if (sim->ev_xdone) cudaEventDestroy(sim->ev_xdone);

@@ -237,7 +237,7 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
     pdl_launch();
     trace_mark(st.trace, 0, 0);
     const int64_t t = use_tf ? *(volatile const int64_t *)&st.ctr->tf : st.ctr->t;
-    constexpr int kSpan = kPart == 2 ? 4 : 0;
+    constexpr int kSpan = (kPart == 2 || kPart == 4) ? 4 : 0;     // (span slot 4: the second front kernel)
     if (st.kspan) kspan_begin(st.kspan, t, kSpan, t_entry, gtimer());
     const uint32_t par = (uint32_t)(t & 1);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -250,16 +250,27 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
     // (Poisson: counter-based, identical on all ranks); the spike bits of the
     // other input neurons arrive by the exchange
     const bool owned = i >= net.R || (i >= net.tgt_lo && i < net.tgt_hi);
-    // ---- (1) neuron dynamics (App. B op order); kPart 3 (the fused step):
-    //      the input neurons [0, R) were updated by k_deliver(t-1)'s epilogue
-    if (kPart != 2 && valid && owned && (kPart != 3 || i >= net.R)) fired = neuron_update(net, st, i, p, t, recent);
+    // ---- (1) neuron dynamics (App. B op order); kPart 3 (the fused / split
+    //      step): the input neurons [0, R) were updated elsewhere (k_deliver(t-1)'s
+    //      epilogue / kPart 4); kPart 4: only those, and the stateless Poisson
+    //      draws of the neurons >= R sharing R's ring word
+    if (kPart == 4) {
+        if (valid && i < net.R) fired = neuron_update(net, st, i, p, t, recent);
+        else if (valid && p.kind == POP_POISSON) {
+            const u32x4 r = philox4x32_10(i, (uint32_t)t, 2u, 0u, net.key0, net.key1);
+            fired = (uint64_t)r.x < p.thr;
+        }
+    } else if (kPart != 2 && valid && owned && (kPart != 3 || i >= net.R)) {
+        fired = neuron_update(net, st, i, p, t, recent);
+    }
     const uint32_t fword = __ballot_sync(0xffffffffu, fired);
     const uint32_t rword = __ballot_sync(0xffffffffu, recent);
     // ring word of ids [i, i + 32): written by the rank owning its input
     // neurons (the word straddling R by the last rank), by all if it has none
     const bool wown = i >= net.R ? true : (i + 32 <= net.R ? (i >= net.tgt_lo && i + 32 <= net.tgt_hi)
                                                            : (i >= net.tgt_lo && net.tgt_hi == net.R));
-    if (kPart != 2 && lane == 0 && valid && wown && (kPart != 3 || i >= net.R)) {   // (kPart 3: i = the warp's first)
+    if (kPart != 2 && lane == 0 && valid && wown && (kPart != 3 || i >= net.R) && (kPart != 4 || i < net.R)) {
+        // (kPart 3 / 4: i = the warp's first neuron -- R's word belongs to kPart 4)
         st.ring[(size_t)(t & (kRingSlots - 1)) * net.ring_stride + (i >> 5)] = fword;
         if (net.nstdp) st.recent[(size_t)(t & 3) * st.rstride + (i >> 5)] = rword;
         // this rank's share of the step's input-neuron words, for the exchange
@@ -267,7 +278,7 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
         if (net.world > 1 && i < net.R && w >= w0 && w < w0 + net.wmax) st.sendbuf[w - w0] = fword;
     }
 
-    if (kPart == 1) {                            // (the list part, kPart 2, advances ctr->tf)
+    if (kPart == 1 || kPart == 4) {              // (the list part, kPart 2 / 3, advances ctr->tf)
         trace_mark(st.trace, 0, 3);
         kspan_end(st.kspan, t, kSpan);
         return;
@@ -2230,8 +2241,13 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 // k_front(t) runs beside k_deliver(t), which advances ctr->t)
 cudaError_t launch_front(const NetDev &net, const StateDev &st, cudaStream_t s, bool pdl, bool ahead, int part,
                          bool use_tf) {
-    void (*k)(NetDev, StateDev, uint32_t) = ahead ? (part == 3 ? k_front<true, 3> : k_front<true, 0>)
+    void (*k)(NetDev, StateDev, uint32_t) = ahead ? (part == 4 ? k_front<true, 4> : part == 3 ? k_front<true, 3>
+                                                                                  : k_front<true, 0>)
                                         : part == 1 ? k_front<false, 1> : part == 2 ? k_front<false, 2> : k_front<false, 0>;
+    if (part == 4) {             // neurons [0, R) and R's word: 512-thread CTAs (one wave beside k_flush)
+        const uint32_t n = std::min((net.R + 31u) & ~31u, net.N);
+        return launch_pdl(k, dim3(std::max(1u, (n + 511u) / 512u)), dim3(512), 0, s, pdl, net, st, 0u);
+    }
     return launch_pdl(k, dim3(front_blocks(net)), dim3(kFrontThreads), 0, s, pdl, net, st, use_tf ? 1u : 0u);
 }
 

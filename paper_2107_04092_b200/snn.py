@@ -45,7 +45,7 @@ FIELD_DTYPE = dict(V=np.float32, REFRACTORY=np.int32, G_EXC=np.float32, G_INH=np
                    FPOT=np.float32, RECENT=np.uint32, KTIME=np.uint64, FPOS=np.uint8)
 METRIC = dict(EVENTS=0, SPIKES=1, STDP_ROWS=2, STDP_SYN=3, STDP_WSTORE=4, FLUSH_ROWS=5, SEGMENTS=6, ELEMS=7,
               STDP_WRW=8, FLUSH_SYN=9, FLUSH_WRW=10, FLUSH_WSTORE=11)
-KTIME_KERNELS = ("front", "stdp", "deliver", "flush", "lists")
+KTIME_KERNELS = ("front", "stdp", "deliver", "flush", "front2")
 PHASE = dict(FRONT=0, STDP=1, DELIVERY=2, EXCHANGE=3, TOTAL=4, BUILD=5)
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
