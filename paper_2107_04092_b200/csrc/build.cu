@@ -385,15 +385,41 @@ cudaError_t build_fill(const NetDev &net, const BuildTabs &tabs, const uint32_t 
     return cudaGetLastError();
 }
 
-// Compressed indices: a target's offset in its slice,
-// (j - tgt_lo) mod C -- every (row, slice) segment indexes only C neurons.
+// Compressed indices: (j - tgt_lo) mod 2^16.  Every
+// (row, slice) segment indexes only C <= 2^16 neurons, so the delivery reads
+// the slice offset as (v - (kC mod 2^16)) mod 2^16; the STDP stream rebuilds j
+// from the row's crossings of multiples of 2^16 (k_b64).
 __global__ void k_idx16(NetDev net, const uint32_t *idx, uint16_t *idx16, int64_t S) {
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < S; c += (int64_t)gridDim.x * blockDim.x)
-        idx16[c] = (uint16_t)((idx[c] - net.tgt_lo) % net.C);
+        idx16[c] = (uint16_t)((idx[c] - net.tgt_lo) & 0xffffu);
+}
+
+// b64[i][m - 1] = #targets j of row i with j - tgt_lo < m 2^16 (lower bound), m = 1..4.
+__global__ void k_b64(NetDev net, const int64_t *row_ptr, const uint32_t *idx, uint32_t *b64) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= net.N) return;
+    const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+    uint32_t r[4];
+#pragma unroll
+    for (int m = 1; m <= 4; m++) {
+        const uint64_t v = (uint64_t)net.tgt_lo + ((uint64_t)m << 16);
+        int64_t a = b, c = e;
+        while (a < c) {
+            const int64_t mid = (a + c) >> 1;
+            if ((uint64_t)idx[mid] < v) a = mid + 1; else c = mid;
+        }
+        r[m - 1] = (uint32_t)(a - b);
+    }
+    reinterpret_cast<uint4 *>(b64)[i] = make_uint4(r[0], r[1], r[2], r[3]);
 }
 
 cudaError_t build_idx16(const NetDev &net, const uint32_t *idx, uint16_t *idx16, int64_t S, cudaStream_t s) {
     if (S > 0) k_idx16<<<1184, 256, 0, s>>>(net, idx, idx16, S);
+    return cudaGetLastError();
+}
+
+cudaError_t build_b64(const NetDev &net, const int64_t *row_ptr, const uint32_t *idx, uint32_t *b64, cudaStream_t s) {
+    k_b64<<<(net.N + 255) / 256, 256, 0, s>>>(net, row_ptr, idx, b64);
     return cudaGetLastError();
 }
 

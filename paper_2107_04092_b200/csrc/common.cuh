@@ -145,7 +145,9 @@ struct StateDev {
     // graph (this rank's target range)
     int64_t *row_ptr;        // [N+1]
     uint32_t *idx;           // [S + pad]
-    uint16_t *idx16;         // [S + pad] slice-local target offsets (SNN_FLAG_IDX16), else null
+    uint16_t *idx16;         // [S + pad] (j - tgt_lo) mod 2^16 (SNN_FLAG_IDX16), else null
+    uint32_t *b64;           // [N][4] a row's element indices where j - tgt_lo reaches m 2^16 (m = 1..4; the
+                             // row length if never) -- k_flush's 16-bit id stream (IDX16 + STDP), else null
     float *w;                // [S + pad]
     uint32_t *piv;           // [N][nslices+1], row-relative
     uint2 *seg;              // [N] plastic segment (lo, hi), row-relative

@@ -28,6 +28,7 @@ cudaError_t build_fill(const NetDev &, const BuildTabs &, const uint32_t *, cons
 cudaError_t build_segments(const NetDev &, const int64_t *, const uint32_t *, uint2 *, cudaStream_t);
 cudaError_t init_state(const NetDev &, const StateDev &, cudaStream_t);
 cudaError_t build_idx16(const NetDev &, const uint32_t *, uint16_t *, int64_t, cudaStream_t);
+cudaError_t build_b64(const NetDev &, const int64_t *, const uint32_t *, uint32_t *, cudaStream_t);
 uint32_t front_blocks(const NetDev &);
 cudaError_t launch_front(const NetDev &, const StateDev &, cudaStream_t, bool, bool, int, bool);
 size_t stdp_smem_bytes(const NetDev &, uint32_t, uint32_t);
@@ -571,9 +572,18 @@ static snn_status finalize(snn_sim *sim) {
         for (auto &e : bev) cudaEventDestroy(e);
     }
     st.idx16 = nullptr;
+    st.b64 = nullptr;
     if (cfg.flags & SNN_FLAG_IDX16) {
         ALLOC(st.idx16, uint16_t, (size_t)sim->nsyn + 16);
         CK(build_idx16(net, st.idx, st.idx16, sim->nsyn, s));
+        // k_flush's 16-bit stream: every plastic target j - tgt_lo < 5 2^16 (<= 4 crossings)
+        uint32_t pmax = 0;
+        for (uint32_t k = 0; k < net.npop; k++)
+            if (net.pop[k].flags & PF_POST_PLASTIC) pmax = std::max(pmax, net.pop[k].base + net.pop[k].n);
+        if (net.nstdp && (uint64_t)pmax <= (uint64_t)net.tgt_lo + 5ull * 65536ull) {
+            ALLOC(st.b64, uint32_t, 4ull * N);
+            CK(build_b64(net, st.row_ptr, st.idx, st.b64, s));
+        }
     }
     CK(init_state(net, st, s));
     {

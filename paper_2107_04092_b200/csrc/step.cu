@@ -1388,6 +1388,7 @@ struct FlSmem {
     uint32_t wsum[kFlWarps];
     float4 par[4];
     float dplus[4 * (kMaxHist + 1)];
+    uint4 bnd[kFlRows];                 // (kI16) the row's 2^16 crossings relative to cb (0xffffffff: none)
 };
 
 // table: fpos bytes [pp_lo & ~15, pp_hi) (16-byte units), else the bitmap
@@ -1401,7 +1402,11 @@ size_t flush_smem_bytes(uint32_t pp_lo, uint32_t pp_hi) {
     return ((sizeof(FlSmem) + 15) & ~(size_t)15) + fl_tab_bytes(pp_lo, pp_hi, flush_staged(pp_lo, pp_hi));
 }
 
-template <bool kH128, bool kStaged>
+// kI16 (SNN_FLAG_IDX16, SURVEY 8(f1) on the STDP stream): the ids streamed
+// as 16-bit (j - tgt_lo) mod 2^16 (2 instead of 4 B per visited synapse); j is
+// rebuilt from the row's crossings of multiples of 2^16 (st.b64, at most four
+// inside a plastic span), a chunk = 8 synapses.
+template <bool kH128, bool kStaged, bool kI16>
 __global__ void __launch_bounds__(kFlT, kFlT >= 1024 ? 1 : 1024 / kFlT)
 k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1457,15 +1462,21 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
         if (threadIdx.x < nrows) {
             const RowDesc d = Vl[cap_back - (f_begin + r0 + threadIdx.x)];
             const int64_t cs = d.start + d.s0, ce = d.start + d.s1;
-            er.cb = cs & ~3ll;
+            er.cb = kI16 ? cs & ~7ll : cs & ~3ll;
             er.lo = (uint32_t)(cs - er.cb);
             er.hi = (uint32_t)(ce - er.cb);
             er.xp = d.xp;
             er.meta = d.meta;
             er.pad = 0;
             if (cs < ce && d.xp != 0.0f) {
-                npc = (((er.hi + 3) >> 2) + kFlPieceCh - 1) / kFlPieceCh;
+                npc = kI16 ? (((er.hi + 7) >> 3) + 63) / 64 : (((er.hi + 3) >> 2) + kFlPieceCh - 1) / kFlPieceCh;
                 n_syn += (uint32_t)(ce - cs);
+            }
+            if (kI16) {        // the row's 2^16 crossings, relative to cb
+                const uint4 b = reinterpret_cast<const uint4 *>(st.b64)[d.row];
+                const int64_t off = er.cb - d.start;     // row-relative index of cb (<= s0)
+                auto rel = [&](uint32_t v) { return (int64_t)v <= off ? 0u : (uint32_t)((int64_t)v - off); };
+                sm.bnd[threadIdx.x] = make_uint4(rel(b.x), rel(b.y), rel(b.z), rel(b.w));
             }
         }
         // (warp-level prefix + one pass over the warp totals)
@@ -1505,6 +1516,72 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
         }
         // ---- the warp's pieces: p = warp + 32 i
         uint32_t cur = 0;
+        if constexpr (kI16) {
+        for (uint32_t p = warp; p < P; p += kFlWarps) {
+            while (p >= sm.incl[cur]) cur++;
+            const EvRow &rr = sm.rows[cur];
+            const uint32_t c0 = (p - rr.first) * 64u;            // chunks of 8 synapses, 64 per piece
+            const uint32_t lo = rr.lo, hi = rr.hi, nch = (hi + 7) >> 3;
+            const int64_t cb = rr.cb;
+            const uint4 bnd = sm.bnd[cur];
+            uint4 J[2], Wa[2], Wb[2];
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                const uint32_t c = c0 + lane + 32u * q;
+                const bool ok = c < nch;
+                J[q] = ok ? __ldg(reinterpret_cast<const uint4 *>(st.idx16 + cb + 8ll * c)) : make_uint4(0, 0, 0, 0);
+                Wa[q] = ok ? __ldg(reinterpret_cast<const uint4 *>(gw + cb + 8ll * c)) : make_uint4(0, 0, 0, 0);
+                Wb[q] = ok ? __ldg(reinterpret_cast<const uint4 *>(gw + cb + 8ll * c + 4)) : make_uint4(0, 0, 0, 0);
+            }
+            const uint32_t age = rr.meta & kMetaAge, si = (rr.meta >> 12) & 0x3u;
+            const float4 pr = sm.par[si];
+            const float xp = rr.xp;
+            const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                const uint32_t x0 = 8u * (c0 + lane + 32u * q);
+                const bool edge = x0 < lo || x0 + 8 > hi;       // a row's first / last chunk (or past it)
+                // j = tgt_lo + 2^16 (crossings <= x) + v; per element only if one falls inside the chunk
+                const uint32_t h0 = (uint32_t)(bnd.x <= x0) + (uint32_t)(bnd.y <= x0) + (uint32_t)(bnd.z <= x0) +
+                                    (uint32_t)(bnd.w <= x0);
+                const bool cross = (bnd.x > x0 && bnd.x < x0 + 8) || (bnd.y > x0 && bnd.y < x0 + 8) ||
+                                   (bnd.z > x0 && bnd.z < x0 + 8) || (bnd.w > x0 && bnd.w < x0 + 8);
+                const uint32_t vw[4] = {J[q].x, J[q].y, J[q].z, J[q].w};
+                const uint32_t wb[8] = {Wa[q].x, Wa[q].y, Wa[q].z, Wa[q].w, Wb[q].x, Wb[q].y, Wb[q].z, Wb[q].w};
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const bool in = !edge || (x0 + e >= lo && x0 + e < hi);
+                    uint32_t hh = h0;
+                    if (cross)
+                        hh = (uint32_t)(bnd.x <= x0 + e) + (uint32_t)(bnd.y <= x0 + e) + (uint32_t)(bnd.z <= x0 + e) +
+                             (uint32_t)(bnd.w <= x0 + e);
+                    const uint32_t v = (vw[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+                    const uint32_t j = in ? net.tgt_lo + (hh << 16) + v : pp_lo;
+                    uint32_t pos;
+                    if (kStaged) {
+                        pos = in ? lds_u8(tab_a + j) : 0xfeu;
+                    } else {
+                        const uint32_t b = (lds_u32(tab_a + ((j >> 5) << 2)) >> (j & 31)) & 1u;
+                        pos = (in && b) ? ldg_u8_if(fpos + j, 1u) : 0xfeu;
+                    }
+                    const float w0 = __uint_as_float(wb[e]);
+                    float w = w0;
+                    if (pos < age) {
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, lds_f32(dp + 4u * (age - pos)))));
+                        w = nw < pr.z ? nw : pr.z;
+                    } else if (pos == 0xffu) {
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, __ldg((age == H ? fpot : fpot1) + j))));
+                        w = nw < pr.z ? nw : pr.z;
+                    }
+                    n_hit += pos != 0xfeu ? 1u : 0u;
+                    if (__float_as_uint(w) != __float_as_uint(w0)) {
+                        gw[cb + x0 + e] = w;
+                        n_w++;
+                    }
+                }
+            }
+        }
+        } else {
         for (uint32_t p = warp; p < P; p += kFlWarps) {
             while (p >= sm.incl[cur]) cur++;
             const EvRow &rr = sm.rows[cur];
@@ -1560,6 +1637,7 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
                 }
             }
         }
+        }                                          // (the 32-bit id stream)
         __syncthreads();                           // row table reused next round
     }
     if (!tab_ready && threadIdx.x == 0) mbar_wait(bmap_a, 0);   // (no rows) the copy has landed
@@ -1723,6 +1801,7 @@ __device__ __forceinline__ void deliver_pass(const NetDev &net, const StateDev &
                                              uint32_t acc_a, uint64_t dw, float scale, uint32_t slo, DelStdp &ps) {
     uint32_t jj[kDelU], rr[kDelU], gg[kDelU];
     float ww[kDelU];
+    const uint32_t slo16 = (slo - net.tgt_lo) & 0xffffu;   // (kIdx16: the slice's first offset mod 2^16)
 #pragma unroll
     for (int u = 0; u < kDelU; u++) {
         // ragged pass: a thread past the end re-reads the last element (no
@@ -1735,7 +1814,7 @@ __device__ __forceinline__ void deliver_pass(const NetDev &net, const StateDev &
         gg[u] = gi;
         if (kIdx16) {
             const uint64_t a = lds_u64(ptr_a + (gi << 3)) + 2ull * (w0 + x);
-            jj[u] = ldg_nc_u16(a);
+            jj[u] = (ldg_nc_u16(a) - slo16) & 0xffffu;          // the slice offset j - slo
             ww[u] = ldg_nc_f32(2ull * a + dw);
         } else {
             const uint64_t a = lds_u64(ptr_a + (gi << 3)) + 4ull * (w0 + x);
@@ -2302,8 +2381,9 @@ cudaError_t kernels_configure(int device) {
                                                           k_stdp_ev<false, 2, 512>, k_stdp_ev<true, 2, 512>};
     for (auto k : ke)
         if ((e = set_max((const void *)k)) != cudaSuccess) return e;
-    void (*kf[4])(NetDev, StateDev, uint32_t, uint32_t) = {k_flush<false, true>, k_flush<true, true>,
-                                                                    k_flush<false, false>, k_flush<true, false>};
+    void (*kf[8])(NetDev, StateDev, uint32_t, uint32_t) = {
+        k_flush<false, false, false>, k_flush<false, true, false>, k_flush<true, false, false>, k_flush<true, true, false>,
+        k_flush<false, false, true>, k_flush<false, true, true>, k_flush<true, false, true>, k_flush<true, true, true>};
     for (auto k : kf)
         if ((e = set_max((const void *)k)) != cudaSuccess) return e;
     done.insert(device);
@@ -2337,9 +2417,11 @@ cudaError_t launch_stdp_ev(const NetDev &net, const StateDev &st, uint32_t grid,
                           ev_smem_bytes(pp_lo, pp_hi), s, pdl, net, st, pp_lo, pp_hi);
     if (mode == 2) {
         const bool stg = flush_staged(pp_lo, pp_hi);
-        return launch_pdl(h ? (stg ? k_flush<true, true> : k_flush<true, false>)
-                            : (stg ? k_flush<false, true> : k_flush<false, false>),
-                          dim3(grid), dim3(kFlT), flush_smem_bytes(pp_lo, pp_hi), s, pdl, net, st, pp_lo, pp_hi);
+        void (*kf[8])(NetDev, StateDev, uint32_t, uint32_t) = {
+            k_flush<false, false, false>, k_flush<false, true, false>, k_flush<true, false, false>, k_flush<true, true, false>,
+            k_flush<false, false, true>, k_flush<false, true, true>, k_flush<true, false, true>, k_flush<true, true, true>};
+        const uint32_t v = (st.b64 ? 4u : 0u) | (h ? 2u : 0u) | (stg ? 1u : 0u);
+        return launch_pdl(kf[v], dim3(grid), dim3(kFlT), flush_smem_bytes(pp_lo, pp_hi), s, pdl, net, st, pp_lo, pp_hi);
     }
     void (*k)(NetDev, StateDev, uint32_t, uint32_t) =
         mode == 1 ? (h ? k_stdp_ev<true, 1, 512> : k_stdp_ev<false, 1, 512>)

@@ -197,14 +197,15 @@ def test_ablation_schedules_same_result(plasticity, delivery):
 
 @pytest.mark.parametrize("C", [64, 96, 1024])
 def test_idx16_offsets_and_delivery_bit_exact(C):
-    """SURVEY 8(f1) compressed indices: the 16-bit slice-local offsets equal
-    (j - tgt_lo) mod C of the oracle's ids, and delivery through them
+    """SURVEY 8(f1) compressed indices: the 16-bit ids equal (j - tgt_lo)
+    mod 2^16 of the oracle's ids, and delivery through them (slice offset
+    (v - kC) mod 2^16)
     reproduces Vogels config 1 (two receptors) bit-exactly."""
     from paper_2107_04092_b200 import FLAG_IDX16
     rc = W.config(1)
     g, o = _pair(rc, slice_width=C, flags=FLAG_IDX16)
     lo = g.info()["tgt_lo"]
-    assert np.array_equal(g.read_state("IDX16").astype(np.int64), (o.array("idx").astype(np.int64) - lo) % C)
+    assert np.array_equal(g.read_state("IDX16").astype(np.int64), (o.array("idx").astype(np.int64) - lo) & 0xffff)
     _run_compare(g, o, 200, every=20)
     assert g.metrics()["EVENTS"] == o.events
 
@@ -215,6 +216,29 @@ def test_idx16_brunel_plus_parity():
     g, o = _pair(rc, slice_width=512, flags=FLAG_IDX16)
     _run_compare(g, o, 200, exact_v=False, every=25)
     _compare_weights(g, o, rc)
+
+
+def test_idx16_stdp_stream_crossings_equal_32bit_ids():
+    """SURVEY 8(f1) on the STDP stream: k_flush streams 16-bit ids and rebuilds
+    j from each row's crossings of multiples of 2^16 (b64).  With E = 80,000
+    post-synaptic neurons every plastic span crosses 65,536: the run must equal
+    the 32-bit run (whose flushes the oracle pins) bit for bit -- rasters,
+    weights, event and STDP counters."""
+    from paper_2107_04092_b200 import Snn, FLAG_IDX16
+    rc = W.brunel(200_000, p=0.005, plastic=True, delay=15, seed=23)
+    runs = []
+    for flags in (0, FLAG_IDX16):
+        g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, flags=flags)
+        rc.apply(g)
+        g.step(300)
+        runs.append((g.read_state("HIST"), g.read_state("WEIGHTS"), g.metrics()))
+        g.close()
+    (h0, w0, m0), (h1, w1, m1) = runs
+    assert rc.pops[0].n > 65536 and m0["FLUSH_ROWS"] > 0
+    assert np.array_equal(h0, h1)
+    assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
+    for k in ("EVENTS", "STDP_SYN", "STDP_WSTORE", "FLUSH_SYN", "FLUSH_WRW"):
+        assert m0[k] == m1[k], k
 
 
 def test_rowwise_delivery_static_bit_exact():
