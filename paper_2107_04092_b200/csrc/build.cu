@@ -340,7 +340,7 @@ __global__ void k_init_state(NetDev net, StateDev st) {
     st.hist[i] = 0ull;
     if (net.H > 64) st.hist_hi[i] = 0ull;
     for (int b = 0; b < 4; b++) st.fpos[(size_t)b * st.fstride + i] = 0xfeu;
-    for (int b = 0; b < 8; b++) st.fpot[(size_t)b * st.fstride + i] = 0.0f;
+    for (int b = 0; b < 12; b++) st.fpot[(size_t)b * st.fstride + i] = 0.0f;
     st.nspk[i] = 0u;
     st.xpre[i] = 0.0f;
     st.tlu[i] = -1;

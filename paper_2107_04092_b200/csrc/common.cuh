@@ -57,6 +57,7 @@ struct NetDev {
     uint32_t D;          // delay
     uint32_t H;          // history bits: 64 or 128 (forced flush at age H, R3)
     uint32_t flush_period; // 0: flush at age H; K: every K steps the rows of age >= H - K (R33)
+    uint32_t fl_lag;     // the ahead step's flush deadline L (2 or 3): k_flush(t) ends before k_deliver(t+L) (R36)
     uint32_t plast_mode; // SNN_PLAST_EVENT / LAZY / NAIVE (ablation)
     uint32_t deliv_mode; // SNN_DELIV_SLICED / ROWWISE (ablation)
     uint32_t npop, nstdp;
@@ -132,8 +133,8 @@ struct StateDev {
     uint64_t *hist_hi;       // H = 128: bits 64..127 (else unused)
     // four buffers by step (buffer t & 3 at + (t & 3) * fstride / rstride): k_flush(t) reads step t's
     // while k_front(t+1), k_front(t+2) write theirs
-    float *fpot;             // post-plastic j with spikes in its H-bit window: sum of D+[H - s] over them
-                             // (buffers 0-3), and of D+[H - 1 - s] over those with s <= H - 2 (4-7)
+    float *fpot;             // post-plastic j with spikes in its H-bit window, for a flush of age H - k
+                             // (k = 0, 1, 2): sum of D+[H - k - s] over its spikes s <= H - 1 - k, buffer 4k + (t & 3)
     uint8_t *fpos;           // post-plastic j: 0xfe no spike in its H-bit window, 0xff several, else the bit of the only one
     uint32_t fstride;        // elements per fpos / fpot buffer
     uint32_t rstride;        // words per `recent` buffer

@@ -137,7 +137,7 @@ struct snn_sim {
     int pipe = 0, fl_lag = 2, prio_hi = 0, prio_lo = 0;
     bool use_prio = false;
     cudaStream_t cap_side = nullptr;
-    cudaEvent_t ev_front = nullptr, ev_flush[2] = {nullptr, nullptr};
+    cudaEvent_t ev_front = nullptr, ev_flush[4] = {nullptr, nullptr, nullptr, nullptr};
     // world > 1, D >= 1: the exchange of step t on a branch of the step graph
     // (after k_front(t), joined before k_front(t+1)), overlapping the delivery
     cudaStream_t cap_xside = nullptr;
@@ -472,7 +472,7 @@ static snn_status finalize(snn_sim *sim) {
     ALLOC(st.hist, uint64_t, N);
     ALLOC(st.hist_hi, uint64_t, cfg.history_bits > 64 ? N : 1);
     st.fstride = (N + 16 + 15) & ~15u;
-    ALLOC(st.fpot, float, 8ull * st.fstride);         // [4] fpot (age H) + [4] fpot1 (age H - 1) by t & 3
+    ALLOC(st.fpot, float, 12ull * st.fstride);        // [3][4]: flush factors for ages H, H-1, H-2, by t & 3
     ALLOC(st.fpos, uint8_t, 4ull * st.fstride);
     ALLOC(st.nspk, uint32_t, N);
     // exchange geometry: rank r owns words [rank_lo[r] / 32, ...), at most
@@ -633,7 +633,9 @@ static snn_status finalize(snn_sim *sim) {
     // flush slows them more than it gains)
     sim->pipe = sim->ahead && sim->plastic ? 1 : 0;
     if (const char *e = getenv("SNN_PIPE")) sim->pipe = atoi(e);          // (experiments)
-    if (const char *e = getenv("SNN_FL_LAG")) sim->fl_lag = atoi(e) < 2 ? 1 : 2;
+    // k_flush's deadline: 2 steps (R36), or 3 (SNN_FL_LAG=3, D >= 3: rows of age >= H - 2)
+    if (const char *e = getenv("SNN_FL_LAG")) sim->fl_lag = (atoi(e) >= 3 && net.D >= 3) ? 3 : 2;
+    net.fl_lag = sim->ahead ? (uint32_t)sim->fl_lag : 2u;
     if (sim->pipe == 2) sim->ahead = false;
     if (sim->pipe == 1 && !sim->ahead) sim->pipe = 0;
     if (!sim->plastic || !sim->ev_kernel || flush_smem_bytes(sim->pp_lo, sim->pp_hi) > 227 * 1024)
@@ -791,13 +793,13 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
             // (experiments) the forced flushes on a side branch of the graph
             CK(cudaEventRecord(sim->ev_front, s));
             const uint32_t lag = sim->pipe == 1 ? (uint32_t)sim->fl_lag : 1u;
-            if (gk >= lag) CK(cudaStreamWaitEvent(s, sim->ev_flush[(gk - lag) & 1], 0));
+            if (gk >= lag) CK(cudaStreamWaitEvent(s, sim->ev_flush[(gk - lag) & 3], 0));
             if (sim->pipe == 2) CK(launch_stdp_ev(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl, 1));
             CK(cudaStreamWaitEvent(side, sim->ev_front, 0));
             if (sim->use_prio) set_launch_priority(sim->prio_lo);
             CK(launch_stdp_ev(net, st, sim->flush_grid_side, sim->pp_lo, sim->pp_hi, side, false, 2));
             if (sim->use_prio) set_launch_priority(sim->prio_hi);
-            CK(cudaEventRecord(sim->ev_flush[gk & 1], side));
+            CK(cudaEventRecord(sim->ev_flush[gk & 3], side));
         } else if (sim->ahead) {
             // the plastic arrivals run inside k_deliver(t), the forced flushes of t
             // in k_flush(t) after it (below)
@@ -913,8 +915,8 @@ static snn_status capture(snn_sim *sim, uint32_t nsteps, cudaGraphExec_t *out) {
     }
     if (sim->cap_xside && nsteps > 0) CK(cudaStreamWaitEvent(sim->cap_stream, sim->ev_xdone, 0));   // join
     if (sim->cap_side && sim->pipe != 0)                            // join the side branch
-        for (uint32_t k = nsteps > 2 ? nsteps - 2 : 0; k < nsteps; k++)
-            CK(cudaStreamWaitEvent(sim->cap_stream, sim->ev_flush[k & 1], 0));
+        for (uint32_t k = nsteps > 3 ? nsteps - 3 : 0; k < nsteps; k++)
+            CK(cudaStreamWaitEvent(sim->cap_stream, sim->ev_flush[k & 3], 0));
     CK(cudaStreamEndCapture(sim->cap_stream, &g));
     CK(cudaGraphInstantiate(out, g, 0));
     CK(cudaGraphDestroy(g));

@@ -189,29 +189,32 @@ __device__ __forceinline__ bool neuron_update(const NetDev &net, const StateDev 
                                 : (uint8_t)(h ? 63 - __clzll((long long)h) : 127 - __clzll((long long)hh));
         }
         // potentiation factors of a forced flush for this target, oldest
-        // spike first (k_flush: w = min(w + A+ (x_pre f), w_max)): age H --
-        // fpot = sum over its spikes s in the window of D+[H - s]; age H - 1
-        // (flushed a step early) -- fpot1 = sum over s <= H - 2 of
-        // D+[H - 1 - s].  k_flush(t) runs beside k_front(t+1), so it reads
-        // these step-t buffers, never the live history words
+        // spike first (k_flush: w = min(w + A+ (x_pre f), w_max)), for a flush
+        // of age H - k (flushed k steps early, R36): f_k = sum over its spikes
+        // s <= H - 1 - k of D+[H - k - s] (buffer 4k + (t & 3); k <= 1, or 2 with
+        // the 3-step deadline).  k_flush(t) runs beside k_front(t+1), so it
+        // reads these step-t buffers, never the live history words
         if (recent) {
             const float *dpl = net.stdp[p.post_stdp].dplus;
             const int H = (int)net.H;
-            float f = 0.0f, f1 = 0.0f;
+            float f = 0.0f, f1 = 0.0f, f2 = 0.0f;
             for (uint64_t m = hh; m; ) {
                 const int b = 63 - __clzll((long long)m);
                 m &= ~(1ull << b);
                 f = __fadd_rn(f, dpl[H - 64 - b]);
                 if (64 + b <= H - 2) f1 = __fadd_rn(f1, dpl[H - 1 - 64 - b]);
+                if (64 + b <= H - 3) f2 = __fadd_rn(f2, dpl[H - 2 - 64 - b]);
             }
             for (uint64_t m = h; m; ) {
                 const int b = 63 - __clzll((long long)m);
                 m &= ~(1ull << b);
                 f = __fadd_rn(f, dpl[H - b]);
                 if (b <= H - 2) f1 = __fadd_rn(f1, dpl[H - 1 - b]);
+                if (b <= H - 3) f2 = __fadd_rn(f2, dpl[H - 2 - b]);
             }
             st.fpot[(size_t)(t & 3) * st.fstride + i] = f;
             st.fpot[(size_t)(4 + (t & 3)) * st.fstride + i] = f1;
+            if (net.fl_lag >= 3) st.fpot[(size_t)(8 + (t & 3)) * st.fstride + i] = f2;
         }
         const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
         st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
@@ -322,7 +325,11 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
             // waits for that arrival (age H there); a row of age H - 1 arriving at
             // t + 2 is flushed one step early (age H - 1) -- then no row of age H
             // arrives at t + 1 (D >= 2: known one step ahead).  Exact by R4.
-            flush = !arr && !arr1 && (age >= H || (age == H - 1 && arr2));
+            // With the 3-step deadline (fl_lag 3, D >= 3): a row of age >= H - 2
+            // is flushed unless it arrives at t, t+1 or t+2 (then that arrival,
+            // age <= H, replays it) -- no row flushed at t arrives before t + 3.
+            if (net.fl_lag >= 3) flush = !arr && !arr1 && !arr2 && age >= H - 2;
+            else flush = !arr && !arr1 && (age >= H || (age == H - 1 && arr2));
             visit = arr || flush;
         } else {
             // forced flush (R3): at age H, or -- batched schedule (R33) -- every
@@ -1423,7 +1430,6 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
     if (st.kspan) kspan_begin(st.kspan, t, 3, t_entry, t_entry);
     const uint8_t *__restrict__ fpos = st.fpos + (size_t)(t & 3) * st.fstride;
     const float *__restrict__ fpot = st.fpot + (size_t)(t & 3) * st.fstride;
-    const float *__restrict__ fpot1 = st.fpot + (size_t)(4 + (t & 3)) * st.fstride;
     const uint32_t f_lo = pp_lo & ~15u, wlo = ev_bm_lo(pp_lo);
     const uint32_t tab_bytes = fl_tab_bytes(pp_lo, pp_hi, kStaged);
     if (threadIdx.x == 0) {
@@ -1570,7 +1576,7 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
                         const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, lds_f32(dp + 4u * (age - pos)))));
                         w = nw < pr.z ? nw : pr.z;
                     } else if (pos == 0xffu) {
-                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, __ldg((age == H ? fpot : fpot1) + j))));
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, __ldg(fpot + (size_t)4 * (H - age) * st.fstride + j))));
                         w = nw < pr.z ? nw : pr.z;
                     }
                     n_hit += pos != 0xfeu ? 1u : 0u;
@@ -1626,7 +1632,7 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
                         w = nw < pr.z ? nw : pr.z;
                     } else if (pos == 0xffu) {
                         // several spikes: the step's factor for age H or H - 1 (k_front)
-                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, __ldg((age == H ? fpot : fpot1) + j))));
+                        const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, __ldg(fpot + (size_t)4 * (H - age) * st.fstride + j))));
                         w = nw < pr.z ? nw : pr.z;
                     }
                     n_hit += pos != 0xfeu ? 1u : 0u;

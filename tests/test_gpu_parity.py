@@ -109,7 +109,7 @@ def _compare_weights(g, o, rc):
     return err.max()
 
 
-@pytest.mark.parametrize("mode", ["SNN_FUSE", "SNN_SPLIT"])
+@pytest.mark.parametrize("mode", ["SNN_FUSE", "SNN_SPLIT", "SNN_FL_LAG"])
 @pytest.mark.parametrize("plastic,delay,H", [(True, 15, 64), (True, 2, 64), (True, 15, 128), (False, 15, 64),
                                               (True, 3, 64)])
 def test_fused_step_graph_parity(plastic, delay, H, mode):
@@ -117,13 +117,15 @@ def test_fused_step_graph_parity(plastic, delay, H, mode):
     neurons of t + 1 updated in k_deliver(t)'s epilogue, k_front (neurons
     without inputs, lists) and k_flush on branches; SNN_SPLIT: the neurons
     [0, R) in a slim k_front part on the critical path instead of the
-    epilogue; D = 2 falls back to the default step there) against the oracle at
+    epilogue; SNN_FL_LAG=3: forced flushes of rows of age >= H - 2 that do not
+    arrive within three steps, each with a three-step deadline; D = 2 falls
+    back to the default step there) against the oracle at
     every call boundary: rasters and history bit-exact, V within 1e-4, the
     pending inputs bit-exact for static networks; weights within 1e-4 at the
     end.  D = 2: the arrivals of t + 2 are the spikes of t itself."""
     import os
     rc = W.brunel(10000, p=0.05, plastic=plastic, delay=delay, seed=17)
-    os.environ[mode] = "1"                # (read when the handle is finalized)
+    os.environ[mode] = "3" if mode == "SNN_FL_LAG" else "1"   # (read when the handle is finalized)
     try:
         g, o = _pair(rc, slice_width=512, history_bits=H)
     finally:
