@@ -106,6 +106,10 @@ enum {
                                         every CTA folds %globaltimer marks into its
                                         step's slot (entry, end of the dependency
                                         wait, end); read with SNN_FIELD_KTIME      */
+    SNN_FLAG_EXCHANGE = 1u << 6,     /* run the spike-word exchange (ncclAllGather +
+                                        unpack, on its graph branch) even at world ==
+                                        1 -- a one-GPU run of the NCCL data path;
+                                        needs nccl_unique_id                          */
     SNN_FLAG_IDX16 = 1u << 4         /* compressed indices:
                                         delivery reads 16-bit slice-local target
                                         offsets (j - slice base) instead of 32-bit

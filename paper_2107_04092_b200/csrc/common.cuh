@@ -51,6 +51,7 @@ struct NetDev {
     uint32_t nwords;     // 32-bit words of spike bits per step = ceil(N/32)
     uint32_t ring_stride;// words per ring slot (nwords + exchange padding)
     uint32_t world, rank;        // ranks sharing the target range
+    uint32_t xchg;               // the spike-word exchange runs (world > 1, or SNN_FLAG_EXCHANGE)
     uint32_t debug;              // SNN_DEBUG_KERNELS bits (experiments only; 0 in normal runs)
     uint32_t wmax;               // words exchanged per rank and step (the largest share + 1)
     uint32_t rank_lo[kMaxRanks + 1];   // target range of rank r: [rank_lo[r], rank_lo[r + 1]) (C-aligned)

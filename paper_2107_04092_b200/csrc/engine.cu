@@ -486,7 +486,8 @@ static snn_status finalize(snn_sim *sim) {
         net.wmax = mx + 1;
         sim->wmax = net.wmax;
     }
-    net.ring_stride = net.nwords + (cfg.world > 1 ? net.wmax : 0);
+    net.xchg = (cfg.world > 1 || (cfg.flags & SNN_FLAG_EXCHANGE)) ? 1u : 0u;
+    net.ring_stride = net.nwords + (net.xchg ? net.wmax : 0);
     ALLOC(st.ring, uint32_t, (size_t)kRingSlots * net.ring_stride);
     st.sendbuf = st.gath = nullptr;
     ALLOC(st.xpre, float, N);
@@ -518,7 +519,7 @@ static snn_status finalize(snn_sim *sim) {
     }
     cudaStream_t s = sim->stream;
     CK(cudaMemsetAsync(st.ring, 0, sizeof(uint32_t) * (size_t)kRingSlots * net.ring_stride, s));
-    if (cfg.world > 1) {
+    if (net.xchg) {
         ALLOC(st.sendbuf, uint32_t, net.wmax);
         ALLOC(st.gath, uint32_t, 2ull * net.wmax * cfg.world);
         CK(cudaMemsetAsync(st.sendbuf, 0, 4ull * net.wmax, s));
@@ -611,7 +612,7 @@ static snn_status finalize(snn_sim *sim) {
     // known at t (D >= 2; D >= 3 across ranks, whose words of t - 1 arrive
     // during step t - 1).  Otherwise the unsplit step (front -> STDP -> delivery).
     {
-        const uint32_t dmin = (cfg.world > 1 ? 1u : 0u) + (sim->plastic ? 2u : 1u);
+        const uint32_t dmin = ((cfg.world > 1 || (cfg.flags & SNN_FLAG_EXCHANGE)) ? 1u : 0u) + (sim->plastic ? 2u : 1u);
         sim->ahead = cfg.delivery == SNN_DELIV_SLICED && net.D >= dmin &&
                      (!sim->plastic || (cfg.plasticity == SNN_PLAST_EVENT && cfg.flush_period == 0)) &&
                      !getenv("SNN_NO_AHEAD");   // (tuning knob: the unsplit step)
@@ -651,12 +652,12 @@ static snn_status finalize(snn_sim *sim) {
         }
         // (opt-in, SNN_FUSE: measured slower on cfg3, 50.8 vs 42.8 us/step -- one CTA per
         // slice runs the slice's neuron update in k_deliver's tail)
-        sim->fused = sim->ahead && cfg.world == 1 && straddle_ok && getenv("SNN_FUSE") && sim->pipe != 2;
+        sim->fused = sim->ahead && cfg.world == 1 && !net.xchg && straddle_ok && getenv("SNN_FUSE") && sim->pipe != 2;
         // the split step (opt-in, SNN_SPLIT; needs D >= 3: the front of t reads
         // the ring up to t - 1 while kPart 4 of t writes slot t).  Measured on
         // cfg3: 45.9 vs 42.9 us/step -- k_deliver's CTAs fill the register files
         // of the SMs k_flush leaves, so the branch front waits for them
-        if (!sim->fused && sim->ahead && cfg.world == 1 && straddle_ok && net.D >= 3 && sim->pipe != 2 &&
+        if (!sim->fused && sim->ahead && cfg.world == 1 && !net.xchg && straddle_ok && net.D >= 3 && sim->pipe != 2 &&
             getenv("SNN_SPLIT")) {
             sim->fused = true;
             sim->split_front = true;
@@ -675,7 +676,7 @@ static snn_status finalize(snn_sim *sim) {
         }
         if (sim->plastic && !sim->cap_side) CK(cudaStreamCreateWithFlags(&sim->cap_side, cudaStreamNonBlocking));
     }
-    if (cfg.world > 1 && net.D >= 1 && cfg.nccl_unique_id && !getenv("SNN_NO_XBRANCH")) {
+    if (net.xchg && net.D >= 1 && cfg.nccl_unique_id && !getenv("SNN_NO_XBRANCH")) {
         CK(cudaStreamCreateWithFlags(&sim->cap_xside, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&sim->ev_xfront, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&sim->ev_xdone, cudaEventDisableTiming));
@@ -746,7 +747,7 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
     const StateDev &st = sim->st;
     // programmatic dependent launch between the kernels of the graph (not
     // across event records, whose timing would then overlap)
-    const bool multi = sim->cfg.world > 1;
+    const bool multi = sim->net.xchg != 0;
     const bool pdl = ev == nullptr && !(sim->cfg.flags & SNN_FLAG_NO_PDL) && !multi;
     if (ev) CK(cudaEventRecord(ev[0], s));
     const int64_t t = sim->t + step_k;                              // host copy (direct mode only)
@@ -962,8 +963,9 @@ snn_status snn_create(const snn_config *cfg, snn_sim **out) {
         g_create_error = "snn_config: dev_alloc and dev_free must both be set or both NULL";
         return SNN_E_INVALID;
     }
-    if (cfg->world > 1 && !cfg->nccl_unique_id && cfg->group_key == 0) {
-        g_create_error = "world > 1 needs an nccl_unique_id or a local group_key";
+    if ((cfg->world > 1 && !cfg->nccl_unique_id && cfg->group_key == 0) ||
+        ((cfg->flags & SNN_FLAG_EXCHANGE) && !cfg->nccl_unique_id)) {
+        g_create_error = "world > 1 needs an nccl_unique_id or a local group_key (SNN_FLAG_EXCHANGE: an nccl_unique_id)";
         return SNN_E_INVALID;
     }
     DeviceGuard dg(cfg->device);

@@ -278,7 +278,7 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
         if (net.nstdp) st.recent[(size_t)(t & 3) * st.rstride + (i >> 5)] = rword;
         // this rank's share of the step's input-neuron words, for the exchange
         const uint32_t w = i >> 5, w0 = net.rank_lo[net.rank] >> 5;
-        if (net.world > 1 && i < net.R && w >= w0 && w < w0 + net.wmax) st.sendbuf[w - w0] = fword;
+        if (net.xchg && i < net.R && w >= w0 && w < w0 + net.wmax) st.sendbuf[w - w0] = fword;
     }
 
     if (kPart == 1 || kPart == 4) {              // (the list part, kPart 2 / 3, advances ctr->tf)

@@ -28,6 +28,7 @@ POISSON, LIF_DELTA, LIF_CUBA = 0, 1, 2
 STATIC, STDP = 0, 1
 EXC, INH = 0, 1
 FLAG_NO_GRAPH, FLAG_PHASE_TIMING, FLAG_TRACE, FLAG_NO_PDL, FLAG_IDX16, FLAG_KTIME = 1, 2, 4, 8, 16, 32
+FLAG_EXCHANGE = 64      # the NCCL spike-word exchange even at world == 1 (needs nccl_unique_id)
 PLAST_EVENT, PLAST_LAZY, PLAST_NAIVE = 0, 1, 2        # Fig. 2c / 2b / 2a schedules
 DELIV_SLICED, DELIV_ROWWISE = 0, 1                    # Fig. 3b / 3a delivery
 ALL = 0xFFFFFFFF

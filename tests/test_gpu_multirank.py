@@ -80,3 +80,27 @@ def test_partitioned_d0_equals_single(world):
             assert np.array_equal(g.read_state(f)[lo:hi], r[lo:hi]), f
         ev += g.metrics()["EVENTS"]
     assert ev == ref.metrics()["EVENTS"]
+
+
+@pytest.mark.parametrize("cfg", ["brunel+15", "vogels0"])
+def test_nccl_exchange_path_world1_equals_plain(cfg):
+    """The NCCL data path on one GPU (SNN_FLAG_EXCHANGE, world 1): the
+    communicator from a torch-created ncclUniqueId, ncclAllGather of the step's
+    spike words + k_unpack on the exchange branch of the captured step graph
+    (D >= 1) or between the two k_front parts (D = 0) -- the run equals the
+    plain one bit-exactly (rasters, V, weights)."""
+    import torch
+    from paper_2107_04092_b200 import Snn, FLAG_EXCHANGE
+    rc = W.brunel(9000, p=0.05, plastic=True, delay=15, seed=31) if cfg == "brunel+15" else W.vogels(6000, seed=32)
+    uid = bytes(torch.cuda.nccl.unique_id())
+    out = []
+    for flags, kw in ((0, {}), (FLAG_EXCHANGE, {"nccl_unique_id": uid})):
+        g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, flags=flags, **kw)
+        rc.apply(g)
+        for _ in range(4):
+            g.step(50)
+        out.append((g.read_state("HIST"), g.read_state("V"), g.read_state("WEIGHTS"), g.metrics()["EVENTS"]))
+        g.close()
+    (h0, v0, w0, e0), (h1, v1, w1, e1) = out
+    assert np.array_equal(h0, h1) and np.array_equal(v0, v1) and np.array_equal(w0, w1) and e0 == e1
+    assert int(h0.astype(bool).sum()) > 100
