@@ -481,7 +481,11 @@ def main(argv=None):
                           "allocation excluded; the paper quotes ~200M synapses/ms on its GPU (P:391, context)"},
         "rates_hz": rates,
         "per_step": {k.lower(): v / a.steps for k, v in dm.items()},
-        "gpu_launches": a.steps * ((4 if split else 3) if rc.plastic else 2) + (a.steps if world > 1 else 0),
+        # launches of the library's kernels per step: one per kernel with an in-graph span
+        # (k_front, its second part, k_stdp_ev / k_stdp, k_flush, k_deliver), + k_unpack per exchange
+        "gpu_launches": a.steps * (len([k for k in ("front", "front2", "stdp", "flush", "deliver")
+                                        if spans and k in spans]) or (3 if rc.plastic else 2))
+                        + (a.steps if world > 1 else 0),
         "roofline": roof,
         "kernel_spans": spans,
         "e2e": e2e,
