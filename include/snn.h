@@ -222,7 +222,7 @@ enum {
                                    last step: [kernel][cta][phase], kernels
                                    front / stdp / deliver                        */
     SNN_FIELD_IDX16 = 21,       /* [u16 / S]   slice-local target offsets
-                                   (j - tgt_lo) mod C (SNN_FLAG_IDX16 only)      */
+                                   (j - tgt_lo) mod 2^16 (SNN_FLAG_IDX16 only)   */
     SNN_FIELD_HIST_DEV = 22,    /* [u64 / n]   the device history word, bits 0-63
                                    (bit s: spike at step t - s), that k_stdp
                                    reads; maintained for neurons post-synaptic
