@@ -263,7 +263,9 @@ enum {
                                     synapse of an arriving row, and forced-flush
                                     synapses whose target fired in the window     */
     SNN_METRIC_FLUSH_SYN = 9,    /* of STDP_SYN: forced-flush synapses (event schedule) */
-    SNN_METRIC_FLUSH_WRW = 10    /* of STDP_WRW: their window hits                 */
+    SNN_METRIC_FLUSH_WRW = 10    /* of STDP_WRW: their window hits (the staged flush
+                                    stream counts the hits that changed their weight:
+                                    all but those already at w_max)               */
 };
 
 /* SNN_FIELD_PHASE_TIMES layout: the kernels of a step */

@@ -1066,7 +1066,9 @@ snn_status snn_step(snn_sim *sim, uint32_t n_steps) {
     }
     if (n_steps == 0) return SNN_OK;
     const bool timing = (sim->cfg.flags & SNN_FLAG_PHASE_TIMING) != 0;
-    const bool direct = timing || (sim->cfg.flags & (SNN_FLAG_NO_GRAPH | SNN_FLAG_TRACE)) != 0 || sim->local_group;
+    // (SNN_TRACE_GRAPH, experiments: the per-CTA trace of the graph-replayed step, the last step's marks)
+    const bool trace_direct = (sim->cfg.flags & SNN_FLAG_TRACE) && !getenv("SNN_TRACE_GRAPH");
+    const bool direct = timing || (sim->cfg.flags & SNN_FLAG_NO_GRAPH) || trace_direct || sim->local_group;
     if (direct) {
         for (uint32_t k = 0; k < n_steps; k++) {
             cudaEvent_t *ev = nullptr;

@@ -117,19 +117,51 @@ __device__ __forceinline__ void compact3(Compact2 &sm, uint32_t *len_a, uint32_t
 // the x_post trace.  Returns `fired`; `recent`: a spike in the last H steps.
 // Shared by k_front and k_deliver's epilogue (the fused step), so both compute
 // exactly the same operations.
-__device__ __forceinline__ bool neuron_update(const NetDev &net, const StateDev &st, uint32_t i, const PopDev &p,
-                                              int64_t t, bool &recent) {
+// The update is split into its loads (neuron_load: every state word the step
+// reads, issued together before any store, so a thread waits for one memory
+// round trip instead of a chain of them) and its arithmetic + stores
+// (neuron_step).
+struct NeuronIn {
+    int32_t qe, qi, ref;
+    float V, ge, gi, xq;
+    uint64_t h0, hh0;
+};
+__device__ __forceinline__ void neuron_load(const NetDev &net, const StateDev &st, uint32_t i, const PopDev &p,
+                                            NeuronIn &n) {
+    n.qe = n.qi = n.ref = 0;
+    n.V = n.ge = n.gi = n.xq = 0.0f;
+    n.h0 = n.hh0 = 0ull;
+    if (p.kind == POP_LIF_DELTA) {
+        n.qe = st.in_e[i];
+        n.ref = st.ref[i];
+        n.V = st.V[i];
+    } else if (p.kind == POP_LIF_CUBA) {
+        n.qe = st.in_e[i];
+        n.qi = st.in_i[i];
+        n.ref = st.ref[i];
+        n.V = st.V[i];
+        n.ge = st.ge[i];
+        n.gi = st.gi[i];
+    }
+    if (p.flags & PF_POST_PLASTIC) {
+        n.h0 = st.hist[i];
+        if (net.H > kHistBits) n.hh0 = st.hist_hi[i];
+        n.xq = st.xpost[i];
+    }
+}
+__device__ __forceinline__ bool neuron_step(const NetDev &net, const StateDev &st, uint32_t i, const PopDev &p,
+                                            int64_t t, bool &recent, const NeuronIn &n) {
     bool fired = false;
     recent = false;
     if (p.kind == POP_POISSON) {
         const u32x4 r = philox4x32_10(i, (uint32_t)t, 2u, 0u, net.key0, net.key1);
         fired = (uint64_t)r.x < p.thr;
     } else if (p.kind == POP_LIF_DELTA) {
-        const int32_t q = st.in_e[i];
+        const int32_t q = n.qe;
         const float I = __fmul_rn(__int2float_rn(q), net.inv_scale);
         if (q != 0) st.in_e[i] = 0;
-        int32_t ref = st.ref[i];
-        float V = st.V[i];
+        int32_t ref = n.ref;
+        float V = n.V;
         const float V0 = V;
         const int32_t ref0 = ref;
         if (ref > 0) ref--;
@@ -142,14 +174,14 @@ __device__ __forceinline__ bool neuron_update(const NetDev &net, const StateDev 
         if (__float_as_uint(V) != __float_as_uint(V0)) st.V[i] = V;
         if (ref != ref0) st.ref[i] = ref;
     } else {  // POP_LIF_CUBA
-        const int32_t qe = st.in_e[i], qi = st.in_i[i];
-        float ge = __fadd_rn(st.ge[i], __fmul_rn(__int2float_rn(qe), net.inv_scale));
-        float gi = __fadd_rn(st.gi[i], __fmul_rn(__int2float_rn(qi), net.inv_scale));
+        const int32_t qe = n.qe, qi = n.qi;
+        float ge = __fadd_rn(n.ge, __fmul_rn(__int2float_rn(qe), net.inv_scale));
+        float gi = __fadd_rn(n.gi, __fmul_rn(__int2float_rn(qi), net.inv_scale));
         if (qe != 0) st.in_e[i] = 0;
         if (qi != 0) st.in_i[i] = 0;
-        int32_t ref = st.ref[i];
+        int32_t ref = n.ref;
         const int32_t ref0 = ref;
-        float V = st.V[i];
+        float V = n.V;
         if (ref > 0) {
             ref--;
         } else {
@@ -171,12 +203,12 @@ __device__ __forceinline__ bool neuron_update(const NetDev &net, const StateDev 
         st.gi[i] = gi;
     }
     if (p.flags & PF_POST_PLASTIC) {
-        const uint64_t h0 = st.hist[i];
+        const uint64_t h0 = n.h0;
         const uint64_t h = (h0 << 1) | (uint64_t)fired;
         st.hist[i] = h;
         uint64_t hh = 0ull;
         if (net.H > kHistBits) {                 // H = 128: second word, bits 64..127
-            hh = (st.hist_hi[i] << 1) | (h0 >> 63);
+            hh = (n.hh0 << 1) | (h0 >> 63);
             st.hist_hi[i] = hh;
         }
         recent = (h | hh) != 0ull;
@@ -216,11 +248,17 @@ __device__ __forceinline__ bool neuron_update(const NetDev &net, const StateDev 
             st.fpot[(size_t)(4 + (t & 3)) * st.fstride + i] = f1;
             if (net.fl_lag >= 3) st.fpot[(size_t)(8 + (t & 3)) * st.fstride + i] = f2;
         }
-        const float x = __fmul_rn(st.xpost[i], p.d_minus);   // x_post decay (+1 on a post spike), R7
+        const float x = __fmul_rn(n.xq, p.d_minus);   // x_post decay (+1 on a post spike), R7
         st.xpost[i] = fired ? __fadd_rn(x, 1.0f) : x;
     }
-    if (fired) st.nspk[i] += 1u;
+    if (fired) atomicAdd(st.nspk + i, 1u);          // (fire and forget: no round trip)
     return fired;
+}
+__device__ __forceinline__ bool neuron_update(const NetDev &net, const StateDev &st, uint32_t i, const PopDev &p,
+                                              int64_t t, bool &recent) {
+    NeuronIn n;
+    neuron_load(net, st, i, p, n);
+    return neuron_step(net, st, i, p, t, recent, n);
 }
 
 // kPart (world > 1 with D = 0, where the arrivals of t include the other
@@ -253,18 +291,41 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
     // (Poisson: counter-based, identical on all ranks); the spike bits of the
     // other input neurons arrive by the exchange
     const bool owned = i >= net.R || (i >= net.tgt_lo && i < net.tgt_hi);
+    const bool upd = kPart == 4 ? (valid && i < net.R)
+                                : (kPart != 2 && valid && owned && (kPart != 3 || i >= net.R));
+    // ---- (0) every load of the step's reads that does not depend on this
+    //      step's arithmetic, issued together before any store: the neuron's
+    //      state, the ring words of its arrivals, the row's STDP state
+    NeuronIn nin;
+    if (upd) neuron_load(net, st, i, p, nin);
+    const bool plastic_row = valid && (p.flags & PF_PRE_PLASTIC);
+    const bool lists = kPart != 1 && kPart != 4;
+    uint32_t rw_arr = 0u, rw_arr1 = 0u, rw_arr2 = 0u, rw_prev = 0u, vm_prev = 0u;
+    int32_t tl0 = 0;
+    float xp0 = 0.0f;
+    if (lists && valid) {
+        const uint32_t *ring = st.ring + (i >> 5);
+        const uint32_t rs = net.ring_stride;
+        auto word = [&](int64_t step) { return ring[(size_t)(step & (kRingSlots - 1)) * rs]; };
+        if (net.D != 0 && t >= (int64_t)net.D) rw_arr = word(t - net.D);
+        if (kAhead && t + 1 >= (int64_t)net.D) rw_arr1 = word(t + 1 - net.D);
+        if (kAhead && net.D != 2 && t + 2 >= (int64_t)net.D) rw_arr2 = word(t + 2 - net.D);
+        if (plastic_row) {
+            tl0 = st.tlu[i];
+            xp0 = st.xpre[i];
+            if (t >= 1) vm_prev = st.vmask[par ^ 1u][i >> 5];
+            if (t - 1 >= (int64_t)net.D) rw_prev = word(t - 1 - net.D);
+        }
+    }
     // ---- (1) neuron dynamics (App. B op order); kPart 3 (the fused / split
     //      step): the input neurons [0, R) were updated elsewhere (k_deliver(t-1)'s
     //      epilogue / kPart 4); kPart 4: only those, and the stateless Poisson
     //      draws of the neurons >= R sharing R's ring word
-    if (kPart == 4) {
-        if (valid && i < net.R) fired = neuron_update(net, st, i, p, t, recent);
-        else if (valid && p.kind == POP_POISSON) {
-            const u32x4 r = philox4x32_10(i, (uint32_t)t, 2u, 0u, net.key0, net.key1);
-            fired = (uint64_t)r.x < p.thr;
-        }
-    } else if (kPart != 2 && valid && owned && (kPart != 3 || i >= net.R)) {
-        fired = neuron_update(net, st, i, p, t, recent);
+    if (upd) {
+        fired = neuron_step(net, st, i, p, t, recent, nin);
+    } else if (kPart == 4 && valid && p.kind == POP_POISSON) {
+        const u32x4 r = philox4x32_10(i, (uint32_t)t, 2u, 0u, net.key0, net.key1);
+        fired = (uint64_t)r.x < p.thr;
     }
     const uint32_t fword = __ballot_sync(0xffffffffu, fired);
     const uint32_t rword = __ballot_sync(0xffffffffu, recent);
@@ -290,27 +351,27 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
     // ---- (2) arrival of row i at step t: its spike of step t - D (hist[delay])
     bool arr = false, arr1 = false, arr2 = false;
     if (valid) {
+        const uint32_t b = i & 31;
         if (net.D == 0) arr = kPart == 2 ? ring_bit(st.ring, net.ring_stride, t, i) != 0u : fired;
-        else if (t >= (int64_t)net.D) arr = ring_bit(st.ring, net.ring_stride, t - net.D, i);
+        else arr = (rw_arr >> b) & 1u;
         // kAhead (D >= 2): the arrivals of t + 1 and t + 2 are spikes of steps <= t - 1
-        if (kAhead && t + 1 >= (int64_t)net.D) arr1 = ring_bit(st.ring, net.ring_stride, t + 1 - net.D, i);
+        if (kAhead) arr1 = (rw_arr1 >> b) & 1u;
         if (kAhead && t + 2 >= (int64_t)net.D) {
             // (D = 2: the spike of this step -- this thread's own `fired` where it
             // updated neuron i, the other CTAs of this grid write the ring slot)
             const bool own = owned && (kPart != 3 || i >= net.R);
-            arr2 = (net.D == 2 && own) ? fired : ring_bit(st.ring, net.ring_stride, t + 2 - net.D, i) != 0u;
+            arr2 = net.D == 2 ? (own ? fired : ring_bit(st.ring, net.ring_stride, t, i) != 0u) : ((rw_arr2 >> b) & 1u);
         }
     }
-    const bool plastic_row = valid && (p.flags & PF_PRE_PLASTIC);
     bool visit = false, flush = false;
     RowDesc d, a;
     if (plastic_row) {
         const StdpDev &sd = net.stdp[p.stdp];
-        int32_t tl = st.tlu[i];
-        float xp = st.xpre[i];
+        int32_t tl = tl0;
+        float xp = xp0;
         // finalise a visit of step t-1 (its synapses were updated at t-1)
-        if (t >= 1 && ((st.vmask[par ^ 1u][i >> 5] >> (i & 31)) & 1u)) {
-            const bool arr_prev = (t - 1 >= (int64_t)net.D) && ring_bit(st.ring, net.ring_stride, t - 1 - net.D, i);
+        if (t >= 1 && ((vm_prev >> (i & 31)) & 1u)) {
+            const bool arr_prev = (rw_prev >> (i & 31)) & 1u;
             xp = xpre_after(sd, xp, (int)(t - 1 - tl), arr_prev);
             tl = (int32_t)(t - 1);
             st.xpre[i] = xp;
@@ -363,6 +424,9 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
             a.s1 = sg.y;
         }
     }
+    // (the arriving row's CSR start: loaded before the list compaction, so the
+    // load and the compaction's atomics share one round trip)
+    if (kAhead ? arr1 : arr) a.start = st.row_ptr[i];
     const uint32_t vword = __ballot_sync(0xffffffffu, visit);
     if (net.nstdp && lane == 0 && valid) st.vmask[par][i >> 5] = vword;
     uint32_t sp, sa, sf, np, na, nf;
@@ -373,7 +437,6 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
                  sp, sa, sf, np, na, nf);
         if (flush) st.vdesc[t & 3][(size_t)st.nblk * kFrontThreads - 1 - sf] = d;
         if (arr1) {
-            a.start = st.row_ptr[i];
             a.row = i;
             a.meta |= kMetaArr | ((uint32_t)(p.rcpt_uniform & 3) << 8);
             if (p.rcpt_uniform < 0) a.meta |= (uint32_t)pi << 16;
@@ -396,7 +459,6 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
         if (parr) st.vdesc[t & 3][sp] = d;
         if (flush) st.vdesc[t & 3][(size_t)st.nblk * kFrontThreads - 1 - sf] = d;
         if (arr) {                                       // every arriving row is delivered
-            a.start = st.row_ptr[i];
             a.row = i;
             a.meta = kMetaArr | ((uint32_t)(p.rcpt_uniform & 3) << 8);
             if (p.rcpt_uniform < 0) a.meta |= (uint32_t)pi << 16;
@@ -479,6 +541,14 @@ __device__ __forceinline__ float ldg_f32_if(const float *p, uint32_t pred) {
     float v;
     asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.b32 %0, 0f00000000;\n @q ld.global.nc.f32 %0, [%1];\n}\n"
                  : "=f"(v) : "l"(p), "r"(pred));
+    return v;
+}
+// p[j] if pred, else 0 (one wide multiply-add for the address)
+__device__ __forceinline__ float ldg_f32_idx_if(const float *p, uint32_t j, uint32_t pred) {
+    float v;
+    asm volatile("{\n .reg .pred q;\n .reg .u64 a;\n setp.ne.u32 q, %3, 0;\n mov.b32 %0, 0f00000000;\n"
+                 " mad.wide.u32 a, %2, 4, %1;\n @q ld.global.nc.f32 %0, [a];\n}\n"
+                 : "=f"(v) : "l"(p), "r"(j), "r"(pred));
     return v;
 }
 __device__ __forceinline__ uint32_t ldg_u8_if(const uint8_t *p, uint32_t pred) {
@@ -1379,6 +1449,9 @@ k_stdp_ev(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
 #ifndef SNN_FL_T
 #define SNN_FL_T 1024
 #endif
+#ifndef SNN_FL_BF
+#define SNN_FL_BF 1              // 1: branch-free filter + update (staged table), 0: per-element branches
+#endif
 #ifndef SNN_FL_STAGED
 #define SNN_FL_STAGED 1          // 0: always the bitmap filter (smaller shared memory)
 #endif
@@ -1387,6 +1460,7 @@ constexpr int kFlWarps = kFlT / 32;
 constexpr int kFlRows = 256;
 constexpr int kFlQ = SNN_FL_Q;          // chunks per lane and piece
 constexpr int kFlPieceCh = 32 * kFlQ;   // chunks per piece
+constexpr bool kFlBF = SNN_FL_BF != 0;
 
 struct FlSmem {
     uint64_t bmap;                      // mbarrier of the table's bulk copies
@@ -1397,6 +1471,17 @@ struct FlSmem {
     float dplus[4 * (kMaxHist + 1)];
     uint4 bnd[kFlRows];                 // (kI16) the row's 2^16 crossings relative to cb (0xffffffff: none)
 };
+
+// The row of piece p (warp-uniform): the first r >= cur with incl[r] > p,
+// 32 rows per probe (incl[nrows] = 0xffffffff)
+__device__ __forceinline__ uint32_t fl_row_of(const uint32_t *incl, uint32_t cur, uint32_t nrows, uint32_t p,
+                                              uint32_t lane) {
+    for (;;) {
+        const uint32_t b = __ballot_sync(0xffffffffu, p >= incl[min(cur + lane, nrows)]);
+        cur += __popc(b);
+        if (b != 0xffffffffu) return cur;
+    }
+}
 
 // table: fpos bytes [pp_lo & ~15, pp_hi) (16-byte units), else the bitmap
 __host__ __device__ inline uint32_t fl_tab_bytes(uint32_t pp_lo, uint32_t pp_hi, bool staged) {
@@ -1441,8 +1526,11 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
         for (uint32_t off = 0; off < tab_bytes; off += 32768u)      // (bulk copies of at most 32 KB)
             bulk_g2s(smem_u32(tab) + off, src + off, min(32768u, tab_bytes - off), bmap_a);
     }
+    // (entry 0 of each table is 0: a flush never reads D+[0] (n = age - pos
+    // >= 1), so the branch-free update selects it for a target without a
+    // spike in the window -- w + A+ (x_pre 0) = w, bit for bit)
     for (uint32_t x = threadIdx.x; x < net.nstdp * (kMaxHist + 1); x += kFlT)
-        sm.dplus[x] = st.stdp[x / (kMaxHist + 1)].dplus[x % (kMaxHist + 1)];
+        sm.dplus[x] = (kFlBF && x % (kMaxHist + 1) == 0) ? 0.0f : st.stdp[x / (kMaxHist + 1)].dplus[x % (kMaxHist + 1)];
     if (threadIdx.x < net.nstdp)
         sm.par[threadIdx.x] = make_float4(st.stdp[threadIdx.x].a_plus, st.stdp[threadIdx.x].a_minus,
                                           st.stdp[threadIdx.x].w_max, 0.0f);
@@ -1524,7 +1612,7 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
         uint32_t cur = 0;
         if constexpr (kI16) {
         for (uint32_t p = warp; p < P; p += kFlWarps) {
-            while (p >= sm.incl[cur]) cur++;
+            cur = fl_row_of(sm.incl, cur, nrows, p, lane);
             const EvRow &rr = sm.rows[cur];
             const uint32_t c0 = (p - rr.first) * 64u;            // chunks of 8 synapses, 64 per piece
             const uint32_t lo = rr.lo, hi = rr.hi, nch = (hi + 7) >> 3;
@@ -1543,6 +1631,51 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
             const float4 pr = sm.par[si];
             const float xp = rr.xp;
             const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+            if constexpr (kFlBF && kStaged) {      // (the branch-free form of the 32-bit stream's loop)
+                const float *__restrict__ fpf = fpot + (size_t)4 * (H - age) * st.fstride;
+                float F[2][8];
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    const uint32_t x0 = 8u * (c0 + lane + 32u * q);
+                    const uint32_t h0 = (uint32_t)(bnd.x <= x0) + (uint32_t)(bnd.y <= x0) + (uint32_t)(bnd.z <= x0) +
+                                        (uint32_t)(bnd.w <= x0);
+                    const bool cross = (bnd.x > x0 && bnd.x < x0 + 8) || (bnd.y > x0 && bnd.y < x0 + 8) ||
+                                       (bnd.z > x0 && bnd.z < x0 + 8) || (bnd.w > x0 && bnd.w < x0 + 8);
+                    const uint32_t vw[4] = {J[q].x, J[q].y, J[q].z, J[q].w};
+                    const bool full = __all_sync(0xffffffffu, x0 >= lo && x0 + 8u <= hi);
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const bool in = full || x0 + e - lo < hi - lo;
+                        uint32_t hh = h0;
+                        if (cross)
+                            hh = (uint32_t)(bnd.x <= x0 + e) + (uint32_t)(bnd.y <= x0 + e) + (uint32_t)(bnd.z <= x0 + e) +
+                                 (uint32_t)(bnd.w <= x0 + e);
+                        const uint32_t v = (vw[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+                        const uint32_t j = in ? net.tgt_lo + (hh << 16) + v : pp_lo;
+                        const uint32_t p8 = lds_u8(tab_a + j);
+                        const uint32_t pos = in ? p8 : 0xfeu;
+                        const uint32_t n = pos < age ? age - pos : 0u;
+                        const float f1 = lds_f32(dp + 4u * n);
+                        const float fm = ldg_f32_idx_if(fpf, j, pos == 0xffu);
+                        F[q][e] = pos == 0xffu ? fm : f1;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    const uint32_t x0 = 8u * (c0 + lane + 32u * q);
+                    const uint32_t wb[8] = {Wa[q].x, Wa[q].y, Wa[q].z, Wa[q].w, Wb[q].x, Wb[q].y, Wb[q].z, Wb[q].w};
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const float w0 = __uint_as_float(wb[e]);
+                        const float nw = __fadd_rn(w0, __fmul_rn(pr.x, __fmul_rn(xp, F[q][e])));
+                        const float w = nw < pr.z ? nw : pr.z;
+                        const bool ch = __float_as_uint(w) != __float_as_uint(w0);
+                        stg_f32_if(gw + cb + x0 + e, w, ch);
+                        n_w += ch ? 1u : 0u;
+                    }
+                }
+                continue;
+            }
 #pragma unroll
             for (int q = 0; q < 2; q++) {
                 const uint32_t x0 = 8u * (c0 + lane + 32u * q);
@@ -1589,7 +1722,7 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
         }
         } else {
         for (uint32_t p = warp; p < P; p += kFlWarps) {
-            while (p >= sm.incl[cur]) cur++;
+            cur = fl_row_of(sm.incl, cur, nrows, p, lane);
             const EvRow &rr = sm.rows[cur];
             const uint32_t c0 = (p - rr.first) * kFlPieceCh;
             const uint32_t lo = rr.lo, hi = rr.hi, nch = (hi + 3) >> 2;
@@ -1607,6 +1740,48 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
             const float4 pr = sm.par[si];
             const float xp = rr.xp;
             const uint32_t dp = dp_addr + si * 4u * (kMaxHist + 1);
+            if constexpr (kFlBF && kStaged) {
+                // (1) every element's factor f: D+[age - pos] for one spike in the
+                // window, the step's flush factor for several (fpot, k_front), 0
+                // for none -- no branch; the several-spike loads of the whole
+                // piece are issued together
+                const float *__restrict__ fpf = fpot + (size_t)4 * (H - age) * st.fstride;
+                float F[kFlQ][4];
+#pragma unroll
+                for (int q = 0; q < kFlQ; q++) {
+                    const uint32_t x0 = 4u * (c0 + lane + 32u * q);
+                    const uint32_t jj[4] = {J[q].x, J[q].y, J[q].z, J[q].w};
+                    // (warp-uniform: no lane holds a span edge -> no per-element bounds)
+                    const bool full = __all_sync(0xffffffffu, x0 >= lo && x0 + 4u <= hi);
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const bool in = full || x0 + e - lo < hi - lo;   // inside [lo, hi)
+                        const uint32_t j = in ? jj[e] : pp_lo;          // (pp_lo: inside the table)
+                        const uint32_t p8 = lds_u8(tab_a + j);
+                        const uint32_t pos = in ? p8 : 0xfeu;
+                        const uint32_t n = pos < age ? age - pos : 0u;
+                        const float f1 = lds_f32(dp + 4u * n);
+                        const float fm = ldg_f32_idx_if(fpf, j, pos == 0xffu);
+                        F[q][e] = pos == 0xffu ? fm : f1;
+                    }
+                }
+                // (2) w = min(w + A+ (x_pre f), w_max) (= w where f = 0), stored if changed
+#pragma unroll
+                for (int q = 0; q < kFlQ; q++) {
+                    const uint32_t x0 = 4u * (c0 + lane + 32u * q);
+                    const uint32_t wb[4] = {Wt[q].x, Wt[q].y, Wt[q].z, Wt[q].w};
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const float w0 = __uint_as_float(wb[e]);
+                        const float nw = __fadd_rn(w0, __fmul_rn(pr.x, __fmul_rn(xp, F[q][e])));
+                        const float w = nw < pr.z ? nw : pr.z;
+                        const bool ch = __float_as_uint(w) != __float_as_uint(w0);
+                        stg_f32_if(gw + cb + x0 + e, w, ch);
+                        n_w += ch ? 1u : 0u;
+                    }
+                }
+                continue;
+            }
 #pragma unroll
             for (int q = 0; q < kFlQ; q++) {
                 const uint32_t x0 = 4u * (c0 + lane + 32u * q);
@@ -1647,9 +1822,12 @@ k_flush(NetDev net, StateDev st, uint32_t pp_lo, uint32_t pp_hi) {
         __syncthreads();                           // row table reused next round
     }
     if (!tab_ready && threadIdx.x == 0) mbar_wait(bmap_a, 0);   // (no rows) the copy has landed
+    // (the branch-free stream counts no window hits separately: a hit changes
+    // its weight unless it is already at w_max, so the weights read and
+    // written there are counted by the stores)
+    n_hit = __reduce_add_sync(0xffffffffu, (kFlBF && kStaged) ? n_w : n_hit);
     n_syn = __reduce_add_sync(0xffffffffu, n_syn);
     n_w = __reduce_add_sync(0xffffffffu, n_w);
-    n_hit = __reduce_add_sync(0xffffffffu, n_hit);
     if (lane == 0) {
         if (n_syn) {
             atomicAdd(&st.ctr->metric[3], (unsigned long long)n_syn);
@@ -1688,7 +1866,8 @@ constexpr int kDelWin = 32 * kDelThreads;   // flattened elements per owner wind
 #ifndef SNN_DEL_MINB
 #define SNN_DEL_MINB 2
 #endif
-constexpr int kDelU = SNN_DEL_U;   // elements in flight per thread
+constexpr int kDelU = SNN_DEL_U;   // elements in flight per thread (element passes)
+
 
 // Block-wide inclusive scan of a packed pair (low 32 bits: elements, high 32:
 // segments) per thread.
@@ -2031,12 +2210,13 @@ k_deliver(NetDev net, StateDev st, uint32_t epi) {
                 }
             }
             // ---- elements: thread x takes w0 + x + 512 u (coalesced)
-            if (kPlT && pl_on)
+            if (kPlT && pl_on) {
                 deliver_window<kMulti, kIdx16, kPlT, kH128>(net, st, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale,
                                                             slo, ps);
-            else
+            } else {
                 deliver_window<kMulti, kIdx16, false, false>(net, st, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale,
                                                              slo, ps);
+            }
             if (w0 + kDelWin < T) __syncthreads();  // bitmap reused by the next window
         }
         __syncthreads();                           // table reused next round
