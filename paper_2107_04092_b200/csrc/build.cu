@@ -166,66 +166,82 @@ __device__ __forceinline__ void geo_row_warp(const NetDev &net, const BuildTabs 
 constexpr int kGeoWarpThreads = 256;   // 8 rows per CTA
 
 // Pass 1 (warp per row): the pivots directly -- piv[i][k] = #kept targets
-// below tgt_lo + kC (Fig. 1) -- and the row length.  Slices are
-// non-decreasing along the row, so a kept target at rank q in slice kj after
-// one in slice kp writes piv[k] = q for kp < k <= kj.
+// below B_k = tgt_lo + kC (Fig. 1) -- and the row length.  Targets ascend, so
+// after an iteration whose last kept target lies in slice kl, the pivots
+// k <= kl not yet written are final: each is the row's kept count before the
+// iteration plus the iteration's kept targets below B_k (a warp reduction);
+// lane k - k0 holds pivot k and they are stored together, coalesced.
 __global__ void __launch_bounds__(kGeoWarpThreads)
 k_count_warp(NetDev net, BuildTabs tabs, uint32_t *piv, int64_t *len) {
     const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (i >= net.N) return;                           // (warp-uniform)
     const int sp = find_pop(net, i);
     uint32_t *prow = piv + (size_t)i * (net.nslices + 1);
-    int last = -1;                                    // slice of the row's last kept target so far (warp-uniform)
+    const uint32_t C = net.C;
+    uint32_t next = 0;                                // first pivot not yet written (warp-uniform)
     uint32_t total = 0;
     geo_row_warp(net, tabs, i, sp, net.tgt_lo, net.tgt_hi, [&](const uint32_t (&jv)[4], uint32_t mask, uint32_t q0, int) {
-        // the lane's last kept slice, and the max over the lanes before it (slices ascend along the row)
-        int mine = -1;
+        // the iteration's last kept target (every lane: the warp maximum)
+        uint32_t jmax = 0;
+        bool any = false;
 #pragma unroll
         for (int e = 0; e < 4; e++)
-            if ((mask >> e) & 1u) mine = (int)((jv[e] - net.tgt_lo) / net.C);
-        int incl = mine;
+            if ((mask >> e) & 1u) { jmax = jv[e]; any = true; }
+        const uint32_t kb = __ballot_sync(0xffffffffu, any);
+        const uint32_t nk_it = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mask));
+        const uint32_t before = __shfl_sync(0xffffffffu, q0, 0);       // kept before this iteration
+        if (kb) {
+            jmax = __shfl_sync(0xffffffffu, jmax, 31 - __clz(kb));      // (the highest lane with a kept target)
+            const uint32_t kl = (jmax - net.tgt_lo) / C;                // its slice: pivots next .. kl are final
+            for (uint32_t k0 = next; k0 <= kl; k0 += 32) {
+                uint32_t val = 0;
+                const uint32_t kend = min(kl + 1, k0 + 32u);
+                for (uint32_t k = k0; k < kend; k++) {                  // (warp-uniform loop)
+                    const uint32_t Bk = net.tgt_lo + k * C;
+                    uint32_t below = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (uint32_t)o) incl = max(incl, y);
+                    for (int e = 0; e < 4; e++) below += (((mask >> e) & 1u) && jv[e] < Bk) ? 1u : 0u;
+                    below = __reduce_add_sync(0xffffffffu, below);
+                    if (lane == k - k0) val = before + below;
+                }
+                if (k0 + lane < kend) prow[k0 + lane] = val;
+            }
+            next = kl + 1;
         }
-        int prev = __shfl_up_sync(0xffffffffu, incl, 1);
-        if (lane == 0) prev = -1;
-        prev = max(prev, last);
-        uint32_t q = q0;
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            if (!((mask >> e) & 1u)) continue;
-            const int kj = (int)((jv[e] - net.tgt_lo) / net.C);
-            for (int k = prev + 1; k <= kj; k++) prow[k] = q;
-            prev = max(prev, kj);
-            q++;
-        }
-        last = max(last, __shfl_sync(0xffffffffu, incl, 31));
-        total = __shfl_sync(0xffffffffu, q, 31);          // (lane 31's q = the ranks so far)
+        total = before + nk_it;
     });
     // slices after the last kept target: the row length
-    for (int k = last + 1 + (int)lane; k <= (int)net.nslices; k += 32) prow[k] = total;
+    for (uint32_t k = next + lane; k <= net.nslices; k += 32) prow[k] = total;
     if (lane == 0) len[i] = total;
 }
 
-// Pass 3 (warp per row): targets (sorted by construction) and initial weights.
+// Pass 3 (warp per row): targets (sorted by construction) and initial weights;
+// an iteration's kept targets are staged in shared memory by rank, then
+// written out coalesced.
 __global__ void __launch_bounds__(kGeoWarpThreads)
 k_fill_warp(NetDev net, BuildTabs tabs, const int64_t *row_ptr, uint32_t *idx, float *w) {
-    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    __shared__ uint32_t stage[kGeoWarpThreads / 32][128];
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (i >= net.N) return;
+    uint32_t *buf = stage[threadIdx.x >> 5];
     const int sp = find_pop(net, i);
     const int64_t base = row_ptr[i];
     geo_row_warp(net, tabs, i, sp, net.tgt_lo, net.tgt_hi, [&](const uint32_t (&jv)[4], uint32_t mask, uint32_t q0, int d) {
         const float wd = tabs.weight[sp * kMaxPops + d];
-        uint32_t q = q0;
+        const uint32_t before = __shfl_sync(0xffffffffu, q0, 0);
+        uint32_t q = q0 - before;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             if (!((mask >> e) & 1u)) continue;
-            idx[base + q] = jv[e];
-            w[base + q] = wd;
-            q++;
+            buf[q++] = jv[e];
         }
+        const uint32_t n = __shfl_sync(0xffffffffu, q, 31);             // (lane 31's rank end = the count)
+        __syncwarp();
+        for (uint32_t x = lane; x < n; x += 32) {
+            idx[base + before + x] = buf[x];
+            w[base + before + x] = wd;
+        }
+        __syncwarp();
     });
 }
 

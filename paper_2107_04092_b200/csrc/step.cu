@@ -1866,7 +1866,10 @@ constexpr int kDelWin = 32 * kDelThreads;   // flattened elements per owner wind
 #ifndef SNN_DEL_MINB
 #define SNN_DEL_MINB 2
 #endif
-constexpr int kDelU = SNN_DEL_U;   // elements in flight per thread (element passes)
+constexpr int kDelU = SNN_DEL_U;   // elements in flight per thread
+#ifndef SNN_DEL_PRE
+#define SNN_DEL_PRE 1              // kAhead: the static segments delivered before the dependency wait
+#endif
 
 
 // Block-wide inclusive scan of a packed pair (low 32 bits: elements, high 32:
@@ -1932,16 +1935,21 @@ __shared__ uint2 g_del_row[kDelRows];           // segment g: (x_pre at tlu, met
 __shared__ float g_del_dp[4 * (kMaxHist + 1)];  // D+ tables
 __shared__ float4 g_del_par[4];                 // per projection: a_plus, a_minus, w_max
 struct DelStdp {
-    uint32_t xq_a;             // shared: the slice's x_post (by offset j - slo), then its fpos bytes at + 4 C
+    uint32_t xq_a;             // shared, by slice offset jl = j - slo: x_post (f32) at + 4 jl, the history
+                               // words at + 4 C + 8 jl (bits 64..127 at + 12 C + 8 jl, H = 128), the
+                               // spike positions (u8) at + fp_off + jl
     uint32_t n_syn, n_w;       // metrics
 };
-
-// (several post spikes in the H window: rare in the paper's regime)
 template <bool kH128>
-__device__ __noinline__ float deliver_stdp_hist(const uint64_t *hist, const uint64_t *hist_hi, uint32_t j, float w,
-                                                float xq, float xp, uint32_t age, uint32_t dp, float4 pr) {
-    return stdp_synapse(w, window_lo(__ldg(hist + j), (int)age), true, xq, xp, (int)age, dp, pr.x, pr.y, pr.z,
-                        kH128 ? window_hi(__ldg(hist_hi + j), (int)age) : 0ull);
+__host__ __device__ constexpr uint32_t del_fpos_off(uint32_t C) { return 4u * C + (kH128 ? 16u : 8u) * C; }
+
+// (several post spikes in the H window: rare in the paper's regime, P:399;
+// the slice's history words are staged in shared memory)
+template <bool kH128>
+__device__ __noinline__ float deliver_stdp_hist(uint32_t h_a, uint32_t C, float w, float xq, float xp, uint32_t age,
+                                                uint32_t dp, float4 pr) {
+    return stdp_synapse(w, window_lo(lds_u64(h_a), (int)age), true, xq, xp, (int)age, dp, pr.x, pr.y, pr.z,
+                        kH128 ? window_hi(lds_u64(h_a + 8u * C), (int)age) : 0ull);
 }
 
 template <bool kH128>
@@ -1950,13 +1958,13 @@ __device__ __forceinline__ float deliver_stdp(const StateDev &st, uint32_t xq_a,
     const uint2 rw = g_del_row[g];                         // (x_pre bits, meta)
     const float xp = __uint_as_float(rw.x);
     const uint32_t age = rw.y & kMetaAge, si = (rw.y >> 12) & 0x3u;
-    const uint32_t pos = lds_u8(xq_a + 4u * C + jl);
+    const uint32_t pos = lds_u8(xq_a + del_fpos_off<kH128>(C) + jl);
     const float xq = lds_f32(xq_a + 4u * jl);
     const uint32_t dp = smem_u32(g_del_dp) + si * 4u * (kMaxHist + 1);
     const float4 pr = g_del_par[si];
     float w = w0;
     if (pos == 0xffu) {
-        w = deliver_stdp_hist<kH128>(st.hist, st.hist_hi, j, w, xq, xp, age, dp, pr);
+        w = deliver_stdp_hist<kH128>(xq_a + 4u * C + 8u * jl, C, w, xq, xp, age, dp, pr);
     } else {
         if (pos < age) {                     // the window's only post spike (0xfe: none)
             const float nw = __fadd_rn(w, __fmul_rn(pr.x, __fmul_rn(xp, lds_f32(dp + 4u * (age - pos)))));
@@ -2037,10 +2045,10 @@ __device__ __forceinline__ void deliver_pass(const NetDev &net, const StateDev &
 }
 
 template <bool kMulti, bool kIdx16, bool kPl, bool kH128>
-__device__ __forceinline__ void deliver_window(const NetDev &net, const StateDev &st, uint32_t wlen, uint32_t w0,
-                                               uint32_t bw_a, uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a,
+__device__ __forceinline__ void deliver_window(const NetDev &net, const StateDev &st, uint32_t xa, uint32_t wlen,
+                                               uint32_t w0, uint32_t bw_a, uint32_t ptr_a, uint32_t rc_a, uint32_t acc_a,
                                                uint64_t dw, float scale, uint32_t slo, DelStdp &ps) {
-    for (uint32_t x0 = 0; x0 < wlen; x0 += kDelThreads * kDelU) {
+    for (uint32_t x0 = xa; x0 < wlen; x0 += kDelThreads * kDelU) {      // (window elements [xa, wlen))
         if (x0 + kDelThreads * kDelU <= wlen)
             deliver_pass<kMulti, false, kIdx16, kPl, kH128>(net, st, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw,
                                                             scale, slo, ps);
@@ -2048,6 +2056,15 @@ __device__ __forceinline__ void deliver_window(const NetDev &net, const StateDev
             deliver_pass<kMulti, true, kIdx16, kPl, kH128>(net, st, x0, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw,
                                                            scale, slo, ps);
     }
+}
+
+// k_deliver's dependency wait: kAhead, k_front(t) (x_post, histories; inputs
+// consumed); else k_stdp(t) (or k_front(t), already waited)
+__device__ __forceinline__ void del_wait(const StateDev &st, unsigned long long &t_wait) {
+    pdl_wait();
+    pdl_launch();
+    if (st.kspan) t_wait = gtimer();
+    trace_mark(st.trace, 2, 1);
 }
 
 // One CTA per (slice k, split s) (Fig. 3b).  The CTA tabulates the
@@ -2121,6 +2138,7 @@ k_deliver(NetDev net, StateDev st, uint32_t epi) {
     // w[c] at idx[c] + dw, or at 2 idx16[c] + dw (bytes)
     const uint64_t dw = idx16 ? (uint64_t)st.w - 2ull * (uint64_t)st.idx16 : (uint64_t)st.w - (uint64_t)st.idx;
     uint32_t n_ev = 0, n_seg = 0;
+    bool waited = !kAhead && net.nstdp == 0;    // (that case waited above)
     for (uint32_t r0 = r_begin; r0 < r_end; r0 += kDelRows) {
         // ---- tabulate (two rows per thread): descriptor + pivot pair
         uint32_t len2[2] = {0, 0};
@@ -2151,21 +2169,41 @@ k_deliver(NetDev net, StateDev st, uint32_t epi) {
                 if (rcq[q] == 3u) rcq[q] = 3u | (((d2[q].meta >> 16) & 0xfu) << 2);
             }
         }
-        const uint32_t ns = (len2[0] != 0) + (len2[1] != 0);
+        // kAhead: the segments without a plastic part (static synapses: weights
+        // and ids fixed) come first in the flattened order and are delivered
+        // before the dependency wait, while k_front(t) still runs; the plastic
+        // ones (STDP of the arrival, Fig. 2c, needs k_front(t)'s post spikes)
+        // after it.  Else (D < 2) every segment after the wait.
+        bool plq[2] = {false, false};
+#pragma unroll
+        for (int q = 0; q < 2; q++)
+            plq[q] = kAhead && len2[q] != 0 && (net.nstdp != 0) && max(pp[q].x, d2[q].s0) < min(pp[q].y, d2[q].s1);
+        const uint32_t ns_s = (len2[0] != 0 && !plq[0]) + (len2[1] != 0 && !plq[1]);
+        const uint32_t ns_p = (uint32_t)plq[0] + (uint32_t)plq[1];
+        const uint32_t ne_s = (plq[0] ? 0u : len2[0]) + (plq[1] ? 0u : len2[1]);
+        const uint32_t ne_p = (plq[0] ? len2[0] : 0u) + (plq[1] ? len2[1] : 0u);
         n_ev += len2[0] + len2[1];
-        n_seg += ns;
+        n_seg += ns_s + ns_p;
         // ---- compact the non-empty segments: flattened start and slot of each
-        unsigned long long tot = 0;
-        const unsigned long long inc =
-            block_incl_scan64(((unsigned long long)ns << 32) | (len2[0] + len2[1]), wsum64, tot);
-        const uint32_t T = (uint32_t)tot;
+        // (static ones first: slots [0, Ns), elements [0, Ts); then the plastic)
+        unsigned long long tot_s = 0, tot_p = 0;
+        const unsigned long long inc_s =
+            block_incl_scan64(((unsigned long long)ns_s << 32) | ne_s, wsum64, tot_s);
+        __syncthreads();                             // (wsum64 reused)
+        const unsigned long long inc_p =
+            block_incl_scan64(((unsigned long long)ns_p << 32) | ne_p, wsum64, tot_p);
+        const uint32_t Ts = (uint32_t)tot_s, Ns = (uint32_t)(tot_s >> 32);
+        const uint32_t T = Ts + (uint32_t)tot_p;
+        uint32_t es = (uint32_t)inc_s - ne_s, ep = Ts + (uint32_t)inc_p - ne_p;   // next flattened start
+        uint32_t gs = (uint32_t)(inc_s >> 32) - ns_s, gp = Ns + (uint32_t)(inc_p >> 32) - ns_p;
         uint32_t est[2];                             // flattened start of the thread's two segments
-        est[0] = (uint32_t)inc - len2[0] - len2[1];
-        est[1] = est[0] + len2[0];
-        uint32_t g = (uint32_t)(inc >> 32) - ns;     // compacted slot of the first non-empty one
 #pragma unroll
         for (int q = 0; q < 2; q++) {
             if (len2[q] == 0) continue;
+            uint32_t &e = plq[q] ? ep : es;
+            uint32_t &g = plq[q] ? gp : gs;
+            est[q] = e;
+            e += len2[q];
             s_rc[g] = (uint8_t)rcq[q];
             s_ptr[g] = idx16 ? (uint64_t)(st.idx16 + c0q[q]) - 2ull * est[q]
                              : (uint64_t)(st.idx + c0q[q]) - 4ull * est[q];
@@ -2193,33 +2231,46 @@ k_deliver(NetDev net, StateDev st, uint32_t epi) {
             const uint32_t winc = block_incl_scan<kDelThreads>(pc, wsum, wt);
             s_bw[threadIdx.x].y = before + winc - pc - 1u;
             __syncthreads();
-            if (r0 == r_begin && w0 == 0) {   // (the segment tables and the bitmap are ready)
-                pdl_wait();    // kAhead: k_front(t) (x_post, histories; inputs consumed); else k_stdp(t)
-                pdl_launch();
-                if (st.kspan) t_wait = gtimer();
-                trace_mark(st.trace, 2, 1);
+            // ---- elements: thread x takes w0 + x + 512 u (coalesced); the
+            //      static part of the window [0, xs) before the wait (kAhead)
+            const uint32_t xs = (kAhead && SNN_DEL_PRE) ? (Ts > w0 ? min(Ts - w0, wlen) : 0u) : 0u;
+            if (xs)
+                deliver_window<kMulti, kIdx16, false, false>(net, st, 0u, xs, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale,
+                                                             slo, ps);
+            if (xs < wlen && !waited) {
+                del_wait(st, t_wait);
+                waited = true;
                 if (kPlT && pl_on) {
-                    // the slice's x_post and spike positions (k_front(t)) -> shared
+                    // the slice's x_post, history words and spike positions (k_front(t)) -> shared
                     const uint32_t plo = net.pp_lo > slo ? net.pp_lo : slo, phi = net.pp_hi < shi ? net.pp_hi : shi;
                     const uint8_t *fpos = st.fpos + (size_t)(t & 3) * st.fstride;
+                    unsigned char *xs_b = reinterpret_cast<unsigned char *>(acc + net.nrcpt * C);
                     for (uint32_t j = plo + threadIdx.x; j < phi; j += kDelThreads) {
-                        reinterpret_cast<float *>(acc + net.nrcpt * C)[j - slo] = st.xpost[j];
-                        reinterpret_cast<uint8_t *>(acc + (net.nrcpt + 1) * C)[j - slo] = fpos[j];
+                        const uint32_t jl = j - slo;
+                        reinterpret_cast<float *>(xs_b)[jl] = st.xpost[j];
+                        reinterpret_cast<uint64_t *>(xs_b + 4u * C)[jl] = st.hist[j];
+                        if (kH128) reinterpret_cast<uint64_t *>(xs_b + 12u * C)[jl] = st.hist_hi[j];
+                        xs_b[del_fpos_off<kH128>(C) + jl] = fpos[j];
                     }
                     __syncthreads();
                 }
             }
-            // ---- elements: thread x takes w0 + x + 512 u (coalesced)
-            if (kPlT && pl_on) {
-                deliver_window<kMulti, kIdx16, kPlT, kH128>(net, st, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale,
-                                                            slo, ps);
-            } else {
-                deliver_window<kMulti, kIdx16, false, false>(net, st, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw, scale,
-                                                             slo, ps);
+            if (xs < wlen) {
+                if (kPlT && pl_on)
+                    deliver_window<kMulti, kIdx16, kPlT, kH128>(net, st, xs, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw,
+                                                                scale, slo, ps);
+                else
+                    deliver_window<kMulti, kIdx16, false, false>(net, st, xs, wlen, w0, bw_a, ptr_a, rc_a, acc_a, dw,
+                                                                 scale, slo, ps);
             }
             if (w0 + kDelWin < T) __syncthreads();  // bitmap reused by the next window
         }
         __syncthreads();                           // table reused next round
+    }
+    // (the write-back adds to the inputs k_front(t) consumed: after its completion)
+    if (!waited) {
+        del_wait(st, t_wait);
+        waited = true;
     }
     trace_mark(st.trace, 2, 2);
     // ---- write-back (one coalesced pass; several CTAs may share a slice)
@@ -2250,8 +2301,6 @@ k_deliver(NetDev net, StateDev st, uint32_t epi) {
     }
     // kAhead: the arriving rows of the step (k_front counts the arrivals of t + 1)
     if (kAhead && k == 0 && split == 0 && threadIdx.x == 0 && nAs) atomicAdd(&st.ctr->metric[1], (unsigned long long)nAs);
-    pdl_wait();            // (no segments) this grid still completes after its primary
-    pdl_launch();
     if (kAhead && epi && k < net.nslices) {
         // ---- the fused step (SURVEY 8(a4) fusion lever 2): the last CTA of
         //      the slice to finish its write-back updates the slice's neurons
@@ -2535,7 +2584,8 @@ size_t stdp_smem_bytes(const NetDev &net, uint32_t pp_lo, uint32_t pp_hi) {
 // accumulators [nrcpt][C]; + the slice's x_post [C] and fpos [C] with the
 // plastic arrivals' STDP (kAhead with STDP)
 size_t deliver_smem_bytes(const NetDev &net, bool ahead) {
-    return 4ull * net.nrcpt * net.C + (ahead && net.nstdp ? 5ull * net.C + 16 : 0ull);
+    // + (plastic arrivals) the slice's x_post, history words and spike positions
+    return 4ull * net.nrcpt * net.C + (ahead && net.nstdp ? (13ull + (net.H > kHistBits ? 8ull : 0ull)) * net.C + 16 : 0ull);
 }
 
 // The dynamic shared-memory limit is an attribute of the kernel function, not
