@@ -112,11 +112,35 @@ __device__ __forceinline__ void geo_row_warp(const NetDev &net, const BuildTabs 
         int64_t c0 = -1;                              // candidate position of the last draw so far
         for (uint32_t n0 = 0;; n0 += 128) {
             const u32x4 r = philox4x32_10(i, (n0 >> 2) + lane, 4u, (uint32_t)d, net.key0, net.key1);
-            uint32_t g[4], keep = 0;
+            uint32_t g[4], keep = 0, kk[4];
             int64_t gs = 0;
+            // the inverse-CDF estimates of the lane's four gaps and both table
+            // entries that confirm them, loaded together; a draw whose estimate
+            // the table does not confirm takes the corrected search (rare)
+            {
+                uint32_t t0[4], t1[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const uint32_t x = lane_of(r, (uint32_t)e);
+                    int k = kGapTab;
+                    if (x != 0u) {
+                        const float ks = ceilf((__log2f((float)x) - 32.0f) * inv_l2q) - 1.0f;
+                        k = ks < 0.0f ? 0 : ks > (float)kGapTab ? kGapTab : (int)ks;
+                    }
+                    kk[e] = (uint32_t)k;
+                    t0[e] = k > 0 ? __ldg(tab + k - 1) : 0xffffffffu;        // want tab[k-1] > x (or k == 0)
+                    t1[e] = k < kGapTab ? __ldg(tab + k) : 0u;               // want tab[k] <= x (or k == kGapTab)
+                }
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const uint32_t x = lane_of(r, (uint32_t)e);
+                    const bool ok = (kk[e] == 0u || t0[e] > x) && t1[e] <= x;
+                    if (!ok) kk[e] = geo_gap_count(tab, inv_l2q, x);
+                }
+            }
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                const uint32_t k = geo_gap_count(tab, inv_l2q, lane_of(r, (uint32_t)e));
+                const uint32_t k = kk[e];
                 const bool beyond = k == (uint32_t)kGapTab;   // advance kGapTab, keep nothing
                 g[e] = beyond ? (uint32_t)kGapTab : k + 1;
                 keep |= (beyond ? 0u : 1u) << e;
@@ -171,7 +195,7 @@ constexpr int kGeoWarpThreads = 256;   // 8 rows per CTA
 // k <= kl not yet written are final: each is the row's kept count before the
 // iteration plus the iteration's kept targets below B_k (a warp reduction);
 // lane k - k0 holds pivot k and they are stored together, coalesced.
-__global__ void __launch_bounds__(kGeoWarpThreads)
+__global__ void __launch_bounds__(kGeoWarpThreads, 4)
 k_count_warp(NetDev net, BuildTabs tabs, uint32_t *piv, int64_t *len) {
     const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (i >= net.N) return;                           // (warp-uniform)
@@ -218,7 +242,7 @@ k_count_warp(NetDev net, BuildTabs tabs, uint32_t *piv, int64_t *len) {
 // Pass 3 (warp per row): targets (sorted by construction) and initial weights;
 // an iteration's kept targets are staged in shared memory by rank, then
 // written out coalesced.
-__global__ void __launch_bounds__(kGeoWarpThreads)
+__global__ void __launch_bounds__(kGeoWarpThreads, 4)
 k_fill_warp(NetDev net, BuildTabs tabs, const int64_t *row_ptr, uint32_t *idx, float *w) {
     __shared__ uint32_t stage[kGeoWarpThreads / 32][128];
     const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;

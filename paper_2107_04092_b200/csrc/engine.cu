@@ -798,7 +798,8 @@ static snn_status enqueue_step(snn_sim *sim, cudaStream_t s, cudaEvent_t *ev, bo
             if (sim->pipe == 2) CK(launch_stdp_ev(net, st, sim->stdp_grid, sim->pp_lo, sim->pp_hi, s, pdl, 1));
             CK(cudaStreamWaitEvent(side, sim->ev_front, 0));
             if (sim->use_prio) set_launch_priority(sim->prio_lo);
-            CK(launch_stdp_ev(net, st, sim->flush_grid_side, sim->pp_lo, sim->pp_hi, side, false, 2));
+            // (SNN_SKIP_FLUSH: experiments only -- the step without its forced flushes, WRONG weights)
+            if (!getenv("SNN_SKIP_FLUSH")) CK(launch_stdp_ev(net, st, sim->flush_grid_side, sim->pp_lo, sim->pp_hi, side, false, 2));
             if (sim->use_prio) set_launch_priority(sim->prio_hi);
             CK(cudaEventRecord(sim->ev_flush[gk & 3], side));
         } else if (sim->ahead) {
