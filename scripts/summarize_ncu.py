@@ -90,7 +90,8 @@ for d in data:
 tot = sum(sum(m["gpu__time_duration.sum"]) for m in agg.values())
 lines = [os.environ.get("NCU_LAUNCH_CMD",
                         "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                        "--clock-control none -s 3000 -c 300 on `python bench.py --steps 1000 --warmup 1000`")
+                        "--clock-control none -k regex:\"k_front|k_deliver|k_flush\" -s 9000 -c 300 on `python bench.py --steps 200 "
+                        "--warmup 20 --settle 3000 --no-cpu-baseline --no-e2e --no-ktime` (scripts/gpu_evidence.sh)")
          + " (graph replay; cold-cache, serialised)"]
 for k, m in agg.items():
     t = m["gpu__time_duration.sum"]
