@@ -438,6 +438,7 @@ k_front(NetDev net, StateDev st, uint32_t use_tf) {
         if (flush) st.vdesc[t & 3][(size_t)st.nblk * kFrontThreads - 1 - sf] = d;
         if (arr1) {
             a.row = i;
+            if (!plastic_row) a.meta = 0u;
             a.meta |= kMetaArr | ((uint32_t)(p.rcpt_uniform & 3) << 8);
             if (p.rcpt_uniform < 0) a.meta |= (uint32_t)pi << 16;
             if (!plastic_row) {

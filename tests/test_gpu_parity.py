@@ -92,6 +92,22 @@ def test_vogels_cfg1_raster_and_state_bit_exact_300_steps():
     assert g.read_state("SPIKE_COUNT").sum() > 0
 
 
+@pytest.mark.parametrize("delay,flags", [(2, 0), (5, 0), (5, "IDX16")])
+def test_vogels_two_receptors_ahead_step_bit_exact(delay, flags):
+    """Vogels-Abbott (CUBA, excitatory and inhibitory receptors) with D >= 2:
+    the ahead step, whose k_deliver delivers every (static) segment before its
+    dependency wait into the two receptor accumulators -- rasters, V,
+    currents and both pending inputs bit-exact for 200 steps."""
+    from paper_2107_04092_b200 import FLAG_IDX16
+    rc = W.vogels(4000, seed=7, delay=delay)
+    g, o = _pair(rc, slice_width=128, flags=FLAG_IDX16 if flags == "IDX16" else 0)
+    _run_compare(g, o, 200, every=5)
+    assert np.array_equal(g.read_state("G_EXC"), o.array("ge"))
+    assert np.array_equal(g.read_state("G_INH"), o.array("gi"))
+    assert g.read_state("SPIKE_COUNT").sum() > 0
+    assert g.metrics()["EVENTS"] == o.events
+
+
 @pytest.mark.parametrize("C", [64, 160, 1024])
 def test_brunel_static_bit_exact(C):
     rc = W.brunel(12000, p=0.02, plastic=False, seed=4)
