@@ -703,7 +703,10 @@ static snn_status finalize(snn_sim *sim) {
     if (const char *sp = getenv("SNN_DELIVER_SPLITS")) sim->splits = std::max(1, atoi(sp));  // tuning knob
     sim->stdp_grid = (uint32_t)nsm;                 // k_stdp: one CTA per SM
     sim->flush_grid = (uint32_t)nsm * flush_ctas_per_sm();
-    sim->flush_grid_side = std::max(1, nsm / 2);
+    // k_flush's share of the SMs beside the critical path: half of them for
+    // H = 64; H = 128 flushes half as many rows per step, so 2/7 of them
+    // (measured on cfg3: 42 of 148 SMs, 40.5 us/step vs 45.5 on 74)
+    sim->flush_grid_side = std::max(1, net.H > kHistBits ? nsm * 2 / 7 : nsm / 2);
     if (const char *e = getenv("SNN_FL_CTAS")) sim->flush_grid_side = std::max(1, atoi(e));   // (experiments)
 
     CK(cudaStreamSynchronize(s));
