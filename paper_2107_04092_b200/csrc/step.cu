@@ -1862,7 +1862,7 @@ constexpr int kDelWarps = kDelThreads / 32;
 constexpr int kDelRows = 1024;     // row table per round (two rows per thread)
 constexpr int kDelWin = 32 * kDelThreads;   // flattened elements per owner window (one bitmap word per thread)
 #ifndef SNN_DEL_U
-#define SNN_DEL_U 4
+#define SNN_DEL_U 3
 #endif
 #ifndef SNN_DEL_MINB
 #define SNN_DEL_MINB 2
