@@ -17,3 +17,4 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     python bench.py --steps 200 --warmup 20 --settle 3000 --no-cpu-baseline --no-e2e --no-ktime > gpurun_out/ncu_launch.log 2>&1
 echo launches=$?
 NCU_FLAGS=0 NCU_STEPS=3100 NSKIP=9000 NCOUNT=3 KREGEX="k_front|k_deliver|k_flush" bash scripts/gpu_ncu.sh
+timeout 600 python bench.py --steps 10000 --warmup 1000 --history-bits 128 --no-cpu-baseline > gpurun_out/bench_h128.json 2> gpurun_out/bench_h128.err; echo bench_h128=$?
