@@ -390,6 +390,29 @@ __global__ void k_init_state(NetDev net, StateDev st) {
 // (SNN_BUILD_THREAD_PER_ROW: the round-1 thread-per-row builder, for comparison)
 static bool build_thread_per_row() { return getenv("SNN_BUILD_THREAD_PER_ROW") != nullptr; }
 
+// Load the construction kernels' modules (lazy loading would otherwise load
+// each on its first launch, inside the device-timed construction), the CUB
+// scan's included by one scan of a single element.
+cudaError_t build_preload(cudaStream_t s) {
+    cudaFuncAttributes a;
+    cudaError_t e;
+    const void *ks[] = {(const void *)k_count_warp, (const void *)k_fill_warp, (const void *)k_count,
+                        (const void *)k_fill, (const void *)k_pivot_scan, (const void *)k_segments};
+    for (const void *k : ks)
+        if ((e = cudaFuncGetAttributes(&a, k)) != cudaSuccess) return e;
+    int64_t *buf = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, buf, buf, 1, s)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&buf, 2 * sizeof(int64_t), s)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&tmp, tmp_bytes + 16, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(buf, 0, 2 * sizeof(int64_t), s)) != cudaSuccess) return e;
+    if ((e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, buf, buf + 1, 1, s)) != cudaSuccess) return e;
+    cudaFreeAsync(tmp, s);
+    cudaFreeAsync(buf, s);
+    return cudaStreamSynchronize(s);
+}
+
 cudaError_t build_count(const NetDev &net, const BuildTabs &tabs, uint32_t *piv, int64_t *len, cudaStream_t s) {
     if (build_thread_per_row()) {
         k_count<<<(net.N + kGeoThreads - 1) / kGeoThreads, kGeoThreads, 0, s>>>(net, tabs, piv);

@@ -7,13 +7,13 @@ sys.path.insert(0, os.getcwd())
 import numpy as np
 import workloads as W
 from paper_2107_04092_b200 import Snn
-for H in (64, 128):
-    rc = W.brunel(5003, p=0.04, plastic=True, delay=2, seed=13)
+for H, D in ((64, 2), (128, 2), (64, 15)):
+    rc = W.brunel(5003, p=0.04, plastic=True, delay=D, seed=13)
     g = Snn(rc.seed, rc.dt_ms, rc.delay, rc.frac_bits, slice_width=128, history_bits=H)
     rc.apply(g)
     g.step(150)
     w = g.read_state("WEIGHTS")
-    print("H", H, "steps", g.t, "spikes", int(g.read_state("SPIKE_COUNT").sum()), "w_sum", float(np.sum(w)))
+    print("H", H, "D", D, "steps", g.t, "spikes", int(g.read_state("SPIKE_COUNT").sum()), "w_sum", float(np.sum(w)))
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --show-backtrace no python /tmp/san_run.py > gpurun_out/sanitize_$tool.log 2>&1
