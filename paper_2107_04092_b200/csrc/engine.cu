@@ -706,9 +706,30 @@ static snn_status finalize(snn_sim *sim) {
     sim->stdp_grid = (uint32_t)nsm;                 // k_stdp: one CTA per SM
     sim->flush_grid = (uint32_t)nsm * flush_ctas_per_sm();
     // k_flush's share of the SMs beside the critical path: half of them for
-    // H = 64; H = 128 flushes half as many rows per step, so 2/7 of them
-    // (measured on cfg3: 42 of 148 SMs, 40.5 us/step vs 45.5 on 74)
-    sim->flush_grid_side = std::max(1, net.H > kHistBits ? nsm * 2 / 7 : nsm / 2);
+    // H = 64 and 2/7 for H = 128 (half the flush rows per step) at BASELINE
+    // config 3's balance of work (measured: 42 of 148 SMs, 40.5 us/step vs
+    // 45.5 on 74), scaled up by how much heavier the flush is relative to the
+    // critical path than there: expected flush synapses per step (the plastic
+    // synapses / H) against the neurons (k_front) and synapses (k_deliver),
+    // weighted by their per-unit kernel times on 74 B200 SMs (k_flush 6.5 ps
+    // per synapse, k_front 84 ps per neuron, k_deliver 8.5 fs per synapse of
+    // the graph: measured at configs 3 and 4)
+    {
+        double fsyn = 0.0;
+        for (const HostProj &hj : sim->projs)
+            if (hj.prm.kind == SNN_SYN_STDP) {
+                const PopDev &dp = net.pop[hj.dst];
+                const uint32_t lo = std::max(dp.base, net.tgt_lo), hi = std::min(dp.base + dp.n, net.tgt_hi);
+                fsyn += (double)sim->pops[hj.src].n * (double)(hi > lo ? hi - lo : 0u) * hj.prm.p;
+            }
+        const double t_fl = 6.5e-6 * fsyn / (double)net.H;
+        const double t_crit = 8.4e-5 * (double)net.N + 8.5e-9 * (double)sim->nsyn;
+        const double rho_ref = 6.5e-6 * (158114.0 * 126491.0 * 0.02 / 64.0) /
+                               (8.4e-5 * 316228.0 + 8.5e-9 * 1.0000561e9);      // config 3, H = 64
+        const double scale = t_crit > 0.0 ? std::max(1.0, (t_fl / t_crit) * ((double)net.H / 64.0) / rho_ref) : 1.0;
+        const int base = net.H > kHistBits ? nsm * 2 / 7 : nsm / 2;
+        sim->flush_grid_side = std::max(1, std::min((int)(base * scale), nsm * 4 / 5));
+    }
     if (const char *e = getenv("SNN_FL_CTAS")) sim->flush_grid_side = std::max(1, atoi(e));   // (experiments)
 
     CK(cudaStreamSynchronize(s));
