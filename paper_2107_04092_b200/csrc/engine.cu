@@ -726,7 +726,8 @@ static snn_status finalize(snn_sim *sim) {
         const double t_crit = 8.4e-5 * (double)net.N + 8.5e-9 * (double)sim->nsyn;
         const double rho_ref = 6.5e-6 * (158114.0 * 126491.0 * 0.02 / 64.0) /
                                (8.4e-5 * 316228.0 + 8.5e-9 * 1.0000561e9);      // config 3, H = 64
-        const double scale = t_crit > 0.0 ? std::max(1.0, (t_fl / t_crit) * ((double)net.H / 64.0) / rho_ref) : 1.0;
+        double scale = t_crit > 0.0 ? std::max(1.0, (t_fl / t_crit) * ((double)net.H / 64.0) / rho_ref) : 1.0;
+        if (net.H > kHistBits) scale = std::pow(scale, 1.45);   // (H = 128: config 4's optimum, 84 SMs, is 2x config 3's)
         const int base = net.H > kHistBits ? nsm * 2 / 7 : nsm / 2;
         sim->flush_grid_side = std::max(1, std::min((int)(base * scale), nsm * 4 / 5));
     }
